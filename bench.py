@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark of the BRMerge SpGEMM hot path on B200 (BASELINE.json metric:
+SpGEMM GFLOPS = 2*nnz(C_hat)/s, fp64 C = A*A, + achieved HBM GB/s vs peak).
+
+One step = one full C = A*B through the C ABI (n_prod + scan + binning,
+symbolic merge, row_size scan, numeric merge; all kernels), inputs resident in
+HBM. L2 is flushed (256 MiB write) between timed steps, outside the events.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME]
+                  [--mode precise|upper] [--impl ours|reference]
+
+N > 1 (torchrun, NCCL): weak scaling -- the global workload grows with N
+(stencil: 64 x 64 x 64N grid; uniform: N x rows) and rows are partitioned
+across ranks by balanced n_prod (§III.D); B is NCCL-broadcast from rank 0 at
+setup; each step ends with an NCCL all-gather of the per-rank nnz(C) (the
+global row_ptr offsets of the C row blocks). Time = max over ranks.
+`--impl reference` times the CPU oracle (test infrastructure) on a bounded
+row sample, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from inputs import generators as gen  # noqa: E402
+
+CONFIGS = {
+    "uniform2k_k8": 0, "stencil27_64": 1, "uniform1m_k16": 2, "rmat20_ef16": 3, "amg_lap2048_agg2x2": 4,
+}
+DEFAULT_CONFIG = "stencil27_64"
+
+
+def build_workload(name: str, world: int):
+    """(A, B, description) of the global workload for `world` ranks (weak scaling)."""
+    if name == "stencil27_64":
+        if world == 1:
+            A = gen.stencil27(64, seed=1)
+        else:  # 64 x 64 x (64*world) grid
+            A = stencil27_box(64, 64, 64 * world, seed=1)
+        return A, A, f"27-point stencil 64x64x{64 * world}, C=A*A"
+    if name == "uniform2k_k8":
+        A = gen.uniform_random(2000 * world, 2000 * world, 8, seed=1)
+        return A, A, f"uniform {2000 * world}^2, 8/row, C=A*A"
+    if name == "uniform1m_k16":
+        A = gen.uniform_random((1 << 20) * world, (1 << 20) * world, 16, seed=1)
+        return A, A, f"uniform 2^20*{world}, 16/row, C=A*A"
+    if name == "rmat20_ef16":
+        A = gen.rmat(20, 16, 0.57, 0.19, 0.19, 0.05, seed=1)
+        return A, A, "R-MAT scale 20 ef 16 (.57,.19,.19,.05), C=A*A (same graph at every N)"
+    if name == "amg_lap2048_agg2x2":
+        A = gen.laplace2d_5pt(2048)
+        P = gen.aggregation_prolongator(2048, seed=1)
+        return A, P, "5-pt Laplacian 2048^2 x 2x2 aggregation, C=A*P (same at every N)"
+    raise KeyError(name)
+
+
+def stencil27_box(nx, ny, nz, seed):
+    """27-point stencil on an nx*ny*nz box (row id (z*ny + y)*nx + x)."""
+    rng = np.random.default_rng(seed)
+    N = nx * ny * nz
+    idx = np.arange(N, dtype=np.int64)
+    x, y, z = idx % nx, (idx // nx) % ny, idx // (nx * ny)
+    cols, diag = [], []
+    for dz in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                ok = ((x + dx >= 0) & (x + dx < nx) & (y + dy >= 0) & (y + dy < ny)
+                      & (z + dz >= 0) & (z + dz < nz))
+                cols.append(np.where(ok, idx + (dz * ny + dy) * nx + dx, -1))
+                diag.append(dx == 0 and dy == 0 and dz == 0)
+    cm = np.stack(cols, axis=1)
+    valid = cm >= 0
+    vm = np.where(np.array(diag)[None, :], 26.0, -1.0) + rng.uniform(-0.01, 0.01, size=cm.shape)
+    rpt = np.zeros(N + 1, np.int64)
+    np.cumsum(valid.sum(axis=1), out=rpt[1:])
+    return gen.Csr(N, N, rpt, cm[valid].astype(np.int32), vm[valid])
+
+
+# tier table mirrored from csrc/brm_internal.cuh (checked by tests/test_bench_host.py)
+TIER_CAP = [0, 64, 256, 1024, 4096, 8192]
+TIER_LCAP = [0, 32, 128, 256, 1024, 1024]
+
+
+def tier_of(nprod: np.ndarray, nl: np.ndarray) -> np.ndarray:
+    t = np.full(nprod.shape, 6, np.int64)
+    for b in range(5, 0, -1):
+        t = np.where((nprod <= TIER_CAP[b]) & (nl <= TIER_LCAP[b]), b, t)
+    return np.where(nprod == 0, 0, t)
+
+
+def algorithmic_bytes(A, B, rows: np.ndarray, nnz_c_rows: int) -> int:
+    """Compulsory HBM bytes for computing C's `rows`: A rows (rpt pair + 12 B
+    per nonzero), every DISTINCT B row they touch (rpt pair + 12 B per
+    nonzero), C rows written (12 B per nonzero + 8 B rpt). DESIGN.md §8(d)."""
+    if rows.size == 0:
+        return 0
+    lens = A.rpt[rows + 1] - A.rpt[rows]
+    a_bytes = int(rows.size) * 16 + int(lens.sum()) * 12
+    idx = np.concatenate([np.arange(A.rpt[r], A.rpt[r + 1]) for r in rows]) if rows.size < 5000 else \
+        np.repeat(A.rpt[rows], lens) + (np.arange(int(lens.sum())) - np.repeat(np.cumsum(lens) - lens, lens))
+    touched = np.unique(A.col[idx])
+    b_bytes = int(touched.size) * 16 + int((B.rpt[touched + 1] - B.rpt[touched]).sum()) * 12
+    c_bytes = int(nnz_c_rows) * 12 + int(rows.size) * 8
+    return a_bytes + b_bytes + c_bytes
+
+
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        for line in (getattr(self, "out", "") or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (Eq. (2) Gustavson, single thread) on
+    a bounded row sample of the same workload, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    A, B, desc = build_workload(args.config, 1)
+    nprod = oracle.row_nprod(A, B)
+    rows, sample = _sample_rows(nprod, target_prod=args.ref_sample_prod)
+    sub_np = int(nprod[rows].sum())
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.spgemm_gustavson(A, B, rows=rows)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    sec = float(np.mean(times))
+    v = 2.0 * sub_np / sec / 1e9
+    line = {"impl": "reference", "metric": "SpGEMM GFLOPS (2*nnz(C_hat)/s), fp64 C=A*A",
+            "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "desc": desc, "rows_sampled": int(rows.size)},
+            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _sample_rows(nprod, target_prod):
+    """Evenly strided row sample whose n_prod sum is about target_prod."""
+    M = nprod.size
+    total = int(nprod.sum())
+    frac = min(1.0, target_prod / max(total, 1))
+    n = max(1, int(M * frac))
+    rows = np.unique(np.linspace(0, M - 1, n).astype(np.int64))
+    return rows, f"{rows.size} of {M} rows (evenly strided), n_prod {int(nprod[rows].sum())} of {total}"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="precise", choices=["precise", "upper"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-prod", type=float, default=1.5e7)
+    ap.add_argument("--ref-sample-prod", type=float, default=1.5e7)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2206_06611_b200 import Context, TorchCsr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    A, B, desc = build_workload(args.config, world)
+    ctx = Context(dev)
+    Bd = TorchCsr.from_csr(B) if rank == 0 or world == 1 else None
+    if world > 1:  # B broadcast with NCCL from rank 0 (setup)
+        if rank != 0:
+            Bd = TorchCsr(B.rows, B.cols, torch.empty(B.rows + 1, dtype=torch.int64, device=dev),
+                          torch.empty(B.nnz, dtype=torch.int32, device=dev),
+                          torch.empty(B.nnz, dtype=torch.float64, device=dev))
+        for t in (Bd.rpt, Bd.col, Bd.val):
+            dist.broadcast(t, 0)
+    Afull = TorchCsr.from_csr(A)
+    # row partition by balanced n_prod (§III.D), computed by the library's kernels
+    nprod_dev = ctx.brm_row_nprod(Afull, Bd)
+    off = ctx.brm_exclusive_scan_i64(nprod_dev)
+    bounds = ctx.brm_partition_rows(off, world).cpu().numpy()
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    nprod_h = nprod_dev.cpu().numpy()
+    del Afull
+    a0, a1 = int(A.rpt[r0]), int(A.rpt[r1])
+    Ablk = gen.Csr(r1 - r0, A.cols, (A.rpt[r0:r1 + 1] - a0).astype(np.int64), A.col[a0:a1].copy(), A.val[a0:a1].copy())
+    Ad = TorchCsr.from_csr(Ablk)
+    local_nprod = int(nprod_h[r0:r1].sum())
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        C = ctx.spgemm(Ad, Bd, args.mode)
+        if world > 1:
+            cnt = torch.tensor([C.nnz], dtype=torch.int64, device=dev)
+            allc = torch.empty(world, dtype=torch.int64, device=dev)
+            dist.all_gather_into_tensor(allc, cnt)
+        return C
+
+    for _ in range(args.warmup):
+        C = step()
+    torch.cuda.synchronize(dev)
+    ctx.set_timing(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    bin_ms = np.zeros(7)
+    sym_ms = num_ms = pre_ms = scan_ms = cmp_ms = 0.0
+    launches = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            C = step()
+            ev[k][1].record(stream)
+            s = ctx.stats()
+            bin_ms += np.array(s["ms_bin_numeric"])
+            sym_ms += s["ms_symbolic"]
+            num_ms += s["ms_numeric"]
+            pre_ms += s["ms_nprod_scan"]
+            scan_ms += s["ms_rowsize_scan"]
+            cmp_ms += s["ms_compact"]
+            launches += s["launches"]
+        torch.cuda.synchronize(dev)
+    ctx.set_timing(False)
+    if world > 1:
+        dist.barrier()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    stats = ctx.stats()
+    nnz_local = C.nnz
+    tot = torch.tensor([local_nprod, nnz_local], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot)
+    nprod_all, nnz_all = int(tot[0]), int(tot[1])
+    ms_step = total_ms / args.steps
+    gflops = 2.0 * nprod_all / (ms_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (numeric merge of the busiest tier)
+    peak, peak_kind = measured_peak_hbm()
+    dom = int(np.argmax(bin_ms))
+    nl_loc = np.diff(Ablk.rpt)
+    np_loc = nprod_h[r0:r1]
+    tiers = tier_of(np_loc, nl_loc)
+    dom_rows = np.nonzero(tiers == dom)[0]
+    crpt = C.rpt.cpu().numpy()
+    nnz_dom = int((crpt[dom_rows + 1] - crpt[dom_rows]).sum())
+    dom_bytes = algorithmic_bytes(Ablk, B, dom_rows, nnz_dom)
+    dom_ms = bin_ms[dom] / args.steps
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
+    all_rows = np.arange(Ablk.rows)
+    step_bytes = algorithmic_bytes(Ablk, B, all_rows, nnz_local)
+    b_all = torch.tensor([step_bytes], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(b_all)
+    step_gbs = int(b_all.item()) / (ms_step * 1e-3) / 1e9
+
+    # end to end through the host-buffer C entry (pinned H2D, D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        Ah = TorchCsr.from_csr(Ablk, pin=True)
+        Bh = TorchCsr.from_csr(B, pin=True)
+        ctx.brmerge_spgemm_host(Ah, Bh, args.mode)  # warm
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k_e2e = max(1, min(args.steps, 5))
+        e0.record(stream)
+        for _ in range(k_e2e):
+            out = ctx.brmerge_spgemm_host(Ah, Bh, args.mode)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms = e0.elapsed_time(e1) / k_e2e
+        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_ms = float(te.item())
+        h2d = sum(x.numel() * x.element_size() for X in (Ah, Bh) for x in (X.rpt, X.col, X.val))
+        d2h = (Ablk.rows + 1) * 8 + out[3].size * 4 + out[4].size * 8
+        e2e = {"value": 2.0 * nprod_all / (e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            import oracle
+            rows, sample = _sample_rows(nprod_h[r0:r1], args.cpu_sample_prod)
+            t0 = time.perf_counter()
+            oracle.spgemm_gustavson(Ablk, B, rows=rows)
+            dt = time.perf_counter() - t0
+            cpu = {"value": 2.0 * int(np_loc[rows].sum()) / dt / 1e9, "unit": "GFLOP/s", "cores": 1,
+                   "kind": "oracle", "sample": sample + f"; {dt:.1f} s single-threaded"}
+        except Exception as e:  # report, never fake
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": "SpGEMM GFLOPS (2*nnz(C_hat)/s), fp64 C=A*A, + achieved HBM GB/s vs peak",
+            "value": gflops, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "desc": desc, "mode": args.mode, "rows": A.rows,
+                       "nnz_a": A.nnz, "nprod": nprod_all, "nnz_c": nnz_all,
+                       "compression_ratio": nprod_all / max(nnz_all, 1),
+                       "l2": "flushed (256 MiB write) between timed steps, outside the events",
+                       "parallelism": f"dp{world} rows by balanced n_prod"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": f"k_tier bin {dom} (numeric merge)" if dom < 6 else "k_global_tier",
+                         "kernel_ms": dom_ms, "algorithmic_bytes": dom_bytes, "peak_kind": peak_kind},
+            "hbm_step": {"achieved_gbs": step_gbs, "frac": step_gbs / peak, "algorithmic_bytes": int(b_all.item())},
+            "phases_ms": {"nprod_scan_bin": pre_ms / args.steps, "symbolic": sym_ms / args.steps,
+                          "numeric": num_ms / args.steps, "rowsize_scan": scan_ms / args.steps,
+                          "compact": cmp_ms / args.steps, "numeric_per_bin": (bin_ms / args.steps).tolist()},
+            "bin_rows": stats["bin_rows"],
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,607 @@
+// api.cu -- the C ABI of include/brmerge.h: context, workspace, and the
+// orchestration of Fig. 4a (BRMerge-Upper) and Fig. 4b (BRMerge-Precise),
+// PAPER.md:284-300, on one device stream.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "brmerge.h"
+#include "kernels.cuh"
+
+using namespace brm;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+}  // namespace
+
+struct brm_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  bool timing = false;
+  // workspace (grow-only)
+  DevBuf nprod_off, row_size, bins, status, small, cbar_col, cbar_val, gws, gws_off, heavy_info;
+  DevBuf stA_rpt, stA_col, stA_val, stB_rpt, stB_col, stB_val, stC_rpt, stC_col, stC_val;
+  HostBuf h_small, h_heavy, h_gws_off, h_C;
+  // plan (structure -> fill)
+  bool planned = false;
+  brm_mode_t mode = BRM_PRECISE;
+  CsrView A{}, B{};
+  int64_t M = 0, K = 0, N = 0, nnz_c = 0;
+  int64_t bin_start[BRM_NUM_BINS] = {};
+  int64_t bin_rows[BRM_NUM_BINS] = {};
+  DevSummary sum{};
+  bool heavy_loaded = false;
+  std::vector<int64_t> heavy;  // (n_prod, nl) per global-tier row
+  brm_stats_t stats{};
+  cudaEvent_t ev[32] = {};
+  unsigned ev_mask = 0;  // events recorded since the last structure call
+  int64_t launches = 0;  // kernels launched since the last structure call
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+brm_status_t fail(brm_context_t* c, brm_status_t s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+brm_status_t cuda_fail(brm_context_t* c, cudaError_t e, const char* what) {
+  const bool oom = e == cudaErrorMemoryAllocation;
+  cudaGetLastError();
+  return fail(c, oom ? BRM_ERR_OOM : BRM_ERR_CUDA,
+              std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+
+#define CK(call, what)                               \
+  do {                                               \
+    cudaError_t e_ = (call);                         \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, what); \
+  } while (0)
+
+cudaError_t ensure(brm_context_t* ctx, DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return cudaSuccess;
+  if (b.p) {
+    cudaError_t e = cudaFreeAsync(b.p, ctx->stream);
+    if (e != cudaSuccess) return e;
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  const size_t want = (bytes + 255) & ~size_t(255);
+  cudaError_t e = cudaMallocAsync(&b.p, want, ctx->stream);
+  if (e != cudaSuccess) {
+    b.p = nullptr;
+    return e;
+  }
+  b.cap = want;
+  return cudaSuccess;
+}
+
+cudaError_t ensure_host(HostBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return cudaSuccess;
+  if (b.p) cudaFreeHost(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  const size_t want = std::max(bytes, b.cap * 3 / 2);
+  cudaError_t e = cudaMallocHost(&b.p, want);
+  if (e != cudaSuccess) {
+    b.p = nullptr;
+    return e;
+  }
+  b.cap = want;
+  return cudaSuccess;
+}
+
+void free_dev(brm_context_t* ctx, DevBuf& b) {
+  if (b.p) cudaFreeAsync(b.p, ctx->stream);
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+brm_status_t check_csr(brm_context_t* ctx, const brm_csr_t* X, const char* name) {
+  if (!X) return fail(ctx, BRM_ERR_INVALID, std::string(name) + " is null");
+  if (X->rows < 0 || X->cols < 0 || X->nnz < 0)
+    return fail(ctx, BRM_ERR_INVALID, std::string(name) + " has a negative size");
+  if (!X->rpt) return fail(ctx, BRM_ERR_INVALID, std::string(name) + ".rpt is null");
+  if (X->nnz > 0 && (!X->col || !X->val))
+    return fail(ctx, BRM_ERR_INVALID, std::string(name) + ".col/.val is null");
+  return BRM_OK;
+}
+
+// Small device block: summary + scan counters + bin cursor + nnz total.
+struct SmallDev {
+  DevSummary summary;
+  unsigned long long cursor[BRM_NUM_BINS];
+  unsigned int counter[4];
+  int64_t nnz_total;
+};
+
+SmallDev* small_dev(brm_context_t* ctx) { return static_cast<SmallDev*>(ctx->small.p); }
+
+// Timing events (no synchronisation when recorded; resolved in brm_get_stats):
+// 0/1 n_prod+scan+bin, 2/3 structure merge, 3/4 row_size scan, 5/6 fill,
+// 10+2b / 11+2b numeric merge of bin b.
+constexpr int kEvBin = 10;
+void ev_record(brm_context_t* ctx, int i) {
+  if (!ctx->timing) return;
+  cudaEventRecord(ctx->ev[i], ctx->stream);
+  ctx->ev_mask |= 1u << i;
+}
+
+float ev_ms(const brm_context_t* ctx, int a, int b) {
+  float ms = 0.f;
+  if (ctx->timing && (ctx->ev_mask >> a & 1u) && (ctx->ev_mask >> b & 1u))
+    cudaEventElapsedTime(&ms, ctx->ev[a], ctx->ev[b]);
+  return ms;
+}
+
+// Exclusive scan with fresh look-back state.
+brm_status_t run_scan(brm_context_t* ctx, const int64_t* in, int64_t n, int64_t* out, int64_t* total_out) {
+  const int64_t tiles = scan_tiles(n);
+  CK(ensure(ctx, ctx->status, (size_t)(tiles + 1) * 8), "alloc scan status");
+  CK(cudaMemsetAsync(ctx->status.p, 0, (size_t)(tiles + 1) * 8, ctx->stream), "memset scan status");
+  SmallDev* sd = small_dev(ctx);
+  CK(cudaMemsetAsync(&sd->counter[1], 0, 4, ctx->stream), "memset scan counter");
+  if (n == 0) {
+    CK(cudaMemsetAsync(out, 0, 8, ctx->stream), "memset scan out");
+    if (total_out) CK(cudaMemsetAsync(total_out, 0, 8, ctx->stream), "memset scan total");
+    return BRM_OK;
+  }
+  CK(launch_scan_i64(in, n, out, static_cast<unsigned long long*>(ctx->status.p), &sd->counter[1],
+                     total_out, ctx->stream),
+     "k_scan_i64");
+  ++ctx->launches;
+  return BRM_OK;
+}
+
+// Launch the merge of every non-empty bin with output kind `out`.
+brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bin) {
+  const int32_t* bins = static_cast<const int32_t*>(ctx->bins.p);
+  for (int b = 1; b < kBinGlobal; ++b) {
+    if (!ctx->bin_rows[b]) continue;
+    if (per_bin) ev_record(ctx, kEvBin + 2 * b);
+    CK(launch_tier(b, out, ctx->A, ctx->B, bins + ctx->bin_start[b], ctx->bin_rows[b], o, ctx->stream),
+       "k_tier");
+    ++ctx->launches;
+    if (per_bin) ev_record(ctx, kEvBin + 2 * b + 1);
+  }
+  const int64_t nh = ctx->bin_rows[kBinGlobal];
+  if (!nh) return BRM_OK;
+  if (per_bin) ev_record(ctx, kEvBin + 2 * kBinGlobal);
+  const int32_t* hrows = bins + ctx->bin_start[kBinGlobal];
+  if (!ctx->heavy_loaded) {
+    CK(ensure(ctx, ctx->heavy_info, (size_t)nh * 16), "alloc heavy info");
+    CK(launch_heavy_info(ctx->A, static_cast<const int64_t*>(ctx->nprod_off.p), hrows, nh,
+                         static_cast<int64_t*>(ctx->heavy_info.p), ctx->stream),
+       "k_heavy_info");
+    ++ctx->launches;
+    CK(ensure_host(ctx->h_heavy, (size_t)nh * 16), "alloc pinned heavy info");
+    CK(cudaMemcpyAsync(ctx->h_heavy.p, ctx->heavy_info.p, (size_t)nh * 16, cudaMemcpyDeviceToHost,
+                       ctx->stream),
+       "copy heavy info");
+    CK(cudaStreamSynchronize(ctx->stream), "sync heavy info");
+    const int64_t* hi = static_cast<const int64_t*>(ctx->h_heavy.p);
+    ctx->heavy.assign(hi, hi + 2 * nh);
+    ctx->heavy_loaded = true;
+  }
+  const bool vals = out != OUT_SYMBOLIC;
+  // batch the heavy rows so their ping-pong slices fit the workspace budget
+  int64_t max_row = 0;
+  for (int64_t t = 0; t < nh; ++t)
+    max_row = std::max(max_row, global_row_bytes(ctx->heavy[2 * t], ctx->heavy[2 * t + 1], vals));
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  int64_t budget = std::min<int64_t>((int64_t)(free_b / 2) + (int64_t)ctx->gws.cap, 16ll << 30);
+  budget = std::max(budget, max_row);
+  CK(ensure_host(ctx->h_gws_off, (size_t)nh * 16), "alloc pinned ws offsets");
+  CK(ensure(ctx, ctx->gws_off, (size_t)nh * 16), "alloc ws offsets");
+  int64_t* hoff = static_cast<int64_t*>(ctx->h_gws_off.p);
+  // first pass: offsets for all rows, batch boundaries
+  std::vector<int64_t> cuts{0};
+  int64_t acc = 0, need = 0;
+  for (int64_t t = 0; t < nh; ++t) {
+    const int64_t bytes = global_row_bytes(ctx->heavy[2 * t], ctx->heavy[2 * t + 1], vals);
+    if (acc + bytes > budget) {
+      cuts.push_back(t);
+      acc = 0;
+    }
+    hoff[2 * t] = acc;
+    hoff[2 * t + 1] = ctx->heavy[2 * t];
+    acc += bytes;
+    need = std::max(need, acc);
+  }
+  cuts.push_back(nh);
+  CK(ensure(ctx, ctx->gws, (size_t)need), "alloc global-tier workspace");
+  CK(cudaMemcpyAsync(ctx->gws_off.p, hoff, (size_t)nh * 16, cudaMemcpyHostToDevice, ctx->stream),
+     "copy ws offsets");
+  for (size_t c = 0; c + 1 < cuts.size(); ++c) {
+    const int64_t b0 = cuts[c], n = cuts[c + 1] - b0;
+    if (n <= 0) continue;
+    CK(launch_global_tier(out, ctx->A, ctx->B, hrows + b0, n,
+                          static_cast<const int64_t*>(ctx->gws_off.p) + 2 * b0,
+                          static_cast<unsigned char*>(ctx->gws.p), o, ctx->stream),
+       "k_global_tier");
+    ++ctx->launches;
+  }
+  if (per_bin) ev_record(ctx, kEvBin + 2 * kBinGlobal + 1);
+  return BRM_OK;
+}
+
+brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_csr_t* B, brm_mode_t mode,
+                            int64_t* c_rpt, int64_t* c_nnz) {
+  brm_status_t s;
+  if ((s = check_csr(ctx, A, "A")) != BRM_OK) return s;
+  if ((s = check_csr(ctx, B, "B")) != BRM_OK) return s;
+  if (mode != BRM_UPPER && mode != BRM_PRECISE) return fail(ctx, BRM_ERR_INVALID, "mode must be BRM_UPPER or BRM_PRECISE");
+  if (A->cols != B->rows) return fail(ctx, BRM_ERR_DIM, "A.cols != B.rows");
+  if (B->cols >= INT32_MAX) return fail(ctx, BRM_ERR_INVALID, "B.cols must be < 2^31 - 1");
+  if (!c_rpt || !c_nnz) return fail(ctx, BRM_ERR_INVALID, "c_rpt / c_nnz is null");
+  ctx->planned = false;
+  ctx->heavy_loaded = false;
+  ctx->mode = mode;
+  ctx->A = CsrView{A->rpt, A->col, A->val};
+  ctx->B = CsrView{B->rpt, B->col, B->val};
+  ctx->M = A->rows;
+  ctx->K = A->cols;
+  ctx->N = B->cols;
+  const int64_t M = ctx->M;
+  memset(&ctx->stats, 0, sizeof(ctx->stats));
+  ctx->ev_mask = 0;
+  ctx->launches = 0;
+  ctx->stats.rows = M;
+  ctx->stats.mode = mode;
+  ctx->stats.timing_enabled = ctx->timing ? 1 : 0;
+
+  CK(ensure(ctx, ctx->small, sizeof(SmallDev)), "alloc small");
+  CK(ensure_host(ctx->h_small, sizeof(SmallDev)), "alloc pinned small");
+  CK(ensure(ctx, ctx->nprod_off, (size_t)(M + 1) * 8), "alloc nprod_off");
+  CK(ensure(ctx, ctx->row_size, (size_t)(M + 1) * 8), "alloc row_size");
+  CK(ensure(ctx, ctx->bins, (size_t)M * 4), "alloc bins");
+  const int64_t tiles = scan_tiles(M);
+  CK(ensure(ctx, ctx->status, (size_t)(tiles + 1) * 8), "alloc scan status");
+  SmallDev* sd = small_dev(ctx);
+  ev_record(ctx, 0);
+  CK(cudaMemsetAsync(sd, 0, sizeof(SmallDev), ctx->stream), "memset small");
+  CK(cudaMemsetAsync(ctx->status.p, 0, (size_t)(tiles + 1) * 8, ctx->stream), "memset status");
+  int64_t* nprod_off = static_cast<int64_t*>(ctx->nprod_off.p);
+  int64_t* row_size = static_cast<int64_t*>(ctx->row_size.p);
+  if (M == 0) {
+    CK(cudaMemsetAsync(nprod_off, 0, 8, ctx->stream), "memset");
+  }
+  // Step 1: n_prod per row + prefix sum (+ bin histogram)
+  CK(launch_nprod_scan(ctx->A, B->rpt, M, nprod_off, static_cast<unsigned long long*>(ctx->status.p),
+                       &sd->counter[0], &sd->summary, ctx->stream),
+     "k_nprod_scan");
+  // row binning
+  CK(launch_bin_scatter(ctx->A, nprod_off, M, &sd->summary, sd->cursor, static_cast<int32_t*>(ctx->bins.p),
+                        row_size, ctx->stream),
+     "k_bin_scatter");
+  if (M > 0) ctx->launches += 2;
+  ev_record(ctx, 1);
+  CK(cudaMemcpyAsync(ctx->h_small.p, sd, sizeof(SmallDev), cudaMemcpyDeviceToHost, ctx->stream), "copy summary");
+  CK(cudaStreamSynchronize(ctx->stream), "sync summary");
+  ctx->sum = static_cast<SmallDev*>(ctx->h_small.p)->summary;
+  ctx->stats.nprod_total = ctx->sum.nprod_total;
+  ctx->stats.nprod_max = (int64_t)ctx->sum.nprod_max;
+  if (ctx->sum.nprod_max >= (1ull << 31))
+    return fail(ctx, BRM_ERR_OVERFLOW, "a row has n_prod >= 2^31");
+  int64_t acc = 0;
+  for (int b = 0; b < BRM_NUM_BINS; ++b) {
+    ctx->bin_rows[b] = (int64_t)ctx->sum.bin_rows[b];
+    ctx->stats.bin_rows[b] = ctx->bin_rows[b];
+    ctx->stats.bin_nprod[b] = (int64_t)ctx->sum.bin_nprod[b];
+    ctx->bin_start[b] = acc;
+    if (b != kBinEmpty) acc += ctx->bin_rows[b];
+  }
+  // UPPER: Steps 3-4 (C_bar by n_prod offsets, numeric merge);
+  // PRECISE: Step 3 (symbolic merge)
+  RowOut o{};
+  int out;
+  if (mode == BRM_UPPER) {
+    const int64_t np = ctx->sum.nprod_total;
+    CK(ensure(ctx, ctx->cbar_col, (size_t)np * 4), "alloc C_bar col");
+    CK(ensure(ctx, ctx->cbar_val, (size_t)np * 8), "alloc C_bar val");
+    o.base = nprod_off;
+    o.col = static_cast<int32_t*>(ctx->cbar_col.p);
+    o.val = static_cast<double*>(ctx->cbar_val.p);
+    o.row_size = row_size;
+    out = OUT_CBAR;
+  } else {
+    o.row_size = row_size;
+    out = OUT_SYMBOLIC;
+  }
+  ev_record(ctx, 2);
+  if ((s = run_merge(ctx, out, o, mode == BRM_UPPER)) != BRM_OK) return s;
+  ev_record(ctx, 3);
+  // Step 5 (UPPER) / Step 4 (PRECISE): prefix sum of row sizes -> rpt, nnz(C)
+  if ((s = run_scan(ctx, row_size, M, c_rpt, &sd->nnz_total)) != BRM_OK) return s;
+  ev_record(ctx, 4);
+  CK(cudaMemcpyAsync(ctx->h_small.p, sd, sizeof(SmallDev), cudaMemcpyDeviceToHost, ctx->stream), "copy nnz");
+  CK(cudaStreamSynchronize(ctx->stream), "sync nnz");
+  ctx->nnz_c = static_cast<SmallDev*>(ctx->h_small.p)->nnz_total;
+  *c_nnz = ctx->nnz_c;
+  ctx->stats.nnz_c = ctx->nnz_c;
+  ctx->planned = true;
+  return BRM_OK;
+}
+
+brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
+  if (!ctx->planned) return fail(ctx, BRM_ERR_STATE, "fill without a preceding structure call");
+  if (!C || !C->rpt || (ctx->nnz_c > 0 && (!C->col || !C->val)))
+    return fail(ctx, BRM_ERR_INVALID, "C arrays are null");
+  C->rows = ctx->M;
+  C->cols = ctx->N;
+  C->nnz = ctx->nnz_c;
+  ev_record(ctx, 5);
+  if (ctx->mode == BRM_UPPER) {
+    // Step 6 of Fig. 4a: copy C_bar -> C
+    CK(launch_compact(ctx->M, static_cast<const int64_t*>(ctx->nprod_off.p), C->rpt,
+                      static_cast<const int32_t*>(ctx->cbar_col.p), static_cast<const double*>(ctx->cbar_val.p),
+                      C->col, C->val, ctx->stream),
+       "k_compact");
+    ++ctx->launches;
+    ev_record(ctx, 6);
+  } else {
+    // Step 5 of Fig. 4b: numeric merge straight into C
+    RowOut o{};
+    o.base = C->rpt;
+    o.col = C->col;
+    o.val = C->val;
+    brm_status_t s = run_merge(ctx, OUT_C, o, true);
+    if (s != BRM_OK) return s;
+    ev_record(ctx, 6);
+  }
+  return BRM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* brm_status_string(brm_status_t s) {
+  switch (s) {
+    case BRM_OK: return "BRM_OK";
+    case BRM_ERR_INVALID: return "BRM_ERR_INVALID";
+    case BRM_ERR_DIM: return "BRM_ERR_DIM";
+    case BRM_ERR_CUDA: return "BRM_ERR_CUDA";
+    case BRM_ERR_OOM: return "BRM_ERR_OOM";
+    case BRM_ERR_OVERFLOW: return "BRM_ERR_OVERFLOW";
+    case BRM_ERR_STATE: return "BRM_ERR_STATE";
+  }
+  return "BRM_ERR_UNKNOWN";
+}
+
+brm_status_t brm_create(brm_context_t** out, int device, void* stream) {
+  if (!out) return BRM_ERR_INVALID;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+    cudaGetLastError();
+    return BRM_ERR_CUDA;
+  }
+  brm_context_t* ctx = new brm_context_t;
+  ctx->device = device;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  DeviceGuard g(device);
+  for (auto& e : ctx->ev) cudaEventCreate(&e);
+  *out = ctx;
+  return BRM_OK;
+}
+
+brm_status_t brm_destroy(brm_context_t* ctx) {
+  if (!ctx) return BRM_ERR_INVALID;
+  {
+    DeviceGuard g(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (DevBuf* b : {&ctx->nprod_off, &ctx->row_size, &ctx->bins, &ctx->status, &ctx->small, &ctx->cbar_col,
+                      &ctx->cbar_val, &ctx->gws, &ctx->gws_off, &ctx->heavy_info, &ctx->stA_rpt, &ctx->stA_col,
+                      &ctx->stA_val, &ctx->stB_rpt, &ctx->stB_col, &ctx->stB_val, &ctx->stC_rpt, &ctx->stC_col,
+                      &ctx->stC_val})
+      free_dev(ctx, *b);
+    cudaStreamSynchronize(ctx->stream);
+    for (HostBuf* b : {&ctx->h_small, &ctx->h_heavy, &ctx->h_gws_off, &ctx->h_C})
+      if (b->p) cudaFreeHost(b->p);
+    for (auto& e : ctx->ev)
+      if (e) cudaEventDestroy(e);
+  }
+  delete ctx;
+  return BRM_OK;
+}
+
+brm_status_t brm_set_stream(brm_context_t* ctx, void* stream) {
+  if (!ctx) return BRM_ERR_INVALID;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return BRM_OK;
+}
+
+brm_status_t brm_set_timing(brm_context_t* ctx, int enable) {
+  if (!ctx) return BRM_ERR_INVALID;
+  ctx->timing = enable != 0;
+  return BRM_OK;
+}
+
+const char* brm_last_error(const brm_context_t* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+brm_status_t brm_get_stats(const brm_context_t* ctx, brm_stats_t* out) {
+  if (!ctx || !out) return BRM_ERR_INVALID;
+  *out = ctx->stats;
+  out->launches = ctx->launches;
+  if (ctx->timing && ctx->ev_mask) {
+    DeviceGuard g(ctx->device);
+    for (int i = 31; i >= 0; --i)  // wait for everything recorded
+      if (ctx->ev_mask >> i & 1u) cudaEventSynchronize(ctx->ev[i]);
+    out->ms_nprod_scan = ev_ms(ctx, 0, 1);
+    if (ctx->mode == BRM_UPPER) {
+      out->ms_numeric = ev_ms(ctx, 2, 3);
+      out->ms_compact = ev_ms(ctx, 5, 6);
+    } else {
+      out->ms_symbolic = ev_ms(ctx, 2, 3);
+      out->ms_numeric = ev_ms(ctx, 5, 6);
+    }
+    out->ms_rowsize_scan = ev_ms(ctx, 3, 4);
+    for (int b = 0; b < BRM_NUM_BINS; ++b) out->ms_bin_numeric[b] = ev_ms(ctx, kEvBin + 2 * b, kEvBin + 2 * b + 1);
+  }
+  return BRM_OK;
+}
+
+brm_status_t brmerge_spgemm_structure(brm_context_t* ctx, const brm_csr_t* A, const brm_csr_t* B,
+                                      brm_mode_t mode, int64_t* c_rpt, int64_t* c_nnz) {
+  if (!ctx) return BRM_ERR_INVALID;
+  DeviceGuard g(ctx->device);
+  return structure_impl(ctx, A, B, mode, c_rpt, c_nnz);
+}
+
+brm_status_t brmerge_spgemm_fill(brm_context_t* ctx, brm_csr_t* C) {
+  if (!ctx) return BRM_ERR_INVALID;
+  DeviceGuard g(ctx->device);
+  return fill_impl(ctx, C);
+}
+
+brm_status_t brmerge_spgemm(brm_context_t* ctx, const brm_csr_t* A, const brm_csr_t* B, brm_mode_t mode,
+                            brm_csr_t* C) {
+  if (!ctx) return BRM_ERR_INVALID;
+  if (!C) return fail(ctx, BRM_ERR_INVALID, "C is null");
+  if (!A) return fail(ctx, BRM_ERR_INVALID, "A is null");
+  DeviceGuard g(ctx->device);
+  memset(C, 0, sizeof(*C));
+  int64_t* rpt = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&rpt), (size_t)(A->rows + 1) * 8, ctx->stream), "alloc C.rpt");
+  int64_t nnz = 0;
+  brm_status_t s = structure_impl(ctx, A, B, mode, rpt, &nnz);
+  if (s != BRM_OK) {
+    cudaFreeAsync(rpt, ctx->stream);
+    return s;
+  }
+  C->rpt = rpt;
+  cudaError_t e1 = cudaMallocAsync(reinterpret_cast<void**>(&C->col), (size_t)std::max<int64_t>(nnz, 1) * 4, ctx->stream);
+  cudaError_t e2 = e1 == cudaSuccess
+                       ? cudaMallocAsync(reinterpret_cast<void**>(&C->val), (size_t)std::max<int64_t>(nnz, 1) * 8, ctx->stream)
+                       : e1;
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    brm_csr_free(ctx, C);
+    return cuda_fail(ctx, e1 != cudaSuccess ? e1 : e2, "alloc C.col/val");
+  }
+  s = fill_impl(ctx, C);
+  if (s != BRM_OK) brm_csr_free(ctx, C);
+  return s;
+}
+
+brm_status_t brm_csr_free(brm_context_t* ctx, brm_csr_t* C) {
+  if (!ctx || !C) return BRM_ERR_INVALID;
+  DeviceGuard g(ctx->device);
+  if (C->rpt) cudaFreeAsync(C->rpt, ctx->stream);
+  if (C->col) cudaFreeAsync(C->col, ctx->stream);
+  if (C->val) cudaFreeAsync(C->val, ctx->stream);
+  C->rpt = nullptr;
+  C->col = nullptr;
+  C->val = nullptr;
+  return BRM_OK;
+}
+
+brm_status_t brmerge_spgemm_host(brm_context_t* ctx, const brm_csr_t* Ah, const brm_csr_t* Bh, brm_mode_t mode,
+                                 brm_csr_t* Ch) {
+  if (!ctx) return BRM_ERR_INVALID;
+  brm_status_t s;
+  if ((s = check_csr(ctx, Ah, "A")) != BRM_OK) return s;
+  if ((s = check_csr(ctx, Bh, "B")) != BRM_OK) return s;
+  if (!Ch) return fail(ctx, BRM_ERR_INVALID, "C is null");
+  DeviceGuard g(ctx->device);
+  auto up = [&](DevBuf& d, const void* h, size_t bytes) -> cudaError_t {
+    cudaError_t e = ensure(ctx, d, bytes);
+    if (e != cudaSuccess) return e;
+    if (bytes) e = cudaMemcpyAsync(d.p, h, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    return e;
+  };
+  CK(up(ctx->stA_rpt, Ah->rpt, (size_t)(Ah->rows + 1) * 8), "H2D A.rpt");
+  CK(up(ctx->stA_col, Ah->col, (size_t)Ah->nnz * 4), "H2D A.col");
+  CK(up(ctx->stA_val, Ah->val, (size_t)Ah->nnz * 8), "H2D A.val");
+  CK(up(ctx->stB_rpt, Bh->rpt, (size_t)(Bh->rows + 1) * 8), "H2D B.rpt");
+  CK(up(ctx->stB_col, Bh->col, (size_t)Bh->nnz * 4), "H2D B.col");
+  CK(up(ctx->stB_val, Bh->val, (size_t)Bh->nnz * 8), "H2D B.val");
+  brm_csr_t Ad{Ah->rows, Ah->cols, Ah->nnz, static_cast<int64_t*>(ctx->stA_rpt.p),
+               static_cast<int32_t*>(ctx->stA_col.p), static_cast<double*>(ctx->stA_val.p)};
+  brm_csr_t Bd{Bh->rows, Bh->cols, Bh->nnz, static_cast<int64_t*>(ctx->stB_rpt.p),
+               static_cast<int32_t*>(ctx->stB_col.p), static_cast<double*>(ctx->stB_val.p)};
+  CK(ensure(ctx, ctx->stC_rpt, (size_t)(Ah->rows + 1) * 8), "alloc C.rpt");
+  int64_t nnz = 0;
+  if ((s = structure_impl(ctx, &Ad, &Bd, mode, static_cast<int64_t*>(ctx->stC_rpt.p), &nnz)) != BRM_OK) return s;
+  CK(ensure(ctx, ctx->stC_col, (size_t)nnz * 4), "alloc C.col");
+  CK(ensure(ctx, ctx->stC_val, (size_t)nnz * 8), "alloc C.val");
+  brm_csr_t Cd{0, 0, 0, static_cast<int64_t*>(ctx->stC_rpt.p), static_cast<int32_t*>(ctx->stC_col.p),
+               static_cast<double*>(ctx->stC_val.p)};
+  if ((s = fill_impl(ctx, &Cd)) != BRM_OK) return s;
+  const size_t brpt = (size_t)(Ah->rows + 1) * 8, bcol = (size_t)nnz * 4, bval = (size_t)nnz * 8;
+  CK(ensure_host(ctx->h_C, brpt + bcol + bval + 32), "alloc pinned C");
+  unsigned char* h = static_cast<unsigned char*>(ctx->h_C.p);
+  CK(cudaMemcpyAsync(h, Cd.rpt, brpt, cudaMemcpyDeviceToHost, ctx->stream), "D2H C.rpt");
+  unsigned char* hv = h + ((brpt + 15) & ~size_t(15));
+  if (bval) CK(cudaMemcpyAsync(hv, Cd.val, bval, cudaMemcpyDeviceToHost, ctx->stream), "D2H C.val");
+  unsigned char* hc = hv + ((bval + 15) & ~size_t(15));
+  if (bcol) CK(cudaMemcpyAsync(hc, Cd.col, bcol, cudaMemcpyDeviceToHost, ctx->stream), "D2H C.col");
+  CK(cudaStreamSynchronize(ctx->stream), "sync D2H");
+  Ch->rows = Ah->rows;
+  Ch->cols = Bh->cols;
+  Ch->nnz = nnz;
+  Ch->rpt = reinterpret_cast<int64_t*>(h);
+  Ch->val = reinterpret_cast<double*>(hv);
+  Ch->col = reinterpret_cast<int32_t*>(hc);
+  return BRM_OK;
+}
+
+brm_status_t brm_row_nprod(brm_context_t* ctx, const brm_csr_t* A, const brm_csr_t* B, int64_t* nprod) {
+  if (!ctx) return BRM_ERR_INVALID;
+  brm_status_t s;
+  if ((s = check_csr(ctx, A, "A")) != BRM_OK) return s;
+  if ((s = check_csr(ctx, B, "B")) != BRM_OK) return s;
+  if (A->cols != B->rows) return fail(ctx, BRM_ERR_DIM, "A.cols != B.rows");
+  if (!nprod && A->rows) return fail(ctx, BRM_ERR_INVALID, "nprod is null");
+  DeviceGuard g(ctx->device);
+  CK(launch_row_nprod(CsrView{A->rpt, A->col, A->val}, B->rpt, A->rows, nprod, ctx->stream), "k_row_nprod");
+  return BRM_OK;
+}
+
+brm_status_t brm_exclusive_scan_i64(brm_context_t* ctx, const int64_t* in, int64_t* out, int64_t n) {
+  if (!ctx) return BRM_ERR_INVALID;
+  if (n < 0 || !out || (n > 0 && !in)) return fail(ctx, BRM_ERR_INVALID, "bad scan arguments");
+  DeviceGuard g(ctx->device);
+  CK(ensure(ctx, ctx->small, sizeof(SmallDev)), "alloc small");
+  return run_scan(ctx, in, n, out, nullptr);
+}
+
+brm_status_t brm_partition_rows(brm_context_t* ctx, const int64_t* nprod_off, int64_t rows, int p,
+                                int64_t* bounds) {
+  if (!ctx) return BRM_ERR_INVALID;
+  if (p < 1 || rows < 0 || !nprod_off || !bounds) return fail(ctx, BRM_ERR_INVALID, "bad partition arguments");
+  DeviceGuard g(ctx->device);
+  CK(launch_partition(nprod_off, rows, p, bounds, ctx->stream), "k_partition");
+  return BRM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,526 @@
+// kernels.cu -- every device kernel of libbrmerge (sm_100a).
+//
+//   k_nprod_scan     Step 1 of Fig. 4a/4b: n_prod per row
+//                    (§II.B.2) fused with a single-pass decoupled look-back
+//                    exclusive scan (CUB-free), the per-bin histogram and max.
+//   k_bin_scatter    row binning by n_prod / list count into tiers.
+//   k_tier<...>      BRMerge of one row per thread group, ping-pong buffers in
+//                    shared memory (tiers 1-5: sub-warp, warp, block x3).
+//   k_global_tier    BRMerge of the heaviest rows, ping-pong buffers in a
+//                    global-memory workspace, one CTA per row.
+//   k_scan_i64       exclusive scan (row_size -> rpt; generic).
+//   k_compact        Step 6 of Fig. 4a: C_bar -> C copy (BRMerge-Upper).
+//   k_partition      §III.D row partition by balanced n_prod (multi-GPU).
+#include <cstdio>
+
+#include "engine.cuh"
+#include "kernels.cuh"
+
+namespace brm {
+
+// ---------------------------------------------------------------------------
+// Single-pass exclusive scan with decoupled look-back (Merrill & Garland
+// style, hand-written). Tile status words pack a 2-bit flag over a 62-bit sum.
+// ---------------------------------------------------------------------------
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPre = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Called by all threads of warp 0 of the tile's CTA; returns the exclusive
+// prefix of this tile and publishes its inclusive prefix.
+__device__ int64_t lookback(unsigned long long* status, int tile, int64_t aggregate) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_status(status, kFlagPre | (unsigned long long)aggregate);
+    return 0;
+  }
+  if (lane == 0) st_status(status + tile, kFlagAgg | (unsigned long long)aggregate);
+  int64_t excl = 0;
+  int t = tile - 1;
+  while (true) {
+    const int idx = t - lane;
+    unsigned long long w = kFlagPre;  // virtual prefix 0 before tile 0
+    if (idx >= 0) {
+      do {
+        w = ld_status(status + idx);
+      } while ((w >> 62) == 0);
+    }
+    const unsigned pmask = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+    int64_t v = (int64_t)(w & kValMask);
+    if (pmask) {
+      const int first = __ffs(pmask) - 1;  // closest tile with a full prefix
+      if (lane > first) v = 0;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    excl += v;
+    if (pmask) break;
+    t -= 32;
+  }
+  if (lane == 0) st_status(status + tile, kFlagPre | (unsigned long long)(excl + aggregate));
+  return excl;
+}
+
+constexpr int kScanThreads = 256;
+constexpr int kScanIPT = 8;
+constexpr int kScanTile = kScanThreads * kScanIPT;
+
+// Block-wide exclusive scan of int64 thread sums; returns this thread's
+// exclusive offset and the block total.
+__device__ __forceinline__ int64_t block_scan_i64(int64_t x, int64_t& total, int64_t* wsum) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t inc = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    constexpr int NW = kScanThreads / 32;
+    const int64_t w = lane < NW ? wsum[lane] : 0;
+    int64_t wx = w;
+#pragma unroll
+    for (int d = 1; d < NW; d <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, wx, d);
+      if (lane >= d) wx += y;
+    }
+    if (lane < NW) wsum[lane] = wx - w;
+    if (lane == NW - 1) wsum[NW] = wx;
+  }
+  __syncthreads();
+  total = wsum[kScanThreads / 32];
+  return wsum[wid] + inc - x;
+}
+
+// Step 1: n_prod per row + exclusive scan + bin histogram + max.
+__global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const int64_t* __restrict__ brpt,
+                                                             int64_t M, int64_t* __restrict__ nprod_off,
+                                                             unsigned long long* status,
+                                                             unsigned int* tile_counter,
+                                                             DevSummary* summary) {
+  __shared__ int s_tile;
+  __shared__ int64_t s_wsum[kScanThreads / 32 + 1];
+  __shared__ int64_t s_prefix;
+  __shared__ unsigned long long s_bin_rows[BRM_NUM_BINS];
+  __shared__ unsigned long long s_bin_nprod[BRM_NUM_BINS];
+  __shared__ unsigned long long s_max, s_maxnl;
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_counter, 1u);
+  if (threadIdx.x < BRM_NUM_BINS) {
+    s_bin_rows[threadIdx.x] = 0;
+    s_bin_nprod[threadIdx.x] = 0;
+  }
+  if (threadIdx.x == 0) { s_max = 0; s_maxnl = 0; }
+  __syncthreads();
+  const int tile = s_tile;
+  const TierBounds tb = tier_bounds();
+  const int64_t r0 = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanIPT;
+  int64_t v[kScanIPT];
+  int64_t tsum = 0, tmax = 0, tmaxnl = 0;
+#pragma unroll
+  for (int t = 0; t < kScanIPT; ++t) {
+    const int64_t r = r0 + t;
+    int64_t s = 0;
+    if (r < M) {
+      const int64_t p0 = A.rpt[r], p1 = A.rpt[r + 1];
+      for (int64_t p = p0; p < p1; ++p) {
+        const int k = A.col[p];
+        s += brpt[k + 1] - brpt[k];
+      }
+      const int bin = tier_of(s, p1 - p0, tb);
+      atomicAdd(&s_bin_rows[bin], 1ull);
+      atomicAdd(&s_bin_nprod[bin], (unsigned long long)s);
+      tmax = s > tmax ? s : tmax;
+      tmaxnl = (p1 - p0) > tmaxnl ? (p1 - p0) : tmaxnl;
+    }
+    v[t] = s;
+    tsum += s;
+  }
+  int64_t total;
+  const int64_t texcl = block_scan_i64(tsum, total, s_wsum);
+  if (threadIdx.x < 32) {
+    const int64_t pre = lookback(status, tile, total);
+    if (threadIdx.x == 0) s_prefix = pre;
+  }
+  atomicMax(&s_max, (unsigned long long)tmax);
+  atomicMax(&s_maxnl, (unsigned long long)tmaxnl);
+  __syncthreads();
+  int64_t run = s_prefix + texcl;
+#pragma unroll
+  for (int t = 0; t < kScanIPT; ++t) {
+    const int64_t r = r0 + t;
+    if (r < M) nprod_off[r] = run;
+    run += v[t];
+    if (r == M - 1) {
+      nprod_off[M] = run;
+      summary->nprod_total = run;
+    }
+  }
+  if (threadIdx.x < BRM_NUM_BINS) {
+    if (s_bin_rows[threadIdx.x]) {
+      atomicAdd(&summary->bin_rows[threadIdx.x], s_bin_rows[threadIdx.x]);
+      atomicAdd(&summary->bin_nprod[threadIdx.x], s_bin_nprod[threadIdx.x]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    atomicMax(&summary->nprod_max, s_max);
+    atomicMax(&summary->nl_max, s_maxnl);
+  }
+}
+
+// Generic exclusive scan: out[i] = sum_{r<i} in[r], out[n] = total.
+__global__ void __launch_bounds__(kScanThreads) k_scan_i64(const int64_t* __restrict__ in, int64_t n,
+                                                           int64_t* __restrict__ out,
+                                                           unsigned long long* status,
+                                                           unsigned int* tile_counter,
+                                                           int64_t* total_out) {
+  __shared__ int s_tile;
+  __shared__ int64_t s_wsum[kScanThreads / 32 + 1];
+  __shared__ int64_t s_prefix;
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t r0 = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanIPT;
+  int64_t v[kScanIPT];
+  int64_t tsum = 0;
+#pragma unroll
+  for (int t = 0; t < kScanIPT; ++t) {
+    const int64_t r = r0 + t;
+    v[t] = r < n ? in[r] : 0;
+    tsum += v[t];
+  }
+  int64_t total;
+  const int64_t texcl = block_scan_i64(tsum, total, s_wsum);
+  if (threadIdx.x < 32) {
+    const int64_t pre = lookback(status, tile, total);
+    if (threadIdx.x == 0) s_prefix = pre;
+  }
+  __syncthreads();
+  int64_t run = s_prefix + texcl;
+#pragma unroll
+  for (int t = 0; t < kScanIPT; ++t) {
+    const int64_t r = r0 + t;
+    if (r < n) out[r] = run;
+    run += v[t];
+    if (r == n - 1) {
+      out[n] = run;
+      if (total_out) *total_out = run;
+    }
+  }
+}
+
+// Row binning: rows of bin b are written to bins[bin_start[b] + ...]; rows with
+// n_prod == 0 get row_size = 0 and are not stored. One global atomic per
+// (CTA, bin).
+constexpr int kBinThreads = 256;
+constexpr int kBinRowsPerCta = 2048;
+__global__ void __launch_bounds__(kBinThreads) k_bin_scatter(CsrView A, const int64_t* __restrict__ nprod_off,
+                                                             int64_t M, const DevSummary* summary,
+                                                             unsigned long long* bin_cursor,
+                                                             int32_t* __restrict__ bins,
+                                                             int64_t* __restrict__ row_size) {
+  __shared__ unsigned int s_cnt[BRM_NUM_BINS];
+  __shared__ unsigned long long s_base[BRM_NUM_BINS];
+  __shared__ long long s_start[BRM_NUM_BINS];
+  if (threadIdx.x < BRM_NUM_BINS) s_cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    long long acc = 0;
+    for (int b = 0; b < BRM_NUM_BINS; ++b) {
+      s_start[b] = acc;
+      if (b != kBinEmpty) acc += (long long)summary->bin_rows[b];
+    }
+  }
+  __syncthreads();
+  const TierBounds tb = tier_bounds();
+  constexpr int IPT = kBinRowsPerCta / kBinThreads;
+  int bin[IPT];
+  unsigned int rank[IPT];
+  const int64_t base = (int64_t)blockIdx.x * kBinRowsPerCta;
+#pragma unroll
+  for (int t = 0; t < IPT; ++t) {
+    const int64_t r = base + (int64_t)t * kBinThreads + threadIdx.x;
+    bin[t] = -1;
+    if (r < M) {
+      const int64_t s = nprod_off[r + 1] - nprod_off[r];
+      const int b = tier_of(s, A.rpt[r + 1] - A.rpt[r], tb);
+      if (b == kBinEmpty) {
+        row_size[r] = 0;
+      } else {
+        bin[t] = b;
+        // warp-aggregated rank within the CTA
+        const unsigned peers = __match_any_sync(__activemask(), b);
+        const int leader = __ffs(peers) - 1;
+        const int lane = threadIdx.x & 31;
+        unsigned int off = 0;
+        if (lane == leader) off = atomicAdd(&s_cnt[b], (unsigned)__popc(peers));
+        off = __shfl_sync(peers, off, leader);
+        rank[t] = off + __popc(peers & ((1u << lane) - 1u));
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < BRM_NUM_BINS && s_cnt[threadIdx.x])
+    s_base[threadIdx.x] = atomicAdd(&bin_cursor[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < IPT; ++t) {
+    const int64_t r = base + (int64_t)t * kBinThreads + threadIdx.x;
+    if (bin[t] >= 0) bins[s_start[bin[t]] + s_base[bin[t]] + rank[t]] = (int32_t)r;
+  }
+}
+
+// (n_prod, num_list) of the global-tier rows, for host-side batching.
+__global__ void k_heavy_info(CsrView A, const int64_t* __restrict__ nprod_off,
+                             const int32_t* __restrict__ rows, int64_t n, int64_t* __restrict__ info) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) {
+    const int64_t r = rows[t];
+    info[2 * t] = nprod_off[r + 1] - nprod_off[r];
+    info[2 * t + 1] = A.rpt[r + 1] - A.rpt[r];
+  }
+}
+
+// Shared-memory tiers.
+template <int G, int VT, int CAP, int LCAP, int GPC, bool VALS, int OUT>
+__global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const int32_t* __restrict__ rows,
+                                                 int64_t nrows, RowOut o) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr GroupLayout L = group_layout<G, CAP, LCAP, VALS>();
+  const Group<G> g = make_group<G>();
+  unsigned char* base = smem + (threadIdx.x / G) * L.bytes;
+  int* colA = reinterpret_cast<int*>(base + L.colA);
+  int* colB = reinterpret_cast<int*>(base + L.colB);
+  double* valA = VALS ? reinterpret_cast<double*>(base + L.valA) : nullptr;
+  double* valB = VALS ? reinterpret_cast<double*>(base + L.valB) : nullptr;
+  double* scale = VALS ? reinterpret_cast<double*>(base + L.scale) : nullptr;
+  int64_t* bstart = reinterpret_cast<int64_t*>(base + L.bstart);
+  int* offA = reinterpret_cast<int*>(base + L.offA);
+  int* offB = reinterpret_cast<int*>(base + L.offB);
+  int* scan_tmp = reinterpret_cast<int*>(base + L.scan);
+  for (int64_t r = (int64_t)blockIdx.x * GPC + threadIdx.x / G; r < nrows; r += (int64_t)gridDim.x * GPC) {
+    process_row<G, VT, VALS, OUT>(g, A, B, rows[r], o, colA, colB, valA, valB, offA, offB, bstart,
+                                  scale, scan_tmp);
+  }
+}
+
+// Global tier: one CTA per row, ping-pong buffers in a per-row slice of a
+// global workspace at byte offset ws_off[r] (host-batched).
+template <bool VALS, int OUT>
+__global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, const int32_t* __restrict__ rows,
+                                                         const int64_t* __restrict__ ws_off,
+                                                         unsigned char* __restrict__ ws, RowOut o) {
+  __shared__ int scan_tmp[kGlobalG / 32 + 1];
+  const Group<kGlobalG> g = make_group<kGlobalG>();
+  const int64_t row = rows[blockIdx.x];
+  const int64_t P = ws_off[2 * blockIdx.x + 1];  // n_prod of the row
+  const int nl = (int)(A.rpt[row + 1] - A.rpt[row]);
+  unsigned char* p = ws + ws_off[2 * blockIdx.x];
+  auto take = [&](int64_t bytes) {
+    unsigned char* q = p;
+    p += (bytes + 15) & ~15ll;
+    return q;
+  };
+  double* valA = VALS ? reinterpret_cast<double*>(take(P * 8)) : nullptr;
+  double* valB = VALS ? reinterpret_cast<double*>(take(P * 8)) : nullptr;
+  double* scale = VALS ? reinterpret_cast<double*>(take((int64_t)nl * 8)) : nullptr;
+  int64_t* bstart = reinterpret_cast<int64_t*>(take((int64_t)nl * 8));
+  int* colA = reinterpret_cast<int*>(take(P * 4));
+  int* colB = reinterpret_cast<int*>(take(P * 4));
+  int* offA = reinterpret_cast<int*>(take((int64_t)(nl + 1) * 4));
+  int* offB = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
+  process_row<kGlobalG, kGlobalVT, VALS, OUT>(g, A, B, row, o, colA, colB, valA, valB, offA, offB,
+                                              bstart, scale, scan_tmp);
+}
+
+// Step 6 of Fig. 4a: copy each row of C_bar (at its n_prod offset) to C.
+__global__ void __launch_bounds__(256) k_compact(int64_t M, const int64_t* __restrict__ nprod_off,
+                                                 const int64_t* __restrict__ crpt,
+                                                 const int32_t* __restrict__ cbar_col,
+                                                 const double* __restrict__ cbar_val,
+                                                 int32_t* __restrict__ ccol, double* __restrict__ cval) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < M; r += nwarps) {
+    const int64_t s = nprod_off[r], d = crpt[r], n = crpt[r + 1] - d;
+    for (int64_t e = lane; e < n; e += 32) {
+      ccol[d + e] = cbar_col[s + e];
+      cval[d + e] = cbar_val[s + e];
+    }
+  }
+}
+
+// §III.D: bounds[g] = first row r with nprod_off[r] * p >= g * total.
+__global__ void k_partition(const int64_t* __restrict__ nprod_off, int64_t M, int p,
+                            int64_t* __restrict__ bounds) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g > p) return;
+  if (g == 0) { bounds[0] = 0; return; }
+  if (g == p) { bounds[p] = M; return; }
+  const __int128 target = (__int128)g * nprod_off[M];
+  int64_t lo = 0, hi = M;  // answer in [0, M]
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((__int128)nprod_off[mid] * p >= target)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  bounds[g] = lo;
+}
+
+// n_prod per row only (stage entry point).
+__global__ void k_row_nprod(CsrView A, const int64_t* __restrict__ brpt, int64_t M,
+                            int64_t* __restrict__ nprod) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= M) return;
+  int64_t s = 0;
+  for (int64_t p = A.rpt[r]; p < A.rpt[r + 1]; ++p) {
+    const int k = A.col[p];
+    s += brpt[k + 1] - brpt[k];
+  }
+  nprod[r] = s;
+}
+
+// ---------------------------------------------------------------------------
+// Host-side launchers.
+// ---------------------------------------------------------------------------
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+int64_t scan_tiles(int64_t n) { return (n + kScanTile - 1) / kScanTile; }
+
+cudaError_t launch_nprod_scan(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod_off,
+                              unsigned long long* status, unsigned int* counter, DevSummary* summary,
+                              cudaStream_t st) {
+  const int64_t tiles = scan_tiles(M);
+  if (tiles > 0) k_nprod_scan<<<(unsigned)tiles, kScanThreads, 0, st>>>(A, brpt, M, nprod_off, status, counter, summary);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan_i64(const int64_t* in, int64_t n, int64_t* out, unsigned long long* status,
+                            unsigned int* counter, int64_t* total_out, cudaStream_t st) {
+  const int64_t tiles = scan_tiles(n);
+  if (tiles > 0) k_scan_i64<<<(unsigned)tiles, kScanThreads, 0, st>>>(in, n, out, status, counter, total_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bin_scatter(const CsrView& A, const int64_t* nprod_off, int64_t M, const DevSummary* summary,
+                               unsigned long long* cursor, int32_t* bins, int64_t* row_size, cudaStream_t st) {
+  const int64_t blocks = (M + kBinRowsPerCta - 1) / kBinRowsPerCta;
+  if (blocks > 0) k_bin_scatter<<<(unsigned)blocks, kBinThreads, 0, st>>>(A, nprod_off, M, summary, cursor, bins, row_size);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_heavy_info(const CsrView& A, const int64_t* nprod_off, const int32_t* rows, int64_t n,
+                              int64_t* info, cudaStream_t st) {
+  if (n > 0) k_heavy_info<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A, nprod_off, rows, n, info);
+  return cudaGetLastError();
+}
+
+template <int G, int VT, int CAP, int LCAP, int GPC, bool VALS, int OUT>
+static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
+                                 const RowOut& o, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  constexpr GroupLayout L = group_layout<G, CAP, LCAP, VALS>();
+  constexpr int smem = L.bytes * GPC;
+  static_assert(smem <= 232448, "tier shared memory exceeds 227 KB");
+  auto kern = k_tier<G, VT, CAP, LCAP, GPC, VALS, OUT>;
+  // one process drives one device, so per-instantiation caching is safe
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G * GPC, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t want = (n + GPC - 1) / GPC;
+  const int64_t cap = (int64_t)per_sm * num_sms();
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
+  kern<<<grid, G * GPC, smem, st>>>(A, B, rows, n, o);
+  return cudaGetLastError();
+}
+
+template <bool VALS, int OUT>
+static cudaError_t launch_tier_dispatch(int bin, const CsrView& A, const CsrView& B, const int32_t* rows,
+                                        int64_t n, const RowOut& o, cudaStream_t st) {
+  switch (bin) {
+    case 1: return launch_tier_t<BRM_TIER1, VALS, OUT>(A, B, rows, n, o, st);
+    case 2: return launch_tier_t<BRM_TIER2, VALS, OUT>(A, B, rows, n, o, st);
+    case 3: return launch_tier_t<BRM_TIER3, VALS, OUT>(A, B, rows, n, o, st);
+    case 4: return launch_tier_t<BRM_TIER4, VALS, OUT>(A, B, rows, n, o, st);
+    case 5: return launch_tier_t<BRM_TIER5, VALS, OUT>(A, B, rows, n, o, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows,
+                        int64_t n, const RowOut& o, cudaStream_t st) {
+  switch (out_kind) {
+    case OUT_SYMBOLIC: return launch_tier_dispatch<false, OUT_SYMBOLIC>(bin, A, B, rows, n, o, st);
+    case OUT_CBAR: return launch_tier_dispatch<true, OUT_CBAR>(bin, A, B, rows, n, o, st);
+    case OUT_C: return launch_tier_dispatch<true, OUT_C>(bin, A, B, rows, n, o, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int64_t global_row_bytes(int64_t nprod, int64_t nl, bool vals) {
+  auto a = [](int64_t b) { return (b + 15) & ~15ll; };
+  int64_t s = a(nl * 8) + a(nprod * 4) * 2 + a((nl + 1) * 4) + a((nl / 2 + 2) * 4);
+  if (vals) s += a(nprod * 8) * 2 + a(nl * 8);
+  return s;
+}
+
+cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows,
+                               int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o,
+                               cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  switch (out_kind) {
+    case OUT_SYMBOLIC: k_global_tier<false, OUT_SYMBOLIC><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, rows, ws_off, ws, o); break;
+    case OUT_CBAR: k_global_tier<true, OUT_CBAR><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, rows, ws_off, ws, o); break;
+    case OUT_C: k_global_tier<true, OUT_C><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, rows, ws_off, ws, o); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact(int64_t M, const int64_t* nprod_off, const int64_t* crpt, const int32_t* cbar_col,
+                           const double* cbar_val, int32_t* ccol, double* cval, cudaStream_t st) {
+  if (M <= 0) return cudaSuccess;
+  int64_t blocks = (M * 32 + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  k_compact<<<(unsigned)blocks, 256, 0, st>>>(M, nprod_off, crpt, cbar_col, cbar_val, ccol, cval);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_partition(const int64_t* nprod_off, int64_t M, int p, int64_t* bounds, cudaStream_t st) {
+  k_partition<<<(p + 1 + 127) / 128, 128, 0, st>>>(nprod_off, M, p, bounds);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod, cudaStream_t st) {
+  if (M > 0) k_row_nprod<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(A, brpt, M, nprod);
+  return cudaGetLastError();
+}
+
+}  // namespace brm

@@ -1,0 +1,233 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bar (BASELINE.json north_star): rpt and col bit-exact (structural zeros from
+cancellation kept); fp64 values within |c - c_ref| <= 1e-12 * sum|a_ik b_kj|
+per entry. Additionally the values must be bit-identical to Algorithm 1's
+tree order (oracle.spgemm_brmerge), which the kernels follow exactly.
+"""
+import numpy as np
+import pytest
+
+from inputs import Csr, identity, random_sparse, uniform_random
+from parity import compare
+
+pytestmark = pytest.mark.gpu
+
+MODES = ["upper", "precise"]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    from paper_2206_06611_b200 import Context
+    assert torch.cuda.is_available()
+    c = Context()
+    yield c
+    c.close()
+
+
+def run(ctx, A: Csr, B: Csr, mode: str):
+    from paper_2206_06611_b200 import TorchCsr
+    C = ctx.spgemm(TorchCsr.from_csr(A), TorchCsr.from_csr(B), mode)
+    return C.to_numpy()
+
+
+def _lists_matrix(row_specs, list_len, ncols, seed, empty_rows_of_b=0):
+    """A has one row per (num_lists) in row_specs, pointing at distinct rows of
+    B; B rows have `list_len` entries (plus `empty_rows_of_b` empty rows)."""
+    rng = np.random.default_rng(seed)
+    kb = max(max(row_specs) if row_specs else 1, 1) + empty_rows_of_b
+    Bfull = uniform_random(kb - empty_rows_of_b, ncols, list_len, seed=seed) if kb > empty_rows_of_b else None
+    # interleave empty rows into B
+    lens = np.full(kb, list_len, np.int64)
+    empty = rng.choice(kb, size=empty_rows_of_b, replace=False) if empty_rows_of_b else np.zeros(0, np.int64)
+    lens[empty] = 0
+    rpt = np.zeros(kb + 1, np.int64)
+    np.cumsum(lens, out=rpt[1:])
+    B = Csr(kb, ncols, rpt, Bfull.col[:rpt[-1]].copy(), Bfull.val[:rpt[-1]].copy())
+    arpt = [0]
+    acol, aval = [], []
+    for nl in row_specs:
+        cols = np.sort(rng.choice(kb, size=nl, replace=False))
+        acol.append(cols)
+        aval.append(rng.uniform(-1, 1, size=nl))
+        arpt.append(arpt[-1] + nl)
+    A = Csr(len(row_specs), kb, np.array(arpt, np.int64),
+            np.concatenate(acol).astype(np.int32) if acol else np.zeros(0, np.int32),
+            np.concatenate(aval) if aval else np.zeros(0))
+    return A, B
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_config0_full(ctx, oracle_mod, mode):
+    """configs[0]: 2000x2000, 8 per row, seed 1, every row vs the oracle."""
+    A = uniform_random(2000, 2000, 8, seed=1)
+    compare(run(ctx, A, A, mode), A, A)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("seed", range(6))
+def test_random_rectangular(ctx, oracle_mod, mode, seed):
+    rng = np.random.default_rng(seed)
+    m, k, n = (int(x) for x in rng.integers(1, 300, size=3))
+    A = random_sparse(m, k, float(rng.uniform(0.005, 0.3)), seed=seed)
+    B = random_sparse(k, n, float(rng.uniform(0.005, 0.3)), seed=seed + 99)
+    compare(run(ctx, A, B, mode), A, B)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("list_len,specs", [
+    (1, [1, 2, 3, 5, 8, 31, 32, 33]),           # tier 1, tiny lists
+    (7, [1, 2, 9, 10]),                          # tier 1 edges (n_prod 63..70)
+    (16, [4, 15, 16, 17]),                       # tier 2 edges (256)
+    (27, [27, 30, 37, 38]),                      # tier 3 (729, 1024 edge)
+    (33, [100, 124, 125]),                       # tier 4 (4096 edge)
+    (64, [100, 127, 128, 129]),                  # tier 5 (8192 edge)
+    (100, [90, 300]),                            # global tier
+    (3, [40, 129, 300, 600, 1500]),              # many short lists (list caps)
+])
+def test_tier_boundaries(ctx, oracle_mod, mode, list_len, specs):
+    A, B = _lists_matrix(specs, list_len, 5000, seed=list_len)
+    compare(run(ctx, A, B, mode), A, B)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_many_empty_lists(ctx, oracle_mod, mode):
+    """Rows with many empty B rows among their lists: tree shape must keep them."""
+    A, B = _lists_matrix([5, 50, 700, 1100, 2000], 4, 3000, seed=3, empty_rows_of_b=1500)
+    compare(run(ctx, A, B, mode), A, B)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_heavy_rows_global_tier(ctx, oracle_mod, mode):
+    """Rows far beyond the shared-memory tiers (n_prod up to ~200k)."""
+    A, B = _lists_matrix([200, 1000, 2000, 20], 100, 20000, seed=11)
+    compare(run(ctx, A, B, mode), A, B)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_edge_cases(ctx, oracle_mod, mode):
+    # empty matrix
+    E = Csr(0, 5, np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    B5 = uniform_random(5, 7, 2, seed=1)
+    rpt, col, val = run(ctx, E, B5, mode)
+    assert rpt.tolist() == [0] and col.size == 0
+    # no nonzeros at all
+    Z = Csr(4, 4, np.zeros(5, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    rpt, col, val = run(ctx, Z, Z, mode)
+    assert rpt.tolist() == [0] * 5
+    # A's lists all hit empty B rows (n_prod = 0 with num_list > 0)
+    A = Csr(2, 3, np.array([0, 2, 3], np.int64), np.array([0, 2, 1], np.int32), np.ones(3))
+    Bz = Csr(3, 4, np.array([0, 0, 2, 2], np.int64), np.array([1, 3], np.int32), np.array([2.0, 3.0]))
+    compare(run(ctx, A, Bz, mode), A, Bz)
+    # cancellation: C = [[0]] is stored
+    A1 = Csr(1, 2, np.array([0, 2], np.int64), np.array([0, 1], np.int32), np.array([1.0, 1.0]))
+    B1 = Csr(2, 1, np.array([0, 1, 2], np.int64), np.array([0, 0], np.int32), np.array([1.0, -1.0]))
+    rpt, col, val = run(ctx, A1, B1, mode)
+    assert rpt.tolist() == [0, 1] and col.tolist() == [0] and val.tolist() == [0.0]
+    # identity both sides, exact
+    X = uniform_random(3000, 3000, 5, seed=2)
+    I = identity(3000)
+    for L, R in ((X, I), (I, X)):
+        rpt, col, val = run(ctx, L, R, mode)
+        np.testing.assert_array_equal(rpt, X.rpt)
+        np.testing.assert_array_equal(col, X.col)
+        np.testing.assert_array_equal(val, X.val)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_integer_values_exact(ctx, oracle_mod, mode):
+    A = random_sparse(400, 300, 0.05, seed=5, integer_values=True)
+    B = random_sparse(300, 500, 0.05, seed=6, integer_values=True)
+    rpt, col, val = run(ctx, A, B, mode)
+    np.testing.assert_array_equal(_dense(rpt, col, val, 400, 500), A.to_dense() @ B.to_dense())
+    compare((rpt, col, val), A, B)
+
+
+def _dense(rpt, col, val, m, n):
+    d = np.zeros((m, n))
+    r = np.repeat(np.arange(m), np.diff(rpt))
+    d[r, col] = val
+    return d
+
+
+def test_repeatable_and_modes_agree(ctx):
+    A = uniform_random(5000, 5000, 12, seed=4)
+    r1 = run(ctx, A, A, "upper")
+    r2 = run(ctx, A, A, "precise")
+    r3 = run(ctx, A, A, "precise")
+    for x, y in ((r1, r2), (r2, r3)):
+        for a, b in zip(x, y):
+            np.testing.assert_array_equal(a, b)
+
+
+def test_onecall_and_host_forms(ctx, oracle_mod):
+    import torch
+    from paper_2206_06611_b200 import TorchCsr
+    A = uniform_random(3000, 3000, 9, seed=7)
+    c = ctx.brmerge_spgemm(TorchCsr.from_csr(A), TorchCsr.from_csr(A), "precise")
+    torch.cuda.synchronize()
+    n = c.nnz
+    import ctypes
+    host = []
+    for ptr, cnt, dt, ct in ((c.rpt, c.rows + 1, torch.int64, 8), (c.col, n, torch.int32, 4),
+                             (c.val, n, torch.float64, 8)):
+        buf = torch.empty(cnt, dtype=dt)
+        torch.cuda.synchronize()
+        rc = torch.cuda.cudart().cudaMemcpy(buf.data_ptr(), ptr, cnt * ct, 2)  # D2H
+        assert rc == 0 or str(rc).endswith("cudaSuccess")
+        host.append(buf.numpy())
+    ctx.brm_csr_free(c)
+    compare(tuple(host), A, A)
+    Ah = TorchCsr.from_csr(A, pin=True)
+    rows, cols, rpt, col, val = ctx.brmerge_spgemm_host(Ah, Ah, "upper")
+    assert (rows, cols) == (3000, 3000)
+    compare((rpt.copy(), col.copy(), val.copy()), A, A)
+
+
+def test_stage_nprod_scan_partition(ctx, oracle_mod):
+    import torch
+    from paper_2206_06611_b200 import TorchCsr
+    A = random_sparse(3000, 2000, 0.01, seed=8)
+    B = random_sparse(2000, 1000, 0.02, seed=9)
+    nprod = ctx.brm_row_nprod(TorchCsr.from_csr(A), TorchCsr.from_csr(B)).cpu().numpy()
+    np.testing.assert_array_equal(nprod, oracle_mod.row_nprod(A, B))
+    rng = np.random.default_rng(0)
+    for n in (0, 1, 2047, 2048, 2049, 100_000, 3_000_001):
+        x = rng.integers(0, 1 << 40, size=n, dtype=np.int64)
+        out = ctx.brm_exclusive_scan_i64(torch.from_numpy(x).cuda()).cpu().numpy()
+        ref = np.zeros(n + 1, np.int64)
+        np.cumsum(x, out=ref[1:])
+        np.testing.assert_array_equal(out, ref)
+    off = ctx.brm_exclusive_scan_i64(torch.from_numpy(nprod).cuda())
+    for p in (1, 2, 3, 4, 8, 64):
+        got = ctx.brm_partition_rows(off, p).cpu().tolist()
+        assert got == oracle_mod.balance_by_nprod(nprod, p), p
+
+
+def test_errors_are_reported(ctx):
+    from paper_2206_06611_b200 import BrmError, TorchCsr
+    A = uniform_random(10, 8, 2, seed=1)
+    B = uniform_random(9, 8, 2, seed=1)
+    with pytest.raises(BrmError) as e:
+        ctx.spgemm(TorchCsr.from_csr(A), TorchCsr.from_csr(B), "precise")
+    assert e.value.code == 2  # BRM_ERR_DIM
+    import torch
+    from paper_2206_06611_b200 import Context
+    fresh = Context()
+    with pytest.raises(BrmError) as e:
+        fresh.brmerge_spgemm_fill(10, 8, torch.zeros(11, dtype=torch.int64, device="cuda"), 0)
+    assert e.value.code == 6  # BRM_ERR_STATE
+    fresh.close()
+
+
+def test_stats_reported(ctx):
+    from paper_2206_06611_b200 import TorchCsr
+    A = uniform_random(20000, 20000, 8, seed=3)
+    ctx.set_timing(True)
+    ctx.spgemm(TorchCsr.from_csr(A), TorchCsr.from_csr(A), "precise")
+    s = ctx.stats()
+    ctx.set_timing(False)
+    assert s["nprod_total"] == 20000 * 64 and s["nnz_c"] > 0
+    assert sum(s["bin_rows"]) == 20000
+    assert s["ms_numeric"] > 0
