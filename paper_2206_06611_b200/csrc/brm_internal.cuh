@@ -30,23 +30,23 @@ struct TierBounds {
   int lcap[BRM_NUM_BINS];
 };
 
-// (G threads per row group, VT merged positions per thread per tile,
+// (G threads per row group, VT merged positions per thread per chunk,
 //  CAP elements, LCAP lists, GPC groups per CTA)
-#define BRM_TIER1 8, 5, 64, 32, 16
-#define BRM_TIER2 32, 7, 256, 128, 4
-#define BRM_TIER3 128, 7, 1024, 256, 1
-#define BRM_TIER4 256, 9, 4096, 1024, 1
-#define BRM_TIER5 512, 9, 8192, 1024, 1
+#define BRM_TIER1 8, 8, 64, 32, 16
+#define BRM_TIER2 32, 16, 256, 128, 4
+#define BRM_TIER3 32, 16, 768, 128, 1
+#define BRM_TIER4 128, 16, 2560, 512, 1
+#define BRM_TIER5 256, 16, 8192, 1024, 1
 constexpr int kGlobalG = 512;
-constexpr int kGlobalVT = 9;
+constexpr int kGlobalVT = 16;
 
 __host__ __device__ inline TierBounds tier_bounds() {
   TierBounds t{};
   t.cap[0] = 0;    t.lcap[0] = 0;
   t.cap[1] = 64;   t.lcap[1] = 32;
   t.cap[2] = 256;  t.lcap[2] = 128;
-  t.cap[3] = 1024; t.lcap[3] = 256;
-  t.cap[4] = 4096; t.lcap[4] = 1024;
+  t.cap[3] = 768;  t.lcap[3] = 128;
+  t.cap[4] = 2560; t.lcap[4] = 512;
   t.cap[5] = 8192; t.lcap[5] = 1024;
   t.cap[6] = INT_MAX; t.lcap[6] = INT_MAX;
   return t;
@@ -62,7 +62,7 @@ __host__ __device__ inline int tier_of(int64_t nprod, int64_t nl, const TierBoun
 
 // Shared-memory layout of one row group (bytes, 16-aligned pieces).
 struct GroupLayout {
-  int valA, valB, scale, bstart, colA, colB, offA, offB, scan, bytes;
+  int valA, valB, scale, bstart, colA, colB, offA, offB, cst, scan, bytes;
 };
 
 __host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
@@ -79,6 +79,7 @@ __host__ __device__ constexpr GroupLayout group_layout() {
   L.colB = o;   o += align16(CAP * 4);
   L.offA = o;   o += align16((LCAP + 1) * 4);
   L.offB = o;   o += align16((LCAP / 2 + 2) * 4);
+  L.cst = o;    o += align16((LCAP / 2 + 2) * 4);
   L.scan = o;   o += G > 32 ? align16((G / 32 + 1) * 4) : 0;
   L.bytes = o;
   return L;

@@ -4,20 +4,18 @@
 //   multiplying phase (lines 10-15): the B rows selected by A_i* are gathered,
 //     coalesced, into the ping buffer as consecutive sorted lists; list
 //     offsets come from a group scan of the B row lengths. The scaling by
-//     A_ik is fused into the first merge round (one rounding, same value).
+//     A_ik is fused into the first merge round (same single rounding).
 //   accumulating phase (lines 21-35): ceil(log2 num_list) rounds; round r
 //     merges lists (0,1),(2,3),... of src into dst, an odd trailing list is
-//     copied, then src/dst swap. Every round is ONE segmented merge-path pass
-//     over the whole concatenated merged space of all pairs: thread t owns
-//     merged positions [t*VT, t*VT+VT) of each tile, finds its pair by binary
-//     search over the pair starts and its split by a merge-path search, and
-//     merges sequentially into registers, summing equal columns (Fig. 2). A
-//     duplicate whose two halves straddle a thread boundary is taken by the
-//     left thread (look-ahead) and skipped by the right one, so no cross-thread
-//     fix-up is needed. A group exclusive scan of the per-thread output counts
-//     gives every output its compacted dst position, which is exactly the
-//     sequential layout of Alg. 1 ("consume two lists and store to
-//     dst_buffer"), and the dst list offsets of the next round.
+//     copied, then src/dst swap. A round is cut into chunks of VT merged
+//     positions that never straddle a pair; one thread merges one chunk:
+//     binary search of its pair over the chunk table, merge-path split inside
+//     the pair, then VT branch-free merge steps into registers summing equal
+//     columns (Fig. 2). A duplicate whose halves straddle a chunk boundary is
+//     taken by the left chunk (look-ahead) and skipped by the right one. A
+//     group exclusive scan of per-thread output counts gives each output its
+//     compacted dst position -- exactly Alg. 1's sequential layout ("consume
+//     two lists and store to dst_buffer") -- and the next round's offsets.
 //
 // The same code runs with the buffers in shared memory (tiers 1-5) or in a
 // global-memory workspace (tier 6); the pointers decide.
@@ -35,43 +33,57 @@ struct RowOut {
   int64_t* row_size;    // OUT_SYMBOLIC / OUT_CBAR: nnz of each output row
 };
 
+// Chunk table of a round: cst[p] = first chunk of pair p, cst[npairs] = total.
+template <int G, int VT>
+__device__ __forceinline__ int build_chunks(const Group<G>& g, const int* so, int nl, int npairs, int* cst,
+                                            int* scan_tmp) {
+  int run = 0;
+  for (int pb = 0; pb < npairs; pb += G) {
+    const int p = pb + g.rank;
+    int c = 0;
+    if (p < npairs) {
+      const int len = so[min(2 * p + 2, nl)] - so[2 * p];
+      c = (len + VT - 1) / VT;
+    }
+    int tot;
+    const int ex = group_excl_scan<G>(g, c, tot, scan_tmp);
+    if (p < npairs) cst[p] = run + ex;
+    run += tot;
+  }
+  if (g.rank == 0) cst[npairs] = run;
+  g.sync();
+  return run;
+}
+
 // One merge round over `nl` >= 2 lists of src (offsets `so`, nl + 1 entries).
 // Writes ceil(nl/2) lists to dst with offsets `dof`. Returns total outputs.
 template <int G, int VT, bool FIRST, bool VALS>
 __device__ __forceinline__ int merge_round(const Group<G>& g, const int* sc, const double* sv,
                                            const int* so, int nl, int* dc, double* dv, int* dof,
-                                           const double* scale, int* scan_tmp) {
-  const int E = so[nl];
+                                           const double* scale, int* cst, int* scan_tmp) {
   const int npairs = (nl + 1) >> 1;
+  const int T = build_chunks<G, VT>(g, so, nl, npairs, cst, scan_tmp);
   int out_base = 0;
-  for (int tile = 0; tile < E; tile += G * VT) {
-    const int d0 = tile + g.rank * VT;
-    const int dend = min(d0 + VT, E);
+  for (int tb = 0; tb < T; tb += G) {
+    const int t = tb + g.rank;
     int cnt = 0;
     int ocol[VT];
     double oval[VT];
-    int pfirst = 0, plast = -1;  // pairs whose first output this thread emits
-    if (d0 < E) {
-      int p = upper_search<2>(so, npairs, d0);
-      int as = so[2 * p];
-      int ae = so[min(2 * p + 1, nl)];
-      int be = so[min(2 * p + 2, nl)];
-      int la = ae - as, lb = be - ae;
-      const int dd = d0 - as;
-      int i = merge_path(sc + as, la, sc + ae, lb, dd);
-      int j = dd - i;
-      int pos = d0;
-      if (dd == 0) {
-        // this thread starts pair p (and any empty pairs sharing its start)
-        int q = p;
-        while (q > 0 && so[2 * (q - 1)] == d0) --q;
-        for (int r = q; r <= p; ++r) dof[r] = 0;
-        pfirst = q;
-        plast = p;
-      } else if (i > 0 && j < lb && sc[as + i - 1] == sc[ae + j]) {
-        // b[j] duplicates a[i-1], already summed by the thread to the left
-        ++j;
-        ++pos;
+    int first_of_pair = -1;
+    if (t < T) {
+      const int p = upper_search<1>(cst, npairs, t);
+      const int k = t - cst[p];
+      const int as = so[2 * p];
+      const int ae = so[min(2 * p + 1, nl)];
+      const int be = so[min(2 * p + 2, nl)];
+      const int la = ae - as, lb = be - ae;
+      int d = k * VT;
+      const int dend = min(d + VT, la + lb);
+      int i = merge_path(sc + as, la, sc + ae, lb, d);
+      int j = d - i;
+      if (i > 0 && j < lb && sc[as + i - 1] == sc[ae + j]) {
+        ++j;  // b[j] duplicates a[i-1]: summed by the chunk to the left
+        ++d;
       }
       double sa = 1.0, sb = 1.0;
       if (FIRST && VALS) {
@@ -82,58 +94,30 @@ __device__ __forceinline__ int merge_round(const Group<G>& g, const int* sc, con
       int cb = j < lb ? sc[ae + j] : INT_MAX;
 #pragma unroll
       for (int v = 0; v < VT; ++v) {
-        if (pos < dend) {
-          if (ca == INT_MAX && cb == INT_MAX) {
-            // pair exhausted: the next non-empty pair starts exactly at pos
-            const int q0 = p + 1;
-            do {
-              ++p;
-              as = so[2 * p];
-              ae = so[min(2 * p + 1, nl)];
-              be = so[min(2 * p + 2, nl)];
-            } while (as == be);
-            for (int r = q0; r <= p; ++r) dof[r] = cnt;
-            if (plast < 0) pfirst = q0;
-            plast = p;
-            la = ae - as;
-            lb = be - ae;
-            i = 0;
-            j = 0;
-            if (FIRST && VALS) {
-              sa = scale[2 * p];
-              sb = (2 * p + 1 < nl) ? scale[2 * p + 1] : 0.0;
+        if (d < dend) {
+          const bool ta = ca <= cb;
+          const bool tbb = cb <= ca;
+          ocol[v] = ta ? ca : cb;
+          if (VALS) {
+            double x = 0.0, y = 0.0;
+            if (ta) x = sv[as + i];
+            if (tbb) y = sv[ae + j];
+            if (FIRST) {
+              x = __dmul_rn(sa, x);
+              y = __dmul_rn(sb, y);
             }
-            ca = la > 0 ? sc[as] : INT_MAX;
-            cb = lb > 0 ? sc[ae] : INT_MAX;
+            // "vals with duplicate cols are combined into one val"
+            oval[v] = (ta && tbb) ? __dadd_rn(x, y) : (ta ? x : y);
           }
-          if (ca < cb) {
-            ocol[v] = ca;
-            if (VALS) oval[v] = FIRST ? __dmul_rn(sa, sv[as + i]) : sv[as + i];
-            ++i;
-            ++pos;
-            ca = i < la ? sc[as + i] : INT_MAX;
-          } else if (cb < ca) {
-            ocol[v] = cb;
-            if (VALS) oval[v] = FIRST ? __dmul_rn(sb, sv[ae + j]) : sv[ae + j];
-            ++j;
-            ++pos;
-            cb = j < lb ? sc[ae + j] : INT_MAX;
-          } else {  // equal columns: "vals with duplicate cols are combined"
-            ocol[v] = ca;
-            if (VALS) {
-              const double x = FIRST ? __dmul_rn(sa, sv[as + i]) : sv[as + i];
-              const double y = FIRST ? __dmul_rn(sb, sv[ae + j]) : sv[ae + j];
-              oval[v] = __dadd_rn(x, y);
-            }
-            ++i;
-            ++j;
-            pos += 2;
-            ca = i < la ? sc[as + i] : INT_MAX;
-            cb = j < lb ? sc[ae + j] : INT_MAX;
-          }
+          i += ta;
+          j += tbb;
+          d += (int)ta + (int)tbb;
+          if (ta) ca = i < la ? sc[as + i] : INT_MAX;
+          if (tbb) cb = j < lb ? sc[ae + j] : INT_MAX;
           ++cnt;
         }
       }
+      if (k == 0) first_of_pair = p;
     }
     int total;
     const int excl = group_excl_scan<G>(g, cnt, total, scan_tmp);
@@ -145,13 +129,17 @@ __device__ __forceinline__ int merge_round(const Group<G>& g, const int* sc, con
         if (VALS) dv[base + v] = oval[v];
       }
     }
-    for (int r = pfirst; r <= plast; ++r) dof[r] += base;
+    if (first_of_pair >= 0) {  // this pair's (and preceding empty pairs') dst offset
+      int q = first_of_pair;
+      const int c0 = cst[q];
+      dof[q] = base;
+      while (q > 0 && cst[q - 1] == c0) dof[--q] = base;
+    }
     out_base += total;
   }
-  if (g.rank == 0) {
-    // trailing empty pairs (start == E) and the end sentinel
+  if (g.rank == 0) {  // trailing empty pairs and the end sentinel
     for (int q = npairs; q >= 0; --q) {
-      if (q < npairs && so[2 * q] != E) break;
+      if (q < npairs && cst[q] != T) break;
       dof[q] = out_base;
     }
   }
@@ -161,11 +149,11 @@ __device__ __forceinline__ int merge_round(const Group<G>& g, const int* sc, con
 
 // BRMerge of output row `row` by group g. Buffers: colA/colB (>= n_prod),
 // valA/valB (>= n_prod, VALS), offA (>= nl+1), offB (>= nl/2+2),
-// bstart (>= nl), scale (>= nl, VALS), scan_tmp (G/32+1 ints, shared).
+// cst (>= nl/2+2), bstart (>= nl), scale (>= nl, VALS), scan_tmp (G/32+1).
 template <int G, int VT, bool VALS, int OUT>
 __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A, const CsrView& B,
                                             int64_t row, const RowOut& o, int* colA, int* colB,
-                                            double* valA, double* valB, int* offA, int* offB,
+                                            double* valA, double* valB, int* offA, int* offB, int* cst,
                                             int64_t* bstart, double* scale, int* scan_tmp) {
   const int64_t a0 = A.rpt[row];
   const int nl = static_cast<int>(A.rpt[row + 1] - a0);
@@ -189,12 +177,47 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
   const int P = run;
   if (g.rank == 0) offA[nl] = P;
   g.sync();
-  // multiplying phase: gather the B rows (coalesced within each list)
-  for (int e = g.rank; e < P; e += G) {
-    const int l = upper_search<1>(offA, nl, e);
-    const int64_t src = bstart[l] + (e - offA[l]);
-    colA[e] = B.col[src];
-    if (VALS) valA[e] = B.val[src];
+  // multiplying phase: gather the B rows, list by list (coalesced within a
+  // list), U lists in flight per step for memory-level parallelism
+  {
+    constexpr int U = 4;
+    for (int l0 = 0; l0 < nl; l0 += U) {
+      int cv[U];
+      double vv[U];
+      int dst[U], n[U];
+      int64_t src[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int l = l0 + u;
+        n[u] = 0;
+        if (l < nl) {
+          dst[u] = offA[l];
+          n[u] = offA[l + 1] - dst[u];
+          src[u] = bstart[l];
+        }
+      }
+      bool more = true;
+      for (int e0 = 0; more; e0 += G) {
+        more = false;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + g.rank;
+          if (e < n[u]) {
+            cv[u] = B.col[src[u] + e];
+            if (VALS) vv[u] = B.val[src[u] + e];
+          }
+          more |= e0 + G < n[u];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + g.rank;
+          if (e < n[u]) {
+            colA[dst[u] + e] = cv[u];
+            if (VALS) valA[dst[u] + e] = vv[u];
+          }
+        }
+      }
+    }
   }
   g.sync();
   int* sc = colA;
@@ -206,13 +229,13 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
   int n_out = P;
   if (nl >= 2) {
     int cur = nl;
-    n_out = merge_round<G, VT, true, VALS>(g, sc, sv, so, cur, dc, dv, dof, scale, scan_tmp);
+    n_out = merge_round<G, VT, true, VALS>(g, sc, sv, so, cur, dc, dv, dof, scale, cst, scan_tmp);
     cur = (cur + 1) >> 1;
     { int* t = sc; sc = dc; dc = t; }
     { double* t = sv; sv = dv; dv = t; }
     { int* t = so; so = dof; dof = t; }
     while (cur > 1) {
-      n_out = merge_round<G, VT, false, VALS>(g, sc, sv, so, cur, dc, dv, dof, nullptr, scan_tmp);
+      n_out = merge_round<G, VT, false, VALS>(g, sc, sv, so, cur, dc, dv, dof, nullptr, cst, scan_tmp);
       cur = (cur + 1) >> 1;
       { int* t = sc; sc = dc; dc = t; }
       { double* t = sv; sv = dv; dv = t; }
