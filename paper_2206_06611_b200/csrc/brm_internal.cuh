@@ -33,12 +33,12 @@ struct TierBounds {
 // (G threads per row group, VT merged positions per thread per chunk,
 //  CAP elements, LCAP lists, GPC groups per CTA)
 #define BRM_TIER1 8, 8, 64, 32, 16
-#define BRM_TIER2 32, 16, 256, 128, 4
-#define BRM_TIER3 32, 16, 768, 128, 1
-#define BRM_TIER4 128, 16, 2560, 512, 1
-#define BRM_TIER5 256, 16, 8192, 1024, 1
+#define BRM_TIER2 32, 8, 256, 128, 4
+#define BRM_TIER3 32, 8, 768, 128, 1
+#define BRM_TIER4 128, 8, 2560, 512, 1
+#define BRM_TIER5 256, 8, 8192, 1024, 1
 constexpr int kGlobalG = 512;
-constexpr int kGlobalVT = 16;
+constexpr int kGlobalVT = 8;
 
 __host__ __device__ inline TierBounds tier_bounds() {
   TierBounds t{};

@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
   int* cst = reinterpret_cast<int*>(base + L.cst);
   int* scan_tmp = reinterpret_cast<int*>(base + L.scan);
   for (int64_t r = (int64_t)blockIdx.x * GPC + threadIdx.x / G; r < nrows; r += (int64_t)gridDim.x * GPC) {
-    process_row<G, VT, VALS, OUT>(g, A, B, rows[r], o, colA, colB, valA, valB, offA, offB, cst, bstart,
+    process_row<G, VT, VALS, OUT, true>(g, A, B, rows[r], o, colA, colB, valA, valB, offA, offB, cst, bstart,
                                   scale, scan_tmp);
   }
 }
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
   unsigned char* p = ws + ws_off[2 * blockIdx.x];
   auto take = [&](int64_t bytes) {
     unsigned char* q = p;
-    p += (bytes + 15) & ~15ll;
+    p += ((bytes + 15) & ~15ll) + 16;  // +16: merge reloads may touch one slot past a list
     return q;
   };
   double* valA = VALS ? reinterpret_cast<double*>(take(P * 8)) : nullptr;
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
   int* offA = reinterpret_cast<int*>(take((int64_t)(nl + 1) * 4));
   int* offB = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
   int* cst = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
-  process_row<kGlobalG, kGlobalVT, VALS, OUT>(g, A, B, row, o, colA, colB, valA, valB, offA, offB, cst,
+  process_row<kGlobalG, kGlobalVT, VALS, OUT, false>(g, A, B, row, o, colA, colB, valA, valB, offA, offB, cst,
                                               bstart, scale, scan_tmp);
 }
 
@@ -486,7 +486,7 @@ cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& 
 }
 
 int64_t global_row_bytes(int64_t nprod, int64_t nl, bool vals) {
-  auto a = [](int64_t b) { return (b + 15) & ~15ll; };
+  auto a = [](int64_t b) { return ((b + 15) & ~15ll) + 16; };
   int64_t s = a(nl * 8) + a(nprod * 4) * 2 + a((nl + 1) * 4) + a((nl / 2 + 2) * 4) * 2;
   if (vals) s += a(nprod * 8) * 2 + a(nl * 8);
   return s;
