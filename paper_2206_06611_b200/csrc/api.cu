@@ -39,7 +39,7 @@ struct brm_context {
   bool planned = false;
   brm_mode_t mode = BRM_PRECISE;
   CsrView A{}, B{};
-  int64_t M = 0, K = 0, N = 0, nnz_c = 0;
+  int64_t M = 0, K = 0, N = 0, nnz_c = 0, bnnz = 0;
   int64_t bin_start[BRM_NUM_BINS] = {};
   int64_t bin_rows[BRM_NUM_BINS] = {};
   DevSummary sum{};
@@ -187,7 +187,8 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
   for (int b = 1; b < kBinGlobal; ++b) {
     if (!ctx->bin_rows[b]) continue;
     if (per_bin) ev_record(ctx, kEvBin + 2 * b);
-    CK(launch_tier(b, out, ctx->A, ctx->B, bins + ctx->bin_start[b], ctx->bin_rows[b], o, ctx->stream),
+    CK(launch_tier(b, out, ctx->A, ctx->B, ctx->bnnz, static_cast<const int64_t*>(ctx->nprod_off.p),
+                   bins + ctx->bin_start[b], ctx->bin_rows[b], o, ctx->stream),
        "k_tier");
     ++ctx->launches;
     if (per_bin) ev_record(ctx, kEvBin + 2 * b + 1);
@@ -244,7 +245,7 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
   for (size_t c = 0; c + 1 < cuts.size(); ++c) {
     const int64_t b0 = cuts[c], n = cuts[c + 1] - b0;
     if (n <= 0) continue;
-    CK(launch_global_tier(out, ctx->A, ctx->B, hrows + b0, n,
+    CK(launch_global_tier(out, ctx->A, ctx->B, ctx->bnnz, hrows + b0, n,
                           static_cast<const int64_t*>(ctx->gws_off.p) + 2 * b0,
                           static_cast<unsigned char*>(ctx->gws.p), o, ctx->stream),
        "k_global_tier");
@@ -271,6 +272,7 @@ brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
   ctx->M = A->rows;
   ctx->K = A->cols;
   ctx->N = B->cols;
+  ctx->bnnz = B->nnz;
   const int64_t M = ctx->M;
   memset(&ctx->stats, 0, sizeof(ctx->stats));
   ctx->ev_mask = 0;

@@ -36,7 +36,7 @@ struct TierBounds {
 #define BRM_TIER2 32, 8, 256, 128, 4
 #define BRM_TIER3 32, 8, 768, 128, 1
 #define BRM_TIER4 128, 8, 2560, 512, 1
-#define BRM_TIER5 256, 8, 8192, 1024, 1
+#define BRM_TIER5 256, 8, 7168, 1024, 1
 constexpr int kGlobalG = 512;
 constexpr int kGlobalVT = 8;
 
@@ -47,7 +47,7 @@ __host__ __device__ inline TierBounds tier_bounds() {
   t.cap[2] = 256;  t.lcap[2] = 128;
   t.cap[3] = 768;  t.lcap[3] = 128;
   t.cap[4] = 2560; t.lcap[4] = 512;
-  t.cap[5] = 8192; t.lcap[5] = 1024;
+  t.cap[5] = 7168; t.lcap[5] = 1024;
   t.cap[6] = INT_MAX; t.lcap[6] = INT_MAX;
   return t;
 }
@@ -60,26 +60,32 @@ __host__ __device__ inline int tier_of(int64_t nprod, int64_t nl, const TierBoun
   return kBinGlobal;
 }
 
-// Shared-memory layout of one row group (bytes, 16-aligned pieces).
+// Shared-memory layout of one row group (bytes, 16-aligned pieces). colA /
+// valA hold the gathered lists in 16-byte TMA windows, so they get padding
+// (capc / capv elements); rows whose windows do not fit use cp.async.
 struct GroupLayout {
-  int valA, valB, scale, bstart, colA, colB, offA, offB, cst, scan, bytes;
+  int valA, valB, colA, colB, cb, vb, offA, offB, cst, cpair, mbar, scan, bytes, capc, capv;
 };
 
 __host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
 
-template <int G, int CAP, int LCAP, bool VALS>
+template <int G, int VT, int CAP, int LCAP, bool VALS>
 __host__ __device__ constexpr GroupLayout group_layout() {
   GroupLayout L{};
+  L.capc = CAP + CAP / 4;
+  L.capv = CAP + CAP / 8;
   int o = 0;
-  L.valA = o;   o += VALS ? align16(CAP * 8) : 0;
-  L.valB = o;   o += VALS ? align16(CAP * 8) : 0;
-  L.scale = o;  o += VALS ? align16(LCAP * 8) : 0;
-  L.bstart = o; o += align16(LCAP * 8);
-  L.colA = o;   o += align16(CAP * 4);
-  L.colB = o;   o += align16(CAP * 4);
+  L.valA = o;   o += VALS ? align16(L.capv * 8 + 16) : 0;
+  L.valB = o;   o += VALS ? align16(CAP * 8 + 16) : 0;
+  L.colA = o;   o += align16(L.capc * 4 + 16);
+  L.colB = o;   o += align16(CAP * 4 + 16);
+  L.cb = o;     o += align16(LCAP * 4);
+  L.vb = o;     o += VALS ? align16(LCAP * 4) : 0;
   L.offA = o;   o += align16((LCAP + 1) * 4);
   L.offB = o;   o += align16((LCAP / 2 + 2) * 4);
   L.cst = o;    o += align16((LCAP / 2 + 2) * 4);
+  L.cpair = o;  o += align16((CAP / VT + LCAP / 2 + 2) * 4);
+  L.mbar = o;   o += 16;
   L.scan = o;   o += G > 32 ? align16((G / 32 + 1) * 4) : 0;
   L.bytes = o;
   return L;

@@ -1,24 +1,29 @@
 // engine.cuh -- the BRMerge accumulation of one output row by a thread group
 // (Algorithm 1), parallelised for a GPU:
 //
-//   multiplying phase (lines 10-15): the B rows selected by A_i* are gathered,
-//     coalesced, into the ping buffer as consecutive sorted lists; list
-//     offsets come from a group scan of the B row lengths. The scaling by
-//     A_ik is fused into the first merge round (same single rounding).
+//   multiplying phase (lines 10-15): the B rows selected by A_i* are copied
+//     into the ping buffer as sorted intermediate lists. Shared-memory tiers
+//     stage each list with ONE TMA bulk copy per array (cp.async.bulk on the
+//     16-byte-aligned window around the B row, completion on an mbarrier);
+//     where alignment or capacity forbids it, per-element cp.async is used.
+//     The scaling by A_ik is fused into the first merge round (the product is
+//     rounded once, exactly as in Alg. 1 line 12).
 //   accumulating phase (lines 21-35): ceil(log2 num_list) rounds; round r
 //     merges lists (0,1),(2,3),... of src into dst, an odd trailing list is
 //     copied, then src/dst swap. A round is cut into chunks of VT merged
-//     positions that never straddle a pair; one thread merges one chunk:
-//     binary search of its pair over the chunk table, merge-path split inside
-//     the pair, then VT branch-free merge steps into registers summing equal
-//     columns (Fig. 2). A duplicate whose halves straddle a chunk boundary is
-//     taken by the left chunk (look-ahead) and skipped by the right one. A
-//     group exclusive scan of per-thread output counts gives each output its
-//     compacted dst position -- exactly Alg. 1's sequential layout ("consume
-//     two lists and store to dst_buffer") -- and the next round's offsets.
+//     positions that never straddle a pair (chunk -> pair table, no search);
+//     one thread merges one chunk: merge-path split inside the pair, then VT
+//     branch-free merge steps into registers summing equal columns (Fig. 2).
+//     A duplicate whose halves straddle a chunk boundary is taken by the left
+//     chunk (look-ahead) and skipped by the right one. Each thread runs two
+//     chunks interleaved (ILP). A group exclusive scan of the per-chunk output
+//     counts gives every output its compacted dst position -- exactly Alg. 1's
+//     sequential layout ("consume two lists and store to dst_buffer") -- and
+//     the next round's list offsets.
 //
 // The same code runs with the buffers in shared memory (tiers 1-5) or in a
-// global-memory workspace (tier 6); the pointers decide.
+// global-memory workspace (tier 6); the SMEM template flag and the pointers
+// decide.
 #pragma once
 #include "brm_internal.cuh"
 
@@ -33,10 +38,71 @@ struct RowOut {
   int64_t* row_size;    // OUT_SYMBOLIC / OUT_CBAR: nnz of each output row
 };
 
-// Chunk table of a round: cst[p] = first chunk of pair p, cst[npairs] = total.
+// Working arrays of one row group.
+struct RowBufs {
+  int* colA;
+  int* colB;
+  double* valA;
+  double* valB;
+  int* cb;     // round 1: start of list l's columns in colA
+  int* vb;     // round 1: start of list l's values in valA
+  int* offA;   // list offsets (virtual, contiguous), ping
+  int* offB;   // list offsets, pong
+  int* cst;    // chunk table: first chunk of each pair
+  int* cpair;  // chunk table: pair of each chunk
+  unsigned long long* mbar;
+  int* scan_tmp;
+  int capc, capv;  // capacities of colA / valA (TMA windows need padding)
+};
+
+// ---------------------------------------------------------------------------
+// async-copy primitives (sm_90+ PTX; SASS UBLKCP / LDGSTS / SYNCS)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async_4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(unsigned long long* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* m) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(m))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(m)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_bulk_g2s(void* smem, const void* gmem, unsigned bytes, unsigned long long* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Chunk table of a round: cst[p] = first chunk of pair p (cst[npairs] =
+// total), cpair[t] = pair of chunk t.
+// ---------------------------------------------------------------------------
 template <int G, int VT>
 __device__ __forceinline__ int build_chunks(const Group<G>& g, const int* so, int nl, int npairs, int* cst,
-                                            int* scan_tmp) {
+                                            int* cpair, int* scan_tmp) {
   int run = 0;
   for (int pb = 0; pb < npairs; pb += G) {
     const int p = pb + g.rank;
@@ -47,7 +113,10 @@ __device__ __forceinline__ int build_chunks(const Group<G>& g, const int* so, in
     }
     int tot;
     const int ex = group_excl_scan<G>(g, c, tot, scan_tmp);
-    if (p < npairs) cst[p] = run + ex;
+    if (p < npairs) {
+      cst[p] = run + ex;
+      for (int q = 0; q < c; ++q) cpair[run + ex + q] = p;
+    }
     run += tot;
   }
   if (g.rank == 0) cst[npairs] = run;
@@ -55,45 +124,60 @@ __device__ __forceinline__ int build_chunks(const Group<G>& g, const int* so, in
   return run;
 }
 
-// Merge state of one chunk: cursors i (list a) and j (list b) of pair p,
-// merged position d of the next element, chunk end dend.
+// Merge state of one chunk: list a at colA/valA index ac/av (length la),
+// list b at bc/bv (length lb); cursors i, j; merged position d; end dend.
 struct Chunk {
-  int as, ae, la, lb, i, j, d, dend, ca, cb, cnt, pair_first;
+  int ac, av, bc, bv, la, lb, i, j, d, dend, ca, cb, cnt, pair_first;
   double sa, sb;
 };
 
 template <int VT, bool FIRST, bool VALS>
 __device__ __forceinline__ void chunk_setup(Chunk& c, int t, int T, const int* sc, const int* so, int nl,
-                                            int npairs, const int* cst, const double* scale) {
+                                            const int* cst, const int* cpair, const int* cb, const int* vb,
+                                            const double* aval) {
   c.cnt = 0;
   c.pair_first = -1;
   c.d = 0;
   c.dend = 0;  // inactive
-  c.i = c.j = c.la = c.lb = c.as = c.ae = 0;
+  c.i = c.j = c.la = c.lb = c.ac = c.av = c.bc = c.bv = 0;
   c.ca = c.cb = INT_MAX;
   c.sa = c.sb = 1.0;
   if (t >= T) return;
-  const int p = upper_search<1>(cst, npairs, t);
+  const int p = cpair[t];
   const int k = t - cst[p];
-  c.as = so[2 * p];
-  c.ae = so[min(2 * p + 1, nl)];
-  const int be = so[min(2 * p + 2, nl)];
-  c.la = c.ae - c.as;
-  c.lb = be - c.ae;
+  const int s0 = so[2 * p];
+  const int s1 = so[min(2 * p + 1, nl)];
+  const int s2 = so[min(2 * p + 2, nl)];
+  c.la = s1 - s0;
+  c.lb = s2 - s1;
+  if (FIRST) {
+    c.ac = cb[2 * p];
+    c.av = VALS ? vb[2 * p] : 0;
+    if (2 * p + 1 < nl) {
+      c.bc = cb[2 * p + 1];
+      c.bv = VALS ? vb[2 * p + 1] : 0;
+    } else {
+      c.bc = c.ac + c.la;
+      c.bv = c.av + c.la;
+    }
+  } else {
+    c.ac = c.av = s0;
+    c.bc = c.bv = s1;
+  }
   c.d = k * VT;
   c.dend = min(c.d + VT, c.la + c.lb);
-  c.i = merge_path(sc + c.as, c.la, sc + c.ae, c.lb, c.d);
+  c.i = merge_path(sc + c.ac, c.la, sc + c.bc, c.lb, c.d);
   c.j = c.d - c.i;
-  if (c.i > 0 && c.j < c.lb && sc[c.as + c.i - 1] == sc[c.ae + c.j]) {
+  if (c.i > 0 && c.j < c.lb && sc[c.ac + c.i - 1] == sc[c.bc + c.j]) {
     ++c.j;  // b[j] duplicates a[i-1]: summed by the chunk to the left
     ++c.d;
   }
   if (FIRST && VALS) {
-    c.sa = scale[2 * p];
-    c.sb = (2 * p + 1 < nl) ? scale[2 * p + 1] : 0.0;
+    c.sa = aval[2 * p];
+    c.sb = (2 * p + 1 < nl) ? aval[2 * p + 1] : 0.0;
   }
-  c.ca = c.i < c.la ? sc[c.as + c.i] : INT_MAX;
-  c.cb = c.j < c.lb ? sc[c.ae + c.j] : INT_MAX;
+  c.ca = c.i < c.la ? sc[c.ac + c.i] : INT_MAX;
+  c.cb = c.j < c.lb ? sc[c.bc + c.j] : INT_MAX;
   if (k == 0) c.pair_first = p;
 }
 
@@ -102,16 +186,15 @@ __device__ __forceinline__ void chunk_setup(Chunk& c, int t, int T, const int* s
 // The value of a list not taken is -0.0, the exact additive identity, so the
 // emitted value is bitwise x, y or x + y.
 template <bool FIRST, bool VALS>
-__device__ __forceinline__ void chunk_step(Chunk& c, const int* sc, const double* sv, int& ocol,
-                                           double& oval) {
+__device__ __forceinline__ void chunk_step(Chunk& c, const int* sc, const double* sv, int& ocol, double& oval) {
   const bool act = c.d < c.dend;
   const bool ta = act && c.ca <= c.cb;
   const bool tbb = act && c.cb <= c.ca;
   ocol = min(c.ca, c.cb);
   if (VALS) {
     double x = -0.0, y = -0.0;
-    if (ta) x = sv[c.as + c.i];
-    if (tbb) y = sv[c.ae + c.j];
+    if (ta) x = sv[c.av + c.i];
+    if (tbb) y = sv[c.bv + c.j];
     if (FIRST) {
       if (ta) x = __dmul_rn(c.sa, x);
       if (tbb) y = __dmul_rn(c.sb, y);
@@ -122,28 +205,26 @@ __device__ __forceinline__ void chunk_step(Chunk& c, const int* sc, const double
   c.j += tbb;
   c.d += (int)ta + (int)tbb;
   c.cnt += act;
-  const int na = c.as + min(c.i, c.la);  // in-bounds reload address (value masked below)
-  const int nb = c.ae + min(c.j, c.lb - 1 < 0 ? 0 : c.lb - 1);
-  const int xa = sc[na];
-  const int xb = sc[nb];
+  // reload both heads from in-bounds addresses; exhausted lists read INT_MAX
+  const int xa = sc[c.ac + min(c.i, c.la)];
+  const int xb = sc[c.bc + min(c.j, max(c.lb - 1, 0))];
   c.ca = c.i < c.la ? xa : INT_MAX;
   c.cb = c.j < c.lb ? xb : INT_MAX;
 }
 
 // One merge round over `nl` >= 2 lists of src (offsets `so`, nl + 1 entries).
 // Writes ceil(nl/2) lists to dst with offsets `dof`. Returns total outputs.
-// Each thread merges two chunks (t and t + G) interleaved for ILP.
 template <int G, int VT, bool FIRST, bool VALS>
-__device__ __forceinline__ int merge_round(const Group<G>& g, const int* sc, const double* sv,
+__device__ __forceinline__ int merge_round(const Group<G>& g, const RowBufs& rb, const int* sc, const double* sv,
                                            const int* so, int nl, int* dc, double* dv, int* dof,
-                                           const double* scale, int* cst, int* scan_tmp) {
+                                           const double* aval) {
   const int npairs = (nl + 1) >> 1;
-  const int T = build_chunks<G, VT>(g, so, nl, npairs, cst, scan_tmp);
+  const int T = build_chunks<G, VT>(g, so, nl, npairs, rb.cst, rb.cpair, rb.scan_tmp);
   int out_base = 0;
   for (int tb = 0; tb < T; tb += 2 * G) {
     Chunk c0, c1;
-    chunk_setup<VT, FIRST, VALS>(c0, tb + g.rank, T, sc, so, nl, npairs, cst, scale);
-    chunk_setup<VT, FIRST, VALS>(c1, tb + G + g.rank, T, sc, so, nl, npairs, cst, scale);
+    chunk_setup<VT, FIRST, VALS>(c0, tb + g.rank, T, sc, so, nl, rb.cst, rb.cpair, rb.cb, rb.vb, aval);
+    chunk_setup<VT, FIRST, VALS>(c1, tb + G + g.rank, T, sc, so, nl, rb.cst, rb.cpair, rb.cb, rb.vb, aval);
     int ocol0[VT], ocol1[VT];
     double oval0[VT], oval1[VT];
 #pragma unroll
@@ -151,9 +232,9 @@ __device__ __forceinline__ int merge_round(const Group<G>& g, const int* sc, con
       chunk_step<FIRST, VALS>(c0, sc, sv, ocol0[v], oval0[v]);
       chunk_step<FIRST, VALS>(c1, sc, sv, ocol1[v], oval1[v]);
     }
-    // packed scan: low 16 bits chunk t, high 16 bits chunk t + G
+    // packed scan: low 16 bits chunk tb + rank, high 16 bits chunk tb + G + rank
     int total;
-    const int ex = group_excl_scan<G>(g, c0.cnt | (c1.cnt << 16), total, scan_tmp);
+    const int ex = group_excl_scan<G>(g, c0.cnt | (c1.cnt << 16), total, rb.scan_tmp);
     const int base0 = out_base + (ex & 0xffff);
     const int base1 = out_base + (total & 0xffff) + (ex >> 16);
 #pragma unroll
@@ -173,16 +254,16 @@ __device__ __forceinline__ int merge_round(const Group<G>& g, const int* sc, con
       if (pf >= 0) {  // this pair's (and preceding empty pairs') dst offset
         const int base = h ? base1 : base0;
         int q = pf;
-        const int k0 = cst[q];
+        const int k0 = rb.cst[q];
         dof[q] = base;
-        while (q > 0 && cst[q - 1] == k0) dof[--q] = base;
+        while (q > 0 && rb.cst[q - 1] == k0) dof[--q] = base;
       }
     }
     out_base += (total & 0xffff) + (total >> 16);
   }
   if (g.rank == 0) {  // trailing empty pairs and the end sentinel
     for (int q = npairs; q >= 0; --q) {
-      if (q < npairs && cst[q] != T) break;
+      if (q < npairs && rb.cst[q] != T) break;
       dof[q] = out_base;
     }
   }
@@ -190,106 +271,122 @@ __device__ __forceinline__ int merge_round(const Group<G>& g, const int* sc, con
   return out_base;
 }
 
-__device__ __forceinline__ void cp_async_4(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-// Multiplying phase (Alg. 1 lines 10-15, scaling deferred to round 1): copy
-// list l = B row k_l to [offA[l], offA[l+1]). Shared-memory tiers use
-// cp.async (LDGSTS) so every list of the row is in flight at once; long lists
-// are copied by the whole group (coalesced), short ones one lane per list.
-template <int G, bool VALS, bool SMEM>
-__device__ __forceinline__ void gather_lists(const Group<G>& g, const CsrView& B, int nl, int P,
-                                             const int* offA, const int64_t* bstart, int* colA,
-                                             double* valA) {
-  if (P * 2 >= nl * G || G == 1) {
-    for (int l = 0; l < nl; ++l) {
-      const int dst = offA[l], n = offA[l + 1] - dst;
-      const int64_t s = bstart[l];
-      for (int e = g.rank; e < n; e += G) {
-        if (SMEM) {
-          cp_async_4(colA + dst + e, B.col + s + e);
-          if (VALS) cp_async_8(valA + dst + e, B.val + s + e);
-        } else {
-          colA[dst + e] = B.col[s + e];
-          if (VALS) valA[dst + e] = B.val[s + e];
-        }
-      }
-    }
-  } else {
-    for (int l = g.rank; l < nl; l += G) {
-      const int dst = offA[l], n = offA[l + 1] - dst;
-      const int64_t s = bstart[l];
-      for (int e = 0; e < n; ++e) {
-        if (SMEM) {
-          cp_async_4(colA + dst + e, B.col + s + e);
-          if (VALS) cp_async_8(valA + dst + e, B.val + s + e);
-        } else {
-          colA[dst + e] = B.col[s + e];
-          if (VALS) valA[dst + e] = B.val[s + e];
-        }
-      }
-    }
-  }
-  if (SMEM) cp_async_wait_all();
-}
-
-// BRMerge of output row `row` by group g. Buffers: colA/colB (>= n_prod),
-// valA/valB (>= n_prod, VALS), offA (>= nl+1), offB (>= nl/2+2),
-// cst (>= nl/2+2), bstart (>= nl), scale (>= nl, VALS), scan_tmp (G/32+1).
-// SMEM: the buffers are in shared memory (cp.async gather).
+// BRMerge of output row `row` (n_prod P) by group g.
+// SMEM: buffers in shared memory (TMA / cp.async staging); phase: mbarrier
+// parity of this group, toggled once per row.
 template <int G, int VT, bool VALS, int OUT, bool SMEM>
-__device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A, const CsrView& B,
-                                            int64_t row, const RowOut& o, int* colA, int* colB,
-                                            double* valA, double* valB, int* offA, int* offB, int* cst,
-                                            int64_t* bstart, double* scale, int* scan_tmp) {
+__device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t bnnz,
+                                            int64_t row, int P, const RowOut& o, const RowBufs& rb,
+                                            unsigned& phase) {
   const int64_t a0 = A.rpt[row];
   const int nl = static_cast<int>(A.rpt[row + 1] - a0);
-  // list offsets: exclusive scan of the selected B row lengths
-  int run = 0;
+  const double* aval = VALS ? A.val + a0 : nullptr;
+  // TMA staging: every list's 16-byte window must fit the padded capacity and
+  // B's arrays must be 16-byte aligned
+  const bool tma = SMEM && P + 6 * nl <= rb.capc && (!VALS || P + 2 * nl <= rb.capv) &&
+                   ((reinterpret_cast<uintptr_t>(B.col) | (VALS ? reinterpret_cast<uintptr_t>(B.val) : 0)) & 15) == 0;
+  if (tma) fence_proxy_async();  // order the previous row's generic accesses before async writes
+  // list offsets (exclusive scan of the selected B row lengths) and, for TMA,
+  // the padded window layout; each lane stages its own lists
+  int run = 0, runc = 0, runv = 0;
   for (int lbase = 0; lbase < nl; lbase += G) {
     const int l = lbase + g.rank;
-    int len = 0;
+    int len = 0, wc = 0, wv = 0;
+    int64_t s = 0, wsc = 0, wsv = 0;
     if (l < nl) {
       const int k = A.col[a0 + l];
-      const int64_t s = B.rpt[k];
+      s = B.rpt[k];
       len = static_cast<int>(B.rpt[k + 1] - s);
-      bstart[l] = s;
-      if (VALS) scale[l] = A.val[a0 + l];
+      wsc = wsv = s;
+      if (tma && len > 0) {
+        wsc = s & ~3ll;
+        wc = static_cast<int>(((s + len + 3) & ~3ll) - wsc);
+        wsv = s & ~1ll;
+        wv = static_cast<int>(((s + len + 1) & ~1ll) - wsv);
+      }
     }
     int tot;
-    const int ex = group_excl_scan<G>(g, len, tot, scan_tmp);
-    if (l < nl) offA[l] = run + ex;
+    const int ex = group_excl_scan<G>(g, len, tot, rb.scan_tmp);
+    int pex = 0, ptot = 0;
+    if (tma) pex = group_excl_scan<G>(g, wc | (wv << 16), ptot, rb.scan_tmp);
+    if (l < nl) {
+      rb.offA[l] = run + ex;
+      if (tma) {
+        const int pc = runc + (pex & 0xffff), pv = runv + (pex >> 16);
+        rb.cb[l] = pc + static_cast<int>(s - wsc);
+        if (VALS) rb.vb[l] = pv + static_cast<int>(s - wsv);
+        if (len > 0) {
+          // one bulk copy per array if the window stays inside B's arrays,
+          // else element-wise cp.async into the same window positions
+          const bool bulk_c = wsc + wc <= bnnz;
+          const bool bulk_v = !VALS || wsv + wv <= bnnz;
+          unsigned bytes = (bulk_c ? wc * 4u : 0u) + (VALS && bulk_v ? wv * 8u : 0u);
+          if (bytes) mbar_expect_tx(rb.mbar, bytes);
+          if (bulk_c)
+            tma_bulk_g2s(rb.colA + pc, B.col + wsc, wc * 4u, rb.mbar);
+          else
+            for (int e = 0; e < len; ++e) cp_async_4(rb.colA + rb.cb[l] + e, B.col + s + e);
+          if (VALS) {
+            if (bulk_v)
+              tma_bulk_g2s(rb.valA + pv, B.val + wsv, wv * 8u, rb.mbar);
+            else
+              for (int e = 0; e < len; ++e) cp_async_8(rb.valA + pv + (s - wsv) + e, B.val + s + e);
+          }
+        }
+      } else {
+        rb.cb[l] = run + ex;
+        if (VALS) rb.vb[l] = run + ex;
+      }
+    }
     run += tot;
+    if (tma) {
+      runc += ptot & 0xffff;
+      runv += ptot >> 16;
+    }
   }
-  const int P = run;
-  if (g.rank == 0) offA[nl] = P;
+  if (g.rank == 0) rb.offA[nl] = run;
   g.sync();
-  // multiplying phase: gather the B rows into the ping buffer
-  gather_lists<G, VALS, SMEM>(g, B, nl, P, offA, bstart, colA, valA);
+  if (tma) {
+    if (g.rank == 0) mbar_arrive(rb.mbar);
+    cp_async_wait_all();
+    mbar_wait(rb.mbar, phase);
+    phase ^= 1u;
+  } else {
+    // multiplying phase without TMA: copy list l to [offA[l], offA[l+1])
+    const bool per_list_group = P * 2 >= nl * G;
+    for (int l = per_list_group ? 0 : g.rank; l < nl; l += per_list_group ? 1 : G) {
+      const int dst = rb.offA[l], n = rb.offA[l + 1] - dst;
+      if (!n) continue;
+      const int64_t s = B.rpt[A.col[a0 + l]];
+      for (int e = per_list_group ? g.rank : 0; e < n; e += per_list_group ? G : 1) {
+        if (SMEM) {
+          cp_async_4(rb.colA + dst + e, B.col + s + e);
+          if (VALS) cp_async_8(rb.valA + dst + e, B.val + s + e);
+        } else {
+          rb.colA[dst + e] = B.col[s + e];
+          if (VALS) rb.valA[dst + e] = B.val[s + e];
+        }
+      }
+    }
+    if (SMEM) cp_async_wait_all();
+  }
   g.sync();
-  int* sc = colA;
-  double* sv = valA;
-  int* so = offA;
-  int* dc = colB;
-  double* dv = valB;
-  int* dof = offB;
+  int* sc = rb.colA;
+  double* sv = rb.valA;
+  int* so = rb.offA;
+  int* dc = rb.colB;
+  double* dv = rb.valB;
+  int* dof = rb.offB;
   int n_out = P;
   if (nl >= 2) {
     int cur = nl;
-    n_out = merge_round<G, VT, true, VALS>(g, sc, sv, so, cur, dc, dv, dof, scale, cst, scan_tmp);
+    n_out = merge_round<G, VT, true, VALS>(g, rb, sc, sv, so, cur, dc, dv, dof, aval);
     cur = (cur + 1) >> 1;
     { int* t = sc; sc = dc; dc = t; }
     { double* t = sv; sv = dv; dv = t; }
     { int* t = so; so = dof; dof = t; }
     while (cur > 1) {
-      n_out = merge_round<G, VT, false, VALS>(g, sc, sv, so, cur, dc, dv, dof, nullptr, cst, scan_tmp);
+      n_out = merge_round<G, VT, false, VALS>(g, rb, sc, sv, so, cur, dc, dv, dof, nullptr);
       cur = (cur + 1) >> 1;
       { int* t = sc; sc = dc; dc = t; }
       { double* t = sv; sv = dv; dv = t; }
@@ -300,10 +397,11 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
   if (OUT != OUT_SYMBOLIC) {
     const int64_t dst = o.base[row];
     if (nl == 1) {  // single list: the scaled B row is the result
-      const double s0 = VALS ? scale[0] : 0.0;
+      const double s0 = VALS ? aval[0] : 0.0;
+      const int c0 = rb.cb[0], v0 = VALS ? rb.vb[0] : 0;
       for (int e = g.rank; e < n_out; e += G) {
-        o.col[dst + e] = sc[e];
-        if (VALS) o.val[dst + e] = __dmul_rn(s0, sv[e]);
+        o.col[dst + e] = sc[c0 + e];
+        if (VALS) o.val[dst + e] = __dmul_rn(s0, sv[v0 + e]);
       }
     } else {
       for (int e = g.rank; e < n_out; e += G) {

@@ -290,40 +290,54 @@ __global__ void k_heavy_info(CsrView A, const int64_t* __restrict__ nprod_off,
   }
 }
 
-// Shared-memory tiers.
+// Shared-memory tiers: GPC groups of G threads per CTA, one row per group at a
+// time, both ping-pong buffers in the group's slice of dynamic shared memory.
 template <int G, int VT, int CAP, int LCAP, int GPC, bool VALS, int OUT>
-__global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const int32_t* __restrict__ rows,
-                                                 int64_t nrows, RowOut o) {
+__global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, int64_t bnnz,
+                                                 const int64_t* __restrict__ nprod_off,
+                                                 const int32_t* __restrict__ rows, int64_t nrows, RowOut o) {
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr GroupLayout L = group_layout<G, CAP, LCAP, VALS>();
+  constexpr GroupLayout L = group_layout<G, VT, CAP, LCAP, VALS>();
   const Group<G> g = make_group<G>();
   unsigned char* base = smem + (threadIdx.x / G) * L.bytes;
-  int* colA = reinterpret_cast<int*>(base + L.colA);
-  int* colB = reinterpret_cast<int*>(base + L.colB);
-  double* valA = VALS ? reinterpret_cast<double*>(base + L.valA) : nullptr;
-  double* valB = VALS ? reinterpret_cast<double*>(base + L.valB) : nullptr;
-  double* scale = VALS ? reinterpret_cast<double*>(base + L.scale) : nullptr;
-  int64_t* bstart = reinterpret_cast<int64_t*>(base + L.bstart);
-  int* offA = reinterpret_cast<int*>(base + L.offA);
-  int* offB = reinterpret_cast<int*>(base + L.offB);
-  int* cst = reinterpret_cast<int*>(base + L.cst);
-  int* scan_tmp = reinterpret_cast<int*>(base + L.scan);
+  RowBufs rb;
+  rb.colA = reinterpret_cast<int*>(base + L.colA);
+  rb.colB = reinterpret_cast<int*>(base + L.colB);
+  rb.valA = VALS ? reinterpret_cast<double*>(base + L.valA) : nullptr;
+  rb.valB = VALS ? reinterpret_cast<double*>(base + L.valB) : nullptr;
+  rb.cb = reinterpret_cast<int*>(base + L.cb);
+  rb.vb = VALS ? reinterpret_cast<int*>(base + L.vb) : nullptr;
+  rb.offA = reinterpret_cast<int*>(base + L.offA);
+  rb.offB = reinterpret_cast<int*>(base + L.offB);
+  rb.cst = reinterpret_cast<int*>(base + L.cst);
+  rb.cpair = reinterpret_cast<int*>(base + L.cpair);
+  rb.mbar = reinterpret_cast<unsigned long long*>(base + L.mbar);
+  rb.scan_tmp = reinterpret_cast<int*>(base + L.scan);
+  rb.capc = L.capc;
+  rb.capv = L.capv;
+  if (g.rank == 0) mbar_init(rb.mbar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  unsigned phase = 0;
   for (int64_t r = (int64_t)blockIdx.x * GPC + threadIdx.x / G; r < nrows; r += (int64_t)gridDim.x * GPC) {
-    process_row<G, VT, VALS, OUT, true>(g, A, B, rows[r], o, colA, colB, valA, valB, offA, offB, cst, bstart,
-                                  scale, scan_tmp);
+    const int64_t row = rows[r];
+    const int P = static_cast<int>(nprod_off[row + 1] - nprod_off[row]);
+    process_row<G, VT, VALS, OUT, true>(g, A, B, bnnz, row, P, o, rb, phase);
   }
 }
 
 // Global tier: one CTA per row, ping-pong buffers in a per-row slice of a
-// global workspace at byte offset ws_off[r] (host-batched).
+// global workspace at byte offset ws_off[2r] (host-batched; ws_off[2r+1] is
+// the row's n_prod).
 template <bool VALS, int OUT>
-__global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, int64_t bnnz,
+                                                         const int32_t* __restrict__ rows,
                                                          const int64_t* __restrict__ ws_off,
                                                          unsigned char* __restrict__ ws, RowOut o) {
   __shared__ int scan_tmp[kGlobalG / 32 + 1];
   const Group<kGlobalG> g = make_group<kGlobalG>();
   const int64_t row = rows[blockIdx.x];
-  const int64_t P = ws_off[2 * blockIdx.x + 1];  // n_prod of the row
+  const int64_t P = ws_off[2 * blockIdx.x + 1];
   const int nl = (int)(A.rpt[row + 1] - A.rpt[row]);
   unsigned char* p = ws + ws_off[2 * blockIdx.x];
   auto take = [&](int64_t bytes) {
@@ -331,17 +345,22 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
     p += ((bytes + 15) & ~15ll) + 16;  // +16: merge reloads may touch one slot past a list
     return q;
   };
-  double* valA = VALS ? reinterpret_cast<double*>(take(P * 8)) : nullptr;
-  double* valB = VALS ? reinterpret_cast<double*>(take(P * 8)) : nullptr;
-  double* scale = VALS ? reinterpret_cast<double*>(take((int64_t)nl * 8)) : nullptr;
-  int64_t* bstart = reinterpret_cast<int64_t*>(take((int64_t)nl * 8));
-  int* colA = reinterpret_cast<int*>(take(P * 4));
-  int* colB = reinterpret_cast<int*>(take(P * 4));
-  int* offA = reinterpret_cast<int*>(take((int64_t)(nl + 1) * 4));
-  int* offB = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
-  int* cst = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
-  process_row<kGlobalG, kGlobalVT, VALS, OUT, false>(g, A, B, row, o, colA, colB, valA, valB, offA, offB, cst,
-                                              bstart, scale, scan_tmp);
+  RowBufs rb;
+  rb.valA = VALS ? reinterpret_cast<double*>(take(P * 8)) : nullptr;
+  rb.valB = VALS ? reinterpret_cast<double*>(take(P * 8)) : nullptr;
+  rb.colA = reinterpret_cast<int*>(take(P * 4));
+  rb.colB = reinterpret_cast<int*>(take(P * 4));
+  rb.cb = reinterpret_cast<int*>(take((int64_t)nl * 4));
+  rb.vb = VALS ? reinterpret_cast<int*>(take((int64_t)nl * 4)) : nullptr;
+  rb.offA = reinterpret_cast<int*>(take((int64_t)(nl + 1) * 4));
+  rb.offB = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
+  rb.cst = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
+  rb.cpair = reinterpret_cast<int*>(take((P / kGlobalVT + nl / 2 + 2) * 4));
+  rb.mbar = nullptr;
+  rb.scan_tmp = scan_tmp;
+  rb.capc = rb.capv = 0;
+  unsigned phase = 0;
+  process_row<kGlobalG, kGlobalVT, VALS, OUT, false>(g, A, B, bnnz, row, (int)P, o, rb, phase);
 }
 
 // Step 6 of Fig. 4a: copy each row of C_bar (at its n_prod offset) to C.
@@ -439,10 +458,10 @@ cudaError_t launch_heavy_info(const CsrView& A, const int64_t* nprod_off, const 
 }
 
 template <int G, int VT, int CAP, int LCAP, int GPC, bool VALS, int OUT>
-static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
-                                 const RowOut& o, cudaStream_t st) {
+static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, int64_t bnnz, const int64_t* nprod_off,
+                                 const int32_t* rows, int64_t n, const RowOut& o, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  constexpr GroupLayout L = group_layout<G, CAP, LCAP, VALS>();
+  constexpr GroupLayout L = group_layout<G, VT, CAP, LCAP, VALS>();
   constexpr int smem = L.bytes * GPC;
   static_assert(smem <= 232448, "tier shared memory exceeds 227 KB");
   auto kern = k_tier<G, VT, CAP, LCAP, GPC, VALS, OUT>;
@@ -458,48 +477,50 @@ static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, const int32
   const int64_t want = (n + GPC - 1) / GPC;
   const int64_t cap = (int64_t)per_sm * num_sms();
   const unsigned grid = (unsigned)(want < cap ? want : cap);
-  kern<<<grid, G * GPC, smem, st>>>(A, B, rows, n, o);
+  kern<<<grid, G * GPC, smem, st>>>(A, B, bnnz, nprod_off, rows, n, o);
   return cudaGetLastError();
 }
 
 template <bool VALS, int OUT>
-static cudaError_t launch_tier_dispatch(int bin, const CsrView& A, const CsrView& B, const int32_t* rows,
-                                        int64_t n, const RowOut& o, cudaStream_t st) {
+static cudaError_t launch_tier_dispatch(int bin, const CsrView& A, const CsrView& B, int64_t bnnz,
+                                        const int64_t* nprod_off, const int32_t* rows, int64_t n, const RowOut& o,
+                                        cudaStream_t st) {
   switch (bin) {
-    case 1: return launch_tier_t<BRM_TIER1, VALS, OUT>(A, B, rows, n, o, st);
-    case 2: return launch_tier_t<BRM_TIER2, VALS, OUT>(A, B, rows, n, o, st);
-    case 3: return launch_tier_t<BRM_TIER3, VALS, OUT>(A, B, rows, n, o, st);
-    case 4: return launch_tier_t<BRM_TIER4, VALS, OUT>(A, B, rows, n, o, st);
-    case 5: return launch_tier_t<BRM_TIER5, VALS, OUT>(A, B, rows, n, o, st);
+    case 1: return launch_tier_t<BRM_TIER1, VALS, OUT>(A, B, bnnz, nprod_off, rows, n, o, st);
+    case 2: return launch_tier_t<BRM_TIER2, VALS, OUT>(A, B, bnnz, nprod_off, rows, n, o, st);
+    case 3: return launch_tier_t<BRM_TIER3, VALS, OUT>(A, B, bnnz, nprod_off, rows, n, o, st);
+    case 4: return launch_tier_t<BRM_TIER4, VALS, OUT>(A, B, bnnz, nprod_off, rows, n, o, st);
+    case 5: return launch_tier_t<BRM_TIER5, VALS, OUT>(A, B, bnnz, nprod_off, rows, n, o, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows,
-                        int64_t n, const RowOut& o, cudaStream_t st) {
+cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& B, int64_t bnnz,
+                        const int64_t* nprod_off, const int32_t* rows, int64_t n, const RowOut& o, cudaStream_t st) {
   switch (out_kind) {
-    case OUT_SYMBOLIC: return launch_tier_dispatch<false, OUT_SYMBOLIC>(bin, A, B, rows, n, o, st);
-    case OUT_CBAR: return launch_tier_dispatch<true, OUT_CBAR>(bin, A, B, rows, n, o, st);
-    case OUT_C: return launch_tier_dispatch<true, OUT_C>(bin, A, B, rows, n, o, st);
+    case OUT_SYMBOLIC: return launch_tier_dispatch<false, OUT_SYMBOLIC>(bin, A, B, bnnz, nprod_off, rows, n, o, st);
+    case OUT_CBAR: return launch_tier_dispatch<true, OUT_CBAR>(bin, A, B, bnnz, nprod_off, rows, n, o, st);
+    case OUT_C: return launch_tier_dispatch<true, OUT_C>(bin, A, B, bnnz, nprod_off, rows, n, o, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 int64_t global_row_bytes(int64_t nprod, int64_t nl, bool vals) {
   auto a = [](int64_t b) { return ((b + 15) & ~15ll) + 16; };
-  int64_t s = a(nl * 8) + a(nprod * 4) * 2 + a((nl + 1) * 4) + a((nl / 2 + 2) * 4) * 2;
-  if (vals) s += a(nprod * 8) * 2 + a(nl * 8);
+  int64_t s = a(nprod * 4) * 2 + a(nl * 4) + a((nl + 1) * 4) + a((nl / 2 + 2) * 4) * 2 +
+              a((nprod / kGlobalVT + nl / 2 + 2) * 4);
+  if (vals) s += a(nprod * 8) * 2 + a(nl * 4);
   return s;
 }
 
-cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows,
+cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B, int64_t bnnz, const int32_t* rows,
                                int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o,
                                cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   switch (out_kind) {
-    case OUT_SYMBOLIC: k_global_tier<false, OUT_SYMBOLIC><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, rows, ws_off, ws, o); break;
-    case OUT_CBAR: k_global_tier<true, OUT_CBAR><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, rows, ws_off, ws, o); break;
-    case OUT_C: k_global_tier<true, OUT_C><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, rows, ws_off, ws, o); break;
+    case OUT_SYMBOLIC: k_global_tier<false, OUT_SYMBOLIC><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, bnnz, rows, ws_off, ws, o); break;
+    case OUT_CBAR: k_global_tier<true, OUT_CBAR><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, bnnz, rows, ws_off, ws, o); break;
+    case OUT_C: k_global_tier<true, OUT_C><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, bnnz, rows, ws_off, ws, o); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
