@@ -87,7 +87,7 @@ def stencil27_box(nx, ny, nz, seed):
 
 # tier table mirrored from csrc/brm_internal.cuh (checked by tests/test_bench_host.py)
 TIER_CAP = [0, 64, 256, 768, 2560, 7168]
-TIER_LCAP = [0, 32, 128, 128, 512, 1024]
+TIER_LCAP = [0, 32, 128, 64, 512, 1024]
 
 
 def tier_of(nprod: np.ndarray, nl: np.ndarray) -> np.ndarray:

@@ -34,7 +34,7 @@ struct TierBounds {
 //  CAP elements, LCAP lists, GPC groups per CTA)
 #define BRM_TIER1 8, 8, 64, 32, 16
 #define BRM_TIER2 32, 8, 256, 128, 4
-#define BRM_TIER3 32, 8, 768, 128, 1
+#define BRM_TIER3 32, 8, 768, 64, 1
 #define BRM_TIER4 128, 8, 2560, 512, 1
 #define BRM_TIER5 256, 8, 7168, 1024, 1
 constexpr int kGlobalG = 512;
@@ -45,7 +45,7 @@ __host__ __device__ inline TierBounds tier_bounds() {
   t.cap[0] = 0;    t.lcap[0] = 0;
   t.cap[1] = 64;   t.lcap[1] = 32;
   t.cap[2] = 256;  t.lcap[2] = 128;
-  t.cap[3] = 768;  t.lcap[3] = 128;
+  t.cap[3] = 768;  t.lcap[3] = 64;
   t.cap[4] = 2560; t.lcap[4] = 512;
   t.cap[5] = 7168; t.lcap[5] = 1024;
   t.cap[6] = INT_MAX; t.lcap[6] = INT_MAX;
@@ -72,13 +72,13 @@ __host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
 template <int G, int VT, int CAP, int LCAP, bool VALS>
 __host__ __device__ constexpr GroupLayout group_layout() {
   GroupLayout L{};
-  L.capc = CAP + CAP / 4;
-  L.capv = CAP + CAP / 8;
+  L.capc = CAP + (LCAP > CAP / 4 ? LCAP : CAP / 4);
+  L.capv = CAP + (LCAP > CAP / 8 ? LCAP : CAP / 8);
   int o = 0;
   L.valA = o;   o += VALS ? align16(L.capv * 8 + 16) : 0;
-  L.valB = o;   o += VALS ? align16(CAP * 8 + 16) : 0;
+  L.valB = o;   o += VALS ? align16((CAP + LCAP / 2 + 2) * 8) : 0;
   L.colA = o;   o += align16(L.capc * 4 + 16);
-  L.colB = o;   o += align16(CAP * 4 + 16);
+  L.colB = o;   o += align16((CAP + LCAP / 2 + 2) * 4);
   L.cb = o;     o += align16(LCAP * 4);
   L.vb = o;     o += VALS ? align16(LCAP * 4) : 0;
   L.offA = o;   o += align16((LCAP + 1) * 4);

@@ -124,10 +124,15 @@ __device__ __forceinline__ int build_chunks(const Group<G>& g, const int* so, in
   return run;
 }
 
-// Merge state of one chunk: list a at colA/valA index ac/av (length la),
-// list b at bc/bv (length lb); cursors i, j; merged position d; end dend.
+// Buffer layout: every list is followed by one INT_MAX sentinel column, so a
+// merge cursor needs no bounds check (an exhausted list reads INT_MAX). In the
+// contiguous rounds list l starts at physical index off[l] + l (one sentinel
+// slot per preceding list); round 1 uses the staged positions cb[l] / vb[l].
+
+// Merge state of one chunk: columns at sc[pa] / sc[pb] (physical cursors),
+// values at sv[qa] / sv[qb]; merged position d of the next element, end dend.
 struct Chunk {
-  int ac, av, bc, bv, la, lb, i, j, d, dend, ca, cb, cnt, pair_first;
+  int pa, pb, qa, qb, d, dend, ca, cb, cnt, pair, pair_first;
   double sa, sb;
 };
 
@@ -137,9 +142,10 @@ __device__ __forceinline__ void chunk_setup(Chunk& c, int t, int T, const int* s
                                             const double* aval) {
   c.cnt = 0;
   c.pair_first = -1;
+  c.pair = 0;
   c.d = 0;
   c.dend = 0;  // inactive
-  c.i = c.j = c.la = c.lb = c.ac = c.av = c.bc = c.bv = 0;
+  c.pa = c.pb = c.qa = c.qb = 0;
   c.ca = c.cb = INT_MAX;
   c.sa = c.sb = 1.0;
   if (t >= T) return;
@@ -148,36 +154,41 @@ __device__ __forceinline__ void chunk_setup(Chunk& c, int t, int T, const int* s
   const int s0 = so[2 * p];
   const int s1 = so[min(2 * p + 1, nl)];
   const int s2 = so[min(2 * p + 2, nl)];
-  c.la = s1 - s0;
-  c.lb = s2 - s1;
+  const int la = s1 - s0, lb = s2 - s1;
+  int ac, bc, av = 0, bv = 0;
   if (FIRST) {
-    c.ac = cb[2 * p];
-    c.av = VALS ? vb[2 * p] : 0;
+    ac = cb[2 * p];
+    if (VALS) av = vb[2 * p];
     if (2 * p + 1 < nl) {
-      c.bc = cb[2 * p + 1];
-      c.bv = VALS ? vb[2 * p + 1] : 0;
+      bc = cb[2 * p + 1];
+      if (VALS) bv = vb[2 * p + 1];
     } else {
-      c.bc = c.ac + c.la;
-      c.bv = c.av + c.la;
+      bc = ac + la;  // empty partner: a's sentinel
+      bv = av;
     }
   } else {
-    c.ac = c.av = s0;
-    c.bc = c.bv = s1;
+    ac = av = s0 + 2 * p;
+    bc = bv = (2 * p + 1 < nl) ? s1 + 2 * p + 1 : ac + la;
   }
+  c.pair = p;
   c.d = k * VT;
-  c.dend = min(c.d + VT, c.la + c.lb);
-  c.i = merge_path(sc + c.ac, c.la, sc + c.bc, c.lb, c.d);
-  c.j = c.d - c.i;
-  if (c.i > 0 && c.j < c.lb && sc[c.ac + c.i - 1] == sc[c.bc + c.j]) {
-    ++c.j;  // b[j] duplicates a[i-1]: summed by the chunk to the left
+  c.dend = min(c.d + VT, la + lb);
+  int i = merge_path(sc + ac, la, sc + bc, lb, c.d);
+  int j = c.d - i;
+  if (i > 0 && j < lb && sc[ac + i - 1] == sc[bc + j]) {
+    ++j;  // b[j] duplicates a[i-1]: summed by the chunk to the left
     ++c.d;
   }
   if (FIRST && VALS) {
     c.sa = aval[2 * p];
     c.sb = (2 * p + 1 < nl) ? aval[2 * p + 1] : 0.0;
   }
-  c.ca = c.i < c.la ? sc[c.ac + c.i] : INT_MAX;
-  c.cb = c.j < c.lb ? sc[c.bc + c.j] : INT_MAX;
+  c.pa = ac + i;
+  c.pb = bc + j;
+  c.qa = av + i;
+  c.qb = bv + j;
+  c.ca = sc[c.pa];
+  c.cb = sc[c.pb];
   if (k == 0) c.pair_first = p;
 }
 
@@ -193,27 +204,30 @@ __device__ __forceinline__ void chunk_step(Chunk& c, const int* sc, const double
   ocol = min(c.ca, c.cb);
   if (VALS) {
     double x = -0.0, y = -0.0;
-    if (ta) x = sv[c.av + c.i];
-    if (tbb) y = sv[c.bv + c.j];
+    if (ta) x = sv[FIRST ? c.qa : c.pa];
+    if (tbb) y = sv[FIRST ? c.qb : c.pb];
     if (FIRST) {
       if (ta) x = __dmul_rn(c.sa, x);
       if (tbb) y = __dmul_rn(c.sb, y);
     }
     oval = __dadd_rn(x, y);
   }
-  c.i += ta;
-  c.j += tbb;
+  c.pa += ta;
+  c.pb += tbb;
+  if (FIRST) {
+    c.qa += ta;
+    c.qb += tbb;
+  }
   c.d += (int)ta + (int)tbb;
   c.cnt += act;
-  // reload both heads from in-bounds addresses; exhausted lists read INT_MAX
-  const int xa = sc[c.ac + min(c.i, c.la)];
-  const int xb = sc[c.bc + min(c.j, max(c.lb - 1, 0))];
-  c.ca = c.i < c.la ? xa : INT_MAX;
-  c.cb = c.j < c.lb ? xb : INT_MAX;
+  c.ca = sc[c.pa];
+  c.cb = sc[c.pb];
 }
 
 // One merge round over `nl` >= 2 lists of src (offsets `so`, nl + 1 entries).
-// Writes ceil(nl/2) lists to dst with offsets `dof`. Returns total outputs.
+// Writes ceil(nl/2) lists (each followed by its sentinel) to dst with offsets
+// `dof`. Returns total outputs. Each thread merges two chunks (t and t + G)
+// interleaved for ILP.
 template <int G, int VT, bool FIRST, bool VALS>
 __device__ __forceinline__ int merge_round(const Group<G>& g, const RowBufs& rb, const int* sc, const double* sv,
                                            const int* so, int nl, int* dc, double* dv, int* dof,
@@ -223,8 +237,9 @@ __device__ __forceinline__ int merge_round(const Group<G>& g, const RowBufs& rb,
   int out_base = 0;
   for (int tb = 0; tb < T; tb += 2 * G) {
     Chunk c0, c1;
-    chunk_setup<VT, FIRST, VALS>(c0, tb + g.rank, T, sc, so, nl, rb.cst, rb.cpair, rb.cb, rb.vb, aval);
-    chunk_setup<VT, FIRST, VALS>(c1, tb + G + g.rank, T, sc, so, nl, rb.cst, rb.cpair, rb.cb, rb.vb, aval);
+    const int t0 = tb + g.rank, t1 = tb + G + g.rank;
+    chunk_setup<VT, FIRST, VALS>(c0, t0, T, sc, so, nl, rb.cst, rb.cpair, rb.cb, rb.vb, aval);
+    chunk_setup<VT, FIRST, VALS>(c1, t1, T, sc, so, nl, rb.cst, rb.cpair, rb.cb, rb.vb, aval);
     int ocol0[VT], ocol1[VT];
     double oval0[VT], oval1[VT];
 #pragma unroll
@@ -232,11 +247,13 @@ __device__ __forceinline__ int merge_round(const Group<G>& g, const RowBufs& rb,
       chunk_step<FIRST, VALS>(c0, sc, sv, ocol0[v], oval0[v]);
       chunk_step<FIRST, VALS>(c1, sc, sv, ocol1[v], oval1[v]);
     }
-    // packed scan: low 16 bits chunk tb + rank, high 16 bits chunk tb + G + rank
+    // packed scan: low 16 bits chunk t0, high 16 bits chunk t1
     int total;
     const int ex = group_excl_scan<G>(g, c0.cnt | (c1.cnt << 16), total, rb.scan_tmp);
-    const int base0 = out_base + (ex & 0xffff);
-    const int base1 = out_base + (total & 0xffff) + (ex >> 16);
+    const int vbase0 = out_base + (ex & 0xffff);  // compacted (virtual) positions
+    const int vbase1 = out_base + (total & 0xffff) + (ex >> 16);
+    const int base0 = vbase0 + c0.pair;  // physical: one sentinel per earlier pair
+    const int base1 = vbase1 + c1.pair;
 #pragma unroll
     for (int v = 0; v < VT; ++v) {
       if (v < c0.cnt) {
@@ -248,23 +265,30 @@ __device__ __forceinline__ int merge_round(const Group<G>& g, const RowBufs& rb,
         if (VALS) dv[base1 + v] = oval1[v];
       }
     }
+    // the last chunk of a pair writes the pair's sentinel
+    if (t0 < T && t0 + 1 == rb.cst[c0.pair + 1]) dc[base0 + c0.cnt] = INT_MAX;
+    if (t1 < T && t1 + 1 == rb.cst[c1.pair + 1]) dc[base1 + c1.cnt] = INT_MAX;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int pf = h ? c1.pair_first : c0.pair_first;
       if (pf >= 0) {  // this pair's (and preceding empty pairs') dst offset
-        const int base = h ? base1 : base0;
+        const int vb = h ? vbase1 : vbase0;
         int q = pf;
         const int k0 = rb.cst[q];
-        dof[q] = base;
-        while (q > 0 && rb.cst[q - 1] == k0) dof[--q] = base;
+        dof[q] = vb;
+        while (q > 0 && rb.cst[q - 1] == k0) {
+          dof[--q] = vb;
+          dc[vb + q] = INT_MAX;  // sentinel of the empty pair q
+        }
       }
     }
     out_base += (total & 0xffff) + (total >> 16);
   }
-  if (g.rank == 0) {  // trailing empty pairs and the end sentinel
+  if (g.rank == 0) {  // trailing empty pairs (sentinels too) and the end offset
     for (int q = npairs; q >= 0; --q) {
       if (q < npairs && rb.cst[q] != T) break;
       dof[q] = out_base;
+      if (q < npairs) dc[out_base + q] = INT_MAX;
     }
   }
   g.sync();
@@ -281,9 +305,9 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
   const int64_t a0 = A.rpt[row];
   const int nl = static_cast<int>(A.rpt[row + 1] - a0);
   const double* aval = VALS ? A.val + a0 : nullptr;
-  // TMA staging: every list's 16-byte window must fit the padded capacity and
-  // B's arrays must be 16-byte aligned
-  const bool tma = SMEM && P + 6 * nl <= rb.capc && (!VALS || P + 2 * nl <= rb.capv) &&
+  // TMA staging: every list's 16-byte window (+ room for its sentinel) must
+  // fit the padded capacity and B's arrays must be 16-byte aligned
+  const bool tma = SMEM && P + 7 * nl <= rb.capc && (!VALS || P + 2 * nl <= rb.capv) &&
                    ((reinterpret_cast<uintptr_t>(B.col) | (VALS ? reinterpret_cast<uintptr_t>(B.val) : 0)) & 15) == 0;
   if (tma) fence_proxy_async();  // order the previous row's generic accesses before async writes
   // list offsets (exclusive scan of the selected B row lengths) and, for TMA,
@@ -298,11 +322,13 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
       s = B.rpt[k];
       len = static_cast<int>(B.rpt[k + 1] - s);
       wsc = wsv = s;
-      if (tma && len > 0) {
+      if (tma) {
         wsc = s & ~3ll;
-        wc = static_cast<int>(((s + len + 3) & ~3ll) - wsc);
-        wsv = s & ~1ll;
-        wv = static_cast<int>(((s + len + 1) & ~1ll) - wsv);
+        wc = static_cast<int>(((s + len + 4) & ~3ll) - wsc);  // >= one slot after the list
+        if (len > 0) {
+          wsv = s & ~1ll;
+          wv = static_cast<int>(((s + len + 1) & ~1ll) - wsv);
+        }
       }
     }
     int tot;
@@ -320,7 +346,7 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
           // else element-wise cp.async into the same window positions
           const bool bulk_c = wsc + wc <= bnnz;
           const bool bulk_v = !VALS || wsv + wv <= bnnz;
-          unsigned bytes = (bulk_c ? wc * 4u : 0u) + (VALS && bulk_v ? wv * 8u : 0u);
+          const unsigned bytes = (bulk_c ? wc * 4u : 0u) + (VALS && bulk_v ? wv * 8u : 0u);
           if (bytes) mbar_expect_tx(rb.mbar, bytes);
           if (bulk_c)
             tma_bulk_g2s(rb.colA + pc, B.col + wsc, wc * 4u, rb.mbar);
@@ -334,8 +360,8 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
           }
         }
       } else {
-        rb.cb[l] = run + ex;
-        if (VALS) rb.vb[l] = run + ex;
+        rb.cb[l] = run + ex + l;  // contiguous lists, one sentinel slot each
+        if (VALS) rb.vb[l] = run + ex + l;
       }
     }
     run += tot;
@@ -352,10 +378,10 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
     mbar_wait(rb.mbar, phase);
     phase ^= 1u;
   } else {
-    // multiplying phase without TMA: copy list l to [offA[l], offA[l+1])
+    // multiplying phase without TMA: copy list l to cb[l] .. cb[l] + len
     const bool per_list_group = P * 2 >= nl * G;
     for (int l = per_list_group ? 0 : g.rank; l < nl; l += per_list_group ? 1 : G) {
-      const int dst = rb.offA[l], n = rb.offA[l + 1] - dst;
+      const int dst = rb.cb[l], n = rb.offA[l + 1] - rb.offA[l];
       if (!n) continue;
       const int64_t s = B.rpt[A.col[a0 + l]];
       for (int e = per_list_group ? g.rank : 0; e < n; e += per_list_group ? G : 1) {
@@ -370,6 +396,9 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
     }
     if (SMEM) cp_async_wait_all();
   }
+  g.sync();
+  // sentinel after every gathered list
+  for (int l = g.rank; l < nl; l += G) rb.colA[rb.cb[l] + rb.offA[l + 1] - rb.offA[l]] = INT_MAX;
   g.sync();
   int* sc = rb.colA;
   double* sv = rb.valA;

@@ -346,10 +346,10 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
     return q;
   };
   RowBufs rb;
-  rb.valA = VALS ? reinterpret_cast<double*>(take(P * 8)) : nullptr;
-  rb.valB = VALS ? reinterpret_cast<double*>(take(P * 8)) : nullptr;
-  rb.colA = reinterpret_cast<int*>(take(P * 4));
-  rb.colB = reinterpret_cast<int*>(take(P * 4));
+  rb.valA = VALS ? reinterpret_cast<double*>(take((P + nl + 1) * 8)) : nullptr;
+  rb.valB = VALS ? reinterpret_cast<double*>(take((P + nl / 2 + 2) * 8)) : nullptr;
+  rb.colA = reinterpret_cast<int*>(take((P + nl + 1) * 4));
+  rb.colB = reinterpret_cast<int*>(take((P + nl / 2 + 2) * 4));
   rb.cb = reinterpret_cast<int*>(take((int64_t)nl * 4));
   rb.vb = VALS ? reinterpret_cast<int*>(take((int64_t)nl * 4)) : nullptr;
   rb.offA = reinterpret_cast<int*>(take((int64_t)(nl + 1) * 4));
@@ -507,9 +507,9 @@ cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& 
 
 int64_t global_row_bytes(int64_t nprod, int64_t nl, bool vals) {
   auto a = [](int64_t b) { return ((b + 15) & ~15ll) + 16; };
-  int64_t s = a(nprod * 4) * 2 + a(nl * 4) + a((nl + 1) * 4) + a((nl / 2 + 2) * 4) * 2 +
+  int64_t s = a((nprod + nl + 1) * 4) + a((nprod + nl / 2 + 2) * 4) + a(nl * 4) + a((nl + 1) * 4) + a((nl / 2 + 2) * 4) * 2 +
               a((nprod / kGlobalVT + nl / 2 + 2) * 4);
-  if (vals) s += a(nprod * 8) * 2 + a(nl * 4);
+  if (vals) s += a((nprod + nl + 1) * 8) + a((nprod + nl / 2 + 2) * 8) + a(nl * 4);
   return s;
 }
 
