@@ -99,6 +99,9 @@ typedef struct {
   float ms_compact;                 /* UPPER: C_bar -> C compaction            */
   float ms_bin_numeric[BRM_NUM_BINS]; /* numeric merge per tier              */
   int64_t launches;                 /* kernels launched by the last structure+fill */
+  uint64_t prof[8];                 /* env BRM_PROFILE=1: device cycles summed over row
+                                       groups [stage, seq rounds, chunked rounds, store,
+                                       #seq rounds, #chunked rounds, #rows, -]       */
 } brm_stats_t;
 
 typedef struct brm_context brm_context_t;

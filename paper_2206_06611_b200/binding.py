@@ -45,7 +45,8 @@ class brm_stats_t(ctypes.Structure):
                 ("ms_numeric", ctypes.c_float), ("ms_rowsize_scan", ctypes.c_float),
                 ("ms_compact", ctypes.c_float),
                 ("ms_bin_numeric", ctypes.c_float * BRM_NUM_BINS),
-                ("launches", ctypes.c_int64)]
+                ("launches", ctypes.c_int64),
+                ("prof", ctypes.c_uint64 * 8)]
 
     def as_dict(self) -> dict:
         d = {}

@@ -2,6 +2,7 @@
 // orchestration of Fig. 4a (BRMerge-Upper) and Fig. 4b (BRMerge-Precise),
 // PAPER.md:284-300, on one device stream.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -49,6 +50,8 @@ struct brm_context {
   cudaEvent_t ev[32] = {};
   unsigned ev_mask = 0;  // events recorded since the last structure call
   int64_t launches = 0;  // kernels launched since the last structure call
+  int strategy = 0;      // env BRM_STRATEGY (experiments): 0 auto, 1 one thread per pair, 2 chunked
+  bool profile = false;  // env BRM_PROFILE=1: device cycle counters in brm_stats_t.prof
 };
 
 namespace {
@@ -137,6 +140,7 @@ brm_status_t check_csr(brm_context_t* ctx, const brm_csr_t* X, const char* name)
 
 // Small device block: summary + scan counters + bin cursor + nnz total.
 struct SmallDev {
+  unsigned long long prof[kProfSlots];
   DevSummary summary;
   unsigned long long cursor[BRM_NUM_BINS];
   unsigned int counter[4];
@@ -325,6 +329,8 @@ brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
   // UPPER: Steps 3-4 (C_bar by n_prod offsets, numeric merge);
   // PRECISE: Step 3 (symbolic merge)
   RowOut o{};
+  o.strategy = ctx->strategy;
+  o.prof = ctx->profile ? sd->prof : nullptr;
   int out;
   if (mode == BRM_UPPER) {
     const int64_t np = ctx->sum.nprod_total;
@@ -351,6 +357,7 @@ brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
   *c_nnz = ctx->nnz_c;
   ctx->stats.nnz_c = ctx->nnz_c;
   ctx->planned = true;
+  if (ctx->profile) memcpy(ctx->stats.prof, static_cast<SmallDev*>(ctx->h_small.p)->prof, sizeof(ctx->stats.prof));
   return BRM_OK;
 }
 
@@ -373,6 +380,8 @@ brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
   } else {
     // Step 5 of Fig. 4b: numeric merge straight into C
     RowOut o{};
+    o.strategy = ctx->strategy;
+    o.prof = ctx->profile ? small_dev(ctx)->prof : nullptr;
     o.base = C->rpt;
     o.col = C->col;
     o.val = C->val;
@@ -411,6 +420,8 @@ brm_status_t brm_create(brm_context_t** out, int device, void* stream) {
   brm_context_t* ctx = new brm_context_t;
   ctx->device = device;
   ctx->stream = static_cast<cudaStream_t>(stream);
+  if (const char* e = getenv("BRM_STRATEGY")) ctx->strategy = atoi(e);
+  if (const char* e = getenv("BRM_PROFILE")) ctx->profile = atoi(e) != 0;
   DeviceGuard g(device);
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   *out = ctx;
@@ -455,6 +466,11 @@ brm_status_t brm_get_stats(const brm_context_t* ctx, brm_stats_t* out) {
   if (!ctx || !out) return BRM_ERR_INVALID;
   *out = ctx->stats;
   out->launches = ctx->launches;
+  if (ctx->profile && ctx->small.p) {
+    DeviceGuard g(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaMemcpy(out->prof, ctx->small.p, sizeof(out->prof), cudaMemcpyDeviceToHost);
+  }
   if (ctx->timing && ctx->ev_mask) {
     DeviceGuard g(ctx->device);
     for (int i = 31; i >= 0; --i)  // wait for everything recorded

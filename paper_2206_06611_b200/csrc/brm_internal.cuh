@@ -64,7 +64,7 @@ __host__ __device__ inline int tier_of(int64_t nprod, int64_t nl, const TierBoun
 // valA hold the gathered lists in 16-byte TMA windows, so they get padding
 // (capc / capv elements); rows whose windows do not fit use cp.async.
 struct GroupLayout {
-  int valA, valB, colA, colB, cb, vb, offA, offB, cst, cpair, mbar, scan, bytes, capc, capv;
+  int valA, valB, colA, colB, lstA, llnA, lstB, llnB, vb, cst, cpair, mbar, scan, bytes, capc, capv;
 };
 
 __host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
@@ -79,10 +79,11 @@ __host__ __device__ constexpr GroupLayout group_layout() {
   L.valB = o;   o += VALS ? align16((CAP + LCAP / 2 + 2) * 8) : 0;
   L.colA = o;   o += align16(L.capc * 4 + 16);
   L.colB = o;   o += align16((CAP + LCAP / 2 + 2) * 4);
-  L.cb = o;     o += align16(LCAP * 4);
+  L.lstA = o;   o += align16((LCAP + 1) * 4);
+  L.llnA = o;   o += align16((LCAP + 1) * 4);
+  L.lstB = o;   o += align16((LCAP / 2 + 2) * 4);
+  L.llnB = o;   o += align16((LCAP / 2 + 2) * 4);
   L.vb = o;     o += VALS ? align16(LCAP * 4) : 0;
-  L.offA = o;   o += align16((LCAP + 1) * 4);
-  L.offB = o;   o += align16((LCAP / 2 + 2) * 4);
   L.cst = o;    o += align16((LCAP / 2 + 2) * 4);
   L.cpair = o;  o += align16((CAP / VT + LCAP / 2 + 2) * 4);
   L.mbar = o;   o += 16;

@@ -36,24 +36,35 @@ struct RowOut {
   int32_t* col;
   double* val;
   int64_t* row_size;    // OUT_SYMBOLIC / OUT_CBAR: nnz of each output row
+  int strategy;          // round strategy: 0 cost model, 1 one thread per pair, 2 chunked
+  unsigned long long* prof;  // optional cycle counters (kProf*), null = off
 };
 
-// Working arrays of one row group.
+// Device cycle counters (env BRM_PROFILE=1): summed over groups, lane 0 of
+// each group samples clock64() at phase boundaries.
+enum ProfSlot { kProfStage = 0, kProfSeq = 1, kProfChunk = 2, kProfStore = 3, kProfSeqRounds = 4,
+                kProfChunkRounds = 5, kProfRows = 6, kProfSlots = 8 };
+
+// Working arrays of one row group. A list is (start, len) in a column buffer
+// and is followed by one INT_MAX sentinel column, so merge cursors need no
+// bounds checks. Lists of a round lie in increasing start order.
 struct RowBufs {
   int* colA;
   int* colB;
   double* valA;
   double* valB;
-  int* cb;     // round 1: start of list l's columns in colA
+  int* lstA;   // list starts, ping side (round 1: staged columns in colA)
+  int* llnA;   // list lengths, ping side
+  int* lstB;   // list starts, pong side
+  int* llnB;   // list lengths, pong side
   int* vb;     // round 1: start of list l's values in valA
-  int* offA;   // list offsets (virtual, contiguous), ping
-  int* offB;   // list offsets, pong
   int* cst;    // chunk table: first chunk of each pair
   int* cpair;  // chunk table: pair of each chunk
   unsigned long long* mbar;
   int* scan_tmp;
   int capc, capv;  // capacities of colA / valA (TMA windows need padding)
 };
+
 
 // ---------------------------------------------------------------------------
 // async-copy primitives (sm_90+ PTX; SASS UBLKCP / LDGSTS / SYNCS)
@@ -97,19 +108,122 @@ __device__ __forceinline__ void tma_bulk_g2s(void* smem, const void* gmem, unsig
 }
 
 // ---------------------------------------------------------------------------
-// Chunk table of a round: cst[p] = first chunk of pair p (cst[npairs] =
-// total), cpair[t] = pair of chunk t.
+// Group reductions (sum and max of one int per thread).
+// ---------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ void group_sum_max(const Group<G>& g, int s, int m, int& sum, int& mx, int* tmp) {
+  if constexpr (G <= 32) {
+    sum = __reduce_add_sync(g.mask, s);
+    mx = __reduce_max_sync(g.mask, m);
+  } else {
+    const int ws = __reduce_add_sync(0xffffffffu, s);
+    const int wm = __reduce_max_sync(0xffffffffu, m);
+    if (threadIdx.x == 0) {
+      tmp[0] = 0;
+      tmp[1] = 0;
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&tmp[0], ws);
+      atomicMax(&tmp[1], wm);
+    }
+    __syncthreads();
+    sum = tmp[0];
+    mx = tmp[1];
+    __syncthreads();
+  }
+}
+
+// Lengths of pair p (lists 2p, 2p+1; an odd trailing list has an empty
+// partner). A list is [lst, lend) with its sentinel at lend.
+__device__ __forceinline__ void pair_lens(const int* lst, const int* lend, int nl, int p, int& la, int& lb) {
+  la = lend[2 * p] - lst[2 * p];
+  lb = 2 * p + 1 < nl ? lend[2 * p + 1] - lst[2 * p + 1] : 0;
+}
+
+// ---------------------------------------------------------------------------
+// Strategy S1: one thread merges one whole pair sequentially (Fig. 2's
+// merge loop) -- no search, no scan; used when a round has many short pairs.
+// ---------------------------------------------------------------------------
+template <bool FIRST, bool VALS>
+__device__ __forceinline__ int seq_merge(const int* sc, const double* sv, int pa, int pb, int qa, int qb, double sa,
+                                         double sb, int* dc, double* dv, int out) {
+  int ca = sc[pa], cb = sc[pb];
+  const int o0 = out;
+  while ((ca & cb) != INT_MAX) {  // both exhausted iff both heads are the sentinel
+    const bool ta = ca <= cb;
+    const bool tbb = cb <= ca;
+    dc[out] = min(ca, cb);
+    if (VALS) {
+      double x = -0.0, y = -0.0;
+      if (ta) x = FIRST ? __dmul_rn(sa, sv[qa]) : sv[pa];
+      if (tbb) y = FIRST ? __dmul_rn(sb, sv[qb]) : sv[pb];
+      dv[out] = __dadd_rn(x, y);  // "vals with duplicate cols are combined"
+    }
+    ++out;
+    pa += ta;
+    pb += tbb;
+    if (FIRST) {
+      qa += ta;
+      qb += tbb;
+    }
+    if (ta) ca = sc[pa];
+    if (tbb) cb = sc[pb];
+  }
+  dc[out] = INT_MAX;
+  return out - o0;
+}
+
+template <int G, bool FIRST, bool VALS>
+__device__ __forceinline__ int round_seq(const Group<G>& g, const RowBufs& rb, const int* sc, const double* sv,
+                                         const int* lst, const int* lln, int nl, int* dc, double* dv, int* dst_st,
+                                         int* dst_ln, const double* aval) {
+  const int npairs = (nl + 1) >> 1;
+  int run = 0;
+  for (int qb0 = 0; qb0 < npairs; qb0 += G) {
+    const int q = qb0 + g.rank;
+    int la = 0, lb = 0;
+    if (q < npairs) pair_lens(lst, lln, nl, q, la, lb);
+    int tot;
+    const int pre = group_excl_scan<G>(g, la + lb, tot, rb.scan_tmp);
+    if (q < npairs) {
+      const int ac = lst[2 * q];
+      const int bc = 2 * q + 1 < nl ? lst[2 * q + 1] : ac + la;  // empty partner: a's sentinel
+      int av = 0, bv = 0;
+      double sa = 1.0, sb = 1.0;
+      if (FIRST && VALS) {
+        av = rb.vb[2 * q];
+        bv = 2 * q + 1 < nl ? rb.vb[2 * q + 1] : av;
+        sa = aval[2 * q];
+        sb = 2 * q + 1 < nl ? aval[2 * q + 1] : 0.0;
+      }
+      const int pos = run + pre + q;  // upper-bound layout: pair q gets la + lb + 1 slots
+      const int n = seq_merge<FIRST, VALS>(sc, sv, ac, bc, av, bv, sa, sb, dc, dv, pos);
+      dst_st[q] = pos;
+      dst_ln[q] = pos + n;
+    }
+    run += tot;
+  }
+  g.sync();
+  return run;
+}
+
+// ---------------------------------------------------------------------------
+// Strategy S2: chunks of VT merged positions (never straddling a pair), one
+// merge-path split per chunk, two chunks per thread interleaved, outputs
+// compacted over the whole round by a group scan.
 // ---------------------------------------------------------------------------
 template <int G, int VT>
-__device__ __forceinline__ int build_chunks(const Group<G>& g, const int* so, int nl, int npairs, int* cst,
-                                            int* cpair, int* scan_tmp) {
+__device__ __forceinline__ void build_chunks(const Group<G>& g, const int* lst, const int* lln, int nl, int npairs,
+                                             int* cst, int* cpair, int* scan_tmp) {
   int run = 0;
   for (int pb = 0; pb < npairs; pb += G) {
     const int p = pb + g.rank;
     int c = 0;
     if (p < npairs) {
-      const int len = so[min(2 * p + 2, nl)] - so[2 * p];
-      c = (len + VT - 1) / VT;
+      int la, lb;
+      pair_lens(lst, lln, nl, p, la, lb);
+      c = (la + lb + VT - 1) / VT;
     }
     int tot;
     const int ex = group_excl_scan<G>(g, c, tot, scan_tmp);
@@ -121,13 +235,7 @@ __device__ __forceinline__ int build_chunks(const Group<G>& g, const int* so, in
   }
   if (g.rank == 0) cst[npairs] = run;
   g.sync();
-  return run;
 }
-
-// Buffer layout: every list is followed by one INT_MAX sentinel column, so a
-// merge cursor needs no bounds check (an exhausted list reads INT_MAX). In the
-// contiguous rounds list l starts at physical index off[l] + l (one sentinel
-// slot per preceding list); round 1 uses the staged positions cb[l] / vb[l].
 
 // Merge state of one chunk: columns at sc[pa] / sc[pb] (physical cursors),
 // values at sv[qa] / sv[qb]; merged position d of the next element, end dend.
@@ -137,9 +245,8 @@ struct Chunk {
 };
 
 template <int VT, bool FIRST, bool VALS>
-__device__ __forceinline__ void chunk_setup(Chunk& c, int t, int T, const int* sc, const int* so, int nl,
-                                            const int* cst, const int* cpair, const int* cb, const int* vb,
-                                            const double* aval) {
+__device__ __forceinline__ void chunk_setup(Chunk& c, int t, int T, const int* sc, const int* lst, const int* lln,
+                                            int nl, const RowBufs& rb, const double* aval) {
   c.cnt = 0;
   c.pair_first = -1;
   c.pair = 0;
@@ -149,26 +256,18 @@ __device__ __forceinline__ void chunk_setup(Chunk& c, int t, int T, const int* s
   c.ca = c.cb = INT_MAX;
   c.sa = c.sb = 1.0;
   if (t >= T) return;
-  const int p = cpair[t];
-  const int k = t - cst[p];
-  const int s0 = so[2 * p];
-  const int s1 = so[min(2 * p + 1, nl)];
-  const int s2 = so[min(2 * p + 2, nl)];
-  const int la = s1 - s0, lb = s2 - s1;
-  int ac, bc, av = 0, bv = 0;
-  if (FIRST) {
-    ac = cb[2 * p];
-    if (VALS) av = vb[2 * p];
-    if (2 * p + 1 < nl) {
-      bc = cb[2 * p + 1];
-      if (VALS) bv = vb[2 * p + 1];
-    } else {
-      bc = ac + la;  // empty partner: a's sentinel
-      bv = av;
-    }
-  } else {
-    ac = av = s0 + 2 * p;
-    bc = bv = (2 * p + 1 < nl) ? s1 + 2 * p + 1 : ac + la;
+  const int p = rb.cpair[t];
+  const int k = t - rb.cst[p];
+  int la, lb;
+  pair_lens(lst, lln, nl, p, la, lb);
+  const int ac = lst[2 * p];
+  const int bc = 2 * p + 1 < nl ? lst[2 * p + 1] : ac + la;
+  int av = ac, bv = bc;
+  if (FIRST && VALS) {
+    av = rb.vb[2 * p];
+    bv = 2 * p + 1 < nl ? rb.vb[2 * p + 1] : av;
+    c.sa = aval[2 * p];
+    c.sb = 2 * p + 1 < nl ? aval[2 * p + 1] : 0.0;
   }
   c.pair = p;
   c.d = k * VT;
@@ -178,10 +277,6 @@ __device__ __forceinline__ void chunk_setup(Chunk& c, int t, int T, const int* s
   if (i > 0 && j < lb && sc[ac + i - 1] == sc[bc + j]) {
     ++j;  // b[j] duplicates a[i-1]: summed by the chunk to the left
     ++c.d;
-  }
-  if (FIRST && VALS) {
-    c.sa = aval[2 * p];
-    c.sb = (2 * p + 1 < nl) ? aval[2 * p + 1] : 0.0;
   }
   c.pa = ac + i;
   c.pb = bc + j;
@@ -195,7 +290,7 @@ __device__ __forceinline__ void chunk_setup(Chunk& c, int t, int T, const int* s
 // One branch-free merge step: emits min(ca, cb); on equal columns the two
 // values are summed ("vals with duplicate cols are combined into one val").
 // The value of a list not taken is -0.0, the exact additive identity, so the
-// emitted value is bitwise x, y or x + y.
+// emitted value is bitwise x, y or x + y. Only consumed heads are reloaded.
 template <bool FIRST, bool VALS>
 __device__ __forceinline__ void chunk_step(Chunk& c, const int* sc, const double* sv, int& ocol, double& oval) {
   const bool act = c.d < c.dend;
@@ -220,26 +315,22 @@ __device__ __forceinline__ void chunk_step(Chunk& c, const int* sc, const double
   }
   c.d += (int)ta + (int)tbb;
   c.cnt += act;
-  c.ca = sc[c.pa];
-  c.cb = sc[c.pb];
+  if (ta) c.ca = sc[c.pa];
+  if (tbb) c.cb = sc[c.pb];
 }
 
-// One merge round over `nl` >= 2 lists of src (offsets `so`, nl + 1 entries).
-// Writes ceil(nl/2) lists (each followed by its sentinel) to dst with offsets
-// `dof`. Returns total outputs. Each thread merges two chunks (t and t + G)
-// interleaved for ILP.
 template <int G, int VT, bool FIRST, bool VALS>
-__device__ __forceinline__ int merge_round(const Group<G>& g, const RowBufs& rb, const int* sc, const double* sv,
-                                           const int* so, int nl, int* dc, double* dv, int* dof,
-                                           const double* aval) {
+__device__ __forceinline__ int round_chunked(const Group<G>& g, const RowBufs& rb, const int* sc, const double* sv,
+                                             const int* lst, const int* lln, int nl, int T, int* dc, double* dv,
+                                             int* dst_st, int* dst_ln, const double* aval) {
   const int npairs = (nl + 1) >> 1;
-  const int T = build_chunks<G, VT>(g, so, nl, npairs, rb.cst, rb.cpair, rb.scan_tmp);
+  build_chunks<G, VT>(g, lst, lln, nl, npairs, rb.cst, rb.cpair, rb.scan_tmp);
   int out_base = 0;
   for (int tb = 0; tb < T; tb += 2 * G) {
     Chunk c0, c1;
     const int t0 = tb + g.rank, t1 = tb + G + g.rank;
-    chunk_setup<VT, FIRST, VALS>(c0, t0, T, sc, so, nl, rb.cst, rb.cpair, rb.cb, rb.vb, aval);
-    chunk_setup<VT, FIRST, VALS>(c1, t1, T, sc, so, nl, rb.cst, rb.cpair, rb.cb, rb.vb, aval);
+    chunk_setup<VT, FIRST, VALS>(c0, t0, T, sc, lst, lln, nl, rb, aval);
+    chunk_setup<VT, FIRST, VALS>(c1, t1, T, sc, lst, lln, nl, rb, aval);
     int ocol0[VT], ocol1[VT];
     double oval0[VT], oval1[VT];
 #pragma unroll
@@ -265,34 +356,79 @@ __device__ __forceinline__ int merge_round(const Group<G>& g, const RowBufs& rb,
         if (VALS) dv[base1 + v] = oval1[v];
       }
     }
-    // the last chunk of a pair writes the pair's sentinel
-    if (t0 < T && t0 + 1 == rb.cst[c0.pair + 1]) dc[base0 + c0.cnt] = INT_MAX;
-    if (t1 < T && t1 + 1 == rb.cst[c1.pair + 1]) dc[base1 + c1.cnt] = INT_MAX;
+    // the last chunk of a pair writes the pair's sentinel and end
+    if (t0 < T && t0 + 1 == rb.cst[c0.pair + 1]) {
+      dc[base0 + c0.cnt] = INT_MAX;
+      dst_ln[c0.pair] = base0 + c0.cnt;
+    }
+    if (t1 < T && t1 + 1 == rb.cst[c1.pair + 1]) {
+      dc[base1 + c1.cnt] = INT_MAX;
+      dst_ln[c1.pair] = base1 + c1.cnt;
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int pf = h ? c1.pair_first : c0.pair_first;
-      if (pf >= 0) {  // this pair's (and preceding empty pairs') dst offset
+      if (pf >= 0) {  // this pair's start; empty pairs just before it
         const int vb = h ? vbase1 : vbase0;
         int q = pf;
         const int k0 = rb.cst[q];
-        dof[q] = vb;
+        dst_st[q] = vb + q;
         while (q > 0 && rb.cst[q - 1] == k0) {
-          dof[--q] = vb;
+          --q;
+          dst_st[q] = dst_ln[q] = vb + q;
           dc[vb + q] = INT_MAX;  // sentinel of the empty pair q
         }
       }
     }
     out_base += (total & 0xffff) + (total >> 16);
   }
-  if (g.rank == 0) {  // trailing empty pairs (sentinels too) and the end offset
-    for (int q = npairs; q >= 0; --q) {
-      if (q < npairs && rb.cst[q] != T) break;
-      dof[q] = out_base;
-      if (q < npairs) dc[out_base + q] = INT_MAX;
+  if (g.rank == 0) {  // trailing empty pairs
+    for (int q = npairs - 1; q >= 0 && rb.cst[q] == T; --q) {
+      dst_st[q] = dst_ln[q] = out_base + q;
+      dc[out_base + q] = INT_MAX;
     }
   }
   g.sync();
   return out_base;
+}
+
+// One BRMerge round (Alg. 1 lines 22-34): lists (0,1),(2,3),... of src merged
+// into dst, an odd trailing list copied. Picks S1 or S2 by estimated cost.
+template <int G, int VT, bool FIRST, bool VALS>
+__device__ __forceinline__ int merge_round(const Group<G>& g, const RowBufs& rb, const int* sc, const double* sv,
+                                           const int* lst, const int* lln, int nl, int* dc, double* dv,
+                                           int* dst_st, int* dst_ln, const double* aval, int strategy,
+                                           unsigned long long* acc) {
+  const int npairs = (nl + 1) >> 1;
+  int csum = 0, lmax = 0;
+  {
+    int cs = 0, lm = 0;
+    for (int pb = 0; pb < npairs; pb += G) {
+      const int p = pb + g.rank;
+      if (p < npairs) {
+        int la, lb;
+        pair_lens(lst, lln, nl, p, la, lb);
+        cs += (la + lb + VT - 1) / VT;
+        lm = max(lm, la + lb);
+      }
+    }
+    group_sum_max<G>(g, cs, lm, csum, lmax, rb.scan_tmp);
+  }
+  // latency model (cycles): a sequential step ~ kSeqStep, a chunk pass ~ kChunkIter
+  const int seq_cost = lmax * (VALS ? 120 : 90) * ((npairs + G - 1) / G);
+  const int chunk_cost = 1500 + ((csum + 2 * G - 1) / (2 * G)) * (VALS ? 3000 : 2400);
+  const bool seq = strategy == 1 || (strategy == 0 && seq_cost <= chunk_cost);
+  const long long t0 = acc ? clock64() : 0;
+  int r;
+  if (seq)
+    r = round_seq<G, FIRST, VALS>(g, rb, sc, sv, lst, lln, nl, dc, dv, dst_st, dst_ln, aval);
+  else
+    r = round_chunked<G, VT, FIRST, VALS>(g, rb, sc, sv, lst, lln, nl, csum, dc, dv, dst_st, dst_ln, aval);
+  if (acc) {
+    acc[seq ? kProfSeq : kProfChunk] += clock64() - t0;
+    acc[seq ? kProfSeqRounds : kProfChunkRounds] += 1;
+  }
+  return r;
 }
 
 // BRMerge of output row `row` (n_prod P) by group g.
@@ -301,7 +437,8 @@ __device__ __forceinline__ int merge_round(const Group<G>& g, const RowBufs& rb,
 template <int G, int VT, bool VALS, int OUT, bool SMEM>
 __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t bnnz,
                                             int64_t row, int P, const RowOut& o, const RowBufs& rb,
-                                            unsigned& phase) {
+                                            unsigned& phase, unsigned long long* acc) {
+  const long long tp0 = acc ? clock64() : 0;
   const int64_t a0 = A.rpt[row];
   const int nl = static_cast<int>(A.rpt[row + 1] - a0);
   const double* aval = VALS ? A.val + a0 : nullptr;
@@ -310,8 +447,8 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
   const bool tma = SMEM && P + 7 * nl <= rb.capc && (!VALS || P + 2 * nl <= rb.capv) &&
                    ((reinterpret_cast<uintptr_t>(B.col) | (VALS ? reinterpret_cast<uintptr_t>(B.val) : 0)) & 15) == 0;
   if (tma) fence_proxy_async();  // order the previous row's generic accesses before async writes
-  // list offsets (exclusive scan of the selected B row lengths) and, for TMA,
-  // the padded window layout; each lane stages its own lists
+  // multiplying phase (Alg. 1 lines 10-15): list l = B row k_l; each lane
+  // computes its lists' lengths and staging positions and issues their copies
   int run = 0, runc = 0, runv = 0;
   for (int lbase = 0; lbase < nl; lbase += G) {
     const int l = lbase + g.rank;
@@ -336,10 +473,10 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
     int pex = 0, ptot = 0;
     if (tma) pex = group_excl_scan<G>(g, wc | (wv << 16), ptot, rb.scan_tmp);
     if (l < nl) {
-      rb.offA[l] = run + ex;
       if (tma) {
         const int pc = runc + (pex & 0xffff), pv = runv + (pex >> 16);
-        rb.cb[l] = pc + static_cast<int>(s - wsc);
+        rb.lstA[l] = pc + static_cast<int>(s - wsc);
+        rb.llnA[l] = pc + static_cast<int>(s - wsc) + len;
         if (VALS) rb.vb[l] = pv + static_cast<int>(s - wsv);
         if (len > 0) {
           // one bulk copy per array if the window stays inside B's arrays,
@@ -351,7 +488,7 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
           if (bulk_c)
             tma_bulk_g2s(rb.colA + pc, B.col + wsc, wc * 4u, rb.mbar);
           else
-            for (int e = 0; e < len; ++e) cp_async_4(rb.colA + rb.cb[l] + e, B.col + s + e);
+            for (int e = 0; e < len; ++e) cp_async_4(rb.colA + pc + (s - wsc) + e, B.col + s + e);
           if (VALS) {
             if (bulk_v)
               tma_bulk_g2s(rb.valA + pv, B.val + wsv, wv * 8u, rb.mbar);
@@ -360,7 +497,8 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
           }
         }
       } else {
-        rb.cb[l] = run + ex + l;  // contiguous lists, one sentinel slot each
+        rb.lstA[l] = run + ex + l;  // contiguous lists, one sentinel slot each
+        rb.llnA[l] = run + ex + l + len;
         if (VALS) rb.vb[l] = run + ex + l;
       }
     }
@@ -370,7 +508,6 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
       runv += ptot >> 16;
     }
   }
-  if (g.rank == 0) rb.offA[nl] = run;
   g.sync();
   if (tma) {
     if (g.rank == 0) mbar_arrive(rb.mbar);
@@ -378,10 +515,9 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
     mbar_wait(rb.mbar, phase);
     phase ^= 1u;
   } else {
-    // multiplying phase without TMA: copy list l to cb[l] .. cb[l] + len
     const bool per_list_group = P * 2 >= nl * G;
     for (int l = per_list_group ? 0 : g.rank; l < nl; l += per_list_group ? 1 : G) {
-      const int dst = rb.cb[l], n = rb.offA[l + 1] - rb.offA[l];
+      const int dst = rb.lstA[l], n = rb.llnA[l] - rb.lstA[l];
       if (!n) continue;
       const int64_t s = B.rpt[A.col[a0 + l]];
       for (int e = per_list_group ? g.rank : 0; e < n; e += per_list_group ? G : 1) {
@@ -397,50 +533,64 @@ __device__ __forceinline__ void process_row(const Group<G>& g, const CsrView& A,
     if (SMEM) cp_async_wait_all();
   }
   g.sync();
-  // sentinel after every gathered list
-  for (int l = g.rank; l < nl; l += G) rb.colA[rb.cb[l] + rb.offA[l + 1] - rb.offA[l]] = INT_MAX;
+  for (int l = g.rank; l < nl; l += G) rb.colA[rb.llnA[l]] = INT_MAX;  // sentinels
   g.sync();
+  if (acc) acc[kProfStage] += clock64() - tp0;
+  // accumulating phase (Alg. 1 lines 21-35)
   int* sc = rb.colA;
   double* sv = rb.valA;
-  int* so = rb.offA;
+  int* lst = rb.lstA;
+  int* lln = rb.llnA;
   int* dc = rb.colB;
   double* dv = rb.valB;
-  int* dof = rb.offB;
+  int* dst_st = rb.lstB;
+  int* dst_ln = rb.llnB;
   int n_out = P;
   if (nl >= 2) {
     int cur = nl;
-    n_out = merge_round<G, VT, true, VALS>(g, rb, sc, sv, so, cur, dc, dv, dof, aval);
+    n_out = merge_round<G, VT, true, VALS>(g, rb, sc, sv, lst, lln, cur, dc, dv, dst_st, dst_ln, aval, o.strategy,
+                                           acc);
     cur = (cur + 1) >> 1;
     { int* t = sc; sc = dc; dc = t; }
     { double* t = sv; sv = dv; dv = t; }
-    { int* t = so; so = dof; dof = t; }
+    { int* t = lst; lst = dst_st; dst_st = t; }
+    { int* t = lln; lln = dst_ln; dst_ln = t; }
     while (cur > 1) {
-      n_out = merge_round<G, VT, false, VALS>(g, rb, sc, sv, so, cur, dc, dv, dof, nullptr);
+      n_out = merge_round<G, VT, false, VALS>(g, rb, sc, sv, lst, lln, cur, dc, dv, dst_st, dst_ln, nullptr,
+                                              o.strategy, acc);
       cur = (cur + 1) >> 1;
       { int* t = sc; sc = dc; dc = t; }
       { double* t = sv; sv = dv; dv = t; }
-      { int* t = so; so = dof; dof = t; }
+      { int* t = lst; lst = dst_st; dst_st = t; }
+      { int* t = lln; lln = dst_ln; dst_ln = t; }
     }
+    n_out = lln[0] - lst[0];  // S1 rounds return the upper bound, the list length is exact
   }
-  // Alg. 1 line 36: store the result row
+  // Alg. 1 line 36: store the result row (list 0 of the last round)
+  const long long ts0 = acc ? clock64() : 0;
   if (OUT != OUT_SYMBOLIC) {
     const int64_t dst = o.base[row];
+    const int c0 = lst[0];
     if (nl == 1) {  // single list: the scaled B row is the result
       const double s0 = VALS ? aval[0] : 0.0;
-      const int c0 = rb.cb[0], v0 = VALS ? rb.vb[0] : 0;
+      const int v0 = VALS ? rb.vb[0] : 0;
       for (int e = g.rank; e < n_out; e += G) {
         o.col[dst + e] = sc[c0 + e];
         if (VALS) o.val[dst + e] = __dmul_rn(s0, sv[v0 + e]);
       }
     } else {
       for (int e = g.rank; e < n_out; e += G) {
-        o.col[dst + e] = sc[e];
-        if (VALS) o.val[dst + e] = sv[e];
+        o.col[dst + e] = sc[c0 + e];
+        if (VALS) o.val[dst + e] = sv[c0 + e];
       }
     }
   }
   if (OUT != OUT_C && g.rank == 0) o.row_size[row] = n_out;
   g.sync();
+  if (acc) {
+    acc[kProfStore] += clock64() - ts0;
+    acc[kProfRows] += 1;
+  }
 }
 
 }  // namespace brm

@@ -305,10 +305,11 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, int64_t 
   rb.colB = reinterpret_cast<int*>(base + L.colB);
   rb.valA = VALS ? reinterpret_cast<double*>(base + L.valA) : nullptr;
   rb.valB = VALS ? reinterpret_cast<double*>(base + L.valB) : nullptr;
-  rb.cb = reinterpret_cast<int*>(base + L.cb);
+  rb.lstA = reinterpret_cast<int*>(base + L.lstA);
+  rb.llnA = reinterpret_cast<int*>(base + L.llnA);
+  rb.lstB = reinterpret_cast<int*>(base + L.lstB);
+  rb.llnB = reinterpret_cast<int*>(base + L.llnB);
   rb.vb = VALS ? reinterpret_cast<int*>(base + L.vb) : nullptr;
-  rb.offA = reinterpret_cast<int*>(base + L.offA);
-  rb.offB = reinterpret_cast<int*>(base + L.offB);
   rb.cst = reinterpret_cast<int*>(base + L.cst);
   rb.cpair = reinterpret_cast<int*>(base + L.cpair);
   rb.mbar = reinterpret_cast<unsigned long long*>(base + L.mbar);
@@ -319,11 +320,15 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, int64_t 
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   unsigned phase = 0;
+  unsigned long long acc_reg[kProfSlots] = {};
+  unsigned long long* acc = (o.prof && g.rank == 0) ? acc_reg : nullptr;
   for (int64_t r = (int64_t)blockIdx.x * GPC + threadIdx.x / G; r < nrows; r += (int64_t)gridDim.x * GPC) {
     const int64_t row = rows[r];
     const int P = static_cast<int>(nprod_off[row + 1] - nprod_off[row]);
-    process_row<G, VT, VALS, OUT, true>(g, A, B, bnnz, row, P, o, rb, phase);
+    process_row<G, VT, VALS, OUT, true>(g, A, B, bnnz, row, P, o, rb, phase, acc);
   }
+  if (acc)
+    for (int i = 0; i < kProfSlots; ++i) atomicAdd(o.prof + i, acc_reg[i]);
 }
 
 // Global tier: one CTA per row, ping-pong buffers in a per-row slice of a
@@ -350,17 +355,22 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
   rb.valB = VALS ? reinterpret_cast<double*>(take((P + nl / 2 + 2) * 8)) : nullptr;
   rb.colA = reinterpret_cast<int*>(take((P + nl + 1) * 4));
   rb.colB = reinterpret_cast<int*>(take((P + nl / 2 + 2) * 4));
-  rb.cb = reinterpret_cast<int*>(take((int64_t)nl * 4));
+  rb.lstA = reinterpret_cast<int*>(take((int64_t)(nl + 1) * 4));
+  rb.llnA = reinterpret_cast<int*>(take((int64_t)(nl + 1) * 4));
+  rb.lstB = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
+  rb.llnB = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
   rb.vb = VALS ? reinterpret_cast<int*>(take((int64_t)nl * 4)) : nullptr;
-  rb.offA = reinterpret_cast<int*>(take((int64_t)(nl + 1) * 4));
-  rb.offB = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
   rb.cst = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
   rb.cpair = reinterpret_cast<int*>(take((P / kGlobalVT + nl / 2 + 2) * 4));
   rb.mbar = nullptr;
   rb.scan_tmp = scan_tmp;
   rb.capc = rb.capv = 0;
   unsigned phase = 0;
-  process_row<kGlobalG, kGlobalVT, VALS, OUT, false>(g, A, B, bnnz, row, (int)P, o, rb, phase);
+  unsigned long long acc_reg[kProfSlots] = {};
+  unsigned long long* acc = (o.prof && g.rank == 0) ? acc_reg : nullptr;
+  process_row<kGlobalG, kGlobalVT, VALS, OUT, false>(g, A, B, bnnz, row, (int)P, o, rb, phase, acc);
+  if (acc)
+    for (int i = 0; i < kProfSlots; ++i) atomicAdd(o.prof + i, acc_reg[i]);
 }
 
 // Step 6 of Fig. 4a: copy each row of C_bar (at its n_prod offset) to C.
@@ -507,7 +517,7 @@ cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& 
 
 int64_t global_row_bytes(int64_t nprod, int64_t nl, bool vals) {
   auto a = [](int64_t b) { return ((b + 15) & ~15ll) + 16; };
-  int64_t s = a((nprod + nl + 1) * 4) + a((nprod + nl / 2 + 2) * 4) + a(nl * 4) + a((nl + 1) * 4) + a((nl / 2 + 2) * 4) * 2 +
+  int64_t s = a((nprod + nl + 1) * 4) + a((nprod + nl / 2 + 2) * 4) + a((nl + 1) * 4) * 2 + a((nl / 2 + 2) * 4) * 3 +
               a((nprod / kGlobalVT + nl / 2 + 2) * 4);
   if (vals) s += a((nprod + nl + 1) * 8) + a((nprod + nl / 2 + 2) * 8) + a(nl * 4);
   return s;
