@@ -1,0 +1,93 @@
+"""Multi-GPU plumbing of the BRMerge SpGEMM.
+
+Output rows of Eq. (2) are independent, so the path shards by
+rows: rank g computes the row block [bounds[g], bounds[g+1]) where the bounds
+balance n_prod across ranks (§III.D; reading R7, computed on the
+device by brm_partition_rows). B is broadcast from one rank, each rank runs
+the whole path on its block through the C ABI, and C's row_ptr offsets (and
+optionally the C row blocks themselves) are assembled with all-gathers.
+
+This module only moves and re-indexes tensors with torch.distributed (NCCL on
+GPUs, gloo in the CPU tests); no step of the SpGEMM itself runs here.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from .binding import TorchCsr
+
+
+def broadcast_csr(X: Optional[TorchCsr], src: int = 0, device=None, group=None) -> TorchCsr:
+    """Broadcast a CSR from rank `src` (X given there, None elsewhere).
+    Shape (rows, cols, nnz) travels first as one int64 triple."""
+    rank = dist.get_rank(group)
+    dev = torch.device(device) if device is not None else (X.device if X is not None else torch.device("cpu"))
+    hdr = torch.zeros(3, dtype=torch.int64, device=dev)
+    if rank == src:
+        hdr[0], hdr[1], hdr[2] = X.rows, X.cols, X.nnz
+    dist.broadcast(hdr, src, group=group)
+    rows, cols, nnz = (int(v) for v in hdr.tolist())
+    if rank == src:
+        out = X
+    else:
+        out = TorchCsr(rows, cols, torch.empty(rows + 1, dtype=torch.int64, device=dev),
+                       torch.empty(nnz, dtype=torch.int32, device=dev),
+                       torch.empty(nnz, dtype=torch.float64, device=dev))
+    for t in (out.rpt, out.col, out.val):
+        if t.numel():
+            dist.broadcast(t, src, group=group)
+    return out
+
+
+def row_block(A: TorchCsr, r0: int, r1: int) -> TorchCsr:
+    """Rows [r0, r1) of A as a CSR of its own (views of col/val, rpt rebased)."""
+    if not (0 <= r0 <= r1 <= A.rows):
+        raise ValueError(f"bad row block [{r0}, {r1}) of {A.rows} rows")
+    a0, a1 = int(A.rpt[r0]), int(A.rpt[r1])
+    return TorchCsr(r1 - r0, A.cols, (A.rpt[r0:r1 + 1] - a0).contiguous(), A.col[a0:a1], A.val[a0:a1])
+
+
+def block_nnz(local_nnz: int, device, group=None) -> torch.Tensor:
+    """All-gather every rank's nnz(C block): int64[world]. The global row_ptr
+    of rank g's block starts at sum(counts[:g])."""
+    world = dist.get_world_size(group)
+    cnt = torch.tensor([local_nnz], dtype=torch.int64, device=device)
+    allc = torch.empty(world, dtype=torch.int64, device=device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(allc, cnt, group=group)
+    else:
+        dist.all_gather(list(allc.split(1)), cnt, group=group)
+    return allc
+
+
+def _all_gather_varlen(x: torch.Tensor, counts: list[int], group=None) -> torch.Tensor:
+    """Concatenate every rank's 1-D tensor (rank order); counts[g] = len on g."""
+    world = len(counts)
+    m = max(counts) if counts else 0
+    buf = torch.zeros(m, dtype=x.dtype, device=x.device)
+    buf[: x.numel()] = x
+    parts = [torch.empty(m, dtype=x.dtype, device=x.device) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([p[:c] for p, c in zip(parts, counts)])
+
+
+def assemble_csr(C_blk: TorchCsr, total_rows: int, group=None) -> TorchCsr:
+    """Whole C on every rank from the row blocks (rank order = row order).
+    rpt of block g is shifted by the nnz of blocks < g."""
+    dev = C_blk.device
+    world = dist.get_world_size(group)
+    nnz = block_nnz(C_blk.nnz, dev, group).tolist()
+    rows = block_nnz(C_blk.rows, dev, group).tolist()
+    if sum(rows) != total_rows:
+        raise ValueError(f"row blocks cover {sum(rows)} rows, expected {total_rows}")
+    col = _all_gather_varlen(C_blk.col, nnz, group)
+    val = _all_gather_varlen(C_blk.val, nnz, group)
+    rp = _all_gather_varlen(C_blk.rpt[1:], rows, group)  # drop each block's leading 0
+    shift = torch.repeat_interleave(
+        torch.tensor([sum(nnz[:g]) for g in range(world)], dtype=torch.int64, device=dev),
+        torch.tensor(rows, dtype=torch.int64, device=dev))
+    rpt = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), rp + shift])
+    return TorchCsr(total_rows, C_blk.cols, rpt, col, val)
