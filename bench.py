@@ -86,13 +86,14 @@ def stencil27_box(nx, ny, nz, seed):
 
 
 # tier table mirrored from csrc/brm_internal.cuh (checked by tests/test_bench_host.py)
-TIER_CAP = [0, 64, 256, 768, 2560, 7168]
-TIER_LCAP = [0, 32, 128, 64, 512, 1024]
+TIER_CAP = [0, 8, 32, 256, 768, 3072, 8192]
+TIER_LCAP = [0, 8, 32, 64, 64, 512, 1024]
+NUM_BINS = 8
 
 
 def tier_of(nprod: np.ndarray, nl: np.ndarray) -> np.ndarray:
-    t = np.full(nprod.shape, 6, np.int64)
-    for b in range(5, 0, -1):
+    t = np.full(nprod.shape, NUM_BINS - 1, np.int64)
+    for b in range(NUM_BINS - 2, 0, -1):
         t = np.where((nprod <= TIER_CAP[b]) & (nl <= TIER_LCAP[b]), b, t)
     return np.where(nprod == 0, 0, t)
 
@@ -227,6 +228,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2206_06611_b200 import Context, TorchCsr
+    from paper_2206_06611_b200 import dist as bdist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -237,14 +239,10 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     A, B, desc = build_workload(args.config, world)
     ctx = Context(dev)
-    Bd = TorchCsr.from_csr(B) if rank == 0 or world == 1 else None
     if world > 1:  # B broadcast with NCCL from rank 0 (setup)
-        if rank != 0:
-            Bd = TorchCsr(B.rows, B.cols, torch.empty(B.rows + 1, dtype=torch.int64, device=dev),
-                          torch.empty(B.nnz, dtype=torch.int32, device=dev),
-                          torch.empty(B.nnz, dtype=torch.float64, device=dev))
-        for t in (Bd.rpt, Bd.col, Bd.val):
-            dist.broadcast(t, 0)
+        Bd = bdist.broadcast_csr(TorchCsr.from_csr(B) if rank == 0 else None, src=0, device=dev)
+    else:
+        Bd = TorchCsr.from_csr(B)
     Afull = TorchCsr.from_csr(A)
     # row partition by balanced n_prod (§III.D), computed by the library's kernels
     nprod_dev = ctx.brm_row_nprod(Afull, Bd)
@@ -263,10 +261,8 @@ def main():
 
     def step():
         C = ctx.spgemm(Ad, Bd, args.mode)
-        if world > 1:
-            cnt = torch.tensor([C.nnz], dtype=torch.int64, device=dev)
-            allc = torch.empty(world, dtype=torch.int64, device=dev)
-            dist.all_gather_into_tensor(allc, cnt)
+        if world > 1:  # row_ptr offsets of the C row blocks (all-gather)
+            bdist.block_nnz(C.nnz, dev)
         return C
 
     for _ in range(args.warmup):
@@ -274,7 +270,7 @@ def main():
     torch.cuda.synchronize(dev)
     ctx.set_timing(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    bin_ms = np.zeros(7)
+    bin_ms = np.zeros(NUM_BINS)
     sym_ms = num_ms = pre_ms = scan_ms = cmp_ms = 0.0
     launches = 0
     if world > 1:
@@ -384,7 +380,7 @@ def main():
                        "parallelism": f"dp{world} rows by balanced n_prod"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
-                         "kernel": f"k_tier bin {dom} (numeric merge)" if dom < 6 else "k_global_tier",
+                         "kernel": f"k_tier bin {dom} (numeric merge)" if dom < NUM_BINS - 1 else "k_global_tier",
                          "kernel_ms": dom_ms, "algorithmic_bytes": dom_bytes, "peak_kind": peak_kind},
             "hbm_step": {"achieved_gbs": step_gbs, "frac": step_gbs / peak, "algorithmic_bytes": int(b_all.item())},
             "phases_ms": {"nprod_scan_bin": pre_ms / args.steps, "symbolic": sym_ms / args.steps,

@@ -79,9 +79,10 @@ typedef struct {
 } brm_csr_t;
 
 /* Number of row bins (tiers) the binning pass sorts rows into; see DESIGN.md
- * "Kernels": 0 = empty rows (n_prod == 0), 1..5 = shared-memory tiers of
- * growing capacity (sub-warp, warp, block x3), 6 = global-memory tier.     */
-#define BRM_NUM_BINS 7
+ * "Kernels": 0 = empty rows (n_prod == 0), 1-2 = register tiers (8-lane
+ * group, warp), 3-6 = shared-memory ping-pong tiers (warp, warp, 128 and
+ * 256 threads), 7 = global-memory ping-pong tier.                         */
+#define BRM_NUM_BINS 8
 
 typedef struct {
   int64_t rows;                     /* A.rows                                  */
@@ -99,9 +100,6 @@ typedef struct {
   float ms_compact;                 /* UPPER: C_bar -> C compaction            */
   float ms_bin_numeric[BRM_NUM_BINS]; /* numeric merge per tier              */
   int64_t launches;                 /* kernels launched by the last structure+fill */
-  uint64_t prof[8];                 /* env BRM_PROFILE=1: device cycles summed over row
-                                       groups [stage, seq rounds, chunked rounds, store,
-                                       #seq rounds, #chunked rounds, #rows, -]       */
 } brm_stats_t;
 
 typedef struct brm_context brm_context_t;

@@ -17,7 +17,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "libbrmerge.so"
 
 BRM_UPPER = 0
 BRM_PRECISE = 1
-BRM_NUM_BINS = 7
+BRM_NUM_BINS = 8
 MODES = {"upper": BRM_UPPER, "precise": BRM_PRECISE, BRM_UPPER: BRM_UPPER, BRM_PRECISE: BRM_PRECISE}
 
 STATUS = {0: "BRM_OK", 1: "BRM_ERR_INVALID", 2: "BRM_ERR_DIM", 3: "BRM_ERR_CUDA", 4: "BRM_ERR_OOM",
@@ -45,8 +45,7 @@ class brm_stats_t(ctypes.Structure):
                 ("ms_numeric", ctypes.c_float), ("ms_rowsize_scan", ctypes.c_float),
                 ("ms_compact", ctypes.c_float),
                 ("ms_bin_numeric", ctypes.c_float * BRM_NUM_BINS),
-                ("launches", ctypes.c_int64),
-                ("prof", ctypes.c_uint64 * 8)]
+                ("launches", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         d = {}

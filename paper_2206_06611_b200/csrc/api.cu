@@ -50,8 +50,6 @@ struct brm_context {
   cudaEvent_t ev[32] = {};
   unsigned ev_mask = 0;  // events recorded since the last structure call
   int64_t launches = 0;  // kernels launched since the last structure call
-  int strategy = 0;      // env BRM_STRATEGY (experiments): 0 auto, 1 one thread per pair, 2 chunked
-  bool profile = false;  // env BRM_PROFILE=1: device cycle counters in brm_stats_t.prof
 };
 
 namespace {
@@ -109,10 +107,10 @@ cudaError_t ensure(brm_context_t* ctx, DevBuf& b, size_t bytes) {
 cudaError_t ensure_host(HostBuf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (b.cap >= bytes) return cudaSuccess;
+  const size_t want = std::max(bytes, b.cap * 3 / 2);
   if (b.p) cudaFreeHost(b.p);
   b.p = nullptr;
   b.cap = 0;
-  const size_t want = std::max(bytes, b.cap * 3 / 2);
   cudaError_t e = cudaMallocHost(&b.p, want);
   if (e != cudaSuccess) {
     b.p = nullptr;
@@ -140,7 +138,6 @@ brm_status_t check_csr(brm_context_t* ctx, const brm_csr_t* X, const char* name)
 
 // Small device block: summary + scan counters + bin cursor + nnz total.
 struct SmallDev {
-  unsigned long long prof[kProfSlots];
   DevSummary summary;
   unsigned long long cursor[BRM_NUM_BINS];
   unsigned int counter[4];
@@ -191,8 +188,7 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
   for (int b = 1; b < kBinGlobal; ++b) {
     if (!ctx->bin_rows[b]) continue;
     if (per_bin) ev_record(ctx, kEvBin + 2 * b);
-    CK(launch_tier(b, out, ctx->A, ctx->B, ctx->bnnz, static_cast<const int64_t*>(ctx->nprod_off.p),
-                   bins + ctx->bin_start[b], ctx->bin_rows[b], o, ctx->stream),
+    CK(launch_tier(b, out, ctx->A, ctx->B, bins + ctx->bin_start[b], ctx->bin_rows[b], o, ctx->stream),
        "k_tier");
     ++ctx->launches;
     if (per_bin) ev_record(ctx, kEvBin + 2 * b + 1);
@@ -249,7 +245,7 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
   for (size_t c = 0; c + 1 < cuts.size(); ++c) {
     const int64_t b0 = cuts[c], n = cuts[c + 1] - b0;
     if (n <= 0) continue;
-    CK(launch_global_tier(out, ctx->A, ctx->B, ctx->bnnz, hrows + b0, n,
+    CK(launch_global_tier(out, ctx->A, ctx->B, hrows + b0, n,
                           static_cast<const int64_t*>(ctx->gws_off.p) + 2 * b0,
                           static_cast<unsigned char*>(ctx->gws.p), o, ctx->stream),
        "k_global_tier");
@@ -329,8 +325,6 @@ brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
   // UPPER: Steps 3-4 (C_bar by n_prod offsets, numeric merge);
   // PRECISE: Step 3 (symbolic merge)
   RowOut o{};
-  o.strategy = ctx->strategy;
-  o.prof = ctx->profile ? sd->prof : nullptr;
   int out;
   if (mode == BRM_UPPER) {
     const int64_t np = ctx->sum.nprod_total;
@@ -357,7 +351,6 @@ brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
   *c_nnz = ctx->nnz_c;
   ctx->stats.nnz_c = ctx->nnz_c;
   ctx->planned = true;
-  if (ctx->profile) memcpy(ctx->stats.prof, static_cast<SmallDev*>(ctx->h_small.p)->prof, sizeof(ctx->stats.prof));
   return BRM_OK;
 }
 
@@ -380,8 +373,6 @@ brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
   } else {
     // Step 5 of Fig. 4b: numeric merge straight into C
     RowOut o{};
-    o.strategy = ctx->strategy;
-    o.prof = ctx->profile ? small_dev(ctx)->prof : nullptr;
     o.base = C->rpt;
     o.col = C->col;
     o.val = C->val;
@@ -420,8 +411,6 @@ brm_status_t brm_create(brm_context_t** out, int device, void* stream) {
   brm_context_t* ctx = new brm_context_t;
   ctx->device = device;
   ctx->stream = static_cast<cudaStream_t>(stream);
-  if (const char* e = getenv("BRM_STRATEGY")) ctx->strategy = atoi(e);
-  if (const char* e = getenv("BRM_PROFILE")) ctx->profile = atoi(e) != 0;
   DeviceGuard g(device);
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   *out = ctx;
@@ -466,11 +455,6 @@ brm_status_t brm_get_stats(const brm_context_t* ctx, brm_stats_t* out) {
   if (!ctx || !out) return BRM_ERR_INVALID;
   *out = ctx->stats;
   out->launches = ctx->launches;
-  if (ctx->profile && ctx->small.p) {
-    DeviceGuard g(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
-    cudaMemcpy(out->prof, ctx->small.p, sizeof(out->prof), cudaMemcpyDeviceToHost);
-  }
   if (ctx->timing && ctx->ev_mask) {
     DeviceGuard g(ctx->device);
     for (int i = 31; i >= 0; --i)  // wait for everything recorded

@@ -16,39 +16,44 @@ struct CsrView {
 };
 
 // ---------------------------------------------------------------------------
-// Row tiers. A row with n_prod > 0 goes to the first tier t (1..5) with
-// n_prod <= cap and num_list (= nnz(A_i*)) <= lcap, else to the global tier 6.
-// Tier t's kernel runs `gpc` groups of `g` threads per CTA; each group owns one
-// row at a time with both ping-pong buffers in shared memory.
+// Row tiers. A row with n_prod = P > 0 and num_list = nl
+// (= nnz(A_i*)) goes to the first tier t whose (cap, lcap) admits it:
+//   1  register BRMerge, 8-lane group   P <= 8,    nl <= 8
+//   2  register BRMerge, one warp       P <= 32,   nl <= 32
+//   3  chunked BRMerge, one warp        P <= 256,  nl <= 64   (smem ping-pong)
+//   4  chunked BRMerge, one warp        P <= 768,  nl <= 64   (smem ping-pong)
+//   5  chunked BRMerge, 128 threads     P <= 3072, nl <= 512  (smem ping-pong)
+//   6  chunked BRMerge, 256 threads     P <= 8192, nl <= 1024 (smem ping-pong)
+//   7  chunked BRMerge, 512 threads, ping-pong buffers in a global workspace
 // ---------------------------------------------------------------------------
 constexpr int kBinEmpty = 0;
-constexpr int kBinGlobal = 6;
-static_assert(BRM_NUM_BINS == 7, "tier table below assumes 7 bins");
+constexpr int kBinGlobal = 7;
+static_assert(BRM_NUM_BINS == 8, "tier table below assumes 8 bins");
 
 struct TierBounds {
   int cap[BRM_NUM_BINS];
   int lcap[BRM_NUM_BINS];
 };
 
-// (G threads per row group, VT merged positions per thread per chunk,
-//  CAP elements, LCAP lists, GPC groups per CTA)
-#define BRM_TIER1 8, 8, 64, 32, 16
-#define BRM_TIER2 32, 8, 256, 128, 4
-#define BRM_TIER3 32, 8, 768, 64, 1
-#define BRM_TIER4 128, 8, 2560, 512, 1
-#define BRM_TIER5 256, 8, 7168, 1024, 1
+// (G threads per row group, CAP elements, LCAP lists, GPC groups per CTA)
+#define BRM_TIER1 8, 8, 8, 32
+#define BRM_TIER2 32, 32, 32, 8
+#define BRM_TIER3 32, 256, 64, 4
+#define BRM_TIER4 32, 768, 64, 2
+#define BRM_TIER5 128, 3072, 512, 1
+#define BRM_TIER6 256, 8192, 1024, 1
 constexpr int kGlobalG = 512;
-constexpr int kGlobalVT = 8;
 
 __host__ __device__ inline TierBounds tier_bounds() {
   TierBounds t{};
   t.cap[0] = 0;    t.lcap[0] = 0;
-  t.cap[1] = 64;   t.lcap[1] = 32;
-  t.cap[2] = 256;  t.lcap[2] = 128;
-  t.cap[3] = 768;  t.lcap[3] = 64;
-  t.cap[4] = 2560; t.lcap[4] = 512;
-  t.cap[5] = 7168; t.lcap[5] = 1024;
-  t.cap[6] = INT_MAX; t.lcap[6] = INT_MAX;
+  t.cap[1] = 8;    t.lcap[1] = 8;
+  t.cap[2] = 32;   t.lcap[2] = 32;
+  t.cap[3] = 256;  t.lcap[3] = 64;
+  t.cap[4] = 768;  t.lcap[4] = 64;
+  t.cap[5] = 3072; t.lcap[5] = 512;
+  t.cap[6] = 8192; t.lcap[6] = 1024;
+  t.cap[7] = INT_MAX; t.lcap[7] = INT_MAX;
   return t;
 }
 
@@ -60,37 +65,7 @@ __host__ __device__ inline int tier_of(int64_t nprod, int64_t nl, const TierBoun
   return kBinGlobal;
 }
 
-// Shared-memory layout of one row group (bytes, 16-aligned pieces). colA /
-// valA hold the gathered lists in 16-byte TMA windows, so they get padding
-// (capc / capv elements); rows whose windows do not fit use cp.async.
-struct GroupLayout {
-  int valA, valB, colA, colB, lstA, llnA, lstB, llnB, vb, cst, cpair, mbar, scan, bytes, capc, capv;
-};
-
 __host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
-
-template <int G, int VT, int CAP, int LCAP, bool VALS>
-__host__ __device__ constexpr GroupLayout group_layout() {
-  GroupLayout L{};
-  L.capc = CAP + (LCAP > CAP / 4 ? LCAP : CAP / 4);
-  L.capv = CAP + (LCAP > CAP / 8 ? LCAP : CAP / 8);
-  int o = 0;
-  L.valA = o;   o += VALS ? align16(L.capv * 8 + 16) : 0;
-  L.valB = o;   o += VALS ? align16((CAP + LCAP / 2 + 2) * 8) : 0;
-  L.colA = o;   o += align16(L.capc * 4 + 16);
-  L.colB = o;   o += align16((CAP + LCAP / 2 + 2) * 4);
-  L.lstA = o;   o += align16((LCAP + 1) * 4);
-  L.llnA = o;   o += align16((LCAP + 1) * 4);
-  L.lstB = o;   o += align16((LCAP / 2 + 2) * 4);
-  L.llnB = o;   o += align16((LCAP / 2 + 2) * 4);
-  L.vb = o;     o += VALS ? align16(LCAP * 4) : 0;
-  L.cst = o;    o += align16((LCAP / 2 + 2) * 4);
-  L.cpair = o;  o += align16((CAP / VT + LCAP / 2 + 2) * 4);
-  L.mbar = o;   o += 16;
-  L.scan = o;   o += G > 32 ? align16((G / 32 + 1) * 4) : 0;
-  L.bytes = o;
-  return L;
-}
 
 // ---------------------------------------------------------------------------
 // Thread groups: G <= 32 is a sub-warp (shuffles of width G), G > 32 is the
@@ -100,6 +75,7 @@ template <int G>
 struct Group {
   int rank;
   unsigned mask;
+  int base;  // first lane of the group inside its warp (G <= 32)
   __device__ __forceinline__ void sync() const {
     if constexpr (G <= 32)
       __syncwarp(mask);
@@ -112,10 +88,13 @@ template <int G>
 __device__ __forceinline__ Group<G> make_group() {
   Group<G> g;
   g.rank = threadIdx.x % G;
-  if constexpr (G >= 32)
+  if constexpr (G >= 32) {
     g.mask = 0xffffffffu;
-  else
-    g.mask = ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1));
+    g.base = 0;
+  } else {
+    g.base = (threadIdx.x & 31) & ~(G - 1);
+    g.mask = ((1u << G) - 1u) << g.base;
+  }
   return g;
 }
 
@@ -160,21 +139,6 @@ __device__ __forceinline__ int group_excl_scan(const Group<G>& g, int v, int& to
     __syncthreads();
     return res;
   }
-}
-
-// Largest l in [0, n) with off[l * stride] <= e (n >= 1). With empty lists
-// sharing a start, this is the non-empty list that contains position e.
-template <int STRIDE>
-__device__ __forceinline__ int upper_search(const int* off, int n, int e) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (off[mid * STRIDE] <= e)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  return lo;
 }
 
 // Merge path: number of a-elements among the first `diag` merged elements,

@@ -4,10 +4,10 @@
 //                    (§II.B.2) fused with a single-pass decoupled look-back
 //                    exclusive scan (CUB-free), the per-bin histogram and max.
 //   k_bin_scatter    row binning by n_prod / list count into tiers.
-//   k_tier<...>      BRMerge of one row per thread group, ping-pong buffers in
-//                    shared memory (tiers 1-5: sub-warp, warp, block x3).
-//   k_global_tier    BRMerge of the heaviest rows, ping-pong buffers in a
-//                    global-memory workspace, one CTA per row.
+//   k_tier<...>      BRMerge of one row per thread group: register tiers 1-2,
+//                    shared-memory ping-pong tiers 3-6 (warp, warp, 128, 256).
+//   k_global_tier    BRMerge of the heaviest rows (tier 7), ping-pong buffers in
+//                    a global-memory workspace, one 512-thread CTA per row.
 //   k_scan_i64       exclusive scan (row_size -> rpt; generic).
 //   k_compact        Step 6 of Fig. 4a: C_bar -> C copy (BRMerge-Upper).
 //   k_partition      §III.D row partition by balanced n_prod (multi-GPU).
@@ -291,86 +291,76 @@ __global__ void k_heavy_info(CsrView A, const int64_t* __restrict__ nprod_off,
 }
 
 // Shared-memory tiers: GPC groups of G threads per CTA, one row per group at a
-// time, both ping-pong buffers in the group's slice of dynamic shared memory.
-template <int G, int VT, int CAP, int LCAP, int GPC, bool VALS, int OUT>
-__global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, int64_t bnnz,
-                                                 const int64_t* __restrict__ nprod_off,
-                                                 const int32_t* __restrict__ rows, int64_t nrows, RowOut o) {
+// time, the group's buffers in its slice of dynamic shared memory. CAP <= 32:
+// register tier (reg_row), else chunk tier (chunk_row).
+template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT>
+__global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const int32_t* __restrict__ rows,
+                                                 int64_t nrows, RowOut o) {
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr GroupLayout L = group_layout<G, VT, CAP, LCAP, VALS>();
   const Group<G> g = make_group<G>();
-  unsigned char* base = smem + (threadIdx.x / G) * L.bytes;
-  RowBufs rb;
-  rb.colA = reinterpret_cast<int*>(base + L.colA);
-  rb.colB = reinterpret_cast<int*>(base + L.colB);
-  rb.valA = VALS ? reinterpret_cast<double*>(base + L.valA) : nullptr;
-  rb.valB = VALS ? reinterpret_cast<double*>(base + L.valB) : nullptr;
-  rb.lstA = reinterpret_cast<int*>(base + L.lstA);
-  rb.llnA = reinterpret_cast<int*>(base + L.llnA);
-  rb.lstB = reinterpret_cast<int*>(base + L.lstB);
-  rb.llnB = reinterpret_cast<int*>(base + L.llnB);
-  rb.vb = VALS ? reinterpret_cast<int*>(base + L.vb) : nullptr;
-  rb.cst = reinterpret_cast<int*>(base + L.cst);
-  rb.cpair = reinterpret_cast<int*>(base + L.cpair);
-  rb.mbar = reinterpret_cast<unsigned long long*>(base + L.mbar);
-  rb.scan_tmp = reinterpret_cast<int*>(base + L.scan);
-  rb.capc = L.capc;
-  rb.capv = L.capv;
-  if (g.rank == 0) mbar_init(rb.mbar, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
-  unsigned phase = 0;
-  unsigned long long acc_reg[kProfSlots] = {};
-  unsigned long long* acc = (o.prof && g.rank == 0) ? acc_reg : nullptr;
-  for (int64_t r = (int64_t)blockIdx.x * GPC + threadIdx.x / G; r < nrows; r += (int64_t)gridDim.x * GPC) {
-    const int64_t row = rows[r];
-    const int P = static_cast<int>(nprod_off[row + 1] - nprod_off[row]);
-    process_row<G, VT, VALS, OUT, true>(g, A, B, bnnz, row, P, o, rb, phase, acc);
+  const int gid = threadIdx.x / G;
+  if constexpr (CAP <= 32) {
+    constexpr int bytes = reg_group_bytes<G, VALS>();
+    unsigned char* base = smem + gid * bytes;
+    RegBufs rb;
+    rb.col = reinterpret_cast<int*>(base);
+    rb.lid = reinterpret_cast<int*>(base + align16(G * 4));
+    rb.owner = reinterpret_cast<int*>(base + 2 * align16(G * 4));
+    rb.val = VALS ? reinterpret_cast<double*>(base + 3 * align16(G * 4)) : nullptr;
+    for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
+      reg_row<G, VALS, OUT>(g, A, B, rows[r], o, rb);
+  } else {
+    constexpr int bytes = chunk_group_bytes<G, CAP, LCAP, VALS>();
+    unsigned char* p = smem + gid * bytes;
+    auto take = [&](int n) {
+      unsigned char* q = p;
+      p += align16(n);
+      return q;
+    };
+    ChunkBufs cb;
+    cb.col0 = reinterpret_cast<int*>(take((CAP + 2) * 4));
+    cb.col1 = reinterpret_cast<int*>(take((CAP + 2) * 4));
+    cb.val0 = VALS ? reinterpret_cast<double*>(take((CAP + 2) * 8)) : nullptr;
+    cb.val1 = VALS ? reinterpret_cast<double*>(take((CAP + 2) * 8)) : nullptr;
+    cb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
+    cb.off1 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
+    cb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
+    cb.av = VALS ? reinterpret_cast<double*>(take(LCAP * 8)) : nullptr;
+    cb.scan_tmp = G > 32 ? reinterpret_cast<int*>(take((G / 32 + 2) * 4)) : nullptr;
+    for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
+      chunk_row<G, VALS, OUT>(g, A, B, rows[r], o, cb);
   }
-  if (acc)
-    for (int i = 0; i < kProfSlots; ++i) atomicAdd(o.prof + i, acc_reg[i]);
 }
 
 // Global tier: one CTA per row, ping-pong buffers in a per-row slice of a
 // global workspace at byte offset ws_off[2r] (host-batched; ws_off[2r+1] is
 // the row's n_prod).
 template <bool VALS, int OUT>
-__global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, int64_t bnnz,
-                                                         const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, const int32_t* __restrict__ rows,
                                                          const int64_t* __restrict__ ws_off,
                                                          unsigned char* __restrict__ ws, RowOut o) {
-  __shared__ int scan_tmp[kGlobalG / 32 + 1];
+  __shared__ int scan_tmp[kGlobalG / 32 + 2];
   const Group<kGlobalG> g = make_group<kGlobalG>();
   const int64_t row = rows[blockIdx.x];
   const int64_t P = ws_off[2 * blockIdx.x + 1];
-  const int nl = (int)(A.rpt[row + 1] - A.rpt[row]);
+  const int64_t nl = A.rpt[row + 1] - A.rpt[row];
   unsigned char* p = ws + ws_off[2 * blockIdx.x];
   auto take = [&](int64_t bytes) {
     unsigned char* q = p;
-    p += ((bytes + 15) & ~15ll) + 16;  // +16: merge reloads may touch one slot past a list
+    p += (bytes + 15) & ~15ll;
     return q;
   };
-  RowBufs rb;
-  rb.valA = VALS ? reinterpret_cast<double*>(take((P + nl + 1) * 8)) : nullptr;
-  rb.valB = VALS ? reinterpret_cast<double*>(take((P + nl / 2 + 2) * 8)) : nullptr;
-  rb.colA = reinterpret_cast<int*>(take((P + nl + 1) * 4));
-  rb.colB = reinterpret_cast<int*>(take((P + nl / 2 + 2) * 4));
-  rb.lstA = reinterpret_cast<int*>(take((int64_t)(nl + 1) * 4));
-  rb.llnA = reinterpret_cast<int*>(take((int64_t)(nl + 1) * 4));
-  rb.lstB = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
-  rb.llnB = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
-  rb.vb = VALS ? reinterpret_cast<int*>(take((int64_t)nl * 4)) : nullptr;
-  rb.cst = reinterpret_cast<int*>(take((int64_t)(nl / 2 + 2) * 4));
-  rb.cpair = reinterpret_cast<int*>(take((P / kGlobalVT + nl / 2 + 2) * 4));
-  rb.mbar = nullptr;
-  rb.scan_tmp = scan_tmp;
-  rb.capc = rb.capv = 0;
-  unsigned phase = 0;
-  unsigned long long acc_reg[kProfSlots] = {};
-  unsigned long long* acc = (o.prof && g.rank == 0) ? acc_reg : nullptr;
-  process_row<kGlobalG, kGlobalVT, VALS, OUT, false>(g, A, B, bnnz, row, (int)P, o, rb, phase, acc);
-  if (acc)
-    for (int i = 0; i < kProfSlots; ++i) atomicAdd(o.prof + i, acc_reg[i]);
+  ChunkBufs cb;
+  cb.col0 = reinterpret_cast<int*>(take((P + 2) * 4));
+  cb.col1 = reinterpret_cast<int*>(take((P + 2) * 4));
+  cb.val0 = VALS ? reinterpret_cast<double*>(take((P + 2) * 8)) : nullptr;
+  cb.val1 = VALS ? reinterpret_cast<double*>(take((P + 2) * 8)) : nullptr;
+  cb.off0 = reinterpret_cast<int*>(take((nl + 2) * 4));
+  cb.off1 = reinterpret_cast<int*>(take((nl + 2) * 4));
+  cb.bst = reinterpret_cast<int64_t*>(take(nl * 8));
+  cb.av = VALS ? reinterpret_cast<double*>(take(nl * 8)) : nullptr;
+  cb.scan_tmp = scan_tmp;
+  chunk_row<kGlobalG, VALS, OUT>(g, A, B, row, o, cb);
 }
 
 // Step 6 of Fig. 4a: copy each row of C_bar (at its n_prod offset) to C.
@@ -467,14 +457,14 @@ cudaError_t launch_heavy_info(const CsrView& A, const int64_t* nprod_off, const 
   return cudaGetLastError();
 }
 
-template <int G, int VT, int CAP, int LCAP, int GPC, bool VALS, int OUT>
-static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, int64_t bnnz, const int64_t* nprod_off,
-                                 const int32_t* rows, int64_t n, const RowOut& o, cudaStream_t st) {
+template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT>
+static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
+                                 cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  constexpr GroupLayout L = group_layout<G, VT, CAP, LCAP, VALS>();
-  constexpr int smem = L.bytes * GPC;
+  constexpr int per_group = CAP <= 32 ? reg_group_bytes<G, VALS>() : chunk_group_bytes<G, CAP, LCAP, VALS>();
+  constexpr int smem = per_group * GPC;
   static_assert(smem <= 232448, "tier shared memory exceeds 227 KB");
-  auto kern = k_tier<G, VT, CAP, LCAP, GPC, VALS, OUT>;
+  auto kern = k_tier<G, CAP, LCAP, GPC, VALS, OUT>;
   // one process drives one device, so per-instantiation caching is safe
   static int per_sm = 0;
   if (!per_sm) {
@@ -487,50 +477,48 @@ static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, int64_t bnn
   const int64_t want = (n + GPC - 1) / GPC;
   const int64_t cap = (int64_t)per_sm * num_sms();
   const unsigned grid = (unsigned)(want < cap ? want : cap);
-  kern<<<grid, G * GPC, smem, st>>>(A, B, bnnz, nprod_off, rows, n, o);
+  kern<<<grid, G * GPC, smem, st>>>(A, B, rows, n, o);
   return cudaGetLastError();
 }
 
 template <bool VALS, int OUT>
-static cudaError_t launch_tier_dispatch(int bin, const CsrView& A, const CsrView& B, int64_t bnnz,
-                                        const int64_t* nprod_off, const int32_t* rows, int64_t n, const RowOut& o,
-                                        cudaStream_t st) {
+static cudaError_t launch_tier_dispatch(int bin, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
+                                        const RowOut& o, cudaStream_t st) {
   switch (bin) {
-    case 1: return launch_tier_t<BRM_TIER1, VALS, OUT>(A, B, bnnz, nprod_off, rows, n, o, st);
-    case 2: return launch_tier_t<BRM_TIER2, VALS, OUT>(A, B, bnnz, nprod_off, rows, n, o, st);
-    case 3: return launch_tier_t<BRM_TIER3, VALS, OUT>(A, B, bnnz, nprod_off, rows, n, o, st);
-    case 4: return launch_tier_t<BRM_TIER4, VALS, OUT>(A, B, bnnz, nprod_off, rows, n, o, st);
-    case 5: return launch_tier_t<BRM_TIER5, VALS, OUT>(A, B, bnnz, nprod_off, rows, n, o, st);
+    case 1: return launch_tier_t<BRM_TIER1, VALS, OUT>(A, B, rows, n, o, st);
+    case 2: return launch_tier_t<BRM_TIER2, VALS, OUT>(A, B, rows, n, o, st);
+    case 3: return launch_tier_t<BRM_TIER3, VALS, OUT>(A, B, rows, n, o, st);
+    case 4: return launch_tier_t<BRM_TIER4, VALS, OUT>(A, B, rows, n, o, st);
+    case 5: return launch_tier_t<BRM_TIER5, VALS, OUT>(A, B, rows, n, o, st);
+    case 6: return launch_tier_t<BRM_TIER6, VALS, OUT>(A, B, rows, n, o, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& B, int64_t bnnz,
-                        const int64_t* nprod_off, const int32_t* rows, int64_t n, const RowOut& o, cudaStream_t st) {
+cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
+                        const RowOut& o, cudaStream_t st) {
   switch (out_kind) {
-    case OUT_SYMBOLIC: return launch_tier_dispatch<false, OUT_SYMBOLIC>(bin, A, B, bnnz, nprod_off, rows, n, o, st);
-    case OUT_CBAR: return launch_tier_dispatch<true, OUT_CBAR>(bin, A, B, bnnz, nprod_off, rows, n, o, st);
-    case OUT_C: return launch_tier_dispatch<true, OUT_C>(bin, A, B, bnnz, nprod_off, rows, n, o, st);
+    case OUT_SYMBOLIC: return launch_tier_dispatch<false, OUT_SYMBOLIC>(bin, A, B, rows, n, o, st);
+    case OUT_CBAR: return launch_tier_dispatch<true, OUT_CBAR>(bin, A, B, rows, n, o, st);
+    case OUT_C: return launch_tier_dispatch<true, OUT_C>(bin, A, B, rows, n, o, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 int64_t global_row_bytes(int64_t nprod, int64_t nl, bool vals) {
-  auto a = [](int64_t b) { return ((b + 15) & ~15ll) + 16; };
-  int64_t s = a((nprod + nl + 1) * 4) + a((nprod + nl / 2 + 2) * 4) + a((nl + 1) * 4) * 2 + a((nl / 2 + 2) * 4) * 3 +
-              a((nprod / kGlobalVT + nl / 2 + 2) * 4);
-  if (vals) s += a((nprod + nl + 1) * 8) + a((nprod + nl / 2 + 2) * 8) + a(nl * 4);
+  auto a = [](int64_t b) { return (b + 15) & ~15ll; };
+  int64_t s = a((nprod + 2) * 4) * 2 + a((nl + 2) * 4) * 2 + a(nl * 8);
+  if (vals) s += a((nprod + 2) * 8) * 2 + a(nl * 8);
   return s;
 }
 
-cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B, int64_t bnnz, const int32_t* rows,
-                               int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o,
-                               cudaStream_t st) {
+cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
+                               const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   switch (out_kind) {
-    case OUT_SYMBOLIC: k_global_tier<false, OUT_SYMBOLIC><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, bnnz, rows, ws_off, ws, o); break;
-    case OUT_CBAR: k_global_tier<true, OUT_CBAR><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, bnnz, rows, ws_off, ws, o); break;
-    case OUT_C: k_global_tier<true, OUT_C><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, bnnz, rows, ws_off, ws, o); break;
+    case OUT_SYMBOLIC: k_global_tier<false, OUT_SYMBOLIC><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, rows, ws_off, ws, o); break;
+    case OUT_CBAR: k_global_tier<true, OUT_CBAR><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, rows, ws_off, ws, o); break;
+    case OUT_C: k_global_tier<true, OUT_C><<<(unsigned)n, kGlobalG, 0, st>>>(A, B, rows, ws_off, ws, o); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

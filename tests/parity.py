@@ -22,20 +22,21 @@ def rows_of(rpt, col, val, rows):
 
 
 def compare(gpu, A: Csr, B: Csr, rows=None, tree_exact: bool = True, tol: float = 1e-12):
-    """gpu = (rpt, col, val) numpy arrays of the full GPU result.
+    """gpu = (rpt, col, val) numpy arrays of the GPU result (all rows, or
+    only `rows` in that order when rows is given).
 
     Checks (north_star): rpt and col bit-exact against Eq. (2) (Gustavson,
     structural zeros kept); |c - c_ref| <= tol * sum|a_ik b_kj| per entry;
     and, when tree_exact, values bit-identical to Algorithm 1's tree order.
     Returns a dict of diagnostics."""
     rpt, col, val = gpu
-    assert rpt.shape == (A.rows + 1,), rpt.shape
+    n = A.rows if rows is None else len(rows)
+    if rows is not None and rpt.shape == (A.rows + 1,) and A.rows != len(rows):
+        rpt, col, val = rows_of(rpt, col, val, rows)  # full result given: cut the rows
+    assert rpt.shape == (n + 1,), rpt.shape
     assert rpt[0] == 0 and np.all(np.diff(rpt) >= 0)
     assert col.shape == val.shape == (int(rpt[-1]),)
-    if rows is None:
-        g_rpt, g_col, g_val = rpt, col, val
-    else:
-        g_rpt, g_col, g_val = rows_of(rpt, col, val, rows)
+    g_rpt, g_col, g_val = rpt, col, val
     ref = oracle.spgemm_gustavson(A, B, rows=rows)
     np.testing.assert_array_equal(g_rpt, ref.rpt, err_msg="row pointers differ")
     np.testing.assert_array_equal(g_col, ref.col, err_msg="column indices differ")

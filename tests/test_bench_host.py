@@ -16,11 +16,11 @@ def test_tier_table_matches_kernels():
     src = (ROOT / "paper_2206_06611_b200" / "csrc" / "brm_internal.cuh").read_text()
     caps = {int(t): (int(c), int(l)) for t, c, l in
             re.findall(r"t\.cap\[(\d)\] = (\d+);\s+t\.lcap\[\d\] = (\d+);", src)}
-    for t in range(1, 6):
+    for t in range(1, bench.NUM_BINS - 1):
         assert caps[t] == (bench.TIER_CAP[t], bench.TIER_LCAP[t]), t
-    for t in range(1, 6):
-        m = re.search(rf"#define BRM_TIER{t} (\d+), (\d+), (\d+), (\d+), (\d+)", src)
-        assert int(m.group(3)) == bench.TIER_CAP[t] and int(m.group(4)) == bench.TIER_LCAP[t]
+        m = re.search(rf"#define BRM_TIER{t} (\d+), (\d+), (\d+), (\d+)", src)
+        assert int(m.group(2)) == bench.TIER_CAP[t] and int(m.group(3)) == bench.TIER_LCAP[t]
+    assert f"#define BRM_NUM_BINS {bench.NUM_BINS}" in (ROOT / "include" / "brmerge.h").read_text()
 
 
 def test_algorithmic_bytes_brute_force():
@@ -41,9 +41,9 @@ def test_algorithmic_bytes_brute_force():
 
 
 def test_tier_of_matches_bounds():
-    nprod = np.array([0, 1, 64, 65, 256, 257, 768, 769, 2560, 2561, 7168, 7169, 10])
-    nl = np.array([0, 1, 32, 1, 128, 1, 64, 1, 512, 1, 1024, 1, 33])
-    assert bench.tier_of(nprod, nl).tolist() == [0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 2]
+    nprod = np.array([0, 1, 8, 9, 32, 33, 256, 257, 768, 769, 3072, 3073, 8192, 8193, 10, 40, 40])
+    nl = np.array([0, 1, 8, 1, 32, 1, 64, 1, 64, 1, 512, 1, 1024, 1, 9, 65, 513])
+    assert bench.tier_of(nprod, nl).tolist() == [0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 2, 5, 6]
 
 
 def test_stencil_box_equals_cube():

@@ -77,12 +77,15 @@ def test_random_rectangular(ctx, oracle_mod, mode, seed):
 
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("list_len,specs", [
-    (1, [1, 2, 3, 5, 8, 31, 32, 33]),           # tier 1, tiny lists
-    (7, [1, 2, 9, 10]),                          # tier 1 edges (n_prod 63..70)
-    (16, [4, 15, 16, 17]),                       # tier 2 edges (256)
-    (27, [27, 30, 37, 38]),                      # tier 3 (729, 1024 edge)
-    (33, [100, 124, 125]),                       # tier 4 (4096 edge)
-    (64, [100, 111, 112, 113]),                  # tier 5 (7168 edge)
+    (1, [1, 2, 3, 5, 8]),                        # tier 1 (register, 8 lanes)
+    (2, [4, 5]),                                 # tier 1 edge P=8 / tier 2 P=10
+    (1, [9, 17, 31, 32]),                        # tier 2 (register, warp), nl up to 32
+    (4, [8, 9]),                                 # tier 2 edge P=32 / tier 3 P=36
+    (16, [15, 16, 17]),                          # tier 3 edge (256)
+    (4, [64, 65]),                               # tier 3 list cap 64 -> tier 5
+    (27, [27, 28, 29]),                          # tier 4 (stencil-like, 768 edge)
+    (33, [90, 93, 94]),                          # tier 5 (3072 edge)
+    (64, [100, 128, 129]),                       # tier 6 (8192 edge) -> global
     (100, [90, 300]),                            # global tier
     (3, [40, 129, 300, 600, 1500]),              # many short lists (list caps)
 ])
@@ -247,3 +250,68 @@ def test_stats_reported(ctx):
     assert s["nprod_total"] == 20000 * 64 and s["nnz_c"] > 0
     assert sum(s["bin_rows"]) == 20000
     assert s["ms_numeric"] > 0
+
+
+def _gather_rows(C, rows):
+    """Rows of a device CSR (TorchCsr) as a numpy (rpt, col, val) triple."""
+    import torch
+    r = torch.as_tensor(np.asarray(rows, np.int64), device=C.rpt.device)
+    s, e = C.rpt[r], C.rpt[r + 1]
+    lens = (e - s)
+    rpt = torch.zeros(r.numel() + 1, dtype=torch.int64, device=r.device)
+    rpt[1:] = torch.cumsum(lens, 0)
+    idx = torch.repeat_interleave(s - rpt[:-1], lens) + torch.arange(int(rpt[-1]), device=r.device)
+    return rpt.cpu().numpy(), C.col[idx].cpu().numpy(), C.val[idx].cpu().numpy()
+
+
+def _sample_rows(A, B, k=1500):
+    """Evenly strided rows plus the heaviest (largest n_prod) rows."""
+    import oracle
+    nprod = oracle.row_nprod(A, B)
+    strided = np.linspace(0, A.rows - 1, min(k, A.rows)).astype(np.int64)
+    heavy = np.argsort(nprod)[-64:]
+    return np.unique(np.concatenate([strided, heavy]))
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", ["stencil", "amg", "rmat", "uniform"])
+def test_workload_shapes_small(ctx, oracle_mod, mode, name):
+    """The paper-workload generators at sizes the oracle finishes in seconds
+    (several tiles of every tier they hit, ragged tails), every row."""
+    from inputs import aggregation_prolongator, laplace2d_5pt, rmat, stencil27
+    if name == "stencil":
+        A = B = stencil27(13, seed=2)
+    elif name == "amg":
+        A, B = laplace2d_5pt(96), aggregation_prolongator(96, seed=3)
+    elif name == "rmat":
+        A = B = rmat(11, 16, 0.57, 0.19, 0.19, 0.05, seed=4)
+    else:
+        A = B = uniform_random(20000, 20000, 16, seed=5)
+    compare(run(ctx, A, B, mode), A, B)
+
+
+FULL = ["uniform2k_k8", "stencil27_64", "uniform1m_k16", "amg_lap2048_agg2x2", "rmat20_ef16"]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_size_sampled(ctx, oracle_mod, name):
+    """BASELINE.json configs at full size, in the mode bench.py times
+    (PRECISE; UPPER too where C_bar fits), compared with the oracle on
+    sampled rows (strided + heaviest) and on global invariants."""
+    import torch
+    from inputs import workload
+    from paper_2206_06611_b200 import TorchCsr
+    A, B = workload(name)
+    rows = _sample_rows(A, B)
+    Ad, Bd = TorchCsr.from_csr(A), TorchCsr.from_csr(B)
+    modes = ["precise"] if name == "rmat20_ef16" else ["precise", "upper"]
+    for mode in modes:
+        C = ctx.spgemm(Ad, Bd, mode)
+        torch.cuda.synchronize()
+        rpt = C.rpt.cpu().numpy()
+        assert rpt[0] == 0 and np.all(np.diff(rpt) >= 0) and rpt[-1] == C.nnz
+        s = ctx.stats()
+        assert s["nnz_c"] == C.nnz
+        compare(_gather_rows(C, rows), A, B, rows=rows)
+        del C
+        torch.cuda.empty_cache()
