@@ -13,15 +13,16 @@
 //   ping-pong buffer.
 //
 // chunk_row (tiers 3-7): shared-memory (or global-workspace) ping-pong. The
-//   multiplying phase copies the B rows of A_i* into `src` as compact sorted
-//   lists, scaled by A_ik (one rounding per product, Alg. 1 line 12). Each
-//   round is ONE pass: the round's merged positions (the concatenation of all
-//   pairs) are split into G equal odd-length chunks; a thread locates its
-//   chunk's pair and merge-path split, merges it sequentially with a
-//   branch-free step (sum on equal columns) into `dst`, crossing into later
-//   pairs when one ends; a group scan of the per-thread output counts gives
-//   the compacted positions and the next round's list offsets, and each
-//   thread copies its outputs back to `src` compacted.
+//   multiplying phase copies the B rows of A_i* into the ping buffer as
+//   compact sorted lists (cp.async, coalesced); the scaling by A_ik is fused
+//   into the first merge round (one rounding per product, Alg. 1 line 12).
+//   Each round is ONE pass: the round's merged positions (the concatenation
+//   of all pairs) are split into G equal odd-length chunks; a thread locates
+//   its chunk's pair and merge-path split and merges it with a branch-free
+//   predicated step (sum on equal columns), crossing into later pairs when
+//   one ends, holding its outputs in registers; a group scan of the
+//   per-thread output counts gives each thread its compacted position in the
+//   pong buffer and the next round's list offsets; the buffers swap.
 #pragma once
 #include "brm_internal.cuh"
 
@@ -200,19 +201,75 @@ __device__ __forceinline__ void reg_row(const Group<G>& g, const CsrView& A, con
 // ===========================================================================
 // Chunk tiers
 // ===========================================================================
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// Predicated shared loads: one LDS under a predicate, never a branch.
+__device__ __forceinline__ void lds_if(bool p, unsigned addr, int& v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.b32 %0, [%1];\n\t}"
+               : "+r"(v)
+               : "r"(addr), "r"((unsigned)p));
+}
+__device__ __forceinline__ void lds_if(bool p, unsigned addr, double& v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.f64 %0, [%1];\n\t}"
+               : "+d"(v)
+               : "r"(addr), "r"((unsigned)p));
+}
+__device__ __forceinline__ void cp_async_4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Merge state of one thread's chunk inside pair p = lists (2p, 2p+1):
+// list a = [as, bs), list b = [bs, be) of src; heads ca/cb (INT_MAX once a
+// list is consumed), head values va/vb; sa/sb = A_ik of the two lists (round
+// 1 only: the scaling of Alg. 1 line 12 is fused into the first merge).
+struct Cursor {
+  int p, as, bs, be, ia, ib, lim, ca, cb;
+  double va, vb, sa, sb;
+};
+
+template <bool VALS, bool FIRST>
+__device__ __forceinline__ void cursor_load(Cursor& c, const int* sc, const double* sv, const double* av, int nl) {
+  c.ca = c.ia < c.bs ? sc[c.ia] : INT_MAX;
+  c.cb = c.ib < c.be ? sc[c.ib] : INT_MAX;
+  if (VALS) {
+    c.va = sv[c.ia];
+    c.vb = sv[c.ib];
+    if (FIRST) {
+      c.sa = av[2 * c.p];
+      c.sb = 2 * c.p + 1 < nl ? av[2 * c.p + 1] : 0.0;
+    }
+  }
+}
 
 // One BRMerge round (Alg. 1 lines 22-34) over compact lists in sc/sv with
-// offsets off[0..nl]; merged lists end up compact in sc/sv again with offsets
-// noff[0..npairs]. Returns the new element total.
-template <int G, bool VALS>
+// offsets off[0..nl]. The round's merged positions are split into G chunks of
+// VT (odd) positions; the merged lists are written COMPACT with offsets
+// noff[0..npairs]:
+//   NV > 0: into dc/dv (the other ping-pong buffer), each thread holding its
+//           <= NV outputs in registers until the group scan gives its base;
+//   NV = 0: (global tier, unbounded VT) into dc/dv at the chunk's own
+//           positions, then copied back compacted into sc/sv.
+// Returns the new element total.
+template <int G, int NV, bool VALS, bool FIRST, bool SMEM>
 __device__ __forceinline__ int chunk_round(const Group<G>& g, int* __restrict__ sc, double* __restrict__ sv,
                                            int* __restrict__ dc, double* __restrict__ dv, const int* off,
-                                           int* noff, int nl, int T, int* scan_tmp) {
+                                           int* noff, int nl, int T, int* scan_tmp, const double* av) {
   const int npairs = (nl + 1) >> 1;
-  const int VT = ((T + G - 1) / G) | 1;  // odd: conflict-free strided smem access
+  const int VT = ((T + G - 1) / G) | 1;  // odd: conflict-free strided shared-memory access
   const int g0 = min(g.rank * VT, T), g1 = min(g0 + VT, T);
-  int out = g0;
-  int pf = 0, pl = -1;  // pairs whose start this thread records: [pf, pl]
+  int cnt = 0;
+  int pf = 0, pl = -1;  // pairs whose output start this thread records: [pf, pl]
+  Cursor c;
+  c.ia = c.ib = c.lim = 0;
+  c.ca = c.cb = INT_MAX;
+  c.va = c.vb = c.sa = c.sb = 0.0;
+  c.p = 0;
+  c.as = c.bs = c.be = 0;
   if (g0 < g1) {
     int lo = 0, hi = npairs - 1;  // last pair starting at or before g0 (it is non-empty)
     while (lo < hi) {
@@ -222,78 +279,115 @@ __device__ __forceinline__ int chunk_round(const Group<G>& g, int* __restrict__ 
       else
         hi = mid - 1;
     }
-    int p = lo;
-    int as = off[2 * p];
-    int bs = off[min(2 * p + 1, nl)];
-    int be = off[min(2 * p + 2, nl)];
-    const int d = g0 - as;
+    c.p = lo;
+    c.as = off[2 * c.p];
+    c.bs = off[min(2 * c.p + 1, nl)];
+    c.be = off[min(2 * c.p + 2, nl)];
+    const int d = g0 - c.as;
     if (d == 0) {  // this chunk starts pair p (and any empty pairs just before it)
-      pf = p;
+      pf = c.p;
       while (pf > 0 && off[2 * (pf - 1)] == g0) --pf;
-      for (int q = pf; q <= p; ++q) noff[q] = 0;
-      pl = p;
+      for (int q = pf; q <= c.p; ++q) noff[q] = 0;
+      pl = c.p;
     }
-    const int i = merge_path(sc + as, bs - as, sc + bs, be - bs, d);
+    const int i = merge_path(sc + c.as, c.bs - c.as, sc + c.bs, c.be - c.bs, d);
     int j = d - i;
-    if (i > 0 && j < be - bs && sc[as + i - 1] == sc[bs + j]) ++j;  // b[j] was summed by the chunk on the left
-    int ia = as + i, ib = bs + j;
-    int lim = g1 + bs;  // merged position = ia + ib - bs
-    int ca = ia < bs ? sc[ia] : INT_MAX;
-    int cb = ib < be ? sc[ib] : INT_MAX;
-    double va = 0.0, vb = 0.0;
-    if (VALS) {
-      va = sv[ia];
-      vb = sv[ib];
+    if (i > 0 && j < c.be - c.bs && sc[c.as + i - 1] == sc[c.bs + j]) ++j;  // b[j] summed by the chunk on the left
+    c.ia = c.as + i;
+    c.ib = c.bs + j;
+    c.lim = g1 + c.bs;  // merged position = ia + ib - bs
+    cursor_load<VALS, FIRST>(c, sc, sv, av, nl);
+  }
+  const unsigned scb = SMEM ? smem_u32(sc) : 0u;
+  const unsigned svb = (SMEM && VALS) ? smem_u32(sv) : 0u;
+  constexpr int NR = NV > 0 ? NV : 1;
+  int ocol[NR];
+  double oval[NR];
+  auto step = [&](int v) {
+    const bool act = c.ia + c.ib < c.lim;
+    if (act && (c.ca & c.cb) == INT_MAX) {  // pair p consumed: enter the next non-empty pair
+      if (pl < 0) pf = c.p + 1;
+      do {
+        ++c.p;
+        noff[c.p] = cnt;
+        c.as = off[2 * c.p];
+        c.bs = off[min(2 * c.p + 1, nl)];
+        c.be = off[min(2 * c.p + 2, nl)];
+      } while (c.as == c.be);
+      pl = c.p;
+      c.ia = c.as;
+      c.ib = c.bs;
+      c.lim = g1 + c.bs;
+      cursor_load<VALS, FIRST>(c, sc, sv, av, nl);
     }
-    while (ia + ib < lim) {
-      if ((ca & cb) == INT_MAX) {  // both lists of pair p consumed: enter the next non-empty pair
-        if (pl < 0) pf = p + 1;
-        do {
-          ++p;
-          noff[p] = out - g0;
-          as = off[2 * p];
-          bs = off[min(2 * p + 1, nl)];
-          be = off[min(2 * p + 2, nl)];
-        } while (as == be);
-        pl = p;
-        ia = as;
-        ib = bs;
-        lim = g1 + bs;
-        ca = ia < bs ? sc[ia] : INT_MAX;
-        cb = ib < be ? sc[ib] : INT_MAX;
-        if (VALS) {
-          va = sv[ia];
-          vb = sv[ib];
-        }
-      }
-      const bool ta = ca <= cb, tb = cb <= ca;
-      dc[out] = min(ca, cb);
+    const bool ta = act && c.ca <= c.cb;
+    const bool tb = act && c.cb <= c.ca;
+    const int oc = min(c.ca, c.cb);
+    double ov = 0.0;
+    if (VALS) {
+      double x = FIRST ? __dmul_rn(c.sa, c.va) : c.va;  // the product, rounded once
+      double y = FIRST ? __dmul_rn(c.sb, c.vb) : c.vb;
+      x = ta ? x : -0.0;  // -0.0 is the exact additive identity
+      y = tb ? y : -0.0;
+      ov = __dadd_rn(x, y);  // "vals with duplicate cols are combined into one val"
+    }
+    if (NV > 0) {
+      ocol[v] = oc;
+      if (VALS) oval[v] = ov;
+    } else if (act) {
+      dc[g0 + cnt] = oc;
+      if (VALS) dv[g0 + cnt] = ov;
+    }
+    cnt += act;
+    c.ia += ta;
+    c.ib += tb;
+    if (SMEM) {
+      lds_if(ta, scb + 4u * c.ia, c.ca);
+      lds_if(tb, scb + 4u * c.ib, c.cb);
       if (VALS) {
-        const double x = ta ? va : -0.0;  // -0.0 is the exact additive identity
-        const double y = tb ? vb : -0.0;
-        dv[out] = __dadd_rn(x, y);
+        lds_if(ta, svb + 8u * c.ia, c.va);
+        lds_if(tb, svb + 8u * c.ib, c.vb);
       }
-      ++out;
-      ia += ta;
-      ib += tb;
+    } else {
       if (ta) {
-        ca = ia < bs ? sc[ia] : INT_MAX;
-        if (VALS) va = sv[ia];
+        c.ca = sc[c.ia];
+        if (VALS) c.va = sv[c.ia];
       }
       if (tb) {
-        cb = ib < be ? sc[ib] : INT_MAX;
-        if (VALS) vb = sv[ib];
+        c.cb = sc[c.ib];
+        if (VALS) c.vb = sv[c.ib];
       }
     }
+    c.ca = c.ia < c.bs ? c.ca : INT_MAX;
+    c.cb = c.ib < c.be ? c.cb : INT_MAX;
+  };
+  if constexpr (NV > 0) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (v >= VT) break;  // group-uniform
+      step(v);
+    }
+  } else {
+    for (int v = 0; v < VT; ++v) step(0);
   }
-  const int cnt = out - g0;
   int total;
   const int base = group_excl_scan<G>(g, cnt, total, scan_tmp);
-  g.sync();  // every merge has finished reading sc
   for (int q = pf; q <= pl; ++q) noff[q] += base;
-  for (int e = 0; e < cnt; ++e) {
-    sc[base + e] = dc[g0 + e];
-    if (VALS) sv[base + e] = dv[g0 + e];
+  if constexpr (NV > 0) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (v >= VT) break;
+      if (v < cnt) {
+        dc[base + v] = ocol[v];
+        if (VALS) dv[base + v] = oval[v];
+      }
+    }
+  } else {
+    g.sync();  // every merge has finished reading sc
+    for (int e = 0; e < cnt; ++e) {
+      sc[base + e] = dc[g0 + e];
+      if (VALS) sv[base + e] = dv[g0 + e];
+    }
   }
   if (g.rank == G - 1) {
     for (int q = npairs - 1; q >= 0 && off[2 * q] == T; --q) noff[q] = total;  // trailing empty pairs
@@ -303,14 +397,20 @@ __device__ __forceinline__ int chunk_round(const Group<G>& g, int* __restrict__ 
   return total;
 }
 
-template <int G, bool VALS, int OUT>
+// BRMerge of one output row by a group. NV > 0: buffers in shared memory,
+// rounds ping-pong between (col0, val0) and (col1, val1); NV = 0: buffers in
+// a global workspace, every round lands back in (col0, val0).
+template <int G, int NV, bool VALS, int OUT>
 __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
                                           const RowOut& o, const ChunkBufs& cb) {
+  constexpr bool SMEM = NV > 0;
   const int rank = g.rank;
   const int64_t a0 = A.rpt[row];
   const int nl = static_cast<int>(A.rpt[row + 1] - a0);
   int* sc = cb.col0;
   double* sv = cb.val0;
+  int* dc = cb.col1;
+  double* dv = cb.val1;
   int* off = cb.off0;
   int* noff = cb.off1;
   // multiplying phase (Alg. 1 lines 10-15): list offsets by a group scan ...
@@ -332,7 +432,8 @@ __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, c
   }
   if (rank == 0) off[nl] = T;
   g.sync();
-  // ... then the scaled B rows, S consecutive threads per list (S ~ mean list length)
+  // ... then the B rows themselves (unscaled; round 1 multiplies), S
+  // consecutive threads per list (S ~ mean list length), coalesced.
   {
     const int avg = (T + nl - 1) / nl;
     int ls = 0;
@@ -345,43 +446,43 @@ __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, c
       if (l < nl) {
         const int o0 = off[l], n = off[l + 1] - o0;
         const int64_t st = cb.bst[l];
-        const double a = VALS ? cb.av[l] : 0.0;
-        for (int e = e0; e < n; e += 2 * S) {
-          const int e1 = e + S;
-          const bool h1 = e1 < n;
-          const int c0 = __ldg(B.col + st + e);
-          const int c1 = h1 ? __ldg(B.col + st + e1) : 0;
-          double v0 = 0.0, v1 = 0.0;
-          if (VALS) {
-            v0 = __ldg(B.val + st + e);
-            if (h1) v1 = __ldg(B.val + st + e1);
-          }
-          sc[o0 + e] = c0;
-          if (VALS) sv[o0 + e] = __dmul_rn(a, v0);
-          if (h1) {
-            sc[o0 + e1] = c1;
-            if (VALS) sv[o0 + e1] = __dmul_rn(a, v1);
+        for (int e = e0; e < n; e += S) {
+          if (SMEM) {
+            cp_async_4(sc + o0 + e, B.col + st + e);
+            if (VALS) cp_async_8(sv + o0 + e, B.val + st + e);
+          } else {
+            sc[o0 + e] = __ldg(B.col + st + e);
+            if (VALS) sv[o0 + e] = __ldg(B.val + st + e);
           }
         }
       }
     }
+    if (SMEM) cp_async_wait_all();
   }
   g.sync();
   // accumulating phase (lines 21-35)
   int cur = nl;
+  bool first = true;
   while (cur > 1) {
-    T = chunk_round<G, VALS>(g, sc, sv, cb.col1, cb.val1, off, noff, cur, T, cb.scan_tmp);
+    if (first)
+      T = chunk_round<G, NV, VALS, true, SMEM>(g, sc, sv, dc, dv, off, noff, cur, T, cb.scan_tmp, cb.av);
+    else
+      T = chunk_round<G, NV, VALS, false, SMEM>(g, sc, sv, dc, dv, off, noff, cur, T, cb.scan_tmp, cb.av);
+    first = false;
     cur = (cur + 1) >> 1;
-    int* t = off;
-    off = noff;
-    noff = t;
+    { int* t = off; off = noff; noff = t; }
+    if (SMEM) {  // lines 33-34: swap the ping-pong buffers
+      { int* t = sc; sc = dc; dc = t; }
+      { double* t = sv; sv = dv; dv = t; }
+    }
   }
   // line 36: the result row is list 0 of src, [0, T)
   if (OUT != OUT_SYMBOLIC) {
     const int64_t ob = o.base[row];
+    const double s0 = (VALS && nl == 1) ? cb.av[0] : 1.0;  // a single list was never scaled
     for (int e = rank; e < T; e += G) {
       o.col[ob + e] = sc[e];
-      if (VALS) o.val[ob + e] = sv[e];
+      if (VALS) o.val[ob + e] = nl == 1 ? __dmul_rn(s0, sv[e]) : sv[e];
     }
   }
   if (OUT != OUT_C && rank == 0) o.row_size[row] = T;

@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
     cb.av = VALS ? reinterpret_cast<double*>(take(LCAP * 8)) : nullptr;
     cb.scan_tmp = G > 32 ? reinterpret_cast<int*>(take((G / 32 + 2) * 4)) : nullptr;
     for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
-      chunk_row<G, VALS, OUT>(g, A, B, rows[r], o, cb);
+      chunk_row<G, ((CAP + G - 1) / G) | 1, VALS, OUT>(g, A, B, rows[r], o, cb);
   }
 }
 
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
   cb.bst = reinterpret_cast<int64_t*>(take(nl * 8));
   cb.av = VALS ? reinterpret_cast<double*>(take(nl * 8)) : nullptr;
   cb.scan_tmp = scan_tmp;
-  chunk_row<kGlobalG, VALS, OUT>(g, A, B, row, o, cb);
+  chunk_row<kGlobalG, 0, VALS, OUT>(g, A, B, row, o, cb);
 }
 
 // Step 6 of Fig. 4a: copy each row of C_bar (at its n_prod offset) to C.
