@@ -65,9 +65,12 @@ struct ChunkBufs {
   int* scan_tmp;
 };
 
+// Buffers hold P products + one sentinel per list + the lone partner
+// sentinel + one slack slot: CAP + LCAP + 2 slots.
 template <int G, int CAP, int LCAP, bool VALS>
 __host__ __device__ constexpr int chunk_group_bytes() {
-  return align16((CAP + 2) * 4) * 2 + (VALS ? align16((CAP + 2) * 8) * 2 : 0) + align16((LCAP + 2) * 4) * 2 +
+  return align16((CAP + LCAP + 2) * 4) * 2 + (VALS ? align16((CAP + LCAP + 2) * 8) * 2 : 0) +
+         align16((LCAP + 2) * 4) * 2 +
          align16(LCAP * 8) + (VALS ? align16(LCAP * 8) : 0) + (G > 32 ? align16((G / 32 + 2) * 4) : 0);
 }
 
@@ -223,55 +226,65 @@ __device__ __forceinline__ void cp_async_8(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Merge state of one thread's chunk inside pair p = lists (2p, 2p+1):
-// list a = [as, bs), list b = [bs, be) of src; heads ca/cb (INT_MAX once a
-// list is consumed), head values va/vb; sa/sb = A_ik of the two lists (round
-// 1 only: the scaling of Alg. 1 line 12 is fused into the first merge).
+// Lists of a round are sentinel-terminated: list l = [off[l], off[l+1]-1)
+// followed by one INT_MAX slot at off[l+1]-1. If nl is odd, the trailing
+// list's empty partner is a lone sentinel at off[nl]. The round's position
+// space is the src index space: pair p covers [off[2p], off[2p+2]) (the odd
+// trailing pair [off[nl-1], off[nl]+1)). Merging a pair emits its merged
+// list followed by ONE sentinel: the two input sentinels are equal columns
+// and are consumed together, like any duplicate. Empty lists and pairs need
+// no special case, and merge cursors need no bounds checks.
 struct Cursor {
-  int p, as, bs, be, ia, ib, lim, ca, cb;
+  int p, bs, ia, ib, lim, ca, cb;
   double va, vb, sa, sb;
 };
 
 template <bool VALS, bool FIRST>
-__device__ __forceinline__ void cursor_load(Cursor& c, const int* sc, const double* sv, const double* av, int nl) {
-  c.ca = c.ia < c.bs ? sc[c.ia] : INT_MAX;
-  c.cb = c.ib < c.be ? sc[c.ib] : INT_MAX;
+__device__ __forceinline__ void enter_pair(Cursor& c, int p, const int* sc, const double* sv, const int* off,
+                                           const double* av, int nl, int g1) {
+  c.p = p;
+  c.ia = off[2 * p];
+  c.bs = off[2 * p + 1];  // 2p+1 == nl: the lone sentinel of an odd trailing list
+  c.ib = c.bs;
+  c.lim = g1 + c.bs;      // merged position = ia + ib - bs
+  c.ca = sc[c.ia];
+  c.cb = sc[c.ib];
   if (VALS) {
     c.va = sv[c.ia];
     c.vb = sv[c.ib];
     if (FIRST) {
-      c.sa = av[2 * c.p];
-      c.sb = 2 * c.p + 1 < nl ? av[2 * c.p + 1] : 0.0;
+      c.sa = av[2 * p];
+      c.sb = 2 * p + 1 < nl ? av[2 * p + 1] : 0.0;
     }
   }
 }
 
-// One BRMerge round (Alg. 1 lines 22-34) over compact lists in sc/sv with
-// offsets off[0..nl]. The round's merged positions are split into G chunks of
-// VT (odd) positions; the merged lists are written COMPACT with offsets
-// noff[0..npairs]:
+// One BRMerge round (Alg. 1 lines 22-34) over the nl sentinel-terminated
+// lists of sc/sv (offsets off[0..nl]). The round's positions are split into
+// G chunks of VT (odd) positions. The merged lists are written compact and
+// sentinel-terminated, with offsets noff[0..npairs]:
 //   NV > 0: into dc/dv (the other ping-pong buffer), each thread holding its
 //           <= NV outputs in registers until the group scan gives its base;
 //   NV = 0: (global tier, unbounded VT) into dc/dv at the chunk's own
 //           positions, then copied back compacted into sc/sv.
-// Returns the new element total.
+// Returns the new end offset (noff[npairs]).
 template <int G, int NV, bool VALS, bool FIRST, bool SMEM>
 __device__ __forceinline__ int chunk_round(const Group<G>& g, int* __restrict__ sc, double* __restrict__ sv,
                                            int* __restrict__ dc, double* __restrict__ dv, const int* off,
-                                           int* noff, int nl, int T, int* scan_tmp, const double* av) {
+                                           int* noff, int nl, int* scan_tmp, const double* av) {
   const int npairs = (nl + 1) >> 1;
-  const int VT = ((T + G - 1) / G) | 1;  // odd: conflict-free strided shared-memory access
-  const int g0 = min(g.rank * VT, T), g1 = min(g0 + VT, T);
+  const int npos = off[nl] + (nl & 1);
+  const int VT = ((npos + G - 1) / G) | 1;  // odd: conflict-free strided shared-memory access
+  const int g0 = min(g.rank * VT, npos), g1 = min(g0 + VT, npos);
   int cnt = 0;
   int pf = 0, pl = -1;  // pairs whose output start this thread records: [pf, pl]
   Cursor c;
-  c.ia = c.ib = c.lim = 0;
+  c.p = 0;
+  c.bs = c.ia = c.ib = c.lim = 0;
   c.ca = c.cb = INT_MAX;
   c.va = c.vb = c.sa = c.sb = 0.0;
-  c.p = 0;
-  c.as = c.bs = c.be = 0;
   if (g0 < g1) {
-    int lo = 0, hi = npairs - 1;  // last pair starting at or before g0 (it is non-empty)
+    int lo = 0, hi = npairs - 1;  // last pair starting at or before g0
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (off[2 * mid] <= g0)
@@ -279,24 +292,41 @@ __device__ __forceinline__ int chunk_round(const Group<G>& g, int* __restrict__ 
       else
         hi = mid - 1;
     }
-    c.p = lo;
-    c.as = off[2 * c.p];
-    c.bs = off[min(2 * c.p + 1, nl)];
-    c.be = off[min(2 * c.p + 2, nl)];
-    const int d = g0 - c.as;
-    if (d == 0) {  // this chunk starts pair p (and any empty pairs just before it)
-      pf = c.p;
-      while (pf > 0 && off[2 * (pf - 1)] == g0) --pf;
-      for (int q = pf; q <= c.p; ++q) noff[q] = 0;
-      pl = c.p;
+    const int p = lo;
+    const int as = off[2 * p], bs = off[2 * p + 1];
+    const int bend = 2 * p + 2 <= nl ? off[2 * p + 2] : off[nl] + 1;
+    const int na = bs - as, nb = bend - bs;  // list lengths including the sentinels
+    const int d = g0 - as;
+    if (d == 0) {
+      pf = pl = p;
+      noff[p] = 0;
     }
-    const int i = merge_path(sc + c.as, c.bs - c.as, sc + c.bs, c.be - c.bs, d);
+    const int i = merge_path(sc + as, na, sc + bs, nb, d);
     int j = d - i;
-    if (i > 0 && j < c.be - c.bs && sc[c.as + i - 1] == sc[c.bs + j]) ++j;  // b[j] summed by the chunk on the left
-    c.ia = c.as + i;
-    c.ib = c.bs + j;
-    c.lim = g1 + c.bs;  // merged position = ia + ib - bs
-    cursor_load<VALS, FIRST>(c, sc, sv, av, nl);
+    if (i > 0 && j < nb && sc[as + i - 1] == sc[bs + j]) ++j;  // b[j] was summed by the chunk on the left
+    if (i == na) {  // pair p already finished (its two sentinels were consumed on the left)
+      if (g0 + 1 < g1) {
+        enter_pair<VALS, FIRST>(c, p + 1, sc, sv, off, av, nl, g1);
+        pf = pl = p + 1;
+        noff[p + 1] = 0;
+      }
+    } else {
+      c.p = p;
+      c.bs = bs;
+      c.ia = as + i;
+      c.ib = bs + j;
+      c.lim = g1 + bs;
+      c.ca = sc[c.ia];
+      c.cb = sc[c.ib];
+      if (VALS) {
+        c.va = sv[c.ia];
+        c.vb = sv[c.ib];
+        if (FIRST) {
+          c.sa = av[2 * p];
+          c.sb = 2 * p + 1 < nl ? av[2 * p + 1] : 0.0;
+        }
+      }
+    }
   }
   const unsigned scb = SMEM ? smem_u32(sc) : 0u;
   const unsigned svb = (SMEM && VALS) ? smem_u32(sv) : 0u;
@@ -305,21 +335,6 @@ __device__ __forceinline__ int chunk_round(const Group<G>& g, int* __restrict__ 
   double oval[NR];
   auto step = [&](int v) {
     const bool act = c.ia + c.ib < c.lim;
-    if (act && (c.ca & c.cb) == INT_MAX) {  // pair p consumed: enter the next non-empty pair
-      if (pl < 0) pf = c.p + 1;
-      do {
-        ++c.p;
-        noff[c.p] = cnt;
-        c.as = off[2 * c.p];
-        c.bs = off[min(2 * c.p + 1, nl)];
-        c.be = off[min(2 * c.p + 2, nl)];
-      } while (c.as == c.be);
-      pl = c.p;
-      c.ia = c.as;
-      c.ib = c.bs;
-      c.lim = g1 + c.bs;
-      cursor_load<VALS, FIRST>(c, sc, sv, av, nl);
-    }
     const bool ta = act && c.ca <= c.cb;
     const bool tb = act && c.cb <= c.ca;
     const int oc = min(c.ca, c.cb);
@@ -358,8 +373,12 @@ __device__ __forceinline__ int chunk_round(const Group<G>& g, int* __restrict__ 
         if (VALS) c.vb = sv[c.ib];
       }
     }
-    c.ca = c.ia < c.bs ? c.ca : INT_MAX;
-    c.cb = c.ib < c.be ? c.cb : INT_MAX;
+    if (act && oc == INT_MAX && c.ia + c.ib < c.lim) {  // pair p done, chunk not: enter pair p+1
+      if (pl < 0) pf = c.p + 1;
+      pl = c.p + 1;
+      noff[c.p + 1] = cnt;
+      enter_pair<VALS, FIRST>(c, c.p + 1, sc, sv, off, av, nl, g1);
+    }
   };
   if constexpr (NV > 0) {
 #pragma unroll
@@ -382,16 +401,20 @@ __device__ __forceinline__ int chunk_round(const Group<G>& g, int* __restrict__ 
         if (VALS) dv[base + v] = oval[v];
       }
     }
+    if (g.rank == G - 1) {
+      noff[npairs] = total;
+      dc[total] = INT_MAX;  // lone partner sentinel, used if npairs is odd
+    }
   } else {
     g.sync();  // every merge has finished reading sc
     for (int e = 0; e < cnt; ++e) {
       sc[base + e] = dc[g0 + e];
       if (VALS) sv[base + e] = dv[g0 + e];
     }
-  }
-  if (g.rank == G - 1) {
-    for (int q = npairs - 1; q >= 0 && off[2 * q] == T; --q) noff[q] = total;  // trailing empty pairs
-    noff[npairs] = total;
+    if (g.rank == G - 1) {
+      noff[npairs] = total;
+      sc[total] = INT_MAX;
+    }
   }
   g.sync();
   return total;
@@ -413,8 +436,9 @@ __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, c
   double* dv = cb.val1;
   int* off = cb.off0;
   int* noff = cb.off1;
-  // multiplying phase (Alg. 1 lines 10-15): list offsets by a group scan ...
-  int T = 0;
+  // multiplying phase (Alg. 1 lines 10-15): list offsets by a group scan
+  // (list l starts at product index E_l and at slot off[l] = E_l + l) ...
+  int P = 0;
   for (int lb = 0; lb < nl; lb += G) {
     const int l = lb + rank;
     int n = 0;
@@ -427,34 +451,31 @@ __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, c
     }
     int tot;
     const int ex = group_excl_scan<G>(g, n, tot, cb.scan_tmp);
-    if (l < nl) off[l] = T + ex;
-    T += tot;
+    if (l < nl) {
+      off[l] = P + ex + l;
+      sc[P + ex + l + n] = INT_MAX;  // sentinel of list l
+    }
+    P += tot;
   }
-  if (rank == 0) off[nl] = T;
+  if (rank == 0) {
+    off[nl] = P + nl;
+    sc[P + nl] = INT_MAX;  // lone partner sentinel if nl is odd
+  }
   g.sync();
-  // ... then the B rows themselves (unscaled; round 1 multiplies), S
-  // consecutive threads per list (S ~ mean list length), coalesced.
+  // ... then the B rows themselves (unscaled; round 1 multiplies): product e
+  // of list l goes to slot e + l; consecutive threads take consecutive
+  // products (coalesced), each tracking its current list.
   {
-    const int avg = (T + nl - 1) / nl;
-    int ls = 0;
-    while ((1 << ls) < avg && (1 << ls) < G) ++ls;
-    const int S = 1 << ls;
-    const int per = G >> ls;
-    const int sub = rank >> ls, e0 = rank & (S - 1);
-    for (int lb = 0; lb < nl; lb += per) {
-      const int l = lb + sub;
-      if (l < nl) {
-        const int o0 = off[l], n = off[l + 1] - o0;
-        const int64_t st = cb.bst[l];
-        for (int e = e0; e < n; e += S) {
-          if (SMEM) {
-            cp_async_4(sc + o0 + e, B.col + st + e);
-            if (VALS) cp_async_8(sv + o0 + e, B.val + st + e);
-          } else {
-            sc[o0 + e] = __ldg(B.col + st + e);
-            if (VALS) sv[o0 + e] = __ldg(B.val + st + e);
-          }
-        }
+    int l = 0;
+    for (int e = rank; e < P; e += G) {
+      while (off[l + 1] - (l + 1) <= e) ++l;  // E_{l+1} <= e
+      const int64_t src = cb.bst[l] + (e - (off[l] - l));
+      if (SMEM) {
+        cp_async_4(sc + e + l, B.col + src);
+        if (VALS) cp_async_8(sv + e + l, B.val + src);
+      } else {
+        sc[e + l] = __ldg(B.col + src);
+        if (VALS) sv[e + l] = __ldg(B.val + src);
       }
     }
     if (SMEM) cp_async_wait_all();
@@ -462,12 +483,13 @@ __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, c
   g.sync();
   // accumulating phase (lines 21-35)
   int cur = nl;
+  int end = P + nl;
   bool first = true;
   while (cur > 1) {
     if (first)
-      T = chunk_round<G, NV, VALS, true, SMEM>(g, sc, sv, dc, dv, off, noff, cur, T, cb.scan_tmp, cb.av);
+      end = chunk_round<G, NV, VALS, true, SMEM>(g, sc, sv, dc, dv, off, noff, cur, cb.scan_tmp, cb.av);
     else
-      T = chunk_round<G, NV, VALS, false, SMEM>(g, sc, sv, dc, dv, off, noff, cur, T, cb.scan_tmp, cb.av);
+      end = chunk_round<G, NV, VALS, false, SMEM>(g, sc, sv, dc, dv, off, noff, cur, cb.scan_tmp, cb.av);
     first = false;
     cur = (cur + 1) >> 1;
     { int* t = off; off = noff; noff = t; }
@@ -476,7 +498,8 @@ __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, c
       { double* t = sv; sv = dv; dv = t; }
     }
   }
-  // line 36: the result row is list 0 of src, [0, T)
+  const int T = end - 1;  // the result row: list 0 = [0, end - 1), then its sentinel
+  // line 36: store the result row
   if (OUT != OUT_SYMBOLIC) {
     const int64_t ob = o.base[row];
     const double s0 = (VALS && nl == 1) ? cb.av[0] : 1.0;  // a single list was never scaled

@@ -318,17 +318,17 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
       return q;
     };
     ChunkBufs cb;
-    cb.col0 = reinterpret_cast<int*>(take((CAP + 2) * 4));
-    cb.col1 = reinterpret_cast<int*>(take((CAP + 2) * 4));
-    cb.val0 = VALS ? reinterpret_cast<double*>(take((CAP + 2) * 8)) : nullptr;
-    cb.val1 = VALS ? reinterpret_cast<double*>(take((CAP + 2) * 8)) : nullptr;
+    cb.col0 = reinterpret_cast<int*>(take((CAP + LCAP + 2) * 4));
+    cb.col1 = reinterpret_cast<int*>(take((CAP + LCAP + 2) * 4));
+    cb.val0 = VALS ? reinterpret_cast<double*>(take((CAP + LCAP + 2) * 8)) : nullptr;
+    cb.val1 = VALS ? reinterpret_cast<double*>(take((CAP + LCAP + 2) * 8)) : nullptr;
     cb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
     cb.off1 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
     cb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
     cb.av = VALS ? reinterpret_cast<double*>(take(LCAP * 8)) : nullptr;
     cb.scan_tmp = G > 32 ? reinterpret_cast<int*>(take((G / 32 + 2) * 4)) : nullptr;
     for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
-      chunk_row<G, ((CAP + G - 1) / G) | 1, VALS, OUT>(g, A, B, rows[r], o, cb);
+      chunk_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, VALS, OUT>(g, A, B, rows[r], o, cb);
   }
 }
 
@@ -351,10 +351,10 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
     return q;
   };
   ChunkBufs cb;
-  cb.col0 = reinterpret_cast<int*>(take((P + 2) * 4));
-  cb.col1 = reinterpret_cast<int*>(take((P + 2) * 4));
-  cb.val0 = VALS ? reinterpret_cast<double*>(take((P + 2) * 8)) : nullptr;
-  cb.val1 = VALS ? reinterpret_cast<double*>(take((P + 2) * 8)) : nullptr;
+  cb.col0 = reinterpret_cast<int*>(take((P + nl + 2) * 4));
+  cb.col1 = reinterpret_cast<int*>(take((P + nl + 2) * 4));
+  cb.val0 = VALS ? reinterpret_cast<double*>(take((P + nl + 2) * 8)) : nullptr;
+  cb.val1 = VALS ? reinterpret_cast<double*>(take((P + nl + 2) * 8)) : nullptr;
   cb.off0 = reinterpret_cast<int*>(take((nl + 2) * 4));
   cb.off1 = reinterpret_cast<int*>(take((nl + 2) * 4));
   cb.bst = reinterpret_cast<int64_t*>(take(nl * 8));
@@ -507,8 +507,8 @@ cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& 
 
 int64_t global_row_bytes(int64_t nprod, int64_t nl, bool vals) {
   auto a = [](int64_t b) { return (b + 15) & ~15ll; };
-  int64_t s = a((nprod + 2) * 4) * 2 + a((nl + 2) * 4) * 2 + a(nl * 8);
-  if (vals) s += a((nprod + 2) * 8) * 2 + a(nl * 8);
+  int64_t s = a((nprod + nl + 2) * 4) * 2 + a((nl + 2) * 4) * 2 + a(nl * 8);
+  if (vals) s += a((nprod + nl + 2) * 8) * 2 + a(nl * 8);
   return s;
 }
 
