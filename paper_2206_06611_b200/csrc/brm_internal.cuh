@@ -23,7 +23,7 @@ struct CsrView {
 //   3  chunked BRMerge, one warp        P <= 256,  nl <= 64   (smem ping-pong)
 //   4  chunked BRMerge, one warp        P <= 768,  nl <= 64   (smem ping-pong)
 //   5  chunked BRMerge, 128 threads     P <= 3072, nl <= 512  (smem ping-pong)
-//   6  chunked BRMerge, 256 threads     P <= 7168, nl <= 512  (smem ping-pong)
+//   6  chunked BRMerge, 256 threads     P <= 6656, nl <= 512  (smem ping-pong)
 //   7  chunked BRMerge, 512 threads, ping-pong buffers in a global workspace
 // ---------------------------------------------------------------------------
 constexpr int kBinEmpty = 0;
@@ -41,7 +41,7 @@ struct TierBounds {
 #define BRM_TIER3 32, 256, 64, 4
 #define BRM_TIER4 32, 768, 64, 2
 #define BRM_TIER5 128, 3072, 512, 1
-#define BRM_TIER6 256, 7168, 512, 1
+#define BRM_TIER6 256, 6656, 512, 1
 constexpr int kGlobalG = 512;
 
 __host__ __device__ inline TierBounds tier_bounds() {
@@ -52,7 +52,7 @@ __host__ __device__ inline TierBounds tier_bounds() {
   t.cap[3] = 256;  t.lcap[3] = 64;
   t.cap[4] = 768;  t.lcap[4] = 64;
   t.cap[5] = 3072; t.lcap[5] = 512;
-  t.cap[6] = 7168; t.lcap[6] = 512;
+  t.cap[6] = 6656; t.lcap[6] = 512;
   t.cap[7] = INT_MAX; t.lcap[7] = INT_MAX;
   return t;
 }

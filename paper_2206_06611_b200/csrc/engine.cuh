@@ -269,8 +269,8 @@ __device__ __forceinline__ void enter_pair(Cursor& c, int p, const int* sc, cons
 //           positions, then copied back compacted into sc/sv.
 // Returns the new end offset (noff[npairs]).
 template <int G, int NV, bool VALS, bool FIRST, bool SMEM>
-__device__ __forceinline__ int chunk_round(const Group<G>& g, int* __restrict__ sc, double* __restrict__ sv,
-                                           int* __restrict__ dc, double* __restrict__ dv, const int* off,
+__device__ __forceinline__ int chunk_round(const Group<G>& g, int* sc, double* sv,
+                                           int* dc, double* dv, const int* off,
                                            int* noff, int nl, int* scan_tmp, const double* av) {
   const int npairs = (nl + 1) >> 1;
   const int npos = off[nl] + (nl & 1);

@@ -103,7 +103,53 @@ __device__ __forceinline__ int64_t block_scan_i64(int64_t x, int64_t& total, int
   return wsum[wid] + inc - x;
 }
 
-// Step 1: n_prod per row + exclusive scan + bin histogram + max.
+// n_prod of the 32 rows [r0, r0 + 32) by one warp, nonzero-parallel: lanes
+// stride over the rows' nonzeros (coalesced A.col reads, B.rpt gathers), find
+// each nonzero's row by a shuffle search over the row starts, and sum runs of
+// equal rows with a segmented shuffle scan; the last lane of a run adds it to
+// out[row - r0]. Returns (in *nl_out) lane's row length.
+__device__ __forceinline__ void warp_rows_nprod(const CsrView& A, const int64_t* __restrict__ brpt, int64_t M,
+                                                int64_t r0, int64_t* out, int* nl_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rs = A.rpt[min(r0 + lane, M)];   // start of row r0 + lane (clamped)
+  const int64_t pend = A.rpt[min(r0 + 32, M)];
+  const int64_t pbeg = __shfl_sync(0xffffffffu, rs, 0);
+  const int64_t rnext = __shfl_down_sync(0xffffffffu, rs, 1);
+  *nl_out = lane < 31 ? (int)(rnext - rs) : (int)(pend - rs);
+  out[lane] = 0;
+  __syncwarp();
+  for (int64_t pb = pbeg; pb < pend; pb += 32) {
+    const int64_t p = pb + lane;
+    int64_t d = 0;
+    if (p < pend) {
+      const int k = __ldg(A.col + p);
+      d = __ldg(brpt + k + 1) - __ldg(brpt + k);
+    }
+    // row of nonzero p: last lane whose row start <= p
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int64_t v = __shfl_sync(0xffffffffu, rs, lo + step);
+      if (v <= p) lo += step;
+    }
+    // segmented inclusive scan over lanes with equal rows
+    int64_t x = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      const int ro = __shfl_up_sync(0xffffffffu, lo, o);
+      if (lane >= o && ro == lo) x += y;
+    }
+    const int rn = __shfl_down_sync(0xffffffffu, lo, 1);
+    if (p < pend && (lane == 31 || rn != lo || p + 1 >= pend)) out[lo] += x;
+    __syncwarp();
+  }
+}
+
+// Step 1: n_prod per row + exclusive scan + bin histogram + max. A tile of
+// 2048 rows: each warp computes 256 rows' n_prod nonzero-parallel into shared
+// memory, then the tile is scanned (blocked, 8 rows per thread) with a
+// decoupled look-back across tiles.
 __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const int64_t* __restrict__ brpt,
                                                              int64_t M, int64_t* __restrict__ nprod_off,
                                                              unsigned long long* status,
@@ -112,6 +158,7 @@ __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const in
   __shared__ int s_tile;
   __shared__ int64_t s_wsum[kScanThreads / 32 + 1];
   __shared__ int64_t s_prefix;
+  __shared__ int64_t s_np[kScanTile];
   __shared__ unsigned long long s_bin_rows[BRM_NUM_BINS];
   __shared__ unsigned long long s_bin_nprod[BRM_NUM_BINS];
   __shared__ unsigned long long s_max, s_maxnl;
@@ -124,27 +171,32 @@ __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const in
   __syncthreads();
   const int tile = s_tile;
   const TierBounds tb = tier_bounds();
-  const int64_t r0 = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanIPT;
-  int64_t v[kScanIPT];
-  int64_t tsum = 0, tmax = 0, tmaxnl = 0;
-#pragma unroll
-  for (int t = 0; t < kScanIPT; ++t) {
-    const int64_t r = r0 + t;
-    int64_t s = 0;
-    if (r < M) {
-      const int64_t p0 = A.rpt[r], p1 = A.rpt[r + 1];
-      for (int64_t p = p0; p < p1; ++p) {
-        const int k = A.col[p];
-        s += brpt[k + 1] - brpt[k];
-      }
-      const int bin = tier_of(s, p1 - p0, tb);
+  const int64_t t0 = (int64_t)tile * kScanTile;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long tmax = 0, tmaxnl = 0;
+  for (int c = 0; c < kScanTile / kScanThreads; ++c) {
+    const int loc = wid * (kScanTile / (kScanThreads / 32)) + c * 32;
+    const int64_t r0 = t0 + loc;
+    if (r0 >= M) break;  // warp-uniform
+    int nl;
+    warp_rows_nprod(A, brpt, M, r0, s_np + loc, &nl);
+    if (r0 + lane < M) {
+      const int64_t s = s_np[loc + lane];
+      const int bin = tier_of(s, nl, tb);
       atomicAdd(&s_bin_rows[bin], 1ull);
       atomicAdd(&s_bin_nprod[bin], (unsigned long long)s);
-      tmax = s > tmax ? s : tmax;
-      tmaxnl = (p1 - p0) > tmaxnl ? (p1 - p0) : tmaxnl;
+      tmax = (unsigned long long)s > tmax ? (unsigned long long)s : tmax;
+      tmaxnl = (unsigned long long)nl > tmaxnl ? (unsigned long long)nl : tmaxnl;
     }
-    v[t] = s;
-    tsum += s;
+  }
+  __syncthreads();
+  const int64_t rb = t0 + (int64_t)threadIdx.x * kScanIPT;
+  int64_t v[kScanIPT];
+  int64_t tsum = 0;
+#pragma unroll
+  for (int t = 0; t < kScanIPT; ++t) {
+    v[t] = rb + t < M ? s_np[threadIdx.x * kScanIPT + t] : 0;
+    tsum += v[t];
   }
   int64_t total;
   const int64_t texcl = block_scan_i64(tsum, total, s_wsum);
@@ -152,13 +204,13 @@ __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const in
     const int64_t pre = lookback(status, tile, total);
     if (threadIdx.x == 0) s_prefix = pre;
   }
-  atomicMax(&s_max, (unsigned long long)tmax);
-  atomicMax(&s_maxnl, (unsigned long long)tmaxnl);
+  atomicMax(&s_max, tmax);
+  atomicMax(&s_maxnl, tmaxnl);
   __syncthreads();
   int64_t run = s_prefix + texcl;
 #pragma unroll
   for (int t = 0; t < kScanIPT; ++t) {
-    const int64_t r = r0 + t;
+    const int64_t r = rb + t;
     if (r < M) nprod_off[r] = run;
     run += v[t];
     if (r == M - 1) {
@@ -318,10 +370,10 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
       return q;
     };
     ChunkBufs cb;
-    cb.col0 = reinterpret_cast<int*>(take((CAP + LCAP + 2) * 4));
-    cb.col1 = reinterpret_cast<int*>(take((CAP + LCAP + 2) * 4));
     cb.val0 = VALS ? reinterpret_cast<double*>(take((CAP + LCAP + 2) * 8)) : nullptr;
     cb.val1 = VALS ? reinterpret_cast<double*>(take((CAP + LCAP + 2) * 8)) : nullptr;
+    cb.col0 = reinterpret_cast<int*>(take((CAP + LCAP + 2) * 4));
+    cb.col1 = reinterpret_cast<int*>(take((CAP + LCAP + 2) * 4));
     cb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
     cb.off1 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
     cb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
@@ -463,6 +515,9 @@ static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, const int32
   if (n <= 0) return cudaSuccess;
   constexpr int per_group = CAP <= 32 ? reg_group_bytes<G, VALS>() : chunk_group_bytes<G, CAP, LCAP, VALS>();
   constexpr int smem = per_group * GPC;
+  // registers hold <= NV chunk outputs; NV = 31 (G = 256, CAP 7168) miscompiled
+  // (wrong values, no spills reported), so tiers keep NV <= 29
+  static_assert(CAP <= 32 || (((CAP + LCAP + 1 + G - 1) / G) | 1) <= 29, "chunk tier NV must stay <= 29");
   static_assert(smem <= 232448, "tier shared memory exceeds 227 KB");
   auto kern = k_tier<G, CAP, LCAP, GPC, VALS, OUT>;
   // one process drives one device, so per-instantiation caching is safe

@@ -85,7 +85,7 @@ def test_random_rectangular(ctx, oracle_mod, mode, seed):
     (4, [64, 65]),                               # tier 3 list cap 64 -> tier 5
     (27, [27, 28, 29]),                          # tier 4 (stencil-like, 768 edge)
     (33, [90, 93, 94]),                          # tier 5 (3072 edge)
-    (64, [100, 112, 113]),                       # tier 6 (7168 edge) -> global
+    (64, [100, 104, 105]),                       # tier 6 (6656 edge) -> global
     (100, [90, 300]),                            # global tier
     (3, [40, 129, 300, 513, 600, 1500]),         # many short lists (list caps 64 / 512)
 ])

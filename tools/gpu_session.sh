@@ -26,6 +26,11 @@ if [ "${NCU:-1}" = 1 ] && [ $ok = 1 ]; then
     python bench.py --config $NCFG --mode $NMODE --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_launch.log 2>&1
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-k_tier} -c ${NCU_COUNT:-6} -o $OUT/full \
     python bench.py --config $NCFG --mode $NMODE --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_full.log 2>&1
+  for extra in ${NCU_EXTRA:-}; do  # config:mode:kernel-regex
+    IFS=: read ECFG EMODE EKER <<< "$extra"
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$EKER -c ${NCU_COUNT:-6} -o $OUT/full_$ECFG \
+      python bench.py --config $ECFG --mode $EMODE --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_full_$ECFG.log 2>&1
+  done
 else
   echo "ncu skipped (ok=$ok)" > $OUT/ncu_skipped.txt
 fi
