@@ -286,7 +286,7 @@ brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
   CK(ensure(ctx, ctx->nprod_off, (size_t)(M + 1) * 8), "alloc nprod_off");
   CK(ensure(ctx, ctx->row_size, (size_t)(M + 1) * 8), "alloc row_size");
   CK(ensure(ctx, ctx->bins, (size_t)M * 4), "alloc bins");
-  const int64_t tiles = scan_tiles(M);
+  const int64_t tiles = nprod_tiles(M);  // >= scan_tiles(M): the status array serves both scans
   CK(ensure(ctx, ctx->status, (size_t)(tiles + 1) * 8), "alloc scan status");
   SmallDev* sd = small_dev(ctx);
   ev_record(ctx, 0);

@@ -75,6 +75,94 @@ __host__ __device__ constexpr int chunk_group_bytes() {
 }
 
 // ===========================================================================
+// Tiny tier (tier 1: P <= 8, nl <= 8): one THREAD per row runs Algorithm 1
+// literally -- multiplying phase into its ping buffer, then rounds merging
+// lists (0,1),(2,3),... into the pong buffer, odd trailing list copied,
+// swap -- with both buffers in shared memory, thread-interleaved (slot s of
+// thread t at s * NT + t: conflict-free when a warp touches equal slots).
+// ===========================================================================
+constexpr int kTinyP = 8;   // max n_prod of a tiny row
+constexpr int kTinyL = 8;   // max num_list of a tiny row
+
+template <int NT, bool VALS>
+__host__ __device__ constexpr int tiny_block_bytes() {
+  return NT * kTinyP * (4 + 4) + (VALS ? NT * kTinyP * 16 : 0);
+}
+
+template <int NT, bool VALS, int OUT>
+__device__ __forceinline__ void tiny_row(const CsrView& A, const CsrView& B, int64_t row, const RowOut& o,
+                                         int* pc, int* qc, double* pv, double* qv) {
+  const int64_t a0 = A.rpt[row];
+  const int nl = static_cast<int>(A.rpt[row + 1] - a0);
+  // Alg. 1 lines 10-15: list l into the ping buffer at [off[l], off[l+1])
+  int off[kTinyL + 1];
+  int P = 0;
+#pragma unroll
+  for (int l = 0; l < kTinyL; ++l) {
+    off[l] = P;
+    if (l < nl) {
+      const int k = __ldg(A.col + a0 + l);
+      const int64_t b0 = __ldg(B.rpt + k), b1 = __ldg(B.rpt + k + 1);
+      const double a = VALS ? __ldg(A.val + a0 + l) : 0.0;
+      for (int64_t q = b0; q < b1; ++q, ++P) {
+        pc[P * NT] = __ldg(B.col + q);
+        if (VALS) pv[P * NT] = __dmul_rn(a, __ldg(B.val + q));  // line 12: one rounding
+      }
+    }
+  }
+  off[kTinyL] = P;
+  // lines 21-35: rounds of pairwise merges between the two buffers
+  int cur = nl;
+  int n = P;
+  while (cur > 1) {
+    int noff[kTinyL + 1];
+    int out = 0;
+#pragma unroll
+    for (int p = 0; p < kTinyL / 2; ++p) {
+      noff[p] = out;
+      if (2 * p < cur) {  // consume lists 2p and 2p+1 (empty if 2p+1 == cur: line 28 copy)
+        int i = off[2 * p], j = off[2 * p + 1];
+        const int ie = j, je = off[2 * p + 2];
+        while (i < ie || j < je) {
+          const int ci = i < ie ? pc[i * NT] : INT_MAX;
+          const int cj = j < je ? pc[j * NT] : INT_MAX;
+          const bool ti = ci <= cj, tj = cj <= ci;
+          qc[out * NT] = ti ? ci : cj;
+          if (VALS) {
+            const double x = ti ? pv[i * NT] : -0.0;
+            const double y = tj ? pv[j * NT] : -0.0;
+            qv[out * NT] = __dadd_rn(x, y);  // "vals with duplicate cols are combined"
+          }
+          ++out;
+          i += ti;
+          j += tj;
+        }
+      }
+    }
+#pragma unroll
+    for (int p = kTinyL / 2; p <= kTinyL; ++p) noff[p] = out;
+#pragma unroll
+    for (int p = 0; p < kTinyL / 2; ++p)
+      if (2 * p + 1 >= cur + 1) noff[p] = out;  // lists past the last pair are empty
+#pragma unroll
+    for (int l = 0; l <= kTinyL; ++l) off[l] = noff[l];
+    { int* t = pc; pc = qc; qc = t; }  // lines 33-34
+    { double* t = pv; pv = qv; qv = t; }
+    cur = (cur + 1) >> 1;
+    n = out;
+  }
+  // line 36: store the result row
+  if (OUT != OUT_SYMBOLIC) {
+    const int64_t ob = o.base[row];
+    for (int e = 0; e < n; ++e) {
+      o.col[ob + e] = pc[e * NT];
+      if (VALS) o.val[ob + e] = pv[e * NT];
+    }
+  }
+  if (OUT != OUT_C) o.row_size[row] = n;
+}
+
+// ===========================================================================
 // Register tier
 // ===========================================================================
 template <int G>

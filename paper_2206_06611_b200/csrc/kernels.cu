@@ -104,52 +104,61 @@ __device__ __forceinline__ int64_t block_scan_i64(int64_t x, int64_t& total, int
 }
 
 // n_prod of the 32 rows [r0, r0 + 32) by one warp, nonzero-parallel: lanes
-// stride over the rows' nonzeros (coalesced A.col reads, B.rpt gathers), find
-// each nonzero's row by a shuffle search over the row starts, and sum runs of
-// equal rows with a segmented shuffle scan; the last lane of a run adds it to
-// out[row - r0]. Returns (in *nl_out) lane's row length.
+// stride over the rows' nonzeros (coalesced A.col reads, B.rpt gathers; four
+// 32-nonzero batches in flight), find each nonzero's row by a shuffle search
+// over the row starts, and sum runs of equal rows with a segmented shuffle
+// scan; the last lane of a run adds it to out[row - r0]. *nl_out = lane's
+// row length.
 __device__ __forceinline__ void warp_rows_nprod(const CsrView& A, const int64_t* __restrict__ brpt, int64_t M,
                                                 int64_t r0, int64_t* out, int* nl_out) {
+  constexpr int U = 4;
   const int lane = threadIdx.x & 31;
-  const int64_t rs = A.rpt[min(r0 + lane, M)];   // start of row r0 + lane (clamped)
+  const int64_t rs = A.rpt[min(r0 + lane, M)];  // start of row r0 + lane (clamped)
   const int64_t pend = A.rpt[min(r0 + 32, M)];
   const int64_t pbeg = __shfl_sync(0xffffffffu, rs, 0);
   const int64_t rnext = __shfl_down_sync(0xffffffffu, rs, 1);
   *nl_out = lane < 31 ? (int)(rnext - rs) : (int)(pend - rs);
   out[lane] = 0;
   __syncwarp();
-  for (int64_t pb = pbeg; pb < pend; pb += 32) {
-    const int64_t p = pb + lane;
-    int64_t d = 0;
-    if (p < pend) {
-      const int k = __ldg(A.col + p);
-      d = __ldg(brpt + k + 1) - __ldg(brpt + k);
-    }
-    // row of nonzero p: last lane whose row start <= p
-    int lo = 0;
+  for (int64_t pb = pbeg; pb < pend; pb += 32 * U) {
+    int k[U];
+    int64_t d[U];
 #pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-      const int64_t v = __shfl_sync(0xffffffffu, rs, lo + step);
-      if (v <= p) lo += step;
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = pb + 32 * u + lane;
+      k[u] = p < pend ? __ldg(A.col + p) : -1;
     }
-    // segmented inclusive scan over lanes with equal rows
-    int64_t x = d;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-      const int ro = __shfl_up_sync(0xffffffffu, lo, o);
-      if (lane >= o && ro == lo) x += y;
+    for (int u = 0; u < U; ++u) d[u] = k[u] >= 0 ? __ldg(brpt + k[u] + 1) - __ldg(brpt + k[u]) : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = pb + 32 * u + lane;
+      if (pb + 32 * u >= pend) break;  // warp-uniform
+      int lo = 0;  // row of nonzero p: last lane whose row start <= p
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int64_t v = __shfl_sync(0xffffffffu, rs, lo + step);
+        if (v <= p) lo += step;
+      }
+      int64_t x = d[u];  // segmented inclusive scan over lanes with equal rows
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        const int ro = __shfl_up_sync(0xffffffffu, lo, o);
+        if (lane >= o && ro == lo) x += y;
+      }
+      const int rn = __shfl_down_sync(0xffffffffu, lo, 1);
+      if (p < pend && (lane == 31 || rn != lo || p + 1 >= pend)) out[lo] += x;
+      __syncwarp();
     }
-    const int rn = __shfl_down_sync(0xffffffffu, lo, 1);
-    if (p < pend && (lane == 31 || rn != lo || p + 1 >= pend)) out[lo] += x;
-    __syncwarp();
   }
 }
 
 // Step 1: n_prod per row + exclusive scan + bin histogram + max. A tile of
-// 2048 rows: each warp computes 256 rows' n_prod nonzero-parallel into shared
-// memory, then the tile is scanned (blocked, 8 rows per thread) with a
+// 256 rows per CTA: each warp computes 32 rows' n_prod nonzero-parallel into
+// shared memory, then the tile is scanned (one row per thread) with a
 // decoupled look-back across tiles.
+constexpr int kNpTile = kScanThreads;
 __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const int64_t* __restrict__ brpt,
                                                              int64_t M, int64_t* __restrict__ nprod_off,
                                                              unsigned long long* status,
@@ -158,7 +167,7 @@ __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const in
   __shared__ int s_tile;
   __shared__ int64_t s_wsum[kScanThreads / 32 + 1];
   __shared__ int64_t s_prefix;
-  __shared__ int64_t s_np[kScanTile];
+  __shared__ int64_t s_np[kNpTile];
   __shared__ unsigned long long s_bin_rows[BRM_NUM_BINS];
   __shared__ unsigned long long s_bin_nprod[BRM_NUM_BINS];
   __shared__ unsigned long long s_max, s_maxnl;
@@ -171,13 +180,11 @@ __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const in
   __syncthreads();
   const int tile = s_tile;
   const TierBounds tb = tier_bounds();
-  const int64_t t0 = (int64_t)tile * kScanTile;
+  const int64_t t0 = (int64_t)tile * kNpTile;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned long long tmax = 0, tmaxnl = 0;
-  for (int c = 0; c < kScanTile / kScanThreads; ++c) {
-    const int loc = wid * (kScanTile / (kScanThreads / 32)) + c * 32;
-    const int64_t r0 = t0 + loc;
-    if (r0 >= M) break;  // warp-uniform
+  const int loc = wid * 32;
+  const int64_t r0 = t0 + loc;
+  if (r0 < M) {  // warp-uniform
     int nl;
     warp_rows_nprod(A, brpt, M, r0, s_np + loc, &nl);
     if (r0 + lane < M) {
@@ -185,38 +192,24 @@ __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const in
       const int bin = tier_of(s, nl, tb);
       atomicAdd(&s_bin_rows[bin], 1ull);
       atomicAdd(&s_bin_nprod[bin], (unsigned long long)s);
-      tmax = (unsigned long long)s > tmax ? (unsigned long long)s : tmax;
-      tmaxnl = (unsigned long long)nl > tmaxnl ? (unsigned long long)nl : tmaxnl;
+      atomicMax(&s_max, (unsigned long long)s);
+      atomicMax(&s_maxnl, (unsigned long long)nl);
     }
   }
   __syncthreads();
-  const int64_t rb = t0 + (int64_t)threadIdx.x * kScanIPT;
-  int64_t v[kScanIPT];
-  int64_t tsum = 0;
-#pragma unroll
-  for (int t = 0; t < kScanIPT; ++t) {
-    v[t] = rb + t < M ? s_np[threadIdx.x * kScanIPT + t] : 0;
-    tsum += v[t];
-  }
+  const int64_t r = t0 + threadIdx.x;
+  const int64_t v = r < M ? s_np[threadIdx.x] : 0;
   int64_t total;
-  const int64_t texcl = block_scan_i64(tsum, total, s_wsum);
+  const int64_t texcl = block_scan_i64(v, total, s_wsum);
   if (threadIdx.x < 32) {
     const int64_t pre = lookback(status, tile, total);
     if (threadIdx.x == 0) s_prefix = pre;
   }
-  atomicMax(&s_max, tmax);
-  atomicMax(&s_maxnl, tmaxnl);
   __syncthreads();
-  int64_t run = s_prefix + texcl;
-#pragma unroll
-  for (int t = 0; t < kScanIPT; ++t) {
-    const int64_t r = rb + t;
-    if (r < M) nprod_off[r] = run;
-    run += v[t];
-    if (r == M - 1) {
-      nprod_off[M] = run;
-      summary->nprod_total = run;
-    }
+  if (r < M) nprod_off[r] = s_prefix + texcl;
+  if (r == M - 1) {
+    nprod_off[M] = s_prefix + texcl + v;
+    summary->nprod_total = s_prefix + texcl + v;
   }
   if (threadIdx.x < BRM_NUM_BINS) {
     if (s_bin_rows[threadIdx.x]) {
@@ -384,6 +377,20 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
   }
 }
 
+// Tier 1: one thread per row (tiny_row), NT threads per CTA.
+constexpr int kTinyNT = 128;
+template <bool VALS, int OUT>
+__global__ void __launch_bounds__(kTinyNT) k_tiny(CsrView A, CsrView B, const int32_t* __restrict__ rows,
+                                                 int64_t nrows, RowOut o) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int* pc = reinterpret_cast<int*>(smem) + threadIdx.x;
+  int* qc = pc + kTinyNT * kTinyP;
+  double* pv = VALS ? reinterpret_cast<double*>(smem + kTinyNT * kTinyP * 8) + threadIdx.x : nullptr;
+  double* qv = VALS ? pv + kTinyNT * kTinyP : nullptr;
+  for (int64_t t = (int64_t)blockIdx.x * kTinyNT + threadIdx.x; t < nrows; t += (int64_t)gridDim.x * kTinyNT)
+    tiny_row<kTinyNT, VALS, OUT>(A, B, rows[t], o, pc, qc, pv, qv);
+}
+
 // Global tier: one CTA per row, ping-pong buffers in a per-row slice of a
 // global workspace at byte offset ws_off[2r] (host-batched; ws_off[2r+1] is
 // the row's n_prod).
@@ -415,7 +422,10 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
   chunk_row<kGlobalG, 0, VALS, OUT>(g, A, B, row, o, cb);
 }
 
-// Step 6 of Fig. 4a: copy each row of C_bar (at its n_prod offset) to C.
+// Step 6 of Fig. 4a: copy each row of C_bar (at its n_prod offset) to C. A
+// warp copies the rows [r0, r0 + 32) as ONE flattened range of C (coalesced
+// writes): element e's row is found by a shuffle search over the 32 row
+// starts, its source is nprod_off[row] + (e - crpt[row]).
 __global__ void __launch_bounds__(256) k_compact(int64_t M, const int64_t* __restrict__ nprod_off,
                                                  const int64_t* __restrict__ crpt,
                                                  const int32_t* __restrict__ cbar_col,
@@ -424,11 +434,24 @@ __global__ void __launch_bounds__(256) k_compact(int64_t M, const int64_t* __res
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < M; r += nwarps) {
-    const int64_t s = nprod_off[r], d = crpt[r], n = crpt[r + 1] - d;
-    for (int64_t e = lane; e < n; e += 32) {
-      ccol[d + e] = cbar_col[s + e];
-      cval[d + e] = cbar_val[s + e];
+  for (int64_t r0 = warp * 32; r0 < M; r0 += nwarps * 32) {
+    const int64_t r = min(r0 + lane, M);
+    const int64_t cs = crpt[r];
+    const int64_t delta = (r < M ? nprod_off[r] : 0) - cs;  // source - destination
+    const int64_t cbeg = __shfl_sync(0xffffffffu, cs, 0);
+    const int64_t cend = crpt[min(r0 + 32, M)];
+    for (int64_t e = cbeg + lane; e - lane < cend; e += 32) {
+      int lo = 0;  // row of element e: last lane whose C start <= e
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int64_t v = __shfl_sync(0xffffffffu, cs, lo + step);
+        if (v <= e) lo += step;
+      }
+      const int64_t d = __shfl_sync(0xffffffffu, delta, lo);
+      if (e < cend) {
+        ccol[e] = cbar_col[e + d];
+        cval[e] = cbar_val[e + d];
+      }
     }
   }
 }
@@ -481,10 +504,12 @@ static int num_sms() {
 
 int64_t scan_tiles(int64_t n) { return (n + kScanTile - 1) / kScanTile; }
 
+int64_t nprod_tiles(int64_t M) { return (M + kNpTile - 1) / kNpTile; }
+
 cudaError_t launch_nprod_scan(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod_off,
                               unsigned long long* status, unsigned int* counter, DevSummary* summary,
                               cudaStream_t st) {
-  const int64_t tiles = scan_tiles(M);
+  const int64_t tiles = nprod_tiles(M);
   if (tiles > 0) k_nprod_scan<<<(unsigned)tiles, kScanThreads, 0, st>>>(A, brpt, M, nprod_off, status, counter, summary);
   return cudaGetLastError();
 }
@@ -537,10 +562,30 @@ static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, const int32
 }
 
 template <bool VALS, int OUT>
+static cudaError_t launch_tiny(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
+                              cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  constexpr int smem = tiny_block_bytes<kTinyNT, VALS>();
+  auto kern = k_tiny<VALS, OUT>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTinyNT, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t want = (n + kTinyNT - 1) / kTinyNT;
+  const int64_t cap = (int64_t)per_sm * num_sms();
+  kern<<<(unsigned)(want < cap ? want : cap), kTinyNT, smem, st>>>(A, B, rows, n, o);
+  return cudaGetLastError();
+}
+
+template <bool VALS, int OUT>
 static cudaError_t launch_tier_dispatch(int bin, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
                                         const RowOut& o, cudaStream_t st) {
   switch (bin) {
-    case 1: return launch_tier_t<BRM_TIER1, VALS, OUT>(A, B, rows, n, o, st);
+    case 1: return launch_tiny<VALS, OUT>(A, B, rows, n, o, st);
     case 2: return launch_tier_t<BRM_TIER2, VALS, OUT>(A, B, rows, n, o, st);
     case 3: return launch_tier_t<BRM_TIER3, VALS, OUT>(A, B, rows, n, o, st);
     case 4: return launch_tier_t<BRM_TIER4, VALS, OUT>(A, B, rows, n, o, st);
@@ -582,8 +627,8 @@ cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B,
 cudaError_t launch_compact(int64_t M, const int64_t* nprod_off, const int64_t* crpt, const int32_t* cbar_col,
                            const double* cbar_val, int32_t* ccol, double* cval, cudaStream_t st) {
   if (M <= 0) return cudaSuccess;
-  int64_t blocks = (M * 32 + 255) / 256;
-  const int64_t cap = (int64_t)num_sms() * 8;
+  int64_t blocks = (M + 255) / 256;  // one warp per 32 rows
+  const int64_t cap = (int64_t)num_sms() * 16;
   if (blocks > cap) blocks = cap;
   k_compact<<<(unsigned)blocks, 256, 0, st>>>(M, nprod_off, crpt, cbar_col, cbar_val, ccol, cval);
   return cudaGetLastError();

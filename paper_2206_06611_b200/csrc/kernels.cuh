@@ -18,6 +18,7 @@ struct DevSummary {
 };
 
 int64_t scan_tiles(int64_t n);
+int64_t nprod_tiles(int64_t M);
 cudaError_t launch_nprod_scan(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod_off,
                               unsigned long long* status, unsigned int* counter, DevSummary* summary,
                               cudaStream_t st);
