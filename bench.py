@@ -87,7 +87,7 @@ def stencil27_box(nx, ny, nz, seed):
 
 # tier table mirrored from csrc/brm_internal.cuh (checked by tests/test_bench_host.py)
 TIER_CAP = [0, 8, 32, 256, 768, 3072, 6656]
-TIER_LCAP = [0, 8, 32, 64, 64, 512, 512]
+TIER_LCAP = [0, 8, 32, 64, 64, 256, 512]
 NUM_BINS = 8
 
 

@@ -22,7 +22,7 @@ struct CsrView {
 //   2  register BRMerge, one warp       P <= 32,   nl <= 32
 //   3  chunked BRMerge, one warp        P <= 256,  nl <= 64   (smem ping-pong)
 //   4  chunked BRMerge, one warp        P <= 768,  nl <= 64   (smem ping-pong)
-//   5  chunked BRMerge, 128 threads     P <= 3072, nl <= 512  (smem ping-pong)
+//   5  chunked BRMerge, 128 threads     P <= 3072, nl <= 256  (smem ping-pong)
 //   6  chunked BRMerge, 256 threads     P <= 6656, nl <= 512  (smem ping-pong)
 //   7  chunked BRMerge, 512 threads, ping-pong buffers in a global workspace
 // ---------------------------------------------------------------------------
@@ -40,7 +40,7 @@ struct TierBounds {
 #define BRM_TIER2 32, 32, 32, 8
 #define BRM_TIER3 32, 256, 64, 4
 #define BRM_TIER4 32, 768, 64, 2
-#define BRM_TIER5 128, 3072, 512, 1
+#define BRM_TIER5 128, 3072, 256, 1
 #define BRM_TIER6 256, 6656, 512, 1
 constexpr int kGlobalG = 512;
 
@@ -51,7 +51,7 @@ __host__ __device__ inline TierBounds tier_bounds() {
   t.cap[2] = 32;   t.lcap[2] = 32;
   t.cap[3] = 256;  t.lcap[3] = 64;
   t.cap[4] = 768;  t.lcap[4] = 64;
-  t.cap[5] = 3072; t.lcap[5] = 512;
+  t.cap[5] = 3072; t.lcap[5] = 256;
   t.cap[6] = 6656; t.lcap[6] = 512;
   t.cap[7] = INT_MAX; t.lcap[7] = INT_MAX;
   return t;

@@ -187,13 +187,29 @@ __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const in
   if (r0 < M) {  // warp-uniform
     int nl;
     warp_rows_nprod(A, brpt, M, r0, s_np + loc, &nl);
-    if (r0 + lane < M) {
-      const int64_t s = s_np[loc + lane];
-      const int bin = tier_of(s, nl, tb);
-      atomicAdd(&s_bin_rows[bin], 1ull);
-      atomicAdd(&s_bin_nprod[bin], (unsigned long long)s);
-      atomicMax(&s_max, (unsigned long long)s);
-      atomicMax(&s_maxnl, (unsigned long long)nl);
+    const bool valid = r0 + lane < M;
+    const int64_t s = valid ? s_np[loc + lane] : 0;
+    const int bin = valid ? tier_of(s, nl, tb) : -1;
+    // warp-aggregated histogram: one shared atomic per distinct bin per warp
+    unsigned todo = __ballot_sync(0xffffffffu, valid);
+    while (todo) {
+      const int leader = __ffs(todo) - 1;
+      const int b = __shfl_sync(0xffffffffu, bin, leader);
+      const unsigned m = __ballot_sync(0xffffffffu, bin == b);
+      unsigned long long x = bin == b ? (unsigned long long)s : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == leader) {
+        atomicAdd(&s_bin_rows[b], (unsigned long long)__popc(m));
+        atomicAdd(&s_bin_nprod[b], x);
+      }
+      todo &= ~m;
+    }
+    const unsigned smax = __reduce_max_sync(0xffffffffu, (unsigned)min(s, (int64_t)0xffffffffll));
+    const unsigned lmax = __reduce_max_sync(0xffffffffu, valid ? (unsigned)nl : 0u);
+    if (lane == 0) {
+      atomicMax(&s_max, (unsigned long long)smax);
+      atomicMax(&s_maxnl, (unsigned long long)lmax);
     }
   }
   __syncthreads();
@@ -440,18 +456,35 @@ __global__ void __launch_bounds__(256) k_compact(int64_t M, const int64_t* __res
     const int64_t delta = (r < M ? nprod_off[r] : 0) - cs;  // source - destination
     const int64_t cbeg = __shfl_sync(0xffffffffu, cs, 0);
     const int64_t cend = crpt[min(r0 + 32, M)];
-    for (int64_t e = cbeg + lane; e - lane < cend; e += 32) {
-      int lo = 0;  // row of element e: last lane whose C start <= e
+    constexpr int U = 4;  // four 32-element batches in flight
+    for (int64_t eb = cbeg; eb < cend; eb += 32 * U) {
+      int32_t cv[U];
+      double vv[U];
+      int64_t dst[U];
 #pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int64_t v = __shfl_sync(0xffffffffu, cs, lo + step);
-        if (v <= e) lo += step;
+      for (int u = 0; u < U; ++u) {
+        const int64_t e = eb + 32 * u + lane;
+        int lo = 0;  // row of element e: last lane whose C start <= e
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int64_t v = __shfl_sync(0xffffffffu, cs, lo + step);
+          if (v <= e) lo += step;
+        }
+        const int64_t d = __shfl_sync(0xffffffffu, delta, lo);
+        dst[u] = e < cend ? e : -1;
+        cv[u] = 0;
+        vv[u] = 0.0;
+        if (e < cend) {
+          cv[u] = cbar_col[e + d];
+          vv[u] = cbar_val[e + d];
+        }
       }
-      const int64_t d = __shfl_sync(0xffffffffu, delta, lo);
-      if (e < cend) {
-        ccol[e] = cbar_col[e + d];
-        cval[e] = cbar_val[e + d];
-      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (dst[u] >= 0) {
+          ccol[dst[u]] = cv[u];
+          cval[dst[u]] = vv[u];
+        }
     }
   }
 }

@@ -41,9 +41,9 @@ def test_algorithmic_bytes_brute_force():
 
 
 def test_tier_of_matches_bounds():
-    nprod = np.array([0, 1, 8, 9, 32, 33, 256, 257, 768, 769, 3072, 3073, 6656, 6657, 10, 40, 600])
-    nl = np.array([0, 1, 8, 1, 32, 1, 64, 1, 64, 1, 512, 1, 512, 1, 9, 65, 513])
-    assert bench.tier_of(nprod, nl).tolist() == [0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 2, 5, 7]
+    nprod = np.array([0, 1, 8, 9, 32, 33, 256, 257, 768, 769, 3072, 3073, 6656, 6657, 10, 40, 600, 300])
+    nl = np.array([0, 1, 8, 1, 32, 1, 64, 1, 64, 1, 256, 1, 512, 1, 9, 65, 513, 257])
+    assert bench.tier_of(nprod, nl).tolist() == [0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 2, 5, 7, 6]
 
 
 def test_stencil_box_equals_cube():

@@ -87,7 +87,7 @@ def test_random_rectangular(ctx, oracle_mod, mode, seed):
     (33, [90, 93, 94]),                          # tier 5 (3072 edge)
     (64, [100, 104, 105]),                       # tier 6 (6656 edge) -> global
     (100, [90, 300]),                            # global tier
-    (3, [40, 129, 300, 513, 600, 1500]),         # many short lists (list caps 64 / 512)
+    (3, [40, 129, 257, 300, 513, 600, 1500]),    # many short lists (list caps 64 / 256 / 512)
 ])
 def test_tier_boundaries(ctx, oracle_mod, mode, list_len, specs):
     A, B = _lists_matrix(specs, list_len, 5000, seed=list_len)
