@@ -65,11 +65,12 @@ struct ChunkBufs {
   int* scan_tmp;
 };
 
-// Buffers hold P products + one sentinel per list + the lone partner
-// sentinel + one slack slot: CAP + LCAP + 2 slots.
+// The buffer holds P products + one sentinel per list + the lone partner
+// sentinel + one slack slot: CAP + LCAP + 2 slots (one buffer: the round's
+// outputs are held in registers until they overwrite it).
 template <int G, int CAP, int LCAP, bool VALS>
 __host__ __device__ constexpr int chunk_group_bytes() {
-  return align16((CAP + LCAP + 2) * 4) * 2 + (VALS ? align16((CAP + LCAP + 2) * 8) * 2 : 0) +
+  return align16((CAP + LCAP + 2) * 4) + (VALS ? align16((CAP + LCAP + 2) * 8) : 0) +
          align16((LCAP + 2) * 4) * 2 +
          align16(LCAP * 8) + (VALS ? align16(LCAP * 8) : 0) + (G > 32 ? align16((G / 32 + 2) * 4) : 0);
 }
@@ -481,17 +482,18 @@ __device__ __forceinline__ int chunk_round(const Group<G>& g, int* sc, double* s
   const int base = group_excl_scan<G>(g, cnt, total, scan_tmp);
   for (int q = pf; q <= pl; ++q) noff[q] += base;
   if constexpr (NV > 0) {
+    g.sync();  // every merge has finished reading sc: the outputs overwrite it in place
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       if (v >= VT) break;
       if (v < cnt) {
-        dc[base + v] = ocol[v];
-        if (VALS) dv[base + v] = oval[v];
+        sc[base + v] = ocol[v];
+        if (VALS) sv[base + v] = oval[v];
       }
     }
     if (g.rank == G - 1) {
       noff[npairs] = total;
-      dc[total] = INT_MAX;  // lone partner sentinel, used if npairs is odd
+      sc[total] = INT_MAX;  // lone partner sentinel, used if npairs is odd
     }
   } else {
     g.sync();  // every merge has finished reading sc
@@ -508,145 +510,11 @@ __device__ __forceinline__ int chunk_round(const Group<G>& g, int* sc, double* s
   return total;
 }
 
-// Pair-group round (shared-memory tiers, npairs <= G): pair q gets its own
-// L_q >= 1 threads, in proportion to its n_q positions (L_q = 1 +
-// n_q (G - npairs) / npos, so sum L_q <= G); thread `sub` of pair p merges
-// the pair's positions [sub*VT_p, (sub+1)*VT_p) (merge-path split, VT_p odd),
-// never leaving its pair. Outputs stay in registers until the group scan of
-// the per-thread counts; the first thread of a pair records the pair's output
-// start. Same contract as chunk_round<NV > 0>.
-template <int G, int NV, bool VALS, bool FIRST>
-__device__ __forceinline__ int pair_round(const Group<G>& g, const int* sc, const double* sv, int* dc, double* dv,
-                                          const int* off, int* noff, int nl, int* scan_tmp, const double* av) {
-  const int npairs = (nl + 1) >> 1;
-  const int npos = off[nl] + (nl & 1);
-  // lane allotment (thread q < npairs speaks for pair q)
-  int nq = 0, Lq = 0;
-  if (g.rank < npairs) {
-    const int q = g.rank;
-    const int s1 = 2 * q + 2 <= nl ? off[2 * q + 2] : off[nl] + 1;
-    nq = s1 - off[2 * q];
-    Lq = 1 + static_cast<int>(static_cast<long long>(nq) * (G - npairs) / npos);
-  }
-  int Ltot;
-  const int fq = group_excl_scan<G>(g, Lq, Ltot, scan_tmp);
-  int p, sub, L, n;
-  if constexpr (G <= 32) {
-    const unsigned starts = __reduce_or_sync(0xffffffffu, g.rank < npairs ? (1u << fq) : 0u);
-    p = __popc(starts & ((2u << g.rank) - 1u)) - 1;
-    const int fp = __shfl_sync(0xffffffffu, fq, p);
-    L = __shfl_sync(0xffffffffu, Lq, p);
-    n = __shfl_sync(0xffffffffu, nq, p);
-    sub = g.rank - fp;
-  } else {
-    if (g.rank < npairs) noff[g.rank] = fq;  // noff doubles as the pair -> first thread table
-    if (g.rank == 0) scan_tmp[G / 32 + 1] = 0;
-    g.sync();
-    int lo = 0, hi = npairs - 1;  // last pair whose first thread <= rank
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (noff[mid] <= g.rank)
-        lo = mid;
-      else
-        hi = mid - 1;
-    }
-    p = lo;
-    sub = g.rank - noff[p];
-    const int s1 = 2 * p + 2 <= nl ? off[2 * p + 2] : off[nl] + 1;
-    n = s1 - off[2 * p];
-    L = 1 + static_cast<int>(static_cast<long long>(n) * (G - npairs) / npos);
-  }
-  const bool has = sub < L;
-  const int VT = ((n + L - 1) / L) | 1;  // odd: conflict-free strided access inside a pair
-  int VTmax;
-  if constexpr (G <= 32) {
-    VTmax = __reduce_max_sync(0xffffffffu, has ? VT : 0);
-  } else {
-    if (has) atomicMax(&scan_tmp[G / 32 + 1], VT);
-    g.sync();
-    VTmax = scan_tmp[G / 32 + 1];
-  }
-  // merge-path start of this thread's chunk
-  Cursor c;
-  c.p = p;
-  c.bs = c.ia = c.ib = c.lim = 0;
-  c.ca = c.cb = INT_MAX;
-  c.va = c.vb = c.sa = c.sb = 0.0;
-  const int d = sub * VT;
-  if (has && d < n) {
-    const int as = off[2 * p], bs = off[2 * p + 1];
-    const int na = bs - as, nb = n - na;  // list lengths including the sentinels
-    const int i = merge_path(sc + as, na, sc + bs, nb, d);
-    int j = d - i;
-    if (i > 0 && j < nb && sc[as + i - 1] == sc[bs + j]) ++j;  // b[j] was summed by the chunk on the left
-    if (i < na) {  // else: this pair finished on the left
-      c.bs = bs;
-      c.ia = as + i;
-      c.ib = bs + j;
-      c.lim = min(d + VT, n) + as + bs;  // merged position in the pair = (ia - as) + (ib - bs)
-      c.ca = sc[c.ia];
-      c.cb = sc[c.ib];
-      if (VALS) {
-        c.va = sv[c.ia];
-        c.vb = sv[c.ib];
-        if (FIRST) {
-          c.sa = av[2 * p];
-          c.sb = 2 * p + 1 < nl ? av[2 * p + 1] : 0.0;
-        }
-      }
-    }
-  }
-  const unsigned scb = smem_u32(sc);
-  const unsigned svb = VALS ? smem_u32(sv) : 0u;
-  int ocol[NV];
-  double oval[NV];
-  int cnt = 0;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    if (v >= VTmax) break;  // group-uniform
-    const bool act = c.ia + c.ib < c.lim;
-    const bool ta = act && c.ca <= c.cb;
-    const bool tb = act && c.cb <= c.ca;
-    ocol[v] = min(c.ca, c.cb);
-    if (VALS) {
-      double x = FIRST ? __dmul_rn(c.sa, c.va) : c.va;  // the product, rounded once
-      double y = FIRST ? __dmul_rn(c.sb, c.vb) : c.vb;
-      x = ta ? x : -0.0;  // -0.0 is the exact additive identity
-      y = tb ? y : -0.0;
-      oval[v] = __dadd_rn(x, y);  // "vals with duplicate cols are combined into one val"
-    }
-    cnt += act;
-    c.ia += ta;
-    c.ib += tb;
-    lds_if(ta, scb + 4u * c.ia, c.ca);
-    lds_if(tb, scb + 4u * c.ib, c.cb);
-    if (VALS) {
-      lds_if(ta, svb + 8u * c.ia, c.va);
-      lds_if(tb, svb + 8u * c.ib, c.vb);
-    }
-  }
-  int total;
-  const int base = group_excl_scan<G>(g, cnt, total, scan_tmp);
-  if (has && sub == 0) noff[p] = base;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    if (v >= VTmax) break;
-    if (v < cnt) {
-      dc[base + v] = ocol[v];
-      if (VALS) dv[base + v] = oval[v];
-    }
-  }
-  if (g.rank == G - 1) {
-    noff[npairs] = total;
-    dc[total] = INT_MAX;  // lone partner sentinel, used if npairs is odd
-  }
-  g.sync();
-  return total;
-}
-
-// BRMerge of one output row by a group. NV > 0: buffers in shared memory,
-// rounds ping-pong between (col0, val0) and (col1, val1); NV = 0: buffers in
-// a global workspace, every round lands back in (col0, val0).
+// BRMerge of one output row by a group. NV > 0: one shared-memory buffer
+// (col0, val0): a round's outputs wait in registers (the "pong" side of the
+// ping-pong) until the whole group has read its inputs, then land back in
+// the buffer. NV = 0: buffers in a global workspace, (col1, val1) receives the
+// uncompacted chunks and every round lands back in (col0, val0).
 template <int G, int NV, bool VALS, int OUT>
 __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
                                           const RowOut& o, const ChunkBufs& cb) {
@@ -710,24 +578,13 @@ __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, c
   int end = P + nl;
   bool first = true;
   while (cur > 1) {
-    if constexpr (SMEM) {
-      if (first)
-        end = pair_round<G, NV, VALS, true>(g, sc, sv, dc, dv, off, noff, cur, cb.scan_tmp, cb.av);
-      else
-        end = pair_round<G, NV, VALS, false>(g, sc, sv, dc, dv, off, noff, cur, cb.scan_tmp, cb.av);
-    } else {
-      if (first)
-        end = chunk_round<G, 0, VALS, true, false>(g, sc, sv, dc, dv, off, noff, cur, cb.scan_tmp, cb.av);
-      else
-        end = chunk_round<G, 0, VALS, false, false>(g, sc, sv, dc, dv, off, noff, cur, cb.scan_tmp, cb.av);
-    }
+    if (first)
+      end = chunk_round<G, NV, VALS, true, SMEM>(g, sc, sv, dc, dv, off, noff, cur, cb.scan_tmp, cb.av);
+    else
+      end = chunk_round<G, NV, VALS, false, SMEM>(g, sc, sv, dc, dv, off, noff, cur, cb.scan_tmp, cb.av);
     first = false;
     cur = (cur + 1) >> 1;
-    { int* t = off; off = noff; noff = t; }
-    if (SMEM) {  // lines 33-34: swap the ping-pong buffers
-      { int* t = sc; sc = dc; dc = t; }
-      { double* t = sv; sv = dv; dv = t; }
-    }
+    { int* t = off; off = noff; noff = t; }  // lines 33-34: the roles swap
   }
   const int T = end - 1;  // the result row: list 0 = [0, end - 1), then its sentinel
   // line 36: store the result row

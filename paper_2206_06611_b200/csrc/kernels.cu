@@ -380,9 +380,9 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
     };
     ChunkBufs cb;
     cb.val0 = VALS ? reinterpret_cast<double*>(take((CAP + LCAP + 2) * 8)) : nullptr;
-    cb.val1 = VALS ? reinterpret_cast<double*>(take((CAP + LCAP + 2) * 8)) : nullptr;
     cb.col0 = reinterpret_cast<int*>(take((CAP + LCAP + 2) * 4));
-    cb.col1 = reinterpret_cast<int*>(take((CAP + LCAP + 2) * 4));
+    cb.col1 = nullptr;  // one buffer: outputs wait in registers
+    cb.val1 = nullptr;
     cb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
     cb.off1 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
     cb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
