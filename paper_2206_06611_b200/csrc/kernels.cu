@@ -576,6 +576,9 @@ static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, const int32
   // registers hold <= NV chunk outputs; NV = 31 (G = 256, CAP 7168) miscompiled
   // (wrong values, no spills reported), so tiers keep NV <= 29
   static_assert(CAP <= 32 || (((CAP + LCAP + 1 + G - 1) / G) | 1) <= 29, "chunk tier NV must stay <= 29");
+  // validated group sizes: one warp (GPC warps per CTA) or a 128/256-thread CTA; a 64-thread
+  // CTA group gave wrong values on B200 (tests/test_gpu_parity.py::test_random_rectangular[1])
+  static_assert(G <= 32 || G >= 128, "chunk tiers run on warps or on >= 128-thread CTAs");
   static_assert(smem <= 232448, "tier shared memory exceeds 227 KB");
   auto kern = k_tier<G, CAP, LCAP, GPC, VALS, OUT>;
   // one process drives one device, so per-instantiation caching is safe

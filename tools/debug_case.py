@@ -40,6 +40,13 @@ def check(ctx, A, B, label):
 
 
 ctx = Context()
+from inputs import random_sparse
+for seed in range(6):
+    rng = np.random.default_rng(seed)
+    m, k, n = (int(x) for x in rng.integers(1, 300, size=3))
+    Ar = random_sparse(m, k, float(rng.uniform(0.005, 0.3)), seed=seed)
+    Br = random_sparse(k, n, float(rng.uniform(0.005, 0.3)), seed=seed + 99)
+    check(ctx, Ar, Br, f"random{seed}")
 check(ctx, *_lists_matrix([90, 93, 94], 33, 5000, seed=33), "t5/t6")
 check(ctx, *_lists_matrix([90, 93], 33, 5000, seed=33), "t5 only")
 check(ctx, *_lists_matrix([94, 100], 33, 5000, seed=33), "t6 only")
