@@ -510,6 +510,242 @@ __device__ __forceinline__ int chunk_round(const Group<G>& g, int* sc, double* s
   return total;
 }
 
+// ===========================================================================
+// Record tiers (shared memory, tiers 3-6): the rounds move 8-byte records
+// {col, slot} where `slot` names the value slot of the element's partial
+// sum; values never move. A duplicate column adds the right element's
+// partial sum into the left element's slot (left + right, Alg. 1's combine)
+// and keeps the left slot, so after each round every record's slot holds
+// the sum of its column over its subtree -- the Algorithm-1 tree order.
+// ===========================================================================
+__device__ __forceinline__ void lds_if(bool p, unsigned addr, int2& v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q ld.shared.v2.b32 {%0, %1}, [%2];\n\t}"
+               : "+r"(v.x), "+r"(v.y)
+               : "r"(addr), "r"((unsigned)p));
+}
+
+struct RecBufs {
+  int2* rec;      // P + nl + 2 records: sentinel-terminated lists
+  double* val;    // P value slots (products, then partial sums)
+  int* off0;
+  int* off1;
+  int64_t* bst;
+  double* av;
+  int* scan_tmp;
+};
+
+template <int G, int CAP, int LCAP, bool VALS>
+__host__ __device__ constexpr int rec_group_bytes() {
+  return align16((CAP + LCAP + 2) * 8) + (VALS ? align16(CAP * 8) : 0) + align16((LCAP + 2) * 4) * 2 +
+         align16(LCAP * 8) + (VALS ? align16(LCAP * 8) : 0) + (G > 32 ? align16((G / 32 + 2) * 4) : 0);
+}
+
+// merge path over the .x (column) fields of two record lists
+__device__ __forceinline__ int merge_path_rec(const int2* a, int la, const int2* b, int lb, int diag) {
+  int lo = diag - lb > 0 ? diag - lb : 0;
+  int hi = diag < la ? diag : la;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid].x <= b[diag - 1 - mid].x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// One round over the nl sentinel-terminated record lists of `rec` (offsets
+// off[0..nl]); same partition as chunk_round (G chunks of VT odd positions,
+// threads cross into the next pair when both sentinels merge). Outputs wait
+// in registers and overwrite `rec` compacted once the group has read it.
+template <int G, int NV, bool VALS>
+__device__ __forceinline__ int rec_round(const Group<G>& g, int2* rec, double* val, const int* off, int* noff,
+                                         int nl, int* scan_tmp) {
+  const int npairs = (nl + 1) >> 1;
+  const int npos = off[nl] + (nl & 1);
+  const int VT = ((npos + G - 1) / G) | 1;
+  const int g0 = min(g.rank * VT, npos), g1 = min(g0 + VT, npos);
+  int pf = 0, pl = -1;
+  int p = 0, bs = 0, ia = 0, ib = 0, lim = 0;
+  int2 ra = make_int2(INT_MAX, 0), rb = make_int2(INT_MAX, 0);
+  if (g0 < g1) {
+    int lo = 0, hi = npairs - 1;  // last pair starting at or before g0
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (off[2 * mid] <= g0)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    p = lo;
+    const int as = off[2 * p];
+    bs = off[2 * p + 1];
+    const int bend = 2 * p + 2 <= nl ? off[2 * p + 2] : off[nl] + 1;
+    const int na = bs - as, nb = bend - bs;
+    const int d = g0 - as;
+    if (d == 0) {
+      pf = pl = p;
+      noff[p] = 0;
+    }
+    const int i = merge_path_rec(rec + as, na, rec + bs, nb, d);
+    int j = d - i;
+    if (i > 0 && j < nb && rec[as + i - 1].x == rec[bs + j].x) ++j;  // b[j] was summed on the left
+    if (i == na) {  // pair p finished on the left
+      if (g0 + 1 < g1) {
+        ++p;
+        pf = pl = p;
+        noff[p] = 0;
+        ia = off[2 * p];
+        bs = ib = off[2 * p + 1];
+        lim = g1 + bs;
+        ra = rec[ia];
+        rb = rec[ib];
+      }
+    } else {
+      ia = as + i;
+      ib = bs + j;
+      lim = g1 + bs;
+      ra = rec[ia];
+      rb = rec[ib];
+    }
+  }
+  const unsigned recb = smem_u32(rec);
+  const unsigned valb = VALS ? smem_u32(val) : 0u;
+  int ocol[NV], oslot[NV];
+  int cnt = 0;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if (v >= VT) break;  // group-uniform
+    const bool act = ia + ib < lim;
+    const bool ta = act && ra.x <= rb.x;
+    const bool tb = act && rb.x <= ra.x;
+    ocol[v] = min(ra.x, rb.x);
+    oslot[v] = ta ? ra.y : rb.y;
+    if (VALS) {  // equal columns: val[left] = val[left] + val[right]
+      const bool dup = ta && tb && ra.x != INT_MAX;
+      double x = 0.0, y = 0.0;
+      lds_if(dup, valb + 8u * ra.y, x);
+      lds_if(dup, valb + 8u * rb.y, y);
+      if (dup) val[ra.y] = __dadd_rn(x, y);
+    }
+    cnt += act;
+    ia += ta;
+    ib += tb;
+    lds_if(ta, recb + 8u * ia, ra);
+    lds_if(tb, recb + 8u * ib, rb);
+    if (act && ocol[v] == INT_MAX && ia + ib < lim) {  // pair p done, chunk not: enter pair p+1
+      if (pl < 0) pf = p + 1;
+      ++p;
+      pl = p;
+      noff[p] = cnt;
+      ia = off[2 * p];
+      bs = ib = off[2 * p + 1];
+      lim = g1 + bs;
+      ra = rec[ia];
+      rb = rec[ib];
+    }
+  }
+  int total;
+  const int base = group_excl_scan<G>(g, cnt, total, scan_tmp);
+  for (int q = pf; q <= pl; ++q) noff[q] += base;
+  g.sync();  // every merge has finished reading rec: the outputs overwrite it in place
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if (v >= VT) break;
+    if (v < cnt) rec[base + v] = make_int2(ocol[v], oslot[v]);
+  }
+  if (g.rank == G - 1) {
+    noff[npairs] = total;
+    rec[total] = make_int2(INT_MAX, 0);  // lone partner sentinel, used if npairs is odd
+  }
+  g.sync();
+  return total;
+}
+
+template <int G, int NV, bool VALS, int OUT>
+__device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
+                                        const RowOut& o, const RecBufs& rb) {
+  const int rank = g.rank;
+  const int64_t a0 = A.rpt[row];
+  const int nl = static_cast<int>(A.rpt[row + 1] - a0);
+  int* off = rb.off0;
+  int* noff = rb.off1;
+  // multiplying phase (Alg. 1 lines 10-15): list offsets (list l at record
+  // off[l] = E_l + l, products E_l..), then the products themselves
+  int P = 0;
+  for (int lb = 0; lb < nl; lb += G) {
+    const int l = lb + rank;
+    int n = 0;
+    if (l < nl) {
+      const int k = __ldg(A.col + a0 + l);
+      const int64_t st = __ldg(B.rpt + k);
+      n = static_cast<int>(__ldg(B.rpt + k + 1) - st);
+      rb.bst[l] = st;
+      if (VALS) rb.av[l] = __ldg(A.val + a0 + l);
+    }
+    int tot;
+    const int ex = group_excl_scan<G>(g, n, tot, rb.scan_tmp);
+    if (l < nl) {
+      off[l] = P + ex + l;
+      rb.rec[P + ex + l + n] = make_int2(INT_MAX, 0);  // sentinel of list l
+    }
+    P += tot;
+  }
+  if (rank == 0) {
+    off[nl] = P + nl;
+    rb.rec[P + nl] = make_int2(INT_MAX, 0);  // lone partner sentinel if nl is odd
+  }
+  g.sync();
+  {
+    int l = 0;
+    for (int e0 = rank; e0 < P; e0 += 2 * G) {  // two products per thread in flight
+      const int e1 = e0 + G;
+      while (off[l + 1] - (l + 1) <= e0) ++l;
+      int l1 = l;
+      if (e1 < P)
+        while (off[l1 + 1] - (l1 + 1) <= e1) ++l1;
+      const int64_t s0 = rb.bst[l] + (e0 - (off[l] - l));
+      const int64_t s1 = rb.bst[l1] + (e1 - (off[l1] - l1));
+      const int c0 = __ldg(B.col + s0);
+      const int c1 = e1 < P ? __ldg(B.col + s1) : 0;
+      double v0 = 0.0, v1 = 0.0;
+      if (VALS) {
+        v0 = __ldg(B.val + s0);
+        if (e1 < P) v1 = __ldg(B.val + s1);
+      }
+      rb.rec[e0 + l] = make_int2(c0, e0);
+      if (VALS) rb.val[e0] = __dmul_rn(rb.av[l], v0);  // line 12: the product, rounded once
+      if (e1 < P) {
+        rb.rec[e1 + l1] = make_int2(c1, e1);
+        if (VALS) rb.val[e1] = __dmul_rn(rb.av[l1], v1);
+      }
+      l = l1;
+    }
+  }
+  g.sync();
+  // accumulating phase (lines 21-35)
+  int cur = nl;
+  int end = P + nl;
+  while (cur > 1) {
+    end = rec_round<G, NV, VALS>(g, rb.rec, rb.val, off, noff, cur, rb.scan_tmp);
+    cur = (cur + 1) >> 1;
+    int* t = off;  // lines 33-34
+    off = noff;
+    noff = t;
+  }
+  const int T = end - 1;  // the result row: list 0 = records [0, end - 1), then its sentinel
+  if (OUT != OUT_SYMBOLIC) {  // line 36
+    const int64_t ob = o.base[row];
+    for (int e = rank; e < T; e += G) {
+      const int2 r = rb.rec[e];
+      o.col[ob + e] = r.x;
+      if (VALS) o.val[ob + e] = rb.val[r.y];
+    }
+  }
+  if (OUT != OUT_C && rank == 0) o.row_size[row] = T;
+  g.sync();
+}
+
 // BRMerge of one output row by a group. NV > 0: one shared-memory buffer
 // (col0, val0): a round's outputs wait in registers (the "pong" side of the
 // ping-pong) until the whole group has read its inputs, then land back in

@@ -353,7 +353,7 @@ __global__ void k_heavy_info(CsrView A, const int64_t* __restrict__ nprod_off,
 
 // Shared-memory tiers: GPC groups of G threads per CTA, one row per group at a
 // time, the group's buffers in its slice of dynamic shared memory. CAP <= 32:
-// register tier (reg_row), else chunk tier (chunk_row).
+// register tier (reg_row), else record tier (rec_row).
 template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT>
 __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const int32_t* __restrict__ rows,
                                                  int64_t nrows, RowOut o) {
@@ -371,25 +371,23 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
     for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
       reg_row<G, VALS, OUT>(g, A, B, rows[r], o, rb);
   } else {
-    constexpr int bytes = chunk_group_bytes<G, CAP, LCAP, VALS>();
+    constexpr int bytes = rec_group_bytes<G, CAP, LCAP, VALS>();
     unsigned char* p = smem + gid * bytes;
     auto take = [&](int n) {
       unsigned char* q = p;
       p += align16(n);
       return q;
     };
-    ChunkBufs cb;
-    cb.val0 = VALS ? reinterpret_cast<double*>(take((CAP + LCAP + 2) * 8)) : nullptr;
-    cb.col0 = reinterpret_cast<int*>(take((CAP + LCAP + 2) * 4));
-    cb.col1 = nullptr;  // one buffer: outputs wait in registers
-    cb.val1 = nullptr;
-    cb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
-    cb.off1 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
-    cb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
-    cb.av = VALS ? reinterpret_cast<double*>(take(LCAP * 8)) : nullptr;
-    cb.scan_tmp = G > 32 ? reinterpret_cast<int*>(take((G / 32 + 2) * 4)) : nullptr;
+    RecBufs rb;
+    rb.rec = reinterpret_cast<int2*>(take((CAP + LCAP + 2) * 8));
+    rb.val = VALS ? reinterpret_cast<double*>(take(CAP * 8)) : nullptr;
+    rb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
+    rb.off1 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
+    rb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
+    rb.av = VALS ? reinterpret_cast<double*>(take(LCAP * 8)) : nullptr;
+    rb.scan_tmp = G > 32 ? reinterpret_cast<int*>(take((G / 32 + 2) * 4)) : nullptr;
     for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
-      chunk_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, VALS, OUT>(g, A, B, rows[r], o, cb);
+      rec_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, VALS, OUT>(g, A, B, rows[r], o, rb);
   }
 }
 
@@ -571,7 +569,7 @@ template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT>
 static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
                                  cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  constexpr int per_group = CAP <= 32 ? reg_group_bytes<G, VALS>() : chunk_group_bytes<G, CAP, LCAP, VALS>();
+  constexpr int per_group = CAP <= 32 ? reg_group_bytes<G, VALS>() : rec_group_bytes<G, CAP, LCAP, VALS>();
   constexpr int smem = per_group * GPC;
   // registers hold <= NV chunk outputs; NV = 31 (G = 256, CAP 7168) miscompiled
   // (wrong values, no spills reported), so tiers keep NV <= 29
