@@ -117,7 +117,22 @@ __device__ __forceinline__ void warp_rows_nprod(const CsrView& A, const int64_t*
   const int64_t pend = A.rpt[min(r0 + 32, M)];
   const int64_t pbeg = __shfl_sync(0xffffffffu, rs, 0);
   const int64_t rnext = __shfl_down_sync(0xffffffffu, rs, 1);
-  *nl_out = lane < 31 ? (int)(rnext - rs) : (int)(pend - rs);
+  const int nl = lane < 31 ? (int)(rnext - rs) : (int)(pend - rs);
+  *nl_out = nl;
+  if (__reduce_max_sync(0xffffffffu, r0 + lane < M ? (unsigned)nl : 0u) <= 64u) {
+    // short rows: one lane per row, independent gathers (no shuffles)
+    int64_t acc = 0;
+    if (r0 + lane < M) {
+#pragma unroll 4
+      for (int64_t p = rs; p < rs + nl; ++p) {
+        const int k = __ldg(A.col + p);
+        acc += __ldg(brpt + k + 1) - __ldg(brpt + k);
+      }
+    }
+    out[lane] = acc;
+    __syncwarp();
+    return;
+  }
   out[lane] = 0;
   __syncwarp();
   for (int64_t pb = pbeg; pb < pend; pb += 32 * U) {
