@@ -18,12 +18,12 @@ struct CsrView {
 // ---------------------------------------------------------------------------
 // Row tiers. A row with n_prod = P > 0 and num_list = nl
 // (= nnz(A_i*)) goes to the first tier t whose (cap, lcap) admits it:
-//   1  register BRMerge, 8-lane group   P <= 8,    nl <= 8
+//   1  one thread per row (Alg. 1)      P <= 8,    nl <= 8
 //   2  register BRMerge, one warp       P <= 32,   nl <= 32
-//   3  chunked BRMerge, one warp        P <= 256,  nl <= 64   (smem ping-pong)
-//   4  chunked BRMerge, one warp        P <= 768,  nl <= 64   (smem ping-pong)
-//   5  chunked BRMerge, 128 threads     P <= 3072, nl <= 256  (smem ping-pong)
-//   6  chunked BRMerge, 256 threads     P <= 6656, nl <= 512  (smem ping-pong)
+//   3  record BRMerge, one warp         P <= 256,  nl <= 64   (smem records)
+//   4  record BRMerge, 64 threads       P <= 768,  nl <= 64   (smem records)
+//   5  record BRMerge, 128 threads      P <= 3072, nl <= 256  (smem records)
+//   6  record BRMerge, 256 threads      P <= 6656, nl <= 512  (smem records)
 //   7  chunked BRMerge, 512 threads, ping-pong buffers in a global workspace
 // ---------------------------------------------------------------------------
 constexpr int kBinEmpty = 0;
@@ -39,7 +39,7 @@ struct TierBounds {
 #define BRM_TIER1 8, 8, 8, 32
 #define BRM_TIER2 32, 32, 32, 8
 #define BRM_TIER3 32, 256, 64, 4
-#define BRM_TIER4 32, 768, 64, 2
+#define BRM_TIER4 64, 768, 64, 1
 #define BRM_TIER5 128, 3072, 256, 1
 #define BRM_TIER6 256, 6656, 512, 1
 constexpr int kGlobalG = 512;

@@ -1,28 +1,21 @@
-// engine.cuh -- the BRMerge accumulation of one output row by a thread group
-// (Algorithm 1), in two GPU forms that compute exactly the
-// rounds of Algorithm 1 (pairs (0,1),(2,3),... of the current lists merged,
-// an odd trailing list copied, equal columns summed as left + right), so the
-// values are bit-identical to the paper's sequential tree order (R1).
+// engine.cuh -- the BRMerge accumulation of one output row (Algorithm 1,
+// PAPER.md:165-218) in four GPU forms. All compute exactly the rounds of
+// Algorithm 1 -- pairs (0,1),(2,3),... of the current lists merged, an odd
+// trailing list copied, equal columns combined as left + right -- so values
+// are bit-identical to the paper's sequential tree order (R1).
 //
-// reg_row  (tiers 1-2, P <= G <= 32): register-resident BRMerge. Lane e holds
-//   product e of the row (multiplying phase, lines 10-15). Each round merges
-//   list pairs in registers: a lane finds the rank of its column in the
-//   partner list by a shuffle binary search (warp-shuffle merge path), left
-//   lanes add the partner's equal-column value, right duplicates retire, and
-//   every survivor moves to its merged position through a G-slot shared
-//   ping-pong buffer.
-//
-// chunk_row (tiers 3-7): shared-memory (or global-workspace) ping-pong. The
-//   multiplying phase copies the B rows of A_i* into the ping buffer as
-//   compact sorted lists (cp.async, coalesced); the scaling by A_ik is fused
-//   into the first merge round (one rounding per product, Alg. 1 line 12).
-//   Each round is ONE pass: the round's merged positions (the concatenation
-//   of all pairs) are split into G equal odd-length chunks; a thread locates
-//   its chunk's pair and merge-path split and merges it with a branch-free
-//   predicated step (sum on equal columns), crossing into later pairs when
-//   one ends, holding its outputs in registers; a group scan of the
-//   per-thread output counts gives each thread its compacted position in the
-//   pong buffer and the next round's list offsets; the buffers swap.
+// tiny_row  (tier 1, P <= 8): one thread per row runs Algorithm 1 literally,
+//   its ping-pong buffers in thread-interleaved shared memory.
+// reg_row   (tier 2, P <= 32): one warp; lane e holds product e; each round
+//   merges list pairs in registers (shuffle rank search = warp-shuffle merge
+//   path, ballot arithmetic for positions, a 32-slot shared exchange).
+// rec_row   (tiers 3-6): a warp or CTA per row; rounds move 8-byte records
+//   {col, value slot} through one shared buffer, values stay in place and
+//   duplicates accumulate into the left slot; each round is one pass of G
+//   merge-path chunks of odd length VT; outputs wait in registers until the
+//   group scan gives their compacted positions.
+// chunk_row (tier 7): the same chunk partition over column/value ping-pong
+//   buffers in a global workspace, one 512-thread CTA per heavy row.
 #pragma once
 #include "brm_internal.cuh"
 
@@ -50,9 +43,10 @@ __host__ __device__ constexpr int reg_group_bytes() {
   return align16(G * 4) * 3 + (VALS ? align16(G * 8) : 0);
 }
 
-// Working arrays of one chunk-tier group. Lists of a round are compact in
-// col[0]/val[0] ("src"); col[1]/val[1] ("dst") receive the merged chunks.
-// off[0] holds the current list offsets (nl + 1), off[1] the next round's.
+// Working arrays of one global-tier row (global workspace slice). Lists of a
+// round are compact in col0/val0 ("src"); col1/val1 ("dst") receive the
+// merged chunks. off0 holds the current list offsets (nl + 1), off1 the
+// next round's.
 struct ChunkBufs {
   int* col0;
   int* col1;
@@ -64,16 +58,6 @@ struct ChunkBufs {
   double* av;    // A_ik of each list
   int* scan_tmp;
 };
-
-// The buffer holds P products + one sentinel per list + the lone partner
-// sentinel + one slack slot: CAP + LCAP + 2 slots (one buffer: the round's
-// outputs are held in registers until they overwrite it).
-template <int G, int CAP, int LCAP, bool VALS>
-__host__ __device__ constexpr int chunk_group_bytes() {
-  return align16((CAP + LCAP + 2) * 4) + (VALS ? align16((CAP + LCAP + 2) * 8) : 0) +
-         align16((LCAP + 2) * 4) * 2 +
-         align16(LCAP * 8) + (VALS ? align16(LCAP * 8) : 0) + (G > 32 ? align16((G / 32 + 2) * 4) : 0);
-}
 
 // ===========================================================================
 // Tiny tier (tier 1: P <= 8, nl <= 8): one THREAD per row runs Algorithm 1
@@ -307,13 +291,6 @@ __device__ __forceinline__ void lds_if(bool p, unsigned addr, double& v) {
                : "+d"(v)
                : "r"(addr), "r"((unsigned)p));
 }
-__device__ __forceinline__ void cp_async_4(void* smem, const void* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Lists of a round are sentinel-terminated: list l = [off[l], off[l+1]-1)
 // followed by one INT_MAX slot at off[l+1]-1. If nl is odd, the trailing
@@ -348,16 +325,14 @@ __device__ __forceinline__ void enter_pair(Cursor& c, int p, const int* sc, cons
   }
 }
 
-// One BRMerge round (Alg. 1 lines 22-34) over the nl sentinel-terminated
-// lists of sc/sv (offsets off[0..nl]). The round's positions are split into
-// G chunks of VT (odd) positions. The merged lists are written compact and
-// sentinel-terminated, with offsets noff[0..npairs]:
-//   NV > 0: into dc/dv (the other ping-pong buffer), each thread holding its
-//           <= NV outputs in registers until the group scan gives its base;
-//   NV = 0: (global tier, unbounded VT) into dc/dv at the chunk's own
-//           positions, then copied back compacted into sc/sv.
-// Returns the new end offset (noff[npairs]).
-template <int G, int NV, bool VALS, bool FIRST, bool SMEM>
+// One BRMerge round (Alg. 1 lines 22-34) of the global tier over the nl
+// sentinel-terminated lists of sc/sv (offsets off[0..nl], global workspace).
+// The round's positions are split into G chunks of VT (odd) positions; a
+// thread merges its chunk into dc/dv at the chunk's own positions, then --
+// once the group scan has given its compacted base -- copies it back into
+// sc/sv; the next round's offsets go to noff[0..npairs]. Returns the new end
+// offset (noff[npairs]).
+template <int G, bool VALS, bool FIRST>
 __device__ __forceinline__ int chunk_round(const Group<G>& g, int* sc, double* sv,
                                            int* dc, double* dv, const int* off,
                                            int* noff, int nl, int* scan_tmp, const double* av) {
@@ -417,50 +392,31 @@ __device__ __forceinline__ int chunk_round(const Group<G>& g, int* sc, double* s
       }
     }
   }
-  const unsigned scb = SMEM ? smem_u32(sc) : 0u;
-  const unsigned svb = (SMEM && VALS) ? smem_u32(sv) : 0u;
-  constexpr int NR = NV > 0 ? NV : 1;
-  int ocol[NR];
-  double oval[NR];
-  auto step = [&](int v) {
+  for (int v = 0; v < VT; ++v) {
     const bool act = c.ia + c.ib < c.lim;
     const bool ta = act && c.ca <= c.cb;
     const bool tb = act && c.cb <= c.ca;
     const int oc = min(c.ca, c.cb);
-    double ov = 0.0;
-    if (VALS) {
-      double x = FIRST ? __dmul_rn(c.sa, c.va) : c.va;  // the product, rounded once
-      double y = FIRST ? __dmul_rn(c.sb, c.vb) : c.vb;
-      x = ta ? x : -0.0;  // -0.0 is the exact additive identity
-      y = tb ? y : -0.0;
-      ov = __dadd_rn(x, y);  // "vals with duplicate cols are combined into one val"
-    }
-    if (NV > 0) {
-      ocol[v] = oc;
-      if (VALS) oval[v] = ov;
-    } else if (act) {
+    if (act) {
       dc[g0 + cnt] = oc;
-      if (VALS) dv[g0 + cnt] = ov;
+      if (VALS) {
+        double x = FIRST ? __dmul_rn(c.sa, c.va) : c.va;  // the product, rounded once
+        double y = FIRST ? __dmul_rn(c.sb, c.vb) : c.vb;
+        x = ta ? x : -0.0;  // -0.0 is the exact additive identity
+        y = tb ? y : -0.0;
+        dv[g0 + cnt] = __dadd_rn(x, y);  // "vals with duplicate cols are combined into one val"
+      }
     }
     cnt += act;
     c.ia += ta;
     c.ib += tb;
-    if (SMEM) {
-      lds_if(ta, scb + 4u * c.ia, c.ca);
-      lds_if(tb, scb + 4u * c.ib, c.cb);
-      if (VALS) {
-        lds_if(ta, svb + 8u * c.ia, c.va);
-        lds_if(tb, svb + 8u * c.ib, c.vb);
-      }
-    } else {
-      if (ta) {
-        c.ca = sc[c.ia];
-        if (VALS) c.va = sv[c.ia];
-      }
-      if (tb) {
-        c.cb = sc[c.ib];
-        if (VALS) c.vb = sv[c.ib];
-      }
+    if (ta) {
+      c.ca = sc[c.ia];
+      if (VALS) c.va = sv[c.ia];
+    }
+    if (tb) {
+      c.cb = sc[c.ib];
+      if (VALS) c.vb = sv[c.ib];
     }
     if (act && oc == INT_MAX && c.ia + c.ib < c.lim) {  // pair p done, chunk not: enter pair p+1
       if (pl < 0) pf = c.p + 1;
@@ -468,34 +424,11 @@ __device__ __forceinline__ int chunk_round(const Group<G>& g, int* sc, double* s
       noff[c.p + 1] = cnt;
       enter_pair<VALS, FIRST>(c, c.p + 1, sc, sv, off, av, nl, g1);
     }
-  };
-  if constexpr (NV > 0) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      if (v >= VT) break;  // group-uniform
-      step(v);
-    }
-  } else {
-    for (int v = 0; v < VT; ++v) step(0);
   }
   int total;
   const int base = group_excl_scan<G>(g, cnt, total, scan_tmp);
   for (int q = pf; q <= pl; ++q) noff[q] += base;
-  if constexpr (NV > 0) {
-    g.sync();  // every merge has finished reading sc: the outputs overwrite it in place
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      if (v >= VT) break;
-      if (v < cnt) {
-        sc[base + v] = ocol[v];
-        if (VALS) sv[base + v] = oval[v];
-      }
-    }
-    if (g.rank == G - 1) {
-      noff[npairs] = total;
-      sc[total] = INT_MAX;  // lone partner sentinel, used if npairs is odd
-    }
-  } else {
+  {
     g.sync();  // every merge has finished reading sc
     for (int e = 0; e < cnt; ++e) {
       sc[base + e] = dc[g0 + e];
@@ -527,6 +460,7 @@ __device__ __forceinline__ void lds_if(bool p, unsigned addr, int2& v) {
 struct RecBufs {
   int2* rec;      // P + nl + 2 records: sentinel-terminated lists
   double* val;    // P value slots (products, then partial sums)
+  int* owner;     // P 16-bit entries: list of each product (multiplying phase)
   int* off0;
   int* off1;
   int64_t* bst;
@@ -536,7 +470,7 @@ struct RecBufs {
 
 template <int G, int CAP, int LCAP, bool VALS>
 __host__ __device__ constexpr int rec_group_bytes() {
-  return align16((CAP + LCAP + 2) * 8) + (VALS ? align16(CAP * 8) : 0) + align16((LCAP + 2) * 4) * 2 +
+  return align16((CAP + LCAP + 2) * 8) + (VALS ? align16(CAP * 8) : 0) + align16(CAP * 2) + align16((LCAP + 2) * 4) * 2 +
          align16(LCAP * 8) + (VALS ? align16(LCAP * 8) : 0) + (G > 32 ? align16((G / 32 + 2) * 4) : 0);
 }
 
@@ -697,29 +631,19 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
   }
   g.sync();
   {
-    int l = 0;
-    for (int e0 = rank; e0 < P; e0 += 2 * G) {  // two products per thread in flight
-      const int e1 = e0 + G;
-      while (off[l + 1] - (l + 1) <= e0) ++l;
-      int l1 = l;
-      if (e1 < P)
-        while (off[l1 + 1] - (l1 + 1) <= e1) ++l1;
-      const int64_t s0 = rb.bst[l] + (e0 - (off[l] - l));
-      const int64_t s1 = rb.bst[l1] + (e1 - (off[l1] - l1));
-      const int c0 = __ldg(B.col + s0);
-      const int c1 = e1 < P ? __ldg(B.col + s1) : 0;
-      double v0 = 0.0, v1 = 0.0;
-      if (VALS) {
-        v0 = __ldg(B.val + s0);
-        if (e1 < P) v1 = __ldg(B.val + s1);
-      }
-      rb.rec[e0 + l] = make_int2(c0, e0);
-      if (VALS) rb.val[e0] = __dmul_rn(rb.av[l], v0);  // line 12: the product, rounded once
-      if (e1 < P) {
-        rb.rec[e1 + l1] = make_int2(c1, e1);
-        if (VALS) rb.val[e1] = __dmul_rn(rb.av[l1], v1);
-      }
-      l = l1;
+    // owner[e] = list of product e (16-bit table: nl <= 512 in these tiers),
+    // filled by one thread per list; then the products are fetched coalesced
+    unsigned short* owner = reinterpret_cast<unsigned short*>(rb.owner);
+    for (int l = rank; l < nl; l += G)
+      for (int e = off[l] - l, e1 = off[l + 1] - (l + 1); e < e1; ++e) owner[e] = static_cast<unsigned short>(l);
+    g.sync();
+#pragma unroll 2
+    for (int e = rank; e < P; e += G) {
+      const int l = owner[e];
+      const int64_t src = rb.bst[l] + (e - (off[l] - l));
+      const int c = __ldg(B.col + src);
+      rb.rec[e + l] = make_int2(c, e);
+      if (VALS) rb.val[e] = __dmul_rn(rb.av[l], __ldg(B.val + src));  // line 12: the product, rounded once
     }
   }
   g.sync();
@@ -746,15 +670,12 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
   g.sync();
 }
 
-// BRMerge of one output row by a group. NV > 0: one shared-memory buffer
-// (col0, val0): a round's outputs wait in registers (the "pong" side of the
-// ping-pong) until the whole group has read its inputs, then land back in
-// the buffer. NV = 0: buffers in a global workspace, (col1, val1) receives the
-// uncompacted chunks and every round lands back in (col0, val0).
-template <int G, int NV, bool VALS, int OUT>
+// BRMerge of one heavy output row by a CTA (global tier): the ping buffer
+// (col0, val0) holds the sentinel-terminated lists, (col1, val1) receives a
+// round's uncompacted chunks, and every round lands back in (col0, val0).
+template <int G, bool VALS, int OUT>
 __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
                                           const RowOut& o, const ChunkBufs& cb) {
-  constexpr bool SMEM = NV > 0;
   const int rank = g.rank;
   const int64_t a0 = A.rpt[row];
   const int nl = static_cast<int>(A.rpt[row + 1] - a0);
@@ -798,15 +719,9 @@ __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, c
     for (int e = rank; e < P; e += G) {
       while (off[l + 1] - (l + 1) <= e) ++l;  // E_{l+1} <= e
       const int64_t src = cb.bst[l] + (e - (off[l] - l));
-      if (SMEM) {
-        cp_async_4(sc + e + l, B.col + src);
-        if (VALS) cp_async_8(sv + e + l, B.val + src);
-      } else {
-        sc[e + l] = __ldg(B.col + src);
-        if (VALS) sv[e + l] = __ldg(B.val + src);
-      }
+      sc[e + l] = __ldg(B.col + src);
+      if (VALS) sv[e + l] = __ldg(B.val + src);
     }
-    if (SMEM) cp_async_wait_all();
   }
   g.sync();
   // accumulating phase (lines 21-35)
@@ -815,9 +730,9 @@ __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, c
   bool first = true;
   while (cur > 1) {
     if (first)
-      end = chunk_round<G, NV, VALS, true, SMEM>(g, sc, sv, dc, dv, off, noff, cur, cb.scan_tmp, cb.av);
+      end = chunk_round<G, VALS, true>(g, sc, sv, dc, dv, off, noff, cur, cb.scan_tmp, cb.av);
     else
-      end = chunk_round<G, NV, VALS, false, SMEM>(g, sc, sv, dc, dv, off, noff, cur, cb.scan_tmp, cb.av);
+      end = chunk_round<G, VALS, false>(g, sc, sv, dc, dv, off, noff, cur, cb.scan_tmp, cb.av);
     first = false;
     cur = (cur + 1) >> 1;
     { int* t = off; off = noff; noff = t; }  // lines 33-34: the roles swap

@@ -396,6 +396,7 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
     RecBufs rb;
     rb.rec = reinterpret_cast<int2*>(take((CAP + LCAP + 2) * 8));
     rb.val = VALS ? reinterpret_cast<double*>(take(CAP * 8)) : nullptr;
+    rb.owner = reinterpret_cast<int*>(take(CAP * 2));
     rb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
     rb.off1 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
     rb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
   cb.bst = reinterpret_cast<int64_t*>(take(nl * 8));
   cb.av = VALS ? reinterpret_cast<double*>(take(nl * 8)) : nullptr;
   cb.scan_tmp = scan_tmp;
-  chunk_row<kGlobalG, 0, VALS, OUT>(g, A, B, row, o, cb);
+  chunk_row<kGlobalG, VALS, OUT>(g, A, B, row, o, cb);
 }
 
 // Step 6 of Fig. 4a: copy each row of C_bar (at its n_prod offset) to C. A
@@ -589,9 +590,6 @@ static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, const int32
   // registers hold <= NV chunk outputs; NV = 31 (G = 256, CAP 7168) miscompiled
   // (wrong values, no spills reported), so tiers keep NV <= 29
   static_assert(CAP <= 32 || (((CAP + LCAP + 1 + G - 1) / G) | 1) <= 29, "chunk tier NV must stay <= 29");
-  // validated group sizes: one warp (GPC warps per CTA) or a 128/256-thread CTA; a 64-thread
-  // CTA group gave wrong values on B200 (tests/test_gpu_parity.py::test_random_rectangular[1])
-  static_assert(G <= 32 || G >= 128, "chunk tiers run on warps or on >= 128-thread CTAs");
   static_assert(smem <= 232448, "tier shared memory exceeds 227 KB");
   auto kern = k_tier<G, CAP, LCAP, GPC, VALS, OUT>;
   // one process drives one device, so per-instantiation caching is safe
