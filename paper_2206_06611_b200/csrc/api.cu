@@ -50,7 +50,19 @@ struct brm_context {
   cudaEvent_t ev[32] = {};
   unsigned ev_mask = 0;  // events recorded since the last structure call
   int64_t launches = 0;  // kernels launched since the last structure call
+  brm_context* sub = nullptr;  // heavy-row decomposition runs its sub-products here
+  DevBuf split_rows, split_off, glob_rows, a1_rpt, a1_col, a1_val, a2_rpt, a2_col, a2_val;
+  HostBuf h_rows, h_split;
 };
+
+namespace {
+brm_status_t heavy_split_impl(brm_context_t* ctx, int out, const RowOut& o, const int32_t* rows, int64_t n,
+                              const int64_t* info);
+brm_status_t heavy_split(brm_context_t* ctx, int out, const RowOut& o, const int32_t* rows, int64_t n,
+                         const int64_t* info) {
+  return heavy_split_impl(ctx, out, o, rows, n, info);
+}
+}  // namespace
 
 namespace {
 
@@ -182,6 +194,89 @@ brm_status_t run_scan(brm_context_t* ctx, const int64_t* in, int64_t n, int64_t*
   return BRM_OK;
 }
 
+// Heavy-row decomposition (kernels.cu): the rows (host ids `rows`, host
+// (n_prod, nl) pairs `info`) are processed in batches bounded by free memory;
+// per batch C1 = A1 * B over blocks of kSplitListsHost lists, C2 = A2 * C1
+// over the block results (both through the sub-context, recursively), and C2's
+// rows are scattered into this context's output.
+brm_status_t heavy_split_impl(brm_context_t* ctx, int out, const RowOut& o, const int32_t* rows, int64_t n,
+                              const int64_t* info) {
+  if (!ctx->sub) {
+    brm_status_t st = brm_create(&ctx->sub, ctx->device, ctx->stream);
+    if (st != BRM_OK) return fail(ctx, st, "heavy rows: cannot create the sub-context");
+  }
+  brm_context_t* sub = ctx->sub;
+  sub->stream = ctx->stream;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const int64_t budget = std::max<int64_t>((int64_t)(free_b / 3), 256ll << 20);
+  int64_t t0 = 0;
+  while (t0 < n) {
+    // batch [t0, t1): ~5 x 12 B per product (A1, C_bar and C of both sub-products)
+    int64_t t1 = t0, bytes = 0;
+    while (t1 < n && (t1 == t0 || bytes + info[2 * t1] * 60 <= budget)) bytes += info[2 * t1++] * 60;
+    const int nb = (int)(t1 - t0);
+    std::vector<int64_t> hoff(2 * (nb + 1));
+    int64_t* ent = hoff.data();
+    int64_t* blk = hoff.data() + nb + 1;
+    ent[0] = blk[0] = 0;
+    for (int r = 0; r < nb; ++r) {
+      const int64_t nl = info[2 * (t0 + r) + 1];
+      ent[r + 1] = ent[r] + nl;
+      blk[r + 1] = blk[r] + (nl + kSplitListsHost - 1) / kSplitListsHost;
+    }
+    const int64_t ne = ent[nb], nblk = blk[nb];
+    CK(ensure(ctx, ctx->split_rows, (size_t)nb * 4), "alloc split rows");
+    CK(ensure(ctx, ctx->split_off, hoff.size() * 8), "alloc split offsets");
+    CK(ensure_host(ctx->h_split, (size_t)nb * 4 + hoff.size() * 8), "alloc pinned split info");
+    unsigned char* hs = static_cast<unsigned char*>(ctx->h_split.p);
+    memcpy(hs, rows + t0, (size_t)nb * 4);
+    memcpy(hs + (size_t)nb * 4, hoff.data(), hoff.size() * 8);
+    CK(cudaMemcpyAsync(ctx->split_rows.p, hs, (size_t)nb * 4, cudaMemcpyHostToDevice, ctx->stream), "copy split rows");
+    CK(cudaMemcpyAsync(ctx->split_off.p, hs + (size_t)nb * 4, hoff.size() * 8, cudaMemcpyHostToDevice, ctx->stream),
+       "copy split offsets");
+    const int32_t* drows = static_cast<const int32_t*>(ctx->split_rows.p);
+    const int64_t* dent = static_cast<const int64_t*>(ctx->split_off.p);
+    const int64_t* dblk = dent + nb + 1;
+    // level 1: C1 = A1 * B
+    CK(ensure(ctx, ctx->a1_rpt, (size_t)(nblk + 1) * 8), "alloc A1.rpt");
+    CK(ensure(ctx, ctx->a1_col, (size_t)ne * 4), "alloc A1.col");
+    CK(ensure(ctx, ctx->a1_val, (size_t)ne * 8), "alloc A1.val");
+    CK(launch_split_a1(ctx->A, drows, nb, dent, dblk, ne + nblk + 1, static_cast<int64_t*>(ctx->a1_rpt.p),
+                       static_cast<int32_t*>(ctx->a1_col.p), static_cast<double*>(ctx->a1_val.p), ctx->stream),
+       "k_split_a1");
+    ++ctx->launches;
+    const brm_csr_t A1{nblk, ctx->K, ne, static_cast<int64_t*>(ctx->a1_rpt.p), static_cast<int32_t*>(ctx->a1_col.p),
+                       static_cast<double*>(ctx->a1_val.p)};
+    const brm_csr_t Bc{ctx->K, ctx->N, ctx->bnnz, const_cast<int64_t*>(ctx->B.rpt), const_cast<int32_t*>(ctx->B.col),
+                       const_cast<double*>(ctx->B.val)};
+    brm_csr_t C1{};
+    brm_status_t st = brmerge_spgemm(sub, &A1, &Bc, BRM_UPPER, &C1);
+    ctx->launches += sub->launches;
+    if (st != BRM_OK) return fail(ctx, st, std::string("heavy rows, level 1: ") + sub->err);
+    // level 2: C2 = A2 * C1 (A2 = the blocks of each row, value 1.0)
+    CK(ensure(ctx, ctx->a2_rpt, (size_t)(nb + 1) * 8), "alloc A2.rpt");
+    CK(ensure(ctx, ctx->a2_col, (size_t)nblk * 4), "alloc A2.col");
+    CK(ensure(ctx, ctx->a2_val, (size_t)nblk * 8), "alloc A2.val");
+    CK(launch_split_a2(nb, dblk, nblk + nb + 1, static_cast<int64_t*>(ctx->a2_rpt.p),
+                       static_cast<int32_t*>(ctx->a2_col.p), static_cast<double*>(ctx->a2_val.p), ctx->stream),
+       "k_split_a2");
+    ++ctx->launches;
+    const brm_csr_t A2{nb, nblk, nblk, static_cast<int64_t*>(ctx->a2_rpt.p), static_cast<int32_t*>(ctx->a2_col.p),
+                       static_cast<double*>(ctx->a2_val.p)};
+    brm_csr_t C2{};
+    st = brmerge_spgemm(sub, &A2, &C1, BRM_UPPER, &C2);
+    ctx->launches += sub->launches;
+    brm_csr_free(sub, &C1);
+    if (st != BRM_OK) return fail(ctx, st, std::string("heavy rows, level 2: ") + sub->err);
+    CK(launch_scatter_rows(drows, nb, C2.rpt, C2.col, C2.val, out, o, ctx->stream), "k_scatter_rows");
+    ++ctx->launches;
+    brm_csr_free(sub, &C2);
+    t0 = t1;
+  }
+  return BRM_OK;
+}
+
 // Launch the merge of every non-empty bin with output kind `out`.
 brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bin) {
   const int32_t* bins = static_cast<const int32_t*>(ctx->bins.p);
@@ -212,44 +307,68 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
     ctx->heavy.assign(hi, hi + 2 * nh);
     ctx->heavy_loaded = true;
   }
-  const bool vals = out != OUT_SYMBOLIC;
-  // batch the heavy rows so their ping-pong slices fit the workspace budget
-  int64_t max_row = 0;
-  for (int64_t t = 0; t < nh; ++t)
-    max_row = std::max(max_row, global_row_bytes(ctx->heavy[2 * t], ctx->heavy[2 * t + 1], vals));
-  size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
-  int64_t budget = std::min<int64_t>((int64_t)(free_b / 2) + (int64_t)ctx->gws.cap, 16ll << 30);
-  budget = std::max(budget, max_row);
-  CK(ensure_host(ctx->h_gws_off, (size_t)nh * 16), "alloc pinned ws offsets");
-  CK(ensure(ctx, ctx->gws_off, (size_t)nh * 16), "alloc ws offsets");
-  int64_t* hoff = static_cast<int64_t*>(ctx->h_gws_off.p);
-  // first pass: offsets for all rows, batch boundaries
-  std::vector<int64_t> cuts{0};
-  int64_t acc = 0, need = 0;
+  // rows with more than kSplitListsHost lists are decomposed into aligned
+  // blocks of lists (heavy_split); the rest run on the global tier
+  CK(ensure_host(ctx->h_rows, (size_t)nh * 4), "alloc pinned heavy rows");
+  CK(cudaMemcpyAsync(ctx->h_rows.p, hrows, (size_t)nh * 4, cudaMemcpyDeviceToHost, ctx->stream), "copy heavy rows");
+  CK(cudaStreamSynchronize(ctx->stream), "sync heavy rows");
+  const int32_t* hr = static_cast<const int32_t*>(ctx->h_rows.p);
+  std::vector<int32_t> g_rows, s_rows;
+  std::vector<int64_t> g_info, s_info;
   for (int64_t t = 0; t < nh; ++t) {
-    const int64_t bytes = global_row_bytes(ctx->heavy[2 * t], ctx->heavy[2 * t + 1], vals);
-    if (acc + bytes > budget) {
-      cuts.push_back(t);
-      acc = 0;
-    }
-    hoff[2 * t] = acc;
-    hoff[2 * t + 1] = ctx->heavy[2 * t];
-    acc += bytes;
-    need = std::max(need, acc);
+    const bool split = ctx->heavy[2 * t + 1] > kSplitListsHost;
+    (split ? s_rows : g_rows).push_back(hr[t]);
+    (split ? s_info : g_info).push_back(ctx->heavy[2 * t]);
+    (split ? s_info : g_info).push_back(ctx->heavy[2 * t + 1]);
   }
-  cuts.push_back(nh);
-  CK(ensure(ctx, ctx->gws, (size_t)need), "alloc global-tier workspace");
-  CK(cudaMemcpyAsync(ctx->gws_off.p, hoff, (size_t)nh * 16, cudaMemcpyHostToDevice, ctx->stream),
-     "copy ws offsets");
-  for (size_t c = 0; c + 1 < cuts.size(); ++c) {
-    const int64_t b0 = cuts[c], n = cuts[c + 1] - b0;
-    if (n <= 0) continue;
-    CK(launch_global_tier(out, ctx->A, ctx->B, hrows + b0, n,
-                          static_cast<const int64_t*>(ctx->gws_off.p) + 2 * b0,
-                          static_cast<unsigned char*>(ctx->gws.p), o, ctx->stream),
-       "k_global_tier");
-    ++ctx->launches;
+  if (!s_rows.empty()) {
+    brm_status_t st = heavy_split(ctx, out, o, s_rows.data(), (int64_t)s_rows.size(), s_info.data());
+    if (st != BRM_OK) return st;
+  }
+  const int64_t ng = (int64_t)g_rows.size();
+  if (ng > 0) {
+    CK(ensure(ctx, ctx->glob_rows, (size_t)ng * 4), "alloc global-tier rows");
+    CK(ensure_host(ctx->h_split, (size_t)ng * 4), "alloc pinned global-tier rows");
+    memcpy(ctx->h_split.p, g_rows.data(), (size_t)ng * 4);
+    CK(cudaMemcpyAsync(ctx->glob_rows.p, ctx->h_split.p, (size_t)ng * 4, cudaMemcpyHostToDevice, ctx->stream),
+       "copy global-tier rows");
+    const int32_t* grows = static_cast<const int32_t*>(ctx->glob_rows.p);
+    const bool vals = out != OUT_SYMBOLIC;
+    // batch the rows so their ping-pong slices fit the workspace budget
+    int64_t max_row = 0;
+    for (int64_t t = 0; t < ng; ++t) max_row = std::max(max_row, global_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals));
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    int64_t budget = std::min<int64_t>((int64_t)(free_b / 2) + (int64_t)ctx->gws.cap, 16ll << 30);
+    budget = std::max(budget, max_row);
+    CK(ensure_host(ctx->h_gws_off, (size_t)ng * 16), "alloc pinned ws offsets");
+    CK(ensure(ctx, ctx->gws_off, (size_t)ng * 16), "alloc ws offsets");
+    int64_t* hoff = static_cast<int64_t*>(ctx->h_gws_off.p);
+    std::vector<int64_t> cuts{0};
+    int64_t acc = 0, need = 0;
+    for (int64_t t = 0; t < ng; ++t) {
+      const int64_t bytes = global_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals);
+      if (acc + bytes > budget) {
+        cuts.push_back(t);
+        acc = 0;
+      }
+      hoff[2 * t] = acc;
+      hoff[2 * t + 1] = g_info[2 * t];
+      acc += bytes;
+      need = std::max(need, acc);
+    }
+    cuts.push_back(ng);
+    CK(ensure(ctx, ctx->gws, (size_t)need), "alloc global-tier workspace");
+    CK(cudaMemcpyAsync(ctx->gws_off.p, hoff, (size_t)ng * 16, cudaMemcpyHostToDevice, ctx->stream),
+       "copy ws offsets");
+    for (size_t c = 0; c + 1 < cuts.size(); ++c) {
+      const int64_t b0 = cuts[c], n = cuts[c + 1] - b0;
+      if (n <= 0) continue;
+      CK(launch_global_tier(out, ctx->A, ctx->B, grows + b0, n, static_cast<const int64_t*>(ctx->gws_off.p) + 2 * b0,
+                            static_cast<unsigned char*>(ctx->gws.p), o, ctx->stream),
+         "k_global_tier");
+      ++ctx->launches;
+    }
   }
   if (per_bin) ev_record(ctx, kEvBin + 2 * kBinGlobal + 1);
   return BRM_OK;
@@ -425,14 +544,16 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
     for (DevBuf* b : {&ctx->nprod_off, &ctx->row_size, &ctx->bins, &ctx->status, &ctx->small, &ctx->cbar_col,
                       &ctx->cbar_val, &ctx->gws, &ctx->gws_off, &ctx->heavy_info, &ctx->stA_rpt, &ctx->stA_col,
                       &ctx->stA_val, &ctx->stB_rpt, &ctx->stB_col, &ctx->stB_val, &ctx->stC_rpt, &ctx->stC_col,
-                      &ctx->stC_val})
+                      &ctx->stC_val, &ctx->split_rows, &ctx->split_off, &ctx->glob_rows, &ctx->a1_rpt, &ctx->a1_col,
+                      &ctx->a1_val, &ctx->a2_rpt, &ctx->a2_col, &ctx->a2_val})
       free_dev(ctx, *b);
     cudaStreamSynchronize(ctx->stream);
-    for (HostBuf* b : {&ctx->h_small, &ctx->h_heavy, &ctx->h_gws_off, &ctx->h_C})
+    for (HostBuf* b : {&ctx->h_small, &ctx->h_heavy, &ctx->h_gws_off, &ctx->h_C, &ctx->h_rows, &ctx->h_split})
       if (b->p) cudaFreeHost(b->p);
     for (auto& e : ctx->ev)
       if (e) cudaEventDestroy(e);
   }
+  if (ctx->sub) brm_destroy(ctx->sub);
   delete ctx;
   return BRM_OK;
 }

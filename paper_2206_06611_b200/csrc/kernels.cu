@@ -11,12 +11,15 @@
 //   k_scan_i64       exclusive scan (row_size -> rpt; generic).
 //   k_compact        Step 6 of Fig. 4a: C_bar -> C copy (BRMerge-Upper).
 //   k_partition      §III.D row partition by balanced n_prod (multi-GPU).
+#include <algorithm>
 #include <cstdio>
 
 #include "engine.cuh"
 #include "kernels.cuh"
 
 namespace brm {
+
+static int num_sms();
 
 // ---------------------------------------------------------------------------
 // Single-pass exclusive scan with decoupled look-back (Merrill & Garland
@@ -450,6 +453,112 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
   cb.av = VALS ? reinterpret_cast<double*>(take(nl * 8)) : nullptr;
   cb.scan_tmp = scan_tmp;
   chunk_row<kGlobalG, VALS, OUT>(g, A, B, row, o, cb);
+}
+
+// ---------------------------------------------------------------------------
+// Heavy-row decomposition (tier 7 rows with nl > kSplitLists). Algorithm 1's
+// tree over a row's nl lists splits into aligned sub-trees over blocks of
+// kSplitLists = 2^5 consecutive lists (pairs are (2m, 2m+1) at every level,
+// so an aligned block is merged exactly as Algorithm 1 would merge it on its
+// own, a short last block included). Level 1: every block becomes a row of
+// A1 (a copy of the block's A entries) and C1 = A1 * B runs through the
+// ordinary tiers. Level 2: row i of A2 lists its blocks' rows of C1 with
+// value 1.0 (1.0 * v == v exactly), so C2 = A2 * C1 merges the block results
+// in the same tree order; C2 may itself be heavy and split again.
+// ---------------------------------------------------------------------------
+constexpr int kSplitLists = 32;
+
+__device__ __forceinline__ int upper_row(const int64_t* off, int n, int64_t e) {  // last r with off[r] <= e
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= e)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// A1: rows = blocks; ent_off / blk_off = exclusive prefix sums over the
+// batch rows of nl_i and ceil(nl_i / kSplitLists).
+__global__ void k_split_a1(CsrView A, const int32_t* __restrict__ rows, int n, const int64_t* __restrict__ ent_off,
+                           const int64_t* __restrict__ blk_off, int64_t* __restrict__ a1_rpt,
+                           int32_t* __restrict__ a1_col, double* __restrict__ a1_val) {
+  const int64_t ne = ent_off[n], nb = blk_off[n];
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ne + nb + 1;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < ne) {
+      const int r = upper_row(ent_off, n, t);
+      const int64_t src = A.rpt[rows[r]] + (t - ent_off[r]);
+      a1_col[t] = A.col[src];
+      a1_val[t] = A.val[src];
+    } else if (t < ne + nb) {
+      const int64_t b = t - ne;
+      const int r = upper_row(blk_off, n, b);
+      a1_rpt[b] = ent_off[r] + (int64_t)kSplitLists * (b - blk_off[r]);
+    } else {
+      a1_rpt[nb] = ne;
+    }
+  }
+}
+
+// A2: row r lists blocks blk_off[r] .. blk_off[r+1]-1 of C1 with value 1.0.
+__global__ void k_split_a2(int n, const int64_t* __restrict__ blk_off, int64_t* __restrict__ a2_rpt,
+                           int32_t* __restrict__ a2_col, double* __restrict__ a2_val) {
+  const int64_t nb = blk_off[n];
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= nb + n; t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < nb) {
+      a2_col[t] = (int32_t)t;
+      a2_val[t] = 1.0;
+    } else {
+      a2_rpt[t - nb] = blk_off[t - nb];
+    }
+  }
+}
+
+// Row r of C2 (rpt2/col2/val2) is output row rows[r]: its size goes to
+// row_size (OUT_SYMBOLIC / OUT_CBAR), its entries to the output at base[row].
+__global__ void k_scatter_rows(const int32_t* __restrict__ rows, int n, const int64_t* __restrict__ rpt2,
+                               const int32_t* __restrict__ col2, const double* __restrict__ val2, int out_kind,
+                               RowOut o) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w; r < n; r += nw) {
+    const int64_t row = rows[r];
+    const int64_t s = rpt2[r], len = rpt2[r + 1] - s;
+    if (out_kind != OUT_C && lane == 0) o.row_size[row] = len;
+    if (out_kind == OUT_SYMBOLIC) continue;
+    const int64_t d = o.base[row];
+    for (int64_t e = lane; e < len; e += 32) {
+      o.col[d + e] = col2[s + e];
+      o.val[d + e] = val2[s + e];
+    }
+  }
+}
+
+cudaError_t launch_split_a1(const CsrView& A, const int32_t* rows, int n, const int64_t* ent_off,
+                            const int64_t* blk_off, int64_t total, int64_t* a1_rpt, int32_t* a1_col, double* a1_val,
+                            cudaStream_t st) {
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+  k_split_a1<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(A, rows, n, ent_off, blk_off, a1_rpt, a1_col, a1_val);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split_a2(int n, const int64_t* blk_off, int64_t total, int64_t* a2_rpt, int32_t* a2_col,
+                            double* a2_val, cudaStream_t st) {
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+  k_split_a2<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(n, blk_off, a2_rpt, a2_col, a2_val);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_rows(const int32_t* rows, int n, const int64_t* rpt2, const int32_t* col2,
+                                const double* val2, int out_kind, const RowOut& o, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>(((int64_t)n * 32 + 255) / 256, (int64_t)num_sms() * 16);
+  k_scatter_rows<<<(unsigned)blocks, 256, 0, st>>>(rows, n, rpt2, col2, val2, out_kind, o);
+  return cudaGetLastError();
 }
 
 // Step 6 of Fig. 4a: copy each row of C_bar (at its n_prod offset) to C. A

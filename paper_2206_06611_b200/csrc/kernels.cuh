@@ -38,4 +38,14 @@ cudaError_t launch_compact(int64_t M, const int64_t* nprod_off, const int64_t* c
 cudaError_t launch_partition(const int64_t* nprod_off, int64_t M, int p, int64_t* bounds, cudaStream_t st);
 cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod, cudaStream_t st);
 
+// heavy-row decomposition (kernels.cu "Heavy-row decomposition")
+constexpr int kSplitListsHost = 32;
+cudaError_t launch_split_a1(const CsrView& A, const int32_t* rows, int n, const int64_t* ent_off,
+                            const int64_t* blk_off, int64_t total, int64_t* a1_rpt, int32_t* a1_col, double* a1_val,
+                            cudaStream_t st);
+cudaError_t launch_split_a2(int n, const int64_t* blk_off, int64_t total, int64_t* a2_rpt, int32_t* a2_col,
+                            double* a2_val, cudaStream_t st);
+cudaError_t launch_scatter_rows(const int32_t* rows, int n, const int64_t* rpt2, const int32_t* col2,
+                                const double* val2, int out_kind, const RowOut& o, cudaStream_t st);
+
 }  // namespace brm
