@@ -457,8 +457,28 @@ __device__ __forceinline__ void lds_if(bool p, unsigned addr, int2& v) {
                : "r"(addr), "r"((unsigned)p));
 }
 
+// Record of a list element: {col, value slot} (numeric) or just col (symbolic).
+template <bool VALS>
+struct Rec;
+template <>
+struct Rec<true> {
+  using T = int2;
+  static constexpr int kBytes = 8;
+  __device__ static T make(int c, int s) { return make_int2(c, s); }
+  __device__ static int col(const T& r) { return r.x; }
+  __device__ static int slot(const T& r) { return r.y; }
+};
+template <>
+struct Rec<false> {
+  using T = int;
+  static constexpr int kBytes = 4;
+  __device__ static T make(int c, int) { return c; }
+  __device__ static int col(T r) { return r; }
+  __device__ static int slot(T) { return 0; }
+};
+
 struct RecBufs {
-  int2* rec;      // P + nl + 2 records: sentinel-terminated lists
+  void* rec;      // P + nl + 2 records (Rec<VALS>::T): sentinel-terminated lists
   double* val;    // P value slots (products, then partial sums)
   int* owner;     // P 16-bit entries: list of each product (multiplying phase)
   int* off0;
@@ -470,17 +490,20 @@ struct RecBufs {
 
 template <int G, int CAP, int LCAP, bool VALS>
 __host__ __device__ constexpr int rec_group_bytes() {
-  return align16((CAP + LCAP + 2) * 8) + (VALS ? align16(CAP * 8) : 0) + align16(CAP * 2) + align16((LCAP + 2) * 4) * 2 +
+  return align16((CAP + LCAP + 2) * Rec<VALS>::kBytes) + (VALS ? align16(CAP * 8) : 0) + align16(CAP * 2) + align16((LCAP + 2) * 4) * 2 +
          align16(LCAP * 8) + (VALS ? align16(LCAP * 8) : 0) + (G > 32 ? align16((G / 32 + 2) * 4) : 0);
 }
 
-// merge path over the .x (column) fields of two record lists
-__device__ __forceinline__ int merge_path_rec(const int2* a, int la, const int2* b, int lb, int diag) {
+// merge path over the columns of two record lists
+template <bool VALS>
+__device__ __forceinline__ int merge_path_rec(const typename Rec<VALS>::T* a, int la, const typename Rec<VALS>::T* b,
+                                              int lb, int diag) {
+  using R = Rec<VALS>;
   int lo = diag - lb > 0 ? diag - lb : 0;
   int hi = diag < la ? diag : la;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (a[mid].x <= b[diag - 1 - mid].x)
+    if (R::col(a[mid]) <= R::col(b[diag - 1 - mid]))
       lo = mid + 1;
     else
       hi = mid;
@@ -493,15 +516,18 @@ __device__ __forceinline__ int merge_path_rec(const int2* a, int la, const int2*
 // threads cross into the next pair when both sentinels merge). Outputs wait
 // in registers and overwrite `rec` compacted once the group has read it.
 template <int G, int NV, bool VALS>
-__device__ __forceinline__ int rec_round(const Group<G>& g, int2* rec, double* val, const int* off, int* noff,
-                                         int nl, int* scan_tmp) {
+__device__ __forceinline__ int rec_round(const Group<G>& g, typename Rec<VALS>::T* rec, double* val, const int* off,
+                                         int* noff, int nl, int* scan_tmp) {
+  using R = Rec<VALS>;
+  using T = typename R::T;
+  constexpr unsigned RB = R::kBytes;
   const int npairs = (nl + 1) >> 1;
   const int npos = off[nl] + (nl & 1);
   const int VT = ((npos + G - 1) / G) | 1;
   const int g0 = min(g.rank * VT, npos), g1 = min(g0 + VT, npos);
   int pf = 0, pl = -1;
   int p = 0, bs = 0, ia = 0, ib = 0, lim = 0;
-  int2 ra = make_int2(INT_MAX, 0), rb = make_int2(INT_MAX, 0);
+  T ra = R::make(INT_MAX, 0), rb = R::make(INT_MAX, 0);
   if (g0 < g1) {
     int lo = 0, hi = npairs - 1;  // last pair starting at or before g0
     while (lo < hi) {
@@ -521,9 +547,9 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, int2* rec, double* v
       pf = pl = p;
       noff[p] = 0;
     }
-    const int i = merge_path_rec(rec + as, na, rec + bs, nb, d);
+    const int i = merge_path_rec<VALS>(rec + as, na, rec + bs, nb, d);
     int j = d - i;
-    if (i > 0 && j < nb && rec[as + i - 1].x == rec[bs + j].x) ++j;  // b[j] was summed on the left
+    if (i > 0 && j < nb && R::col(rec[as + i - 1]) == R::col(rec[bs + j])) ++j;  // b[j] was summed on the left
     if (i == na) {  // pair p finished on the left
       if (g0 + 1 < g1) {
         ++p;
@@ -545,28 +571,30 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, int2* rec, double* v
   }
   const unsigned recb = smem_u32(rec);
   const unsigned valb = VALS ? smem_u32(val) : 0u;
-  int ocol[NV], oslot[NV];
+  int ocol[NV], oslot[VALS ? NV : 1];
   int cnt = 0;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     if (v >= VT) break;  // group-uniform
     const bool act = ia + ib < lim;
-    const bool ta = act && ra.x <= rb.x;
-    const bool tb = act && rb.x <= ra.x;
-    ocol[v] = min(ra.x, rb.x);
-    oslot[v] = ta ? ra.y : rb.y;
-    if (VALS) {  // equal columns: val[left] = val[left] + val[right]
-      const bool dup = ta && tb && ra.x != INT_MAX;
+    const int ca = R::col(ra), cb = R::col(rb);
+    const bool ta = act && ca <= cb;
+    const bool tb = act && cb <= ca;
+    ocol[v] = min(ca, cb);
+    if (VALS) {
+      oslot[v] = ta ? R::slot(ra) : R::slot(rb);
+      // equal columns: val[left] = val[left] + val[right]
+      const bool dup = ta && tb && ca != INT_MAX;
       double x = 0.0, y = 0.0;
-      lds_if(dup, valb + 8u * ra.y, x);
-      lds_if(dup, valb + 8u * rb.y, y);
-      if (dup) val[ra.y] = __dadd_rn(x, y);
+      lds_if(dup, valb + 8u * R::slot(ra), x);
+      lds_if(dup, valb + 8u * R::slot(rb), y);
+      if (dup) val[R::slot(ra)] = __dadd_rn(x, y);
     }
     cnt += act;
     ia += ta;
     ib += tb;
-    lds_if(ta, recb + 8u * ia, ra);
-    lds_if(tb, recb + 8u * ib, rb);
+    lds_if(ta, recb + RB * ia, ra);
+    lds_if(tb, recb + RB * ib, rb);
     if (act && ocol[v] == INT_MAX && ia + ib < lim) {  // pair p done, chunk not: enter pair p+1
       if (pl < 0) pf = p + 1;
       ++p;
@@ -586,11 +614,11 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, int2* rec, double* v
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     if (v >= VT) break;
-    if (v < cnt) rec[base + v] = make_int2(ocol[v], oslot[v]);
+    if (v < cnt) rec[base + v] = R::make(ocol[v], VALS ? oslot[VALS ? v : 0] : 0);
   }
   if (g.rank == G - 1) {
     noff[npairs] = total;
-    rec[total] = make_int2(INT_MAX, 0);  // lone partner sentinel, used if npairs is odd
+    rec[total] = R::make(INT_MAX, 0);  // lone partner sentinel, used if npairs is odd
   }
   g.sync();
   return total;
@@ -599,6 +627,8 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, int2* rec, double* v
 template <int G, int NV, bool VALS, int OUT>
 __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
                                         const RowOut& o, const RecBufs& rb) {
+  using R = Rec<VALS>;
+  typename R::T* rec = static_cast<typename R::T*>(rb.rec);
   const int rank = g.rank;
   const int64_t a0 = A.rpt[row];
   const int nl = static_cast<int>(A.rpt[row + 1] - a0);
@@ -621,13 +651,13 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
     const int ex = group_excl_scan<G>(g, n, tot, rb.scan_tmp);
     if (l < nl) {
       off[l] = P + ex + l;
-      rb.rec[P + ex + l + n] = make_int2(INT_MAX, 0);  // sentinel of list l
+      rec[P + ex + l + n] = R::make(INT_MAX, 0);  // sentinel of list l
     }
     P += tot;
   }
   if (rank == 0) {
     off[nl] = P + nl;
-    rb.rec[P + nl] = make_int2(INT_MAX, 0);  // lone partner sentinel if nl is odd
+    rec[P + nl] = R::make(INT_MAX, 0);  // lone partner sentinel if nl is odd
   }
   g.sync();
   {
@@ -642,7 +672,7 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
       const int l = owner[e];
       const int64_t src = rb.bst[l] + (e - (off[l] - l));
       const int c = __ldg(B.col + src);
-      rb.rec[e + l] = make_int2(c, e);
+      rec[e + l] = R::make(c, e);
       if (VALS) rb.val[e] = __dmul_rn(rb.av[l], __ldg(B.val + src));  // line 12: the product, rounded once
     }
   }
@@ -651,7 +681,7 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
   int cur = nl;
   int end = P + nl;
   while (cur > 1) {
-    end = rec_round<G, NV, VALS>(g, rb.rec, rb.val, off, noff, cur, rb.scan_tmp);
+    end = rec_round<G, NV, VALS>(g, rec, rb.val, off, noff, cur, rb.scan_tmp);
     cur = (cur + 1) >> 1;
     int* t = off;  // lines 33-34
     off = noff;
@@ -661,9 +691,9 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
   if (OUT != OUT_SYMBOLIC) {  // line 36
     const int64_t ob = o.base[row];
     for (int e = rank; e < T; e += G) {
-      const int2 r = rb.rec[e];
-      o.col[ob + e] = r.x;
-      if (VALS) o.val[ob + e] = rb.val[r.y];
+      const typename R::T r = rec[e];
+      o.col[ob + e] = R::col(r);
+      if (VALS) o.val[ob + e] = rb.val[R::slot(r)];
     }
   }
   if (OUT != OUT_C && rank == 0) o.row_size[row] = T;

@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
       return q;
     };
     RecBufs rb;
-    rb.rec = reinterpret_cast<int2*>(take((CAP + LCAP + 2) * 8));
+    rb.rec = take((CAP + LCAP + 2) * Rec<VALS>::kBytes);
     rb.val = VALS ? reinterpret_cast<double*>(take(CAP * 8)) : nullptr;
     rb.owner = reinterpret_cast<int*>(take(CAP * 2));
     rb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
