@@ -274,6 +274,10 @@ brm_status_t heavy_split_impl(brm_context_t* ctx, int out, const RowOut& o, cons
     brm_csr_free(sub, &C2);
     t0 = t1;
   }
+  // the sub-context's grow-only workspace (C_bar of the sub-products) can be
+  // large: release it before the global tier sizes its own workspace
+  brm_destroy(ctx->sub);
+  ctx->sub = nullptr;
   return BRM_OK;
 }
 
