@@ -168,6 +168,19 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
+def measured_traffic(config: str, mode: str, bin_: int):
+    """DRAM bytes (read + write) per launch of the dominant kernel, from the
+    `ncu --set full` capture recorded in profiles/traffic.json (None if this
+    config/mode/kernel was not captured)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        e = t.get(f"{config}/{mode}/bin{bin_}")
+        return None if e is None else float(e["dram_bytes"])
+    except Exception:
+        return None
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle (Eq. (2) Gustavson, single thread) on
     a bounded row sample of the same workload, rank 0 only."""
@@ -214,7 +227,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
-    ap.add_argument("--mode", default="precise", choices=["precise", "upper"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "precise", "upper"],
+                    help="auto: BRMerge-Upper when its C_bar (12 B per intermediate product) fits in "
+                         "half of the GPU memory, else BRMerge-Precise")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -255,6 +270,9 @@ def main():
     Ablk = gen.Csr(r1 - r0, A.cols, (A.rpt[r0:r1 + 1] - a0).astype(np.int64), A.col[a0:a1].copy(), A.val[a0:a1].copy())
     Ad = TorchCsr.from_csr(Ablk)
     local_nprod = int(nprod_h[r0:r1].sum())
+    if args.mode == "auto":
+        fits = local_nprod * 12 < torch.cuda.get_device_properties(dev).total_memory // 2
+        args.mode = "upper" if fits else "precise"
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -336,7 +354,7 @@ def main():
         e2e = {"value": None, "unit": "GFLOP/s", "skipped": f"C is {nnz_local * 12 / 2**30:.0f} GiB: not staged through pinned host memory"}
     elif not args.no_e2e:
         Ah = TorchCsr.from_csr(Ablk, pin=True)
-        Bh = TorchCsr.from_csr(B, pin=True)
+        Bh = Ah if (B is A and world == 1) else TorchCsr.from_csr(B, pin=True)
         ctx.brmerge_spgemm_host(Ah, Bh, args.mode)  # warm
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -353,7 +371,7 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e_ms = float(te.item())
-        h2d = sum(x.numel() * x.element_size() for X in (Ah, Bh) for x in (X.rpt, X.col, X.val))
+        h2d = sum(x.numel() * x.element_size() for X in ((Ah,) if Bh is Ah else (Ah, Bh)) for x in (X.rpt, X.col, X.val))
         d2h = (Ablk.rows + 1) * 8 + out[3].size * 4 + out[4].size * 8
         e2e = {"value": 2.0 * nprod_all / (e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
@@ -384,7 +402,7 @@ def main():
                        "l2": "flushed (256 MiB write) between timed steps, outside the events",
                        "parallelism": f"dp{world} rows by balanced n_prod"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": measured_traffic(args.config, args.mode, dom),
                          "kernel": f"k_tier bin {dom} (numeric merge)" if dom < NUM_BINS - 1 else "k_global_tier",
                          "kernel_ms": dom_ms, "algorithmic_bytes": dom_bytes, "peak_kind": peak_kind},
             "hbm_step": {"achieved_gbs": step_gbs, "frac": step_gbs / peak, "algorithmic_bytes": int(b_all.item())},

@@ -147,7 +147,8 @@ BRM_API brm_status_t brmerge_spgemm_fill(brm_context_t* ctx, brm_csr_t* C);
 
 /* --- host-buffer form (end-to-end) ---------------------------------------
  * A_h, B_h: HOST CSR (pinned memory recommended). Copies A and B to the
- * device, runs brmerge_spgemm, copies C back. C_h's arrays point into a
+ * device (once if A_h and B_h name the same host arrays, as for C = A*A),
+ * runs brmerge_spgemm, copies C back. C_h's arrays point into a
  * pinned host buffer owned by the context, valid until the next _host call
  * or brm_destroy (caller must not free them).                            */
 BRM_API brm_status_t brmerge_spgemm_host(brm_context_t* ctx, const brm_csr_t* A_h,

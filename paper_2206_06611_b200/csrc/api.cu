@@ -669,13 +669,21 @@ brm_status_t brmerge_spgemm_host(brm_context_t* ctx, const brm_csr_t* Ah, const 
   CK(up(ctx->stA_rpt, Ah->rpt, (size_t)(Ah->rows + 1) * 8), "H2D A.rpt");
   CK(up(ctx->stA_col, Ah->col, (size_t)Ah->nnz * 4), "H2D A.col");
   CK(up(ctx->stA_val, Ah->val, (size_t)Ah->nnz * 8), "H2D A.val");
-  CK(up(ctx->stB_rpt, Bh->rpt, (size_t)(Bh->rows + 1) * 8), "H2D B.rpt");
-  CK(up(ctx->stB_col, Bh->col, (size_t)Bh->nnz * 4), "H2D B.col");
-  CK(up(ctx->stB_val, Bh->val, (size_t)Bh->nnz * 8), "H2D B.val");
+  // C = A * A (the same host arrays): one upload serves both operands
+  const bool same = Ah->rpt == Bh->rpt && Ah->col == Bh->col && Ah->val == Bh->val && Ah->rows == Bh->rows &&
+                    Ah->nnz == Bh->nnz;
+  if (!same) {
+    CK(up(ctx->stB_rpt, Bh->rpt, (size_t)(Bh->rows + 1) * 8), "H2D B.rpt");
+    CK(up(ctx->stB_col, Bh->col, (size_t)Bh->nnz * 4), "H2D B.col");
+    CK(up(ctx->stB_val, Bh->val, (size_t)Bh->nnz * 8), "H2D B.val");
+  }
   brm_csr_t Ad{Ah->rows, Ah->cols, Ah->nnz, static_cast<int64_t*>(ctx->stA_rpt.p),
                static_cast<int32_t*>(ctx->stA_col.p), static_cast<double*>(ctx->stA_val.p)};
-  brm_csr_t Bd{Bh->rows, Bh->cols, Bh->nnz, static_cast<int64_t*>(ctx->stB_rpt.p),
-               static_cast<int32_t*>(ctx->stB_col.p), static_cast<double*>(ctx->stB_val.p)};
+  const DevBuf& br = same ? ctx->stA_rpt : ctx->stB_rpt;
+  const DevBuf& bc = same ? ctx->stA_col : ctx->stB_col;
+  const DevBuf& bv = same ? ctx->stA_val : ctx->stB_val;
+  brm_csr_t Bd{Bh->rows, Bh->cols, Bh->nnz, static_cast<int64_t*>(br.p), static_cast<int32_t*>(bc.p),
+               static_cast<double*>(bv.p)};
   CK(ensure(ctx, ctx->stC_rpt, (size_t)(Ah->rows + 1) * 8), "alloc C.rpt");
   int64_t nnz = 0;
   if ((s = structure_impl(ctx, &Ad, &Bd, mode, static_cast<int64_t*>(ctx->stC_rpt.p), &nnz)) != BRM_OK) return s;
