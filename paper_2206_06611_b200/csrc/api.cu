@@ -319,11 +319,27 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
   const int32_t* hr = static_cast<const int32_t*>(ctx->h_rows.p);
   std::vector<int32_t> g_rows, s_rows;
   std::vector<int64_t> g_info, s_info;
+  // split only rows of many SHORT lists: their 32-list blocks then fit the
+  // shared-memory tiers (a block of long lists would land back on this tier)
+  std::vector<int64_t> order;
   for (int64_t t = 0; t < nh; ++t) {
-    const bool split = ctx->heavy[2 * t + 1] > kSplitListsHost;
-    (split ? s_rows : g_rows).push_back(hr[t]);
-    (split ? s_info : g_info).push_back(ctx->heavy[2 * t]);
-    (split ? s_info : g_info).push_back(ctx->heavy[2 * t + 1]);
+    const int64_t P = ctx->heavy[2 * t], nl = ctx->heavy[2 * t + 1];
+    const bool split = nl > kSplitListsHost && P <= nl * (int64_t)kSplitAvgLen;
+    if (split) {
+      s_rows.push_back(hr[t]);
+      s_info.push_back(P);
+      s_info.push_back(nl);
+    } else {
+      order.push_back(t);
+    }
+  }
+  // global tier in descending n_prod: a launch lasts as long as its heaviest
+  // row, so the heaviest rows share the first launches
+  std::sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return ctx->heavy[2 * x] > ctx->heavy[2 * y]; });
+  for (const int64_t t : order) {
+    g_rows.push_back(hr[t]);
+    g_info.push_back(ctx->heavy[2 * t]);
+    g_info.push_back(ctx->heavy[2 * t + 1]);
   }
   if (!s_rows.empty()) {
     brm_status_t st = heavy_split(ctx, out, o, s_rows.data(), (int64_t)s_rows.size(), s_info.data());

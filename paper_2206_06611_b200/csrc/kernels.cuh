@@ -40,6 +40,7 @@ cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, i
 
 // heavy-row decomposition (kernels.cu "Heavy-row decomposition")
 constexpr int kSplitListsHost = 32;
+constexpr int kSplitAvgLen = 32;  // split rows whose mean list length is at most this
 cudaError_t launch_split_a1(const CsrView& A, const int32_t* rows, int n, const int64_t* ent_off,
                             const int64_t* blk_off, int64_t total, int64_t* a1_rpt, int32_t* a1_col, double* a1_val,
                             cudaStream_t st);

@@ -315,3 +315,18 @@ def test_full_size_sampled(ctx, oracle_mod, name):
         compare(_gather_rows(C, rows), A, B, rows=rows)
         del C
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_heavy_row_recursive_split(ctx, oracle_mod, mode):
+    """A row of 20,000 one-element lists over 50 columns: its 32-list blocks
+    go to the shared-memory tiers, and the 625 block results form a heavy row
+    again (split a second time); plus a row of 3,000 two-element lists."""
+    rng = np.random.default_rng(21)
+    kb = 20000
+    bcol = rng.integers(0, 50, size=kb).astype(np.int32)
+    B = Csr(kb, 60, np.arange(kb + 1, dtype=np.int64), bcol, rng.uniform(-1, 1, size=kb))
+    cols = [np.arange(kb, dtype=np.int32), np.sort(rng.choice(kb, size=3000, replace=False)).astype(np.int32)]
+    A = Csr(2, kb, np.array([0, kb, kb + 3000], np.int64), np.concatenate(cols),
+            rng.uniform(-1, 1, size=kb + 3000))
+    compare(run(ctx, A, B, mode), A, B)
