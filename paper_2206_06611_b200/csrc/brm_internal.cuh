@@ -42,7 +42,7 @@ struct TierBounds {
 #define BRM_TIER4 64, 768, 64, 1
 #define BRM_TIER5 128, 3072, 256, 1
 #define BRM_TIER6 256, 6656, 512, 1
-constexpr int kGlobalG = 512;
+constexpr int kGlobalG = 1024;
 
 __host__ __device__ inline TierBounds tier_bounds() {
   TierBounds t{};

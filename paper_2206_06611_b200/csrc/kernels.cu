@@ -173,10 +173,11 @@ __device__ __forceinline__ void warp_rows_nprod(const CsrView& A, const int64_t*
 }
 
 // Step 1: n_prod per row + exclusive scan + bin histogram + max. A tile of
-// 256 rows per CTA: each warp computes 32 rows' n_prod nonzero-parallel into
-// shared memory, then the tile is scanned (one row per thread) with a
-// decoupled look-back across tiles.
-constexpr int kNpTile = kScanThreads;
+// 2048 rows per CTA: each warp computes 8 chunks of 32 rows (warp_rows_nprod)
+// into shared memory, then the tile is scanned (8 consecutive rows per
+// thread) with a decoupled look-back across tiles. Large tiles keep the
+// look-back chain short (4.2M rows -> 2048 tiles).
+constexpr int kNpTile = kScanTile;
 __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const int64_t* __restrict__ brpt,
                                                              int64_t M, int64_t* __restrict__ nprod_off,
                                                              unsigned long long* status,
@@ -200,9 +201,11 @@ __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const in
   const TierBounds tb = tier_bounds();
   const int64_t t0 = (int64_t)tile * kNpTile;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int loc = wid * 32;
-  const int64_t r0 = t0 + loc;
-  if (r0 < M) {  // warp-uniform
+  constexpr int kChunks = kNpTile / kScanThreads;  // chunks of 32 rows per warp
+  for (int c = 0; c < kChunks; ++c) {
+    const int loc = (wid * kChunks + c) * 32;
+    const int64_t r0 = t0 + loc;
+    if (r0 >= M) break;  // warp-uniform
     int nl;
     warp_rows_nprod(A, brpt, M, r0, s_np + loc, &nl);
     const bool valid = r0 + lane < M;
@@ -231,19 +234,31 @@ __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const in
     }
   }
   __syncthreads();
-  const int64_t r = t0 + threadIdx.x;
-  const int64_t v = r < M ? s_np[threadIdx.x] : 0;
+  const int64_t rb = t0 + (int64_t)threadIdx.x * kScanIPT;
+  int64_t v[kScanIPT];
+  int64_t tsum = 0;
+#pragma unroll
+  for (int t = 0; t < kScanIPT; ++t) {
+    v[t] = rb + t < M ? s_np[threadIdx.x * kScanIPT + t] : 0;
+    tsum += v[t];
+  }
   int64_t total;
-  const int64_t texcl = block_scan_i64(v, total, s_wsum);
+  const int64_t texcl = block_scan_i64(tsum, total, s_wsum);
   if (threadIdx.x < 32) {
     const int64_t pre = lookback(status, tile, total);
     if (threadIdx.x == 0) s_prefix = pre;
   }
   __syncthreads();
-  if (r < M) nprod_off[r] = s_prefix + texcl;
-  if (r == M - 1) {
-    nprod_off[M] = s_prefix + texcl + v;
-    summary->nprod_total = s_prefix + texcl + v;
+  int64_t run = s_prefix + texcl;
+#pragma unroll
+  for (int t = 0; t < kScanIPT; ++t) {
+    const int64_t r = rb + t;
+    if (r < M) nprod_off[r] = run;
+    run += v[t];
+    if (r == M - 1) {
+      nprod_off[M] = run;
+      summary->nprod_total = run;
+    }
   }
   if (threadIdx.x < BRM_NUM_BINS) {
     if (s_bin_rows[threadIdx.x]) {

@@ -1,6 +1,7 @@
-"""Debug aid: a line-by-line Python emulation of the chunk engine's round
-(csrc/engine.cuh chunk_round / chunk_row, sentinel layout) for one row, with
-G emulated threads. Used to check the partitioning logic on the CPU against
+"""Debug aid: a line-by-line Python emulation of the chunk partition used by
+csrc/engine.cuh rec_round (record tiers) and chunk_round (global tier):
+sentinel-terminated lists, G chunks of odd VT positions, pair crossing,
+dedupe at chunk starts; one row, G emulated threads. Used to check the partitioning logic on the CPU against
 the oracle; not used by tests or the product path.
 Usage: python tools/emulate_chunk.py"""
 import os
@@ -99,55 +100,6 @@ def chunk_round(G, sc, sv, off, nl, first, av):
     return dc, dv, [noff[q] for q in range(npairs + 1)]
 
 
-def pair_round(G, sc, sv, off, nl, first, av):
-    """Emulation of engine.cuh pair_round (per-pair thread groups)."""
-    npairs = (nl + 1) // 2
-    npos = off[nl] + (nl & 1)
-    nq = [(off[2 * q + 2] if 2 * q + 2 <= nl else off[nl] + 1) - off[2 * q] for q in range(npairs)]
-    Lq = [1 + (n * (G - npairs)) // npos for n in nq]
-    assert sum(Lq) <= G
-    fq = [sum(Lq[:q]) for q in range(npairs)]
-    outs = []
-    for rank in range(G):
-        p = max(q for q in range(npairs) if fq[q] <= rank)
-        sub, L, n = rank - fq[p], Lq[p], nq[p]
-        oc_l, ov_l = [], []
-        if sub < L:
-            VT = (-(-n // L)) | 1
-            d = sub * VT
-            if d < n:
-                as_, bs = off[2 * p], off[2 * p + 1]
-                na, nb = bs - as_, n - (bs - as_)
-                i = merge_path(sc[as_:bs], sc[bs:bs + nb], d)
-                j = d - i
-                if i > 0 and j < nb and sc[as_ + i - 1] == sc[bs + j]:
-                    j += 1
-                if i < na:
-                    ia, ib = as_ + i, bs + j
-                    lim = min(d + VT, n) + as_ + bs
-                    while ia + ib < lim:
-                        ca, cb = sc[ia], sc[ib]
-                        ta, tb = ca <= cb, cb <= ca
-                        sa = av[2 * p] if first else 1.0
-                        sb = (av[2 * p + 1] if 2 * p + 1 < nl else 0.0) if first else 1.0
-                        oc_l.append(min(ca, cb))
-                        ov_l.append((sa * sv[ia] if ta else -0.0) + (sb * sv[ib] if tb else -0.0))
-                        ia += ta
-                        ib += tb
-        outs.append((p, sub, oc_l, ov_l))
-    base, dc, dv, noff = 0, [], [], {}
-    for p, sub, oc_l, ov_l in outs:
-        if sub == 0:
-            noff[p] = base
-        dc += oc_l
-        dv += ov_l
-        base += len(oc_l)
-    noff[npairs] = base
-    dc.append(INF)
-    dv.append(0.0)
-    return dc, dv, [noff[q] for q in range(npairs + 1)]
-
-
 ROUND = chunk_round
 
 
@@ -182,14 +134,12 @@ if __name__ == "__main__":
     cases = [(_lists_matrix([90, 93, 94], 33, 5000, seed=33), [32, 128, 256]),
              (_lists_matrix([5, 50, 700], 4, 3000, seed=3, empty_rows_of_b=1500), [32, 128, 256]),
              ((stencil27(6), stencil27(6)), [32, 8, 16])]
-    for name, fn in (("chunk_round", chunk_round), ("pair_round", pair_round)):
+    for name, fn in (("chunk_round", chunk_round),):
       ROUND = fn
       for (A, B), Gs in cases:
         ref, _ = oracle.spgemm_brmerge(A, B)
         for G in Gs:
             for r in range(A.rows):
-                if A.rpt[r + 1] - A.rpt[r] > 2 * G and fn is pair_round:
-                    continue
                 c, v = chunk_row(G, A, B, r)
                 s, e = ref.rpt[r], ref.rpt[r + 1]
                 assert list(ref.col[s:e]) == c, (name, G, r, "cols")
