@@ -782,3 +782,88 @@ __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, c
 }
 
 }  // namespace brm
+
+namespace brm {
+
+// ===========================================================================
+// Hash symbolic phase (BRMerge-Precise step 3: "computes the
+// row_size of the C matrix by the hashing method"), tiers 3-6: every product
+// column of the row is inserted into a per-row shared-memory hash table
+// (linear probing, atomicCAS); the row size is the number of first
+// insertions. The table has H = the power of two >= 3P/2 slots (<= HCAP).
+// ===========================================================================
+constexpr int kHashEmpty = -1;
+
+template <int CAP>
+__host__ __device__ constexpr int hash_cap() {
+  int h = 64;
+  while (h < CAP + CAP / 2) h <<= 1;
+  return h;
+}
+
+struct HashBufs {
+  int* table;           // HCAP slots
+  unsigned short* owner;  // CAP: list of each product
+  int* off;             // LCAP + 1 list offsets (product index)
+  int64_t* bst;         // LCAP B row starts
+  int* scan_tmp;
+};
+
+template <int G, int CAP, int LCAP>
+__host__ __device__ constexpr int hash_group_bytes() {
+  return align16(hash_cap<CAP>() * 4) + align16(CAP * 2) + align16((LCAP + 1) * 4) + align16(LCAP * 8) +
+         (G > 32 ? align16((G / 32 + 2) * 4) : 0);
+}
+
+template <int G, int CAP>
+__device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
+                                         const RowOut& o, const HashBufs& hb) {
+  const int rank = g.rank;
+  const int64_t a0 = A.rpt[row];
+  const int nl = static_cast<int>(A.rpt[row + 1] - a0);
+  int P = 0;
+  for (int lb = 0; lb < nl; lb += G) {
+    const int l = lb + rank;
+    int n = 0;
+    if (l < nl) {
+      const int k = __ldg(A.col + a0 + l);
+      const int64_t st = __ldg(B.rpt + k);
+      n = static_cast<int>(__ldg(B.rpt + k + 1) - st);
+      hb.bst[l] = st;
+    }
+    int tot;
+    const int ex = group_excl_scan<G>(g, n, tot, hb.scan_tmp);
+    if (l < nl) hb.off[l] = P + ex;
+    P += tot;
+  }
+  if (rank == 0) hb.off[nl] = P;
+  int H = 64;
+  while (H < P + P / 2) H <<= 1;
+  for (int e = rank; e < H; e += G) hb.table[e] = kHashEmpty;
+  g.sync();
+  for (int l = rank; l < nl; l += G)
+    for (int e = hb.off[l], e1 = hb.off[l + 1]; e < e1; ++e) hb.owner[e] = static_cast<unsigned short>(l);
+  g.sync();
+  int cnt = 0;
+#pragma unroll 2
+  for (int e = rank; e < P; e += G) {
+    const int l = hb.owner[e];
+    const int c = __ldg(B.col + hb.bst[l] + (e - hb.off[l]));
+    unsigned h = (static_cast<unsigned>(c) * 2654435761u) & (H - 1);
+    while (true) {
+      const int old = atomicCAS(&hb.table[h], kHashEmpty, c);
+      if (old == kHashEmpty) {
+        ++cnt;
+        break;
+      }
+      if (old == c) break;
+      h = (h + 1) & (H - 1);
+    }
+  }
+  int total;
+  group_excl_scan<G>(g, cnt, total, hb.scan_tmp);
+  if (rank == 0) o.row_size[row] = total;
+  g.sync();
+}
+
+}  // namespace brm

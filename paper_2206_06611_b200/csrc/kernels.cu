@@ -425,6 +425,29 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
   }
 }
 
+// PRECISE symbolic phase of tiers 3-6: hash_row per group (GPC groups of G).
+template <int G, int CAP, int LCAP, int GPC>
+__global__ void __launch_bounds__(G * GPC) k_hash_symbolic(CsrView A, CsrView B, const int32_t* __restrict__ rows,
+                                                          int64_t nrows, RowOut o) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Group<G> g = make_group<G>();
+  const int gid = threadIdx.x / G;
+  unsigned char* p = smem + gid * hash_group_bytes<G, CAP, LCAP>();
+  auto take = [&](int n) {
+    unsigned char* q = p;
+    p += align16(n);
+    return q;
+  };
+  HashBufs hb;
+  hb.table = reinterpret_cast<int*>(take(hash_cap<CAP>() * 4));
+  hb.owner = reinterpret_cast<unsigned short*>(take(CAP * 2));
+  hb.off = reinterpret_cast<int*>(take((LCAP + 1) * 4));
+  hb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
+  hb.scan_tmp = G > 32 ? reinterpret_cast<int*>(take((G / 32 + 2) * 4)) : nullptr;
+  for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
+    hash_row<G, CAP>(g, A, B, rows[r], o, hb);
+}
+
 // Tier 1: one thread per row (tiny_row), NT threads per CTA.
 constexpr int kTinyNT = 128;
 template <bool VALS, int OUT>
@@ -752,9 +775,39 @@ static cudaError_t launch_tiny(const CsrView& A, const CsrView& B, const int32_t
   return cudaGetLastError();
 }
 
+template <int G, int CAP, int LCAP, int GPC>
+static cudaError_t launch_hash_t(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
+                                 cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  constexpr int smem = hash_group_bytes<G, CAP, LCAP>() * GPC;
+  static_assert(smem <= 232448, "hash tier shared memory exceeds 227 KB");
+  auto kern = k_hash_symbolic<G, CAP, LCAP, GPC>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G * GPC, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t want = (n + GPC - 1) / GPC;
+  const int64_t cap = (int64_t)per_sm * num_sms();
+  kern<<<(unsigned)(want < cap ? want : cap), G * GPC, smem, st>>>(A, B, rows, n, o);
+  return cudaGetLastError();
+}
+
 template <bool VALS, int OUT>
 static cudaError_t launch_tier_dispatch(int bin, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
                                         const RowOut& o, cudaStream_t st) {
+  if constexpr (OUT == OUT_SYMBOLIC) {  // PRECISE step 3: hash counting on tiers 3-6
+    switch (bin) {
+      case 3: return launch_hash_t<BRM_TIER3>(A, B, rows, n, o, st);
+      case 4: return launch_hash_t<BRM_TIER4>(A, B, rows, n, o, st);
+      case 5: return launch_hash_t<BRM_TIER5>(A, B, rows, n, o, st);
+      case 6: return launch_hash_t<BRM_TIER6>(A, B, rows, n, o, st);
+      default: break;
+    }
+  }
   switch (bin) {
     case 1: return launch_tiny<VALS, OUT>(A, B, rows, n, o, st);
     case 2: return launch_tier_t<BRM_TIER2, VALS, OUT>(A, B, rows, n, o, st);
