@@ -430,9 +430,17 @@ __device__ __forceinline__ int chunk_round(const Group<G>& g, int* sc, double* s
   for (int q = pf; q <= pl; ++q) noff[q] += base;
   {
     g.sync();  // every merge has finished reading sc
-    for (int e = 0; e < cnt; ++e) {
-      sc[base + e] = dc[g0 + e];
-      if (VALS) sv[base + e] = dv[g0 + e];
+    // copy back warp-cooperatively: the warp copies each of its 32 threads'
+    // chunks in turn, coalesced (a thread-serial copy is latency-bound here)
+    const int lane = threadIdx.x & 31;
+    for (int j = 0; j < 32; ++j) {
+      const int cj = __shfl_sync(0xffffffffu, cnt, j);
+      const int gj = __shfl_sync(0xffffffffu, g0, j);
+      const int bj = __shfl_sync(0xffffffffu, base, j);
+      for (int e = lane; e < cj; e += 32) {
+        sc[bj + e] = dc[gj + e];
+        if (VALS) sv[bj + e] = dv[gj + e];
+      }
     }
     if (g.rank == G - 1) {
       noff[npairs] = total;
