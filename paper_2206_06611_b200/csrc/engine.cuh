@@ -749,16 +749,17 @@ __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, c
     sc[P + nl] = INT_MAX;  // lone partner sentinel if nl is odd
   }
   g.sync();
-  // ... then the B rows themselves (unscaled; round 1 multiplies): product e
-  // of list l goes to slot e + l; consecutive threads take consecutive
-  // products (coalesced), each tracking its current list.
+  // ... then the B rows themselves (unscaled; round 1 multiplies): a warp
+  // per list, the list's products copied coalesced to its slots.
   {
-    int l = 0;
-    for (int e = rank; e < P; e += G) {
-      while (off[l + 1] - (l + 1) <= e) ++l;  // E_{l+1} <= e
-      const int64_t src = cb.bst[l] + (e - (off[l] - l));
-      sc[e + l] = __ldg(B.col + src);
-      if (VALS) sv[e + l] = __ldg(B.val + src);
+    const int lane = threadIdx.x & 31, warp = rank >> 5;
+    for (int l = warp; l < nl; l += G / 32) {
+      const int o0 = off[l], n = off[l + 1] - 1 - o0;
+      const int64_t st = cb.bst[l];
+      for (int e = lane; e < n; e += 32) {
+        sc[o0 + e] = __ldg(B.col + st + e);
+        if (VALS) sv[o0 + e] = __ldg(B.val + st + e);
+      }
     }
   }
   g.sync();
