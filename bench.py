@@ -377,7 +377,7 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the oracle baseline runs at N=1 only
         try:
             import oracle
             rows, sample = _sample_rows(nprod_h[r0:r1], args.cpu_sample_prod)
