@@ -233,7 +233,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample-prod", type=float, default=1.5e7)
+    ap.add_argument("--cpu-sample-prod", type=float, default=2e6, help="probe sample (products)")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle time of the cpu_baseline")
     ap.add_argument("--ref-sample-prod", type=float, default=1.5e7)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -380,7 +381,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the oracle baseline runs at N=1 only
         try:
             import oracle
-            rows, sample = _sample_rows(nprod_h[r0:r1], args.cpu_sample_prod)
+            # a probe sample sizes the timed sample to ~args.cpu_seconds of oracle work
+            rows, _ = _sample_rows(nprod_h[r0:r1], args.cpu_sample_prod)
+            t0 = time.perf_counter()
+            oracle.spgemm_gustavson(Ablk, B, rows=rows)
+            rate = int(np_loc[rows].sum()) / max(time.perf_counter() - t0, 1e-6)
+            rows, sample = _sample_rows(nprod_h[r0:r1], rate * args.cpu_seconds)
             t0 = time.perf_counter()
             oracle.spgemm_gustavson(Ablk, B, rows=rows)
             dt = time.perf_counter() - t0
