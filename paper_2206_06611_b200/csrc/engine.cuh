@@ -502,21 +502,30 @@ __host__ __device__ constexpr int rec_group_bytes() {
          align16(LCAP * 8) + (VALS ? align16(LCAP * 8) : 0) + (G > 32 ? align16((G / 32 + 2) * 4) : 0);
 }
 
-// merge path over the columns of two record lists
+// merge path over the columns of two record lists (reads only the 4-byte
+// column of each probed record: the record array viewed as ints, stride S)
 template <bool VALS>
 __device__ __forceinline__ int merge_path_rec(const typename Rec<VALS>::T* a, int la, const typename Rec<VALS>::T* b,
                                               int lb, int diag) {
-  using R = Rec<VALS>;
+  constexpr int S = Rec<VALS>::kBytes / 4;
+  const int* ac = reinterpret_cast<const int*>(a);
+  const int* bc = reinterpret_cast<const int*>(b);
   int lo = diag - lb > 0 ? diag - lb : 0;
   int hi = diag < la ? diag : la;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (R::col(a[mid]) <= R::col(b[diag - 1 - mid]))
+    if (ac[S * mid] <= bc[S * (diag - 1 - mid)])
       lo = mid + 1;
     else
       hi = mid;
   }
   return lo;
+}
+
+// column of record i (4-byte load)
+template <bool VALS>
+__device__ __forceinline__ int rec_col(const typename Rec<VALS>::T* r, int i) {
+  return reinterpret_cast<const int*>(r)[(Rec<VALS>::kBytes / 4) * i];
 }
 
 // One round over the nl sentinel-terminated record lists of `rec` (offsets
@@ -557,7 +566,7 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, typename Rec<VALS>::
     }
     const int i = merge_path_rec<VALS>(rec + as, na, rec + bs, nb, d);
     int j = d - i;
-    if (i > 0 && j < nb && R::col(rec[as + i - 1]) == R::col(rec[bs + j])) ++j;  // b[j] was summed on the left
+    if (i > 0 && j < nb && rec_col<VALS>(rec, as + i - 1) == rec_col<VALS>(rec, bs + j)) ++j;  // b[j] summed on the left
     if (i == na) {  // pair p finished on the left
       if (g0 + 1 < g1) {
         ++p;
