@@ -30,7 +30,7 @@ struct RowOut {
   int64_t* row_size;    // OUT_SYMBOLIC / OUT_CBAR: nnz of each output row
 };
 
-// Shared scratch of one register-tier group (G slots each).
+// Shared scratch of one register-tier (tier 2) group (G slots each).
 struct RegBufs {
   int* col;
   double* val;

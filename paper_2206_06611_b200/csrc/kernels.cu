@@ -4,13 +4,19 @@
 //                    (§II.B.2) fused with a single-pass decoupled look-back
 //                    exclusive scan (CUB-free), the per-bin histogram and max.
 //   k_bin_scatter    row binning by n_prod / list count into tiers.
-//   k_tier<...>      BRMerge of one row per thread group: register tiers 1-2,
-//                    shared-memory ping-pong tiers 3-6 (warp, warp, 128, 256).
-//   k_global_tier    BRMerge of the heaviest rows (tier 7), ping-pong buffers in
-//                    a global-memory workspace, one 512-thread CTA per row.
+//   k_tiny           tier 1: one thread per row runs Algorithm 1 literally.
+//   k_tier<...>      tier 2: register BRMerge, one warp per row; tiers 3-6:
+//                    record BRMerge (warp / 64 / 128 / 256 threads per row).
+//   k_hash_symbolic  BRMerge-Precise step 3 on tiers 3-6: per-row shared
+//                    hash table counts the distinct columns.
+//   k_global_tier    tier 7: the heaviest rows, ping-pong buffers in a global
+//                    workspace, one 1024-thread CTA per row.
+//   k_split_a1/a2,   tier 7 heavy-row decomposition into aligned 32-list
+//   k_scatter_rows   blocks (sub-trees of Algorithm 1's tree).
 //   k_scan_i64       exclusive scan (row_size -> rpt; generic).
 //   k_compact        Step 6 of Fig. 4a: C_bar -> C copy (BRMerge-Upper).
 //   k_partition      §III.D row partition by balanced n_prod (multi-GPU).
+//   k_row_nprod      n_prod per row (stage entry point).
 #include <algorithm>
 #include <cstdio>
 
@@ -384,8 +390,8 @@ __global__ void k_heavy_info(CsrView A, const int64_t* __restrict__ nprod_off,
   }
 }
 
-// Shared-memory tiers: GPC groups of G threads per CTA, one row per group at a
-// time, the group's buffers in its slice of dynamic shared memory. CAP <= 32:
+// Tiers 2-6: GPC groups of G threads per CTA, one row per group at a time,
+// the group's buffers in its slice of dynamic shared memory. CAP <= 32:
 // register tier (reg_row), else record tier (rec_row).
 template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT>
 __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const int32_t* __restrict__ rows,
