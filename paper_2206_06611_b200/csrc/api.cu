@@ -51,9 +51,6 @@ struct brm_context {
   unsigned ev_mask = 0;  // events recorded since the last structure call
   int64_t launches = 0;  // kernels launched since the last structure call
   brm_context* sub = nullptr;  // heavy-row decomposition runs its sub-products here
-  brm_context* pipe[2] = {nullptr, nullptr};  // host-buffer form: chunk pipeline contexts
-  cudaStream_t pipe_st[2] = {nullptr, nullptr};
-  cudaEvent_t up_done = nullptr;
   DevBuf split_rows, split_off, glob_rows, a1_rpt, a1_col, a1_val, a2_rpt, a2_col, a2_val;
   HostBuf h_rows, h_split;
 };
@@ -525,96 +522,6 @@ brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
   return BRM_OK;
 }
 
-// Host-buffer form for large A: after A and B are uploaded, A's rows are
-// processed in kPipeChunks row blocks on two pipeline contexts with their own
-// streams, so the device->host copy of block k overlaps the SpGEMM of block
-// k+1. A row block is a view of the uploaded A (its rpt values stay absolute
-// offsets into A's col/val). C's blocks land in one pinned host buffer; each
-// block's row pointers are rebased on the device before the copy.
-constexpr int64_t kPipeRows = 65536;
-constexpr int kPipeChunks = 4;
-
-brm_status_t host_pipelined(brm_context_t* ctx, const brm_csr_t* Ah, const brm_csr_t* Bh, const brm_csr_t* Ad,
-                            const brm_csr_t* Bd, brm_mode_t mode, brm_csr_t* Ch) {
-  const int64_t M = Ah->rows;
-  if (!ctx->up_done) CK(cudaEventCreateWithFlags(&ctx->up_done, cudaEventDisableTiming), "create event");
-  CK(cudaEventRecord(ctx->up_done, ctx->stream), "record uploads");
-  for (int j = 0; j < 2; ++j) {
-    if (!ctx->pipe_st[j]) CK(cudaStreamCreateWithFlags(&ctx->pipe_st[j], cudaStreamNonBlocking), "create stream");
-    if (!ctx->pipe[j]) {
-      brm_status_t st = brm_create(&ctx->pipe[j], ctx->device, ctx->pipe_st[j]);
-      if (st != BRM_OK) return fail(ctx, st, "cannot create a pipeline context");
-    }
-    CK(cudaStreamWaitEvent(ctx->pipe_st[j], ctx->up_done, 0), "wait uploads");
-  }
-  const size_t brpt = (size_t)(M + 1) * 8;
-  const size_t rpt_region = (brpt + 15) & ~size_t(15);
-  auto cap_nnz = [&]() -> int64_t {
-    return ctx->h_C.cap > rpt_region + 32 ? (int64_t)((ctx->h_C.cap - rpt_region - 32) / 12) : 0;
-  };
-  int64_t off = 0;
-  for (int k = 0; k < kPipeChunks; ++k) {
-    brm_context_t* sub = ctx->pipe[k & 1];
-    cudaStream_t st = ctx->pipe_st[k & 1];
-    const int64_t r0 = M * k / kPipeChunks, r1 = M * (k + 1) / kPipeChunks;
-    const brm_csr_t Ak{r1 - r0, Ad->cols, Ah->rpt[r1] - Ah->rpt[r0], Ad->rpt + r0, Ad->col, Ad->val};
-    CK(ensure(sub, sub->stC_rpt, (size_t)(r1 - r0 + 1) * 8), "alloc chunk C.rpt");
-    int64_t nnz = 0;
-    brm_status_t s = structure_impl(sub, &Ak, Bd, mode, static_cast<int64_t*>(sub->stC_rpt.p), &nnz);
-    ctx->launches += sub->launches;
-    if (s != BRM_OK) return fail(ctx, s, std::string("pipelined chunk: ") + sub->err);
-    if (off + nnz > cap_nnz()) {  // grow the pinned output (first calls only)
-      CK(cudaStreamSynchronize(ctx->pipe_st[0]), "sync pipe");
-      CK(cudaStreamSynchronize(ctx->pipe_st[1]), "sync pipe");
-      const int64_t want = 2 * (off + nnz) + 1024;
-      HostBuf nb;
-      CK(ensure_host(nb, rpt_region + (size_t)want * 12 + 32), "alloc pinned C");
-      if (ctx->h_C.p) {
-        const int64_t old_cap = cap_nnz();
-        unsigned char* o = static_cast<unsigned char*>(ctx->h_C.p);
-        unsigned char* n = static_cast<unsigned char*>(nb.p);
-        memcpy(n, o, rpt_region);
-        memcpy(n + rpt_region, o + rpt_region, (size_t)off * 8);                                // values
-        memcpy(n + rpt_region + (size_t)want * 8, o + rpt_region + (size_t)old_cap * 8, (size_t)off * 4);  // cols
-        cudaFreeHost(ctx->h_C.p);
-      }
-      ctx->h_C = nb;
-    }
-    CK(ensure(sub, sub->stC_col, (size_t)std::max<int64_t>(nnz, 1) * 4), "alloc chunk C.col");
-    CK(ensure(sub, sub->stC_val, (size_t)std::max<int64_t>(nnz, 1) * 8), "alloc chunk C.val");
-    brm_csr_t Ck{0, 0, 0, static_cast<int64_t*>(sub->stC_rpt.p), static_cast<int32_t*>(sub->stC_col.p),
-                 static_cast<double*>(sub->stC_val.p)};
-    s = fill_impl(sub, &Ck);
-    ctx->launches += 1;
-    if (s != BRM_OK) return fail(ctx, s, std::string("pipelined chunk: ") + sub->err);
-    CK(launch_add_i64(Ck.rpt, r1 - r0 + 1, off, st), "k_add_i64");
-    ++ctx->launches;
-    const int64_t cap = cap_nnz();
-    unsigned char* h = static_cast<unsigned char*>(ctx->h_C.p);
-    double* hv = reinterpret_cast<double*>(h + rpt_region);
-    int32_t* hc = reinterpret_cast<int32_t*>(h + rpt_region + (size_t)cap * 8);
-    const int64_t nr = (k == kPipeChunks - 1) ? r1 - r0 + 1 : r1 - r0;
-    CK(cudaMemcpyAsync(reinterpret_cast<int64_t*>(h) + r0, Ck.rpt, (size_t)nr * 8, cudaMemcpyDeviceToHost, st),
-       "D2H C.rpt");
-    if (nnz) {
-      CK(cudaMemcpyAsync(hv + off, Ck.val, (size_t)nnz * 8, cudaMemcpyDeviceToHost, st), "D2H C.val");
-      CK(cudaMemcpyAsync(hc + off, Ck.col, (size_t)nnz * 4, cudaMemcpyDeviceToHost, st), "D2H C.col");
-    }
-    off += nnz;
-  }
-  CK(cudaStreamSynchronize(ctx->pipe_st[0]), "sync pipe");
-  CK(cudaStreamSynchronize(ctx->pipe_st[1]), "sync pipe");
-  unsigned char* h = static_cast<unsigned char*>(ctx->h_C.p);
-  Ch->rows = M;
-  Ch->cols = Bh->cols;
-  Ch->nnz = off;
-  Ch->rpt = reinterpret_cast<int64_t*>(h);
-  Ch->val = reinterpret_cast<double*>(h + rpt_region);
-  Ch->col = reinterpret_cast<int32_t*>(h + rpt_region + (size_t)cap_nnz() * 8);
-  ctx->stats = ctx->pipe[0]->stats;  // stats: the last chunk pair is not aggregated
-  return BRM_OK;
-}
-
 }  // namespace
 
 extern "C" {
@@ -667,11 +574,6 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
       if (e) cudaEventDestroy(e);
   }
   if (ctx->sub) brm_destroy(ctx->sub);
-  for (int j = 0; j < 2; ++j) {
-    if (ctx->pipe[j]) brm_destroy(ctx->pipe[j]);
-    if (ctx->pipe_st[j]) cudaStreamDestroy(ctx->pipe_st[j]);
-  }
-  if (ctx->up_done) cudaEventDestroy(ctx->up_done);
   delete ctx;
   return BRM_OK;
 }
@@ -798,7 +700,6 @@ brm_status_t brmerge_spgemm_host(brm_context_t* ctx, const brm_csr_t* Ah, const 
   const DevBuf& bv = same ? ctx->stA_val : ctx->stB_val;
   brm_csr_t Bd{Bh->rows, Bh->cols, Bh->nnz, static_cast<int64_t*>(br.p), static_cast<int32_t*>(bc.p),
                static_cast<double*>(bv.p)};
-  if (Ah->rows >= kPipeRows) return host_pipelined(ctx, Ah, Bh, &Ad, &Bd, mode, Ch);
   CK(ensure(ctx, ctx->stC_rpt, (size_t)(Ah->rows + 1) * 8), "alloc C.rpt");
   int64_t nnz = 0;
   if ((s = structure_impl(ctx, &Ad, &Bd, mode, static_cast<int64_t*>(ctx->stC_rpt.p), &nnz)) != BRM_OK) return s;

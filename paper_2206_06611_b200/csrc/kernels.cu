@@ -499,19 +499,6 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
   chunk_row<kGlobalG, VALS, OUT>(g, A, B, row, o, cb);
 }
 
-// x[i] += add for i < n (row-pointer rebasing of a pipelined chunk).
-__global__ void k_add_i64(int64_t* __restrict__ x, int64_t n, int64_t add) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    x[i] += add;
-}
-
-cudaError_t launch_add_i64(int64_t* x, int64_t n, int64_t add, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
-  k_add_i64<<<(unsigned)blocks, 256, 0, st>>>(x, n, add);
-  return cudaGetLastError();
-}
-
 // ---------------------------------------------------------------------------
 // Heavy-row decomposition (tier 7 rows with nl > kSplitLists). Algorithm 1's
 // tree over a row's nl lists splits into aligned sub-trees over blocks of

@@ -38,8 +38,6 @@ cudaError_t launch_compact(int64_t M, const int64_t* nprod_off, const int64_t* c
 cudaError_t launch_partition(const int64_t* nprod_off, int64_t M, int p, int64_t* bounds, cudaStream_t st);
 cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod, cudaStream_t st);
 
-cudaError_t launch_add_i64(int64_t* x, int64_t n, int64_t add, cudaStream_t st);
-
 // heavy-row decomposition (kernels.cu "Heavy-row decomposition")
 constexpr int kSplitListsHost = 32;
 constexpr int kSplitAvgLen = 32;  // split rows whose mean list length is at most this
