@@ -330,3 +330,20 @@ def test_heavy_row_recursive_split(ctx, oracle_mod, mode):
     A = Csr(2, kb, np.array([0, kb, kb + 3000], np.int64), np.concatenate(cols),
             rng.uniform(-1, 1, size=kb + 3000))
     compare(run(ctx, A, B, mode), A, B)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_host_form_large(ctx, oracle_mod, mode):
+    """The host-buffer entry on 70,001 rows: two calls in a row (pinned
+    output grown, then reused), C = A*A (single upload) and C = A*B."""
+    from paper_2206_06611_b200 import TorchCsr
+    A = uniform_random(70001, 70001, 6, seed=31)
+    B = random_sparse(70001, 300, 0.01, seed=32)
+    Ah = TorchCsr.from_csr(A, pin=True)
+    for _ in range(2):
+        rows, cols, rpt, col, val = ctx.brmerge_spgemm_host(Ah, Ah, mode)
+        assert (rows, cols) == (70001, 70001)
+        compare((rpt.copy(), col.copy(), val.copy()), A, A)
+    Bh = TorchCsr.from_csr(B, pin=True)
+    rows, cols, rpt, col, val = ctx.brmerge_spgemm_host(Ah, Bh, mode)
+    compare((rpt.copy(), col.copy(), val.copy()), A, B)
