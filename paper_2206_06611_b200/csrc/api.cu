@@ -359,7 +359,7 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
     for (int64_t t = 0; t < ng; ++t) max_row = std::max(max_row, global_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals));
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    int64_t budget = std::min<int64_t>((int64_t)(free_b / 2) + (int64_t)ctx->gws.cap, 16ll << 30);
+    int64_t budget = std::min<int64_t>((int64_t)(free_b / 2) + (int64_t)ctx->gws.cap, 64ll << 30);
     budget = std::max(budget, max_row);
     CK(ensure_host(ctx->h_gws_off, (size_t)ng * 16), "alloc pinned ws offsets");
     CK(ensure(ctx, ctx->gws_off, (size_t)ng * 16), "alloc ws offsets");
