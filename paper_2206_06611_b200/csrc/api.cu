@@ -287,7 +287,7 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
   for (int b = 1; b < kBinGlobal; ++b) {
     if (!ctx->bin_rows[b]) continue;
     if (per_bin) ev_record(ctx, kEvBin + 2 * b);
-    CK(launch_tier(b, out, ctx->A, ctx->B, bins + ctx->bin_start[b], ctx->bin_rows[b], o, ctx->stream),
+    CK(launch_tier(b, out, ctx->A, ctx->B, ctx->N, bins + ctx->bin_start[b], ctx->bin_rows[b], o, ctx->stream),
        "k_tier");
     ++ctx->launches;
     if (per_bin) ev_record(ctx, kEvBin + 2 * b + 1);

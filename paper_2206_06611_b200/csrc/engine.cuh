@@ -465,28 +465,65 @@ __device__ __forceinline__ void lds_if(bool p, unsigned addr, int2& v) {
                : "r"(addr), "r"((unsigned)p));
 }
 
-// Record of a list element: {col, value slot} (numeric) or just col (symbolic).
-template <bool VALS>
-struct Rec;
-template <>
-struct Rec<true> {
+__device__ __forceinline__ void lds_if(bool p, unsigned addr, unsigned& v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.b32 %0, [%1];\n\t}"
+               : "+r"(v)
+               : "r"(addr), "r"((unsigned)p));
+}
+
+// Record of a list element. Numeric rounds carry {col, value slot}: 8 bytes
+// (RecWide) or, when the columns fit in 32 - SB bits, one 32-bit word
+// col << SB | slot (RecPacked<SB>, half the shared-memory wavefronts per
+// record move). Symbolic rounds carry the column only (RecCol). kSentCol is
+// the sentinel's column, above every real column.
+struct RecWide {
   using T = int2;
+  static constexpr bool kVals = true;
   static constexpr int kBytes = 8;
+  static constexpr int kSentCol = INT_MAX;
   __device__ static T make(int c, int s) { return make_int2(c, s); }
+  __device__ static T sent() { return make_int2(INT_MAX, 0); }
   __device__ static int col(const T& r) { return r.x; }
   __device__ static int slot(const T& r) { return r.y; }
+  __device__ static int col_at(const T* r, int i) { return reinterpret_cast<const int*>(r)[2 * i]; }  // 4-byte load
 };
-template <>
-struct Rec<false> {
-  using T = int;
+template <int SB>
+struct RecPacked {
+  using T = unsigned;
+  static constexpr bool kVals = true;
   static constexpr int kBytes = 4;
+  static constexpr int kSentCol = static_cast<int>(0xffffffffu >> SB);
+  __device__ static T make(int c, int s) { return (static_cast<unsigned>(c) << SB) | static_cast<unsigned>(s); }
+  __device__ static T sent() { return 0xffffffffu; }
+  __device__ static int col(T r) { return static_cast<int>(r >> SB); }
+  __device__ static int slot(T r) { return static_cast<int>(r & ((1u << SB) - 1u)); }
+  __device__ static int col_at(const T* r, int i) { return col(r[i]); }
+};
+struct RecCol {
+  using T = int;
+  static constexpr bool kVals = false;
+  static constexpr int kBytes = 4;
+  static constexpr int kSentCol = INT_MAX;
   __device__ static T make(int c, int) { return c; }
+  __device__ static T sent() { return INT_MAX; }
   __device__ static int col(T r) { return r; }
   __device__ static int slot(T) { return 0; }
+  __device__ static int col_at(const T* r, int i) { return r[i]; }
 };
 
+// slot bits of a packed record for a tier of CAP products (slots 0..CAP-1)
+__host__ __device__ constexpr int rec_slot_bits(int cap) {
+  int b = 0;
+  while ((1 << b) < cap) ++b;
+  return b;
+}
+// packed records need every column of B below the sentinel's column
+__host__ __device__ constexpr bool rec_pack_ok(int cap, int64_t b_cols) {
+  return b_cols <= static_cast<int64_t>(0xffffffffu >> rec_slot_bits(cap));
+}
+
 struct RecBufs {
-  void* rec;      // P + nl + 2 records (Rec<VALS>::T): sentinel-terminated lists
+  void* rec;      // P + nl + 2 records (R::T): sentinel-terminated lists
   double* val;    // P value slots (products, then partial sums)
   int* owner;     // P 16-bit entries: list of each product (multiplying phase)
   int* off0;
@@ -496,25 +533,23 @@ struct RecBufs {
   int* scan_tmp;
 };
 
-template <int G, int CAP, int LCAP, bool VALS>
+template <int G, int CAP, int LCAP, class R>
 __host__ __device__ constexpr int rec_group_bytes() {
-  return align16((CAP + LCAP + 2) * Rec<VALS>::kBytes) + (VALS ? align16(CAP * 8) : 0) + align16(CAP * 2) + align16((LCAP + 2) * 4) * 2 +
+  constexpr bool VALS = R::kVals;
+  return align16((CAP + LCAP + 2) * R::kBytes) + (VALS ? align16(CAP * 8) : 0) + align16(CAP * 2) + align16((LCAP + 2) * 4) * 2 +
          align16(LCAP * 8) + (VALS ? align16(LCAP * 8) : 0) + (G > 32 ? align16((G / 32 + 2) * 4) : 0);
 }
 
-// merge path over the columns of two record lists (reads only the 4-byte
-// column of each probed record: the record array viewed as ints, stride S)
-template <bool VALS>
-__device__ __forceinline__ int merge_path_rec(const typename Rec<VALS>::T* a, int la, const typename Rec<VALS>::T* b,
-                                              int lb, int diag) {
-  constexpr int S = Rec<VALS>::kBytes / 4;
-  const int* ac = reinterpret_cast<const int*>(a);
-  const int* bc = reinterpret_cast<const int*>(b);
+// merge path over the columns of two record lists (R::col_at reads only the
+// column of each probed record)
+template <class R>
+__device__ __forceinline__ int merge_path_rec(const typename R::T* a, int la, const typename R::T* b, int lb,
+                                              int diag) {
   int lo = diag - lb > 0 ? diag - lb : 0;
   int hi = diag < la ? diag : la;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (ac[S * mid] <= bc[S * (diag - 1 - mid)])
+    if (R::col_at(a, mid) <= R::col_at(b, diag - 1 - mid))
       lo = mid + 1;
     else
       hi = mid;
@@ -522,20 +557,14 @@ __device__ __forceinline__ int merge_path_rec(const typename Rec<VALS>::T* a, in
   return lo;
 }
 
-// column of record i (4-byte load)
-template <bool VALS>
-__device__ __forceinline__ int rec_col(const typename Rec<VALS>::T* r, int i) {
-  return reinterpret_cast<const int*>(r)[(Rec<VALS>::kBytes / 4) * i];
-}
-
 // One round over the nl sentinel-terminated record lists of `rec` (offsets
 // off[0..nl]); same partition as chunk_round (G chunks of VT odd positions,
 // threads cross into the next pair when both sentinels merge). Outputs wait
 // in registers and overwrite `rec` compacted once the group has read it.
-template <int G, int NV, bool VALS>
-__device__ __forceinline__ int rec_round(const Group<G>& g, typename Rec<VALS>::T* rec, double* val, const int* off,
+template <int G, int NV, class R>
+__device__ __forceinline__ int rec_round(const Group<G>& g, typename R::T* rec, double* val, const int* off,
                                          int* noff, int nl, int* scan_tmp) {
-  using R = Rec<VALS>;
+  constexpr bool VALS = R::kVals;
   using T = typename R::T;
   constexpr unsigned RB = R::kBytes;
   const int npairs = (nl + 1) >> 1;
@@ -544,7 +573,7 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, typename Rec<VALS>::
   const int g0 = min(g.rank * VT, npos), g1 = min(g0 + VT, npos);
   int pf = 0, pl = -1;
   int p = 0, bs = 0, ia = 0, ib = 0, lim = 0;
-  T ra = R::make(INT_MAX, 0), rb = R::make(INT_MAX, 0);
+  T ra = R::sent(), rb = R::sent();
   if (g0 < g1) {
     int lo = 0, hi = npairs - 1;  // last pair starting at or before g0
     while (lo < hi) {
@@ -564,9 +593,9 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, typename Rec<VALS>::
       pf = pl = p;
       noff[p] = 0;
     }
-    const int i = merge_path_rec<VALS>(rec + as, na, rec + bs, nb, d);
+    const int i = merge_path_rec<R>(rec + as, na, rec + bs, nb, d);
     int j = d - i;
-    if (i > 0 && j < nb && rec_col<VALS>(rec, as + i - 1) == rec_col<VALS>(rec, bs + j)) ++j;  // b[j] summed on the left
+    if (i > 0 && j < nb && R::col_at(rec, as + i - 1) == R::col_at(rec, bs + j)) ++j;  // b[j] summed on the left
     if (i == na) {  // pair p finished on the left
       if (g0 + 1 < g1) {
         ++p;
@@ -588,7 +617,7 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, typename Rec<VALS>::
   }
   const unsigned recb = smem_u32(rec);
   const unsigned valb = VALS ? smem_u32(val) : 0u;
-  int ocol[NV], oslot[VALS ? NV : 1];
+  T orec[NV];  // the chunk's outputs: the left record on ties (its slot keeps the sum)
   int cnt = 0;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
@@ -597,11 +626,10 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, typename Rec<VALS>::
     const int ca = R::col(ra), cb = R::col(rb);
     const bool ta = act && ca <= cb;
     const bool tb = act && cb <= ca;
-    ocol[v] = min(ca, cb);
+    orec[v] = ta ? ra : rb;
     if (VALS) {
-      oslot[v] = ta ? R::slot(ra) : R::slot(rb);
       // equal columns: val[left] = val[left] + val[right]
-      const bool dup = ta && tb && ca != INT_MAX;
+      const bool dup = ta && tb && ca != R::kSentCol;
       double x = 0.0, y = 0.0;
       lds_if(dup, valb + 8u * R::slot(ra), x);
       lds_if(dup, valb + 8u * R::slot(rb), y);
@@ -612,7 +640,7 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, typename Rec<VALS>::
     ib += tb;
     lds_if(ta, recb + RB * ia, ra);
     lds_if(tb, recb + RB * ib, rb);
-    if (act && ocol[v] == INT_MAX && ia + ib < lim) {  // pair p done, chunk not: enter pair p+1
+    if (act && min(ca, cb) == R::kSentCol && ia + ib < lim) {  // pair p done, chunk not: enter pair p+1
       if (pl < 0) pf = p + 1;
       ++p;
       pl = p;
@@ -631,20 +659,20 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, typename Rec<VALS>::
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     if (v >= VT) break;
-    if (v < cnt) rec[base + v] = R::make(ocol[v], VALS ? oslot[VALS ? v : 0] : 0);
+    if (v < cnt) rec[base + v] = orec[v];
   }
   if (g.rank == G - 1) {
     noff[npairs] = total;
-    rec[total] = R::make(INT_MAX, 0);  // lone partner sentinel, used if npairs is odd
+    rec[total] = R::sent();  // lone partner sentinel, used if npairs is odd
   }
   g.sync();
   return total;
 }
 
-template <int G, int NV, bool VALS, int OUT>
+template <int G, int NV, class R, int OUT>
 __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
                                         const RowOut& o, const RecBufs& rb) {
-  using R = Rec<VALS>;
+  constexpr bool VALS = R::kVals;
   typename R::T* rec = static_cast<typename R::T*>(rb.rec);
   const int rank = g.rank;
   const int64_t a0 = A.rpt[row];
@@ -668,13 +696,13 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
     const int ex = group_excl_scan<G>(g, n, tot, rb.scan_tmp);
     if (l < nl) {
       off[l] = P + ex + l;
-      rec[P + ex + l + n] = R::make(INT_MAX, 0);  // sentinel of list l
+      rec[P + ex + l + n] = R::sent();  // sentinel of list l
     }
     P += tot;
   }
   if (rank == 0) {
     off[nl] = P + nl;
-    rec[P + nl] = R::make(INT_MAX, 0);  // lone partner sentinel if nl is odd
+    rec[P + nl] = R::sent();  // lone partner sentinel if nl is odd
   }
   g.sync();
   {
@@ -698,7 +726,7 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
   int cur = nl;
   int end = P + nl;
   while (cur > 1) {
-    end = rec_round<G, NV, VALS>(g, rec, rb.val, off, noff, cur, rb.scan_tmp);
+    end = rec_round<G, NV, R>(g, rec, rb.val, off, noff, cur, rb.scan_tmp);
     cur = (cur + 1) >> 1;
     int* t = off;  // lines 33-34
     off = noff;
@@ -868,13 +896,19 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
     const int l = hb.owner[e];
     const int c = __ldg(B.col + hb.bst[l] + (e - hb.off[l]));
     unsigned h = (static_cast<unsigned>(c) * 2654435761u) & (H - 1);
+    // a plain load first: most products repeat a column already inserted
+    // (keys are never removed, so a non-empty slot read is final)
+    const volatile int* tv = hb.table;
     while (true) {
-      const int old = atomicCAS(&hb.table[h], kHashEmpty, c);
-      if (old == kHashEmpty) {
-        ++cnt;
-        break;
+      int cur = tv[h];
+      if (cur == kHashEmpty) {
+        cur = atomicCAS(&hb.table[h], kHashEmpty, c);
+        if (cur == kHashEmpty) {
+          ++cnt;
+          break;
+        }
       }
-      if (old == c) break;
+      if (cur == c) break;
       h = (h + 1) & (H - 1);
     }
   }

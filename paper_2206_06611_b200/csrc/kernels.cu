@@ -19,6 +19,7 @@
 //   k_row_nprod      n_prod per row (stage entry point).
 #include <algorithm>
 #include <cstdio>
+#include <type_traits>
 
 #include "engine.cuh"
 #include "kernels.cuh"
@@ -392,8 +393,12 @@ __global__ void k_heavy_info(CsrView A, const int64_t* __restrict__ nprod_off,
 
 // Tiers 2-6: GPC groups of G threads per CTA, one row per group at a time,
 // the group's buffers in its slice of dynamic shared memory. CAP <= 32:
-// register tier (reg_row), else record tier (rec_row).
-template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT>
+// register tier (reg_row), else record tier (rec_row) with records of type
+// RecT<VALS, PACK, CAP> (PACK: 32-bit {col, slot} records).
+template <bool VALS, bool PACK, int CAP>
+using RecT = std::conditional_t<VALS, std::conditional_t<PACK, RecPacked<rec_slot_bits(CAP)>, RecWide>, RecCol>;
+
+template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT, bool PACK>
 __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const int32_t* __restrict__ rows,
                                                  int64_t nrows, RowOut o) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -410,7 +415,8 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
     for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
       reg_row<G, VALS, OUT>(g, A, B, rows[r], o, rb);
   } else {
-    constexpr int bytes = rec_group_bytes<G, CAP, LCAP, VALS>();
+    using R = RecT<VALS, PACK, CAP>;
+    constexpr int bytes = rec_group_bytes<G, CAP, LCAP, R>();
     unsigned char* p = smem + gid * bytes;
     auto take = [&](int n) {
       unsigned char* q = p;
@@ -418,7 +424,7 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
       return q;
     };
     RecBufs rb;
-    rb.rec = take((CAP + LCAP + 2) * Rec<VALS>::kBytes);
+    rb.rec = take((CAP + LCAP + 2) * R::kBytes);
     rb.val = VALS ? reinterpret_cast<double*>(take(CAP * 8)) : nullptr;
     rb.owner = reinterpret_cast<int*>(take(CAP * 2));
     rb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
@@ -427,7 +433,7 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
     rb.av = VALS ? reinterpret_cast<double*>(take(LCAP * 8)) : nullptr;
     rb.scan_tmp = G > 32 ? reinterpret_cast<int*>(take((G / 32 + 2) * 4)) : nullptr;
     for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
-      rec_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, VALS, OUT>(g, A, B, rows[r], o, rb);
+      rec_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, R, OUT>(g, A, B, rows[r], o, rb);
   }
 }
 
@@ -734,17 +740,17 @@ cudaError_t launch_heavy_info(const CsrView& A, const int64_t* nprod_off, const 
   return cudaGetLastError();
 }
 
-template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT>
-static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
-                                 cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  constexpr int per_group = CAP <= 32 ? reg_group_bytes<G, VALS>() : rec_group_bytes<G, CAP, LCAP, VALS>();
+template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT, bool PACK>
+static cudaError_t launch_tier_pk(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
+                                  cudaStream_t st) {
+  constexpr int per_group =
+      CAP <= 32 ? reg_group_bytes<G, VALS>() : rec_group_bytes<G, CAP, LCAP, RecT<VALS, PACK, CAP>>();
   constexpr int smem = per_group * GPC;
   // registers hold <= NV chunk outputs; NV = 31 (G = 256, CAP 7168) miscompiled
   // (wrong values, no spills reported), so tiers keep NV <= 29
   static_assert(CAP <= 32 || (((CAP + LCAP + 1 + G - 1) / G) | 1) <= 29, "chunk tier NV must stay <= 29");
   static_assert(smem <= 232448, "tier shared memory exceeds 227 KB");
-  auto kern = k_tier<G, CAP, LCAP, GPC, VALS, OUT>;
+  auto kern = k_tier<G, CAP, LCAP, GPC, VALS, OUT, PACK>;
   // one process drives one device, so per-instantiation caching is safe
   static int per_sm = 0;
   if (!per_sm) {
@@ -759,6 +765,17 @@ static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, const int32
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   kern<<<grid, G * GPC, smem, st>>>(A, B, rows, n, o);
   return cudaGetLastError();
+}
+
+// numeric record tiers take packed records when B's columns fit beside the slot
+template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT>
+static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows, int64_t n,
+                                 const RowOut& o, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if constexpr (VALS && CAP > 32) {
+    if (rec_pack_ok(CAP, b_cols)) return launch_tier_pk<G, CAP, LCAP, GPC, VALS, OUT, true>(A, B, rows, n, o, st);
+  }
+  return launch_tier_pk<G, CAP, LCAP, GPC, VALS, OUT, false>(A, B, rows, n, o, st);
 }
 
 template <bool VALS, int OUT>
@@ -803,8 +820,8 @@ static cudaError_t launch_hash_t(const CsrView& A, const CsrView& B, const int32
 }
 
 template <bool VALS, int OUT>
-static cudaError_t launch_tier_dispatch(int bin, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
-                                        const RowOut& o, cudaStream_t st) {
+static cudaError_t launch_tier_dispatch(int bin, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
+                                        int64_t n, const RowOut& o, cudaStream_t st) {
   if constexpr (OUT == OUT_SYMBOLIC) {  // PRECISE step 3: hash counting on tiers 3-6
     switch (bin) {
       case 3: return launch_hash_t<BRM_TIER3>(A, B, rows, n, o, st);
@@ -816,21 +833,21 @@ static cudaError_t launch_tier_dispatch(int bin, const CsrView& A, const CsrView
   }
   switch (bin) {
     case 1: return launch_tiny<VALS, OUT>(A, B, rows, n, o, st);
-    case 2: return launch_tier_t<BRM_TIER2, VALS, OUT>(A, B, rows, n, o, st);
-    case 3: return launch_tier_t<BRM_TIER3, VALS, OUT>(A, B, rows, n, o, st);
-    case 4: return launch_tier_t<BRM_TIER4, VALS, OUT>(A, B, rows, n, o, st);
-    case 5: return launch_tier_t<BRM_TIER5, VALS, OUT>(A, B, rows, n, o, st);
-    case 6: return launch_tier_t<BRM_TIER6, VALS, OUT>(A, B, rows, n, o, st);
+    case 2: return launch_tier_t<BRM_TIER2, VALS, OUT>(A, B, b_cols, rows, n, o, st);
+    case 3: return launch_tier_t<BRM_TIER3, VALS, OUT>(A, B, b_cols, rows, n, o, st);
+    case 4: return launch_tier_t<BRM_TIER4, VALS, OUT>(A, B, b_cols, rows, n, o, st);
+    case 5: return launch_tier_t<BRM_TIER5, VALS, OUT>(A, B, b_cols, rows, n, o, st);
+    case 6: return launch_tier_t<BRM_TIER6, VALS, OUT>(A, B, b_cols, rows, n, o, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
-                        const RowOut& o, cudaStream_t st) {
+cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
+                        int64_t n, const RowOut& o, cudaStream_t st) {
   switch (out_kind) {
-    case OUT_SYMBOLIC: return launch_tier_dispatch<false, OUT_SYMBOLIC>(bin, A, B, rows, n, o, st);
-    case OUT_CBAR: return launch_tier_dispatch<true, OUT_CBAR>(bin, A, B, rows, n, o, st);
-    case OUT_C: return launch_tier_dispatch<true, OUT_C>(bin, A, B, rows, n, o, st);
+    case OUT_SYMBOLIC: return launch_tier_dispatch<false, OUT_SYMBOLIC>(bin, A, B, b_cols, rows, n, o, st);
+    case OUT_CBAR: return launch_tier_dispatch<true, OUT_CBAR>(bin, A, B, b_cols, rows, n, o, st);
+    case OUT_C: return launch_tier_dispatch<true, OUT_C>(bin, A, B, b_cols, rows, n, o, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -28,8 +28,10 @@ cudaError_t launch_bin_scatter(const CsrView& A, const int64_t* nprod_off, int64
                                unsigned long long* cursor, int32_t* bins, int64_t* row_size, cudaStream_t st);
 cudaError_t launch_heavy_info(const CsrView& A, const int64_t* nprod_off, const int32_t* rows, int64_t n,
                               int64_t* info, cudaStream_t st);
-cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
-                        const RowOut& o, cudaStream_t st);
+// b_cols = B's column count (numeric record tiers pack {col, slot} into 32
+// bits when the columns fit)
+cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
+                        int64_t n, const RowOut& o, cudaStream_t st);
 int64_t global_row_bytes(int64_t nprod, int64_t nl, bool vals);
 cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
                                const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st);

@@ -94,6 +94,43 @@ def test_tier_boundaries(ctx, oracle_mod, mode, list_len, specs):
     compare(run(ctx, A, B, mode), A, B)
 
 
+def _top_column_matrix(specs, list_len, ncols, seed, pool=64):
+    """Like _lists_matrix, but every B row draws its columns from the `pool`
+    highest columns of an ncols-wide B (ncols - 1 included in every row), so
+    the merges see many duplicates right below the sentinel."""
+    rng = np.random.default_rng(seed)
+    kb = max(specs)
+    top = ncols - pool + np.arange(pool)
+    col = np.concatenate([np.sort(np.append(rng.choice(top[:-1], size=list_len - 1, replace=False), ncols - 1))
+                          for _ in range(kb)]).astype(np.int32)
+    B = Csr(kb, ncols, np.arange(kb + 1, dtype=np.int64) * list_len, col, rng.uniform(-1, 1, size=col.size))
+    arpt, acol = [0], []
+    for nl in specs:
+        acol.append(np.sort(rng.choice(kb, size=nl, replace=False)))
+        arpt.append(arpt[-1] + nl)
+    acol = np.concatenate(acol).astype(np.int32)
+    A = Csr(len(specs), kb, np.array(arpt, np.int64), acol, rng.uniform(-1, 1, size=acol.size))
+    return A, B
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("tier,slot_bits,list_len,nl", [
+    (3, 8, 12, 16),     # P = 192
+    (4, 10, 16, 40),    # P = 640
+    (5, 12, 24, 100),   # P = 2400
+    (6, 13, 20, 300),   # P = 6000
+])
+@pytest.mark.parametrize("wide", [False, True])
+def test_record_packing_boundary(ctx, oracle_mod, mode, tier, slot_bits, list_len, nl, wide):
+    """Record tiers pack {col, slot} into 32 bits while B.cols <=
+    2^(32 - slot_bits) - 1 (the sentinel's column) and fall back to 8-byte
+    records one column above; both sides of the boundary, with column
+    B.cols - 1 in every list."""
+    ncols = (1 << (32 - slot_bits)) - 1 + int(wide)
+    A, B = _top_column_matrix([nl, nl - 1, nl], list_len, ncols, seed=tier)
+    compare(run(ctx, A, B, mode), A, B)
+
+
 @pytest.mark.parametrize("mode", MODES)
 def test_misaligned_b_uses_cp_async_path(ctx, oracle_mod, mode):
     """B arrays not 16-byte aligned: TMA windows are illegal, the kernels must
