@@ -80,8 +80,9 @@ typedef struct {
 
 /* Number of row bins (tiers) the binning pass sorts rows into; see DESIGN.md
  * "Kernels": 0 = empty rows (n_prod == 0), 1-2 = register tiers (8-lane
- * group, warp), 3-6 = shared-memory ping-pong tiers (warp, warp, 128 and
- * 256 threads), 7 = global-memory ping-pong tier.                         */
+ * group, warp), 3-6 = shared-memory record tiers (warp, warp, 128 and
+ * 256 threads), 7 = heavy rows (column slabs, list-block decomposition or
+ * the global-memory tier; see brm_set_heavy_route).                       */
 #define BRM_NUM_BINS 8
 
 typedef struct {
@@ -114,6 +115,14 @@ BRM_API brm_status_t brm_destroy(brm_context_t* ctx);
 BRM_API brm_status_t brm_set_stream(brm_context_t* ctx, void* stream);
 /* Record per-phase CUDA-event times into brm_stats_t (adds syncs; off by default). */
 BRM_API brm_status_t brm_set_timing(brm_context_t* ctx, int enable);
+/* Route of the heavy rows (bin 7): BRM_HEAVY_AUTO (0,
+ * default): rows of <= 512 lists merge in column slabs in shared memory,
+ * rows of more lists are split into aligned list blocks; BRM_HEAVY_GLOBAL
+ * (1): every heavy row runs on the global-memory tier (testing and
+ * comparison). Results are identical. Errors: BRM_ERR_INVALID.            */
+#define BRM_HEAVY_AUTO 0
+#define BRM_HEAVY_GLOBAL 1
+BRM_API brm_status_t brm_set_heavy_route(brm_context_t* ctx, int route);
 /* Last error message of this context (static storage owned by ctx). */
 BRM_API const char* brm_last_error(const brm_context_t* ctx);
 BRM_API const char* brm_status_string(brm_status_t s);

@@ -15,6 +15,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-cudart", "static",
          "--expt-relaxed-constexpr", "-I", str(ROOT / "include"), "-I", str(CSRC)]
+# tuning experiments only (tools/variants.sh): extra nvcc flags, e.g. tier overrides
+FLAGS += os.environ.get("BRM_NVCC_FLAGS", "").split()
 
 
 def _stale() -> bool:

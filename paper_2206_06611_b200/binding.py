@@ -63,6 +63,7 @@ SIGNATURES = {
     "brm_destroy": [_P],
     "brm_set_stream": [_P, _P],
     "brm_set_timing": [_P, ctypes.c_int],
+    "brm_set_heavy_route": [_P, ctypes.c_int],
     "brm_last_error": [_P],
     "brm_status_string": [ctypes.c_int],
     "brm_get_stats": [_P, ctypes.POINTER(brm_stats_t)],
@@ -176,6 +177,13 @@ class Context:
 
     def set_timing(self, on: bool):
         self._check(self.lib.brm_set_timing(self._h, int(on)))
+
+    HEAVY_AUTO, HEAVY_GLOBAL = 0, 1
+
+    def brm_set_heavy_route(self, route: int):
+        """Route of the heavy rows: HEAVY_AUTO (column slabs / list blocks) or
+        HEAVY_GLOBAL (all on the global-memory tier); include/brmerge.h."""
+        self._check(self.lib.brm_set_heavy_route(self._h, int(route)))
 
     def stats(self) -> dict:
         s = brm_stats_t()

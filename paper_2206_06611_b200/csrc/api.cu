@@ -32,6 +32,7 @@ struct brm_context {
   cudaStream_t stream = nullptr;
   std::string err;
   bool timing = false;
+  int heavy_route = BRM_HEAVY_AUTO;
   // workspace (grow-only)
   DevBuf nprod_off, row_size, bins, status, small, cbar_col, cbar_val, gws, gws_off, heavy_info;
   DevBuf stA_rpt, stA_col, stA_val, stB_rpt, stB_col, stB_val, stC_rpt, stC_col, stC_val;
@@ -57,10 +58,10 @@ struct brm_context {
 
 namespace {
 brm_status_t heavy_split_impl(brm_context_t* ctx, int out, const RowOut& o, const int32_t* rows, int64_t n,
-                              const int64_t* info);
+                              const int64_t* info, int bs);
 brm_status_t heavy_split(brm_context_t* ctx, int out, const RowOut& o, const int32_t* rows, int64_t n,
-                         const int64_t* info) {
-  return heavy_split_impl(ctx, out, o, rows, n, info);
+                         const int64_t* info, int bs) {
+  return heavy_split_impl(ctx, out, o, rows, n, info, bs);
 }
 }  // namespace
 
@@ -108,6 +109,15 @@ cudaError_t ensure(brm_context_t* ctx, DevBuf& b, size_t bytes) {
   }
   const size_t want = (bytes + 255) & ~size_t(255);
   cudaError_t e = cudaMallocAsync(&b.p, want, ctx->stream);
+  if (e == cudaErrorMemoryAllocation) {
+    // blocks freed on the stream stay reserved in the pool until it is
+    // trimmed: return them to the device and retry once
+    (void)cudaGetLastError();
+    cudaMemPool_t pool;
+    if (cudaStreamSynchronize(ctx->stream) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess &&
+        cudaMemPoolTrimTo(pool, 0) == cudaSuccess)
+      e = cudaMallocAsync(&b.p, want, ctx->stream);
+  }
   if (e != cudaSuccess) {
     b.p = nullptr;
     return e;
@@ -196,11 +206,11 @@ brm_status_t run_scan(brm_context_t* ctx, const int64_t* in, int64_t n, int64_t*
 
 // Heavy-row decomposition (kernels.cu): the rows (host ids `rows`, host
 // (n_prod, nl) pairs `info`) are processed in batches bounded by free memory;
-// per batch C1 = A1 * B over blocks of kSplitListsHost lists, C2 = A2 * C1
+// per batch C1 = A1 * B over blocks of bs lists, C2 = A2 * C1
 // over the block results (both through the sub-context, recursively), and C2's
 // rows are scattered into this context's output.
 brm_status_t heavy_split_impl(brm_context_t* ctx, int out, const RowOut& o, const int32_t* rows, int64_t n,
-                              const int64_t* info) {
+                              const int64_t* info, int bs) {
   if (!ctx->sub) {
     brm_status_t st = brm_create(&ctx->sub, ctx->device, ctx->stream);
     if (st != BRM_OK) return fail(ctx, st, "heavy rows: cannot create the sub-context");
@@ -223,7 +233,7 @@ brm_status_t heavy_split_impl(brm_context_t* ctx, int out, const RowOut& o, cons
     for (int r = 0; r < nb; ++r) {
       const int64_t nl = info[2 * (t0 + r) + 1];
       ent[r + 1] = ent[r] + nl;
-      blk[r + 1] = blk[r] + (nl + kSplitListsHost - 1) / kSplitListsHost;
+      blk[r + 1] = blk[r] + (nl + bs - 1) / bs;
     }
     const int64_t ne = ent[nb], nblk = blk[nb];
     CK(ensure(ctx, ctx->split_rows, (size_t)nb * 4), "alloc split rows");
@@ -242,7 +252,7 @@ brm_status_t heavy_split_impl(brm_context_t* ctx, int out, const RowOut& o, cons
     CK(ensure(ctx, ctx->a1_rpt, (size_t)(nblk + 1) * 8), "alloc A1.rpt");
     CK(ensure(ctx, ctx->a1_col, (size_t)ne * 4), "alloc A1.col");
     CK(ensure(ctx, ctx->a1_val, (size_t)ne * 8), "alloc A1.val");
-    CK(launch_split_a1(ctx->A, drows, nb, dent, dblk, ne + nblk + 1, static_cast<int64_t*>(ctx->a1_rpt.p),
+    CK(launch_split_a1(ctx->A, drows, nb, dent, dblk, bs, ne + nblk + 1, static_cast<int64_t*>(ctx->a1_rpt.p),
                        static_cast<int32_t*>(ctx->a1_col.p), static_cast<double*>(ctx->a1_val.p), ctx->stream),
        "k_split_a1");
     ++ctx->launches;
@@ -311,55 +321,92 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
     ctx->heavy.assign(hi, hi + 2 * nh);
     ctx->heavy_loaded = true;
   }
-  // rows with more than kSplitListsHost lists are decomposed into aligned
-  // blocks of lists (heavy_split); the rest run on the global tier
   CK(ensure_host(ctx->h_rows, (size_t)nh * 4), "alloc pinned heavy rows");
   CK(cudaMemcpyAsync(ctx->h_rows.p, hrows, (size_t)nh * 4, cudaMemcpyDeviceToHost, ctx->stream), "copy heavy rows");
   CK(cudaStreamSynchronize(ctx->stream), "sync heavy rows");
   const int32_t* hr = static_cast<const int32_t*>(ctx->h_rows.p);
-  std::vector<int32_t> g_rows, s_rows;
-  std::vector<int64_t> g_info, s_info;
-  // split only rows of many SHORT lists: their 32-list blocks then fit the
-  // shared-memory tiers (a block of long lists would land back on this tier)
-  std::vector<int64_t> order;
+  std::vector<int32_t> g_rows, s_rows, l_rows;
+  std::vector<int64_t> g_info, s_info, l_info;
+  // Routes: rows of at most 512 lists merge in column
+  // slabs in shared memory (k_slab, three classes by nl); rows of more, SHORT
+  // lists are split into aligned 32-list blocks (heavy_split: the blocks then
+  // fit the shared-memory tiers); the rest run on the global tier, as does
+  // every heavy row under BRM_HEAVY_GLOBAL.
+  std::vector<int64_t> order, slab[kSlabClasses];
   for (int64_t t = 0; t < nh; ++t) {
     const int64_t P = ctx->heavy[2 * t], nl = ctx->heavy[2 * t + 1];
-    const bool split = nl > kSplitListsHost && P <= nl * (int64_t)kSplitAvgLen;
-    if (split) {
+    int cls = -1;
+    if (ctx->heavy_route != BRM_HEAVY_GLOBAL)
+      for (int c = kSlabClasses - 1; c >= 0; --c)
+        if (nl <= kSlabLists[c]) cls = c;
+    if (cls >= 0) {
+      slab[cls].push_back(t);
+    } else if (ctx->heavy_route != BRM_HEAVY_GLOBAL && P <= nl * (int64_t)kSplitAvgLen) {
       s_rows.push_back(hr[t]);
       s_info.push_back(P);
       s_info.push_back(nl);
+    } else if (ctx->heavy_route != BRM_HEAVY_GLOBAL && kSplitLong > 0) {
+      l_rows.push_back(hr[t]);
+      l_info.push_back(P);
+      l_info.push_back(nl);
     } else {
       order.push_back(t);
     }
   }
-  // global tier in descending n_prod: a launch lasts as long as its heaviest
-  // row, so the heaviest rows share the first launches
-  std::sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return ctx->heavy[2 * x] > ctx->heavy[2 * y]; });
+  // descending n_prod: a launch lasts as long as its heaviest rows, so they
+  // go first
+  auto by_nprod = [&](int64_t x, int64_t y) { return ctx->heavy[2 * x] > ctx->heavy[2 * y]; };
+  std::sort(order.begin(), order.end(), by_nprod);
+  for (auto& v : slab) std::sort(v.begin(), v.end(), by_nprod);
   for (const int64_t t : order) {
     g_rows.push_back(hr[t]);
     g_info.push_back(ctx->heavy[2 * t]);
     g_info.push_back(ctx->heavy[2 * t + 1]);
   }
   if (!s_rows.empty()) {
-    brm_status_t st = heavy_split(ctx, out, o, s_rows.data(), (int64_t)s_rows.size(), s_info.data());
+    brm_status_t st = heavy_split(ctx, out, o, s_rows.data(), (int64_t)s_rows.size(), s_info.data(), kSplitShort);
     if (st != BRM_OK) return st;
   }
+  if (!l_rows.empty()) {
+    brm_status_t st = heavy_split(ctx, out, o, l_rows.data(), (int64_t)l_rows.size(), l_info.data(), kSplitLong);
+    if (st != BRM_OK) return st;
+  }
+  // one device list: [slab classes 0, 1, 2 | global tier]
+  int64_t nslab = 0;
+  for (const auto& v : slab) nslab += (int64_t)v.size();
   const int64_t ng = (int64_t)g_rows.size();
+  const int64_t nall = nslab + ng;
+  if (nall > 0) {
+    CK(ensure(ctx, ctx->glob_rows, (size_t)nall * 4), "alloc heavy rows");
+    CK(ensure_host(ctx->h_split, (size_t)nall * 4), "alloc pinned heavy rows");
+    int32_t* hs = static_cast<int32_t*>(ctx->h_split.p);
+    int64_t k = 0;
+    for (const auto& v : slab)
+      for (const int64_t t : v) hs[k++] = hr[t];
+    if (ng) memcpy(hs + nslab, g_rows.data(), (size_t)ng * 4);
+    CK(cudaMemcpyAsync(ctx->glob_rows.p, hs, (size_t)nall * 4, cudaMemcpyHostToDevice, ctx->stream),
+       "copy heavy rows");
+  }
+  const int32_t* srows = static_cast<const int32_t*>(ctx->glob_rows.p);
+  int64_t s0 = 0;
+  for (int c = 0; c < kSlabClasses; ++c) {
+    const int64_t n = (int64_t)slab[c].size();
+    if (!n) continue;
+    CK(launch_slab(c, out, ctx->A, ctx->B, ctx->N, srows + s0, n, o, ctx->stream), "k_slab");
+    ++ctx->launches;
+    s0 += n;
+  }
   if (ng > 0) {
-    CK(ensure(ctx, ctx->glob_rows, (size_t)ng * 4), "alloc global-tier rows");
-    CK(ensure_host(ctx->h_split, (size_t)ng * 4), "alloc pinned global-tier rows");
-    memcpy(ctx->h_split.p, g_rows.data(), (size_t)ng * 4);
-    CK(cudaMemcpyAsync(ctx->glob_rows.p, ctx->h_split.p, (size_t)ng * 4, cudaMemcpyHostToDevice, ctx->stream),
-       "copy global-tier rows");
-    const int32_t* grows = static_cast<const int32_t*>(ctx->glob_rows.p);
+    const int32_t* grows = srows + nslab;
     const bool vals = out != OUT_SYMBOLIC;
     // batch the rows so their ping-pong slices fit the workspace budget
     int64_t max_row = 0;
     for (int64_t t = 0; t < ng; ++t) max_row = std::max(max_row, global_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals));
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    int64_t budget = std::min<int64_t>((int64_t)(free_b / 2) + (int64_t)ctx->gws.cap, 64ll << 30);
+    // a workspace already held is reused as is; a new one takes at most half
+    // the free memory
+    int64_t budget = std::min<int64_t>(std::max<int64_t>((int64_t)(free_b / 2), (int64_t)ctx->gws.cap), 64ll << 30);
     budget = std::max(budget, max_row);
     CK(ensure_host(ctx->h_gws_off, (size_t)ng * 16), "alloc pinned ws offsets");
     CK(ensure(ctx, ctx->gws_off, (size_t)ng * 16), "alloc ws offsets");
@@ -503,7 +550,7 @@ brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
   ev_record(ctx, 5);
   if (ctx->mode == BRM_UPPER) {
     // Step 6 of Fig. 4a: copy C_bar -> C
-    CK(launch_compact(ctx->M, static_cast<const int64_t*>(ctx->nprod_off.p), C->rpt,
+    CK(launch_compact(ctx->M, ctx->nnz_c, static_cast<const int64_t*>(ctx->nprod_off.p), C->rpt,
                       static_cast<const int32_t*>(ctx->cbar_col.p), static_cast<const double*>(ctx->cbar_val.p),
                       C->col, C->val, ctx->stream),
        "k_compact");
@@ -587,6 +634,12 @@ brm_status_t brm_set_stream(brm_context_t* ctx, void* stream) {
 brm_status_t brm_set_timing(brm_context_t* ctx, int enable) {
   if (!ctx) return BRM_ERR_INVALID;
   ctx->timing = enable != 0;
+  return BRM_OK;
+}
+
+brm_status_t brm_set_heavy_route(brm_context_t* ctx, int route) {
+  if (!ctx || (route != BRM_HEAVY_AUTO && route != BRM_HEAVY_GLOBAL)) return BRM_ERR_INVALID;
+  ctx->heavy_route = route;
   return BRM_OK;
 }
 

@@ -21,7 +21,7 @@ struct CsrView {
 //   1  one thread per row (Alg. 1)      P <= 8,    nl <= 8
 //   2  register BRMerge, one warp       P <= 32,   nl <= 32
 //   3  record BRMerge, one warp         P <= 256,  nl <= 64   (smem records)
-//   4  record BRMerge, 64 threads       P <= 768,  nl <= 64   (smem records)
+//   4  record BRMerge, one warp         P <= 768,  nl <= 64   (smem records)
 //   5  record BRMerge, 128 threads      P <= 3072, nl <= 256  (smem records)
 //   6  record BRMerge, 256 threads      P <= 6656, nl <= 512  (smem records)
 //   7  chunked BRMerge, 1024 threads, ping-pong buffers in a global workspace
@@ -36,12 +36,65 @@ struct TierBounds {
 };
 
 // (G threads per row group, CAP elements, LCAP lists, GPC groups per CTA)
+// (G and GPC may be overridden at build time for tuning experiments, e.g.
+// BRM_NVCC_FLAGS="-DBRM_T4_G=32 -DBRM_T4_GPC=2"; tools/variants.sh)
+#ifndef BRM_T2_GPC
+#define BRM_T2_GPC 8
+#endif
+#ifndef BRM_T3_G
+#define BRM_T3_G 32
+#endif
+#ifndef BRM_T3_GPC
+#define BRM_T3_GPC 8
+#endif
+#ifndef BRM_T4_G
+#define BRM_T4_G 32
+#endif
+#ifndef BRM_T4_GPC
+#define BRM_T4_GPC 2
+#endif
+#ifndef BRM_T5_G
+#define BRM_T5_G 128
+#endif
+#ifndef BRM_T6_G
+#define BRM_T6_G 256
+#endif
 #define BRM_TIER1 8, 8, 8, 32
-#define BRM_TIER2 32, 32, 32, 8
-#define BRM_TIER3 32, 256, 64, 4
-#define BRM_TIER4 64, 768, 64, 1
-#define BRM_TIER5 128, 3072, 256, 1
-#define BRM_TIER6 256, 6656, 512, 1
+#define BRM_TIER2 32, 32, 32, BRM_T2_GPC
+#define BRM_TIER3 BRM_T3_G, 256, 64, BRM_T3_GPC
+#define BRM_TIER4 BRM_T4_G, 768, 64, BRM_T4_GPC
+#define BRM_TIER5 BRM_T5_G, 3072, 256, 1
+#define BRM_TIER6 BRM_T6_G, 6656, 512, 1
+// PRECISE symbolic (hash counting) launch shapes of tiers 3-6, tuned apart
+// from the merges: (G, CAP, LCAP, GPC)
+#ifndef BRM_H3_GPC
+#define BRM_H3_GPC 4
+#endif
+#ifndef BRM_H4_G
+#define BRM_H4_G 64
+#endif
+#ifndef BRM_H4_GPC
+#define BRM_H4_GPC 1
+#endif
+#define BRM_HASH3 32, 256, 64, BRM_H3_GPC
+#define BRM_HASH4 BRM_H4_G, 768, 64, BRM_H4_GPC
+#define BRM_HASH5 128, 3072, 256, 1
+#define BRM_HASH6 256, 6656, 512, 1
+// heavy rows of at most 512 lists, merged in column slabs (G, CAP, LCAP):
+// class c takes the rows of kSlabLists[c-1] < nl <= kSlabLists[c]
+#ifndef BRM_SLAB0
+#define BRM_SLAB0 128, 2048, 64
+#endif
+#ifndef BRM_S1_G
+#define BRM_S1_G 256
+#endif
+#ifndef BRM_S1_CAP
+#define BRM_S1_CAP 4096
+#endif
+#define BRM_SLAB1 BRM_S1_G, BRM_S1_CAP, 256
+#define BRM_SLAB2 256, 6656, 512
+constexpr int kSlabClasses = 3;
+constexpr int kSlabLists[kSlabClasses] = {64, 256, 512};
 constexpr int kGlobalG = 1024;
 
 __host__ __device__ inline TierBounds tier_bounds() {
@@ -138,6 +191,30 @@ __device__ __forceinline__ int group_excl_scan(const Group<G>& g, int v, int& to
     total = tmp[NW];
     __syncthreads();
     return res;
+  }
+}
+
+// Minimum / sum of one int per thread over the group; `tmp` as for
+// group_excl_scan. Ends with the group synchronised.
+template <int G, bool MIN>
+__device__ __forceinline__ int group_reduce(const Group<G>& g, int v, int* tmp) {
+  auto op = [](int a, int b) { return MIN ? min(a, b) : a + b; };
+  if constexpr (G <= 32) {
+#pragma unroll
+    for (int d = G / 2; d >= 1; d >>= 1) v = op(v, __shfl_xor_sync(g.mask, v, d, G));
+    return v;
+  } else {
+    constexpr int NW = G / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, d));
+    if (lane == 0) tmp[wid] = v;
+    __syncthreads();
+    int m = tmp[0];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) m = op(m, tmp[w]);
+    __syncthreads();
+    return m;
   }
 }
 

@@ -486,6 +486,9 @@ struct RecWide {
   __device__ static int col(const T& r) { return r.x; }
   __device__ static int slot(const T& r) { return r.y; }
   __device__ static int col_at(const T* r, int i) { return reinterpret_cast<const int*>(r)[2 * i]; }  // 4-byte load
+  __device__ static bool le(const T& a, const T& b) { return a.x <= b.x; }  // col(a) <= col(b)
+  __device__ static bool le_at(const T* a, int i, const T* b, int j) { return col_at(a, i) <= col_at(b, j); }
+  __device__ static bool is_sent(const T& r) { return r.x == INT_MAX; }
 };
 template <int SB>
 struct RecPacked {
@@ -498,6 +501,10 @@ struct RecPacked {
   __device__ static int col(T r) { return static_cast<int>(r >> SB); }
   __device__ static int slot(T r) { return static_cast<int>(r & ((1u << SB) - 1u)); }
   __device__ static int col_at(const T* r, int i) { return col(r[i]); }
+  // col(a) <= col(b) without unpacking: a <= b with b's slot bits set
+  __device__ static bool le(T a, T b) { return a <= (b | ((1u << SB) - 1u)); }
+  __device__ static bool le_at(const T* a, int i, const T* b, int j) { return le(a[i], b[j]); }
+  __device__ static bool is_sent(T r) { return r == 0xffffffffu; }
 };
 struct RecCol {
   using T = int;
@@ -509,6 +516,9 @@ struct RecCol {
   __device__ static int col(T r) { return r; }
   __device__ static int slot(T) { return 0; }
   __device__ static int col_at(const T* r, int i) { return r[i]; }
+  __device__ static bool le(T a, T b) { return a <= b; }
+  __device__ static bool le_at(const T* a, int i, const T* b, int j) { return a[i] <= b[j]; }
+  __device__ static bool is_sent(T r) { return r == INT_MAX; }
 };
 
 // slot bits of a packed record for a tier of CAP products (slots 0..CAP-1)
@@ -549,7 +559,7 @@ __device__ __forceinline__ int merge_path_rec(const typename R::T* a, int la, co
   int hi = diag < la ? diag : la;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (R::col_at(a, mid) <= R::col_at(b, diag - 1 - mid))
+    if (R::le_at(a, mid, b, diag - 1 - mid))
       lo = mid + 1;
     else
       hi = mid;
@@ -623,13 +633,13 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, typename R::T* rec, 
   for (int v = 0; v < NV; ++v) {
     if (v >= VT) break;  // group-uniform
     const bool act = ia + ib < lim;
-    const int ca = R::col(ra), cb = R::col(rb);
-    const bool ta = act && ca <= cb;
-    const bool tb = act && cb <= ca;
-    orec[v] = ta ? ra : rb;
+    const bool ta = act && R::le(ra, rb);
+    const bool tb = act && R::le(rb, ra);
+    const T out = ta ? ra : rb;
+    orec[v] = out;
     if (VALS) {
       // equal columns: val[left] = val[left] + val[right]
-      const bool dup = ta && tb && ca != R::kSentCol;
+      const bool dup = ta && tb && !R::is_sent(ra);
       double x = 0.0, y = 0.0;
       lds_if(dup, valb + 8u * R::slot(ra), x);
       lds_if(dup, valb + 8u * R::slot(rb), y);
@@ -640,7 +650,7 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, typename R::T* rec, 
     ib += tb;
     lds_if(ta, recb + RB * ia, ra);
     lds_if(tb, recb + RB * ib, rb);
-    if (act && min(ca, cb) == R::kSentCol && ia + ib < lim) {  // pair p done, chunk not: enter pair p+1
+    if (act && R::is_sent(out) && ia + ib < lim) {  // pair p done, chunk not: enter pair p+1
       if (pl < 0) pf = p + 1;
       ++p;
       pl = p;
@@ -667,6 +677,48 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, typename R::T* rec, 
   }
   g.sync();
   return total;
+}
+
+// Multiplying phase (products of the lists, coalesced through a 16-bit
+// product -> list owner table) and accumulating phase of one row's (or row
+// slab's) nl lists. On entry: off[0..nl] = record offsets (list l at off[l],
+// its P_l products then its sentinel), the sentinels written, rb.bst[l] = the
+// B index of list l's first product, rb.av[l] = its A value. Returns the
+// number T of merged records, left in rec[0..T).
+template <int G, int NV, class R>
+__device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView& B, int nl, int P, int* off,
+                                               int* noff, const RecBufs& rb) {
+  constexpr bool VALS = R::kVals;
+  typename R::T* rec = static_cast<typename R::T*>(rb.rec);
+  const int rank = g.rank;
+  {
+    // owner[e] = list of product e (16-bit table: nl <= 512 in these tiers),
+    // filled by one thread per list; then the products are fetched coalesced
+    unsigned short* owner = reinterpret_cast<unsigned short*>(rb.owner);
+    for (int l = rank; l < nl; l += G)
+      for (int e = off[l] - l, e1 = off[l + 1] - (l + 1); e < e1; ++e) owner[e] = static_cast<unsigned short>(l);
+    g.sync();
+#pragma unroll 2
+    for (int e = rank; e < P; e += G) {
+      const int l = owner[e];
+      const int64_t src = rb.bst[l] + (e - (off[l] - l));
+      const int c = __ldg(B.col + src);
+      rec[e + l] = R::make(c, e);
+      if (VALS) rb.val[e] = __dmul_rn(rb.av[l], __ldg(B.val + src));  // line 12: the product, rounded once
+    }
+  }
+  g.sync();
+  // accumulating phase (lines 21-35)
+  int cur = nl;
+  int end = P + nl;
+  while (cur > 1) {
+    end = rec_round<G, NV, R>(g, rec, rb.val, off, noff, cur, rb.scan_tmp);
+    cur = (cur + 1) >> 1;
+    int* t = off;  // lines 33-34
+    off = noff;
+    noff = t;
+  }
+  return end - 1;  // list 0 = records [0, end - 1), then its sentinel
 }
 
 template <int G, int NV, class R, int OUT>
@@ -705,34 +757,7 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
     rec[P + nl] = R::sent();  // lone partner sentinel if nl is odd
   }
   g.sync();
-  {
-    // owner[e] = list of product e (16-bit table: nl <= 512 in these tiers),
-    // filled by one thread per list; then the products are fetched coalesced
-    unsigned short* owner = reinterpret_cast<unsigned short*>(rb.owner);
-    for (int l = rank; l < nl; l += G)
-      for (int e = off[l] - l, e1 = off[l + 1] - (l + 1); e < e1; ++e) owner[e] = static_cast<unsigned short>(l);
-    g.sync();
-#pragma unroll 2
-    for (int e = rank; e < P; e += G) {
-      const int l = owner[e];
-      const int64_t src = rb.bst[l] + (e - (off[l] - l));
-      const int c = __ldg(B.col + src);
-      rec[e + l] = R::make(c, e);
-      if (VALS) rb.val[e] = __dmul_rn(rb.av[l], __ldg(B.val + src));  // line 12: the product, rounded once
-    }
-  }
-  g.sync();
-  // accumulating phase (lines 21-35)
-  int cur = nl;
-  int end = P + nl;
-  while (cur > 1) {
-    end = rec_round<G, NV, R>(g, rec, rb.val, off, noff, cur, rb.scan_tmp);
-    cur = (cur + 1) >> 1;
-    int* t = off;  // lines 33-34
-    off = noff;
-    noff = t;
-  }
-  const int T = end - 1;  // the result row: list 0 = records [0, end - 1), then its sentinel
+  const int T = rec_merge_lists<G, NV, R>(g, B, nl, P, off, noff, rb);
   if (OUT != OUT_SYMBOLIC) {  // line 36
     const int64_t ob = o.base[row];
     for (int e = rank; e < T; e += G) {
@@ -742,6 +767,120 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
     }
   }
   if (OUT != OUT_C && rank == 0) o.row_size[row] = T;
+  g.sync();
+}
+
+// Column slabs of a heavy row (nl <= LCAP lists, any n_prod). Restricting
+// every list to a column range [c0, c1) keeps the number of lists and the
+// pairing of every round (empty lists keep their place in the tree), so each
+// column receives exactly Algorithm 1's additions in Algorithm 1's order; the
+// row is merged slab by slab in shared memory (rec_merge_lists) and the slab
+// results, already in column order, are concatenated. Slab end: every list
+// with r_l products left gets a quota q_l = max(1, (CAP - nl) r_l / sum r)
+// (so sum q_l <= CAP), and c1 = the smallest column found q_l places past a
+// list's cursor: no list contributes more than q_l products (the slab fits
+// CAP) and the list attaining the minimum contributes exactly q_l >= 1 (every
+// slab progresses). Quotas in proportion to what is left fill the slab when
+// the lists spread over the columns alike. A slab in which every list has at
+// most q_l products left is the last one.
+template <int G, int NV, int CAP, int LCAP, class R, int OUT>
+__device__ __forceinline__ void slab_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
+                                         const RowOut& o, const RecBufs& rb) {
+  constexpr bool VALS = R::kVals;
+  constexpr int LPT = (LCAP + G - 1) / G;  // lists per thread: l = rank + j * G
+  typename R::T* rec = static_cast<typename R::T*>(rb.rec);
+  const int rank = g.rank;
+  const int64_t a0 = A.rpt[row];
+  const int nl = static_cast<int>(A.rpt[row + 1] - a0);
+  int64_t bend[LPT];  // end of each of this thread's lists in B; rb.bst[l] is its cursor
+#pragma unroll
+  for (int j = 0; j < LPT; ++j) {
+    const int l = rank + j * G;
+    bend[j] = 0;
+    if (l < nl) {
+      const int k = __ldg(A.col + a0 + l);
+      rb.bst[l] = __ldg(B.rpt + k);
+      bend[j] = __ldg(B.rpt + k + 1);
+      if (VALS) rb.av[l] = __ldg(A.val + a0 + l);
+    }
+  }
+  const int64_t ob = OUT != OUT_SYMBOLIC ? o.base[row] : 0;
+  int64_t written = 0;
+  while (true) {
+    int rem[LPT], qloc[LPT];
+    int rsum = 0;
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) {
+      const int l = rank + j * G;
+      rem[j] = l < nl ? static_cast<int>(bend[j] - rb.bst[l]) : 0;  // r_l (a row has n_prod < 2^31)
+      rsum += rem[j];
+    }
+    rsum = group_reduce<G, false>(g, rsum, rb.scan_tmp);
+    int cmin = INT_MAX;
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) {
+      const int l = rank + j * G;
+      qloc[j] = max(1, static_cast<int>(static_cast<int64_t>(CAP - nl) * rem[j] / rsum));
+      if (l < nl && qloc[j] < rem[j]) cmin = min(cmin, __ldg(B.col + rb.bst[l] + qloc[j]));
+    }
+    const int c1 = group_reduce<G, true>(g, cmin, rb.scan_tmp);  // INT_MAX: the last slab
+    int* off = rb.off0;
+    int* noff = rb.off1;
+    int nloc[LPT];
+    int P = 0;
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) {
+      const int l = rank + j * G;
+      int n = 0;
+      if (l < nl) {
+        const int64_t st = rb.bst[l];
+        const int avail = min(qloc[j], rem[j]);
+        if (c1 == INT_MAX) {
+          n = avail;
+        } else {  // products of list l with column < c1 (lower bound within its next q)
+          int lo = 0, hi = avail;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(B.col + st + mid) < c1)
+              lo = mid + 1;
+            else
+              hi = mid;
+          }
+          n = lo;
+        }
+      }
+      nloc[j] = n;
+      int tot;
+      const int ex = group_excl_scan<G>(g, n, tot, rb.scan_tmp);
+      if (l < nl) {
+        off[l] = P + ex + l;
+        rec[P + ex + l + n] = R::sent();  // sentinel of list l
+      }
+      P += tot;
+    }
+    if (rank == 0) {
+      off[nl] = P + nl;
+      rec[P + nl] = R::sent();  // lone partner sentinel if nl is odd
+    }
+    g.sync();
+    const int T = rec_merge_lists<G, NV, R>(g, B, nl, P, off, noff, rb);
+    if (OUT != OUT_SYMBOLIC) {  // line 36, this slab's part of the row
+      for (int e = rank; e < T; e += G) {
+        const typename R::T r = rec[e];
+        o.col[ob + written + e] = R::col(r);
+        if (VALS) o.val[ob + written + e] = rb.val[R::slot(r)];
+      }
+    }
+    written += T;
+    g.sync();
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) {
+      const int l = rank + j * G;
+      if (l < nl) rb.bst[l] += nloc[j];
+    }
+    if (c1 == INT_MAX) break;
+  }
+  if (OUT != OUT_C && rank == 0) o.row_size[row] = written;
   g.sync();
 }
 

@@ -398,6 +398,26 @@ __global__ void k_heavy_info(CsrView A, const int64_t* __restrict__ nprod_off,
 template <bool VALS, bool PACK, int CAP>
 using RecT = std::conditional_t<VALS, std::conditional_t<PACK, RecPacked<rec_slot_bits(CAP)>, RecWide>, RecCol>;
 
+// carve one record group's buffers (rec_group_bytes) out of shared memory
+template <int G, int CAP, int LCAP, class R>
+__device__ __forceinline__ RecBufs rec_bufs(unsigned char* p) {
+  auto take = [&](int n) {
+    unsigned char* q = p;
+    p += align16(n);
+    return q;
+  };
+  RecBufs rb;
+  rb.rec = take((CAP + LCAP + 2) * R::kBytes);
+  rb.val = R::kVals ? reinterpret_cast<double*>(take(CAP * 8)) : nullptr;
+  rb.owner = reinterpret_cast<int*>(take(CAP * 2));
+  rb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
+  rb.off1 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
+  rb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
+  rb.av = R::kVals ? reinterpret_cast<double*>(take(LCAP * 8)) : nullptr;
+  rb.scan_tmp = G > 32 ? reinterpret_cast<int*>(take((G / 32 + 2) * 4)) : nullptr;
+  return rb;
+}
+
 template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT, bool PACK>
 __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const int32_t* __restrict__ rows,
                                                  int64_t nrows, RowOut o) {
@@ -416,25 +436,24 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
       reg_row<G, VALS, OUT>(g, A, B, rows[r], o, rb);
   } else {
     using R = RecT<VALS, PACK, CAP>;
-    constexpr int bytes = rec_group_bytes<G, CAP, LCAP, R>();
-    unsigned char* p = smem + gid * bytes;
-    auto take = [&](int n) {
-      unsigned char* q = p;
-      p += align16(n);
-      return q;
-    };
-    RecBufs rb;
-    rb.rec = take((CAP + LCAP + 2) * R::kBytes);
-    rb.val = VALS ? reinterpret_cast<double*>(take(CAP * 8)) : nullptr;
-    rb.owner = reinterpret_cast<int*>(take(CAP * 2));
-    rb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
-    rb.off1 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
-    rb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
-    rb.av = VALS ? reinterpret_cast<double*>(take(LCAP * 8)) : nullptr;
-    rb.scan_tmp = G > 32 ? reinterpret_cast<int*>(take((G / 32 + 2) * 4)) : nullptr;
+    const RecBufs rb = rec_bufs<G, CAP, LCAP, R>(smem + gid * rec_group_bytes<G, CAP, LCAP, R>());
     for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
       rec_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, R, OUT>(g, A, B, rows[r], o, rb);
   }
+}
+
+// Heavy rows of at most LCAP lists: one CTA of G threads per row, merged in
+// column slabs of <= CAP products (slab_row); rows sorted by n_prod
+// descending, taken grid-stride.
+template <int G, int CAP, int LCAP, bool VALS, int OUT, bool PACK>
+__global__ void __launch_bounds__(G) k_slab(CsrView A, CsrView B, const int32_t* __restrict__ rows, int64_t nrows,
+                                            RowOut o) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using R = RecT<VALS, PACK, CAP>;
+  const Group<G> g = make_group<G>();
+  const RecBufs rb = rec_bufs<G, CAP, LCAP, R>(smem);
+  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x)
+    slab_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, CAP, LCAP, R, OUT>(g, A, B, rows[r], o, rb);
 }
 
 // PRECISE symbolic phase of tiers 3-6: hash_row per group (GPC groups of G).
@@ -506,9 +525,10 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
 }
 
 // ---------------------------------------------------------------------------
-// Heavy-row decomposition (tier 7 rows with nl > kSplitLists). Algorithm 1's
-// tree over a row's nl lists splits into aligned sub-trees over blocks of
-// kSplitLists = 2^5 consecutive lists (pairs are (2m, 2m+1) at every level,
+// Heavy-row decomposition (tier 7 rows of more lists than the column slabs
+// take). Algorithm 1's tree over a row's nl lists splits into aligned
+// sub-trees over blocks of bs = 2^k consecutive lists (32 for rows of short
+// lists, 512 for long ones; pairs are (2m, 2m+1) at every level,
 // so an aligned block is merged exactly as Algorithm 1 would merge it on its
 // own, a short last block included). Level 1: every block becomes a row of
 // A1 (a copy of the block's A entries) and C1 = A1 * B runs through the
@@ -516,8 +536,6 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
 // value 1.0 (1.0 * v == v exactly), so C2 = A2 * C1 merges the block results
 // in the same tree order; C2 may itself be heavy and split again.
 // ---------------------------------------------------------------------------
-constexpr int kSplitLists = 32;
-
 __device__ __forceinline__ int upper_row(const int64_t* off, int n, int64_t e) {  // last r with off[r] <= e
   int lo = 0, hi = n - 1;
   while (lo < hi) {
@@ -533,7 +551,7 @@ __device__ __forceinline__ int upper_row(const int64_t* off, int n, int64_t e) {
 // A1: rows = blocks; ent_off / blk_off = exclusive prefix sums over the
 // batch rows of nl_i and ceil(nl_i / kSplitLists).
 __global__ void k_split_a1(CsrView A, const int32_t* __restrict__ rows, int n, const int64_t* __restrict__ ent_off,
-                           const int64_t* __restrict__ blk_off, int64_t* __restrict__ a1_rpt,
+                           const int64_t* __restrict__ blk_off, int bs, int64_t* __restrict__ a1_rpt,
                            int32_t* __restrict__ a1_col, double* __restrict__ a1_val) {
   const int64_t ne = ent_off[n], nb = blk_off[n];
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ne + nb + 1;
@@ -546,7 +564,7 @@ __global__ void k_split_a1(CsrView A, const int32_t* __restrict__ rows, int n, c
     } else if (t < ne + nb) {
       const int64_t b = t - ne;
       const int r = upper_row(blk_off, n, b);
-      a1_rpt[b] = ent_off[r] + (int64_t)kSplitLists * (b - blk_off[r]);
+      a1_rpt[b] = ent_off[r] + (int64_t)bs * (b - blk_off[r]);
     } else {
       a1_rpt[nb] = ne;
     }
@@ -589,10 +607,11 @@ __global__ void k_scatter_rows(const int32_t* __restrict__ rows, int n, const in
 }
 
 cudaError_t launch_split_a1(const CsrView& A, const int32_t* rows, int n, const int64_t* ent_off,
-                            const int64_t* blk_off, int64_t total, int64_t* a1_rpt, int32_t* a1_col, double* a1_val,
-                            cudaStream_t st) {
+                            const int64_t* blk_off, int bs, int64_t total, int64_t* a1_rpt, int32_t* a1_col,
+                            double* a1_val, cudaStream_t st) {
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
-  k_split_a1<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(A, rows, n, ent_off, blk_off, a1_rpt, a1_col, a1_val);
+  k_split_a1<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(A, rows, n, ent_off, blk_off, bs, a1_rpt, a1_col,
+                                                                      a1_val);
   return cudaGetLastError();
 }
 
@@ -611,10 +630,16 @@ cudaError_t launch_scatter_rows(const int32_t* rows, int n, const int64_t* rpt2,
   return cudaGetLastError();
 }
 
-// Step 6 of Fig. 4a: copy each row of C_bar (at its n_prod offset) to C. A
-// warp copies the rows [r0, r0 + 32) as ONE flattened range of C (coalesced
-// writes): element e's row is found by a shuffle search over the 32 row
-// starts, its source is nprod_off[row] + (e - crpt[row]).
+// Step 6 of Fig. 4a: copy each row of C_bar (at its n_prod offset) to C.
+// Work is cut by ELEMENTS of C, not rows, so a few very long rows (heavy
+// rows, or a heavy-row decomposition's sub-products) spread over all warps:
+// a warp takes chunks of kCompactChunk consecutive elements of C, finds the
+// row of the chunk's first element by a binary search over C.rpt, then
+// walks the chunk through windows of 32 consecutive rows; element e's row is
+// found by a shuffle search over the window's row starts, its source is
+// nprod_off[row] + (e - crpt[row]). Stores are coalesced.
+constexpr int64_t kCompactChunk = 4096;
+
 __global__ void __launch_bounds__(256) k_compact(int64_t M, const int64_t* __restrict__ nprod_off,
                                                  const int64_t* __restrict__ crpt,
                                                  const int32_t* __restrict__ cbar_col,
@@ -623,41 +648,56 @@ __global__ void __launch_bounds__(256) k_compact(int64_t M, const int64_t* __res
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r0 = warp * 32; r0 < M; r0 += nwarps * 32) {
-    const int64_t r = min(r0 + lane, M);
-    const int64_t cs = crpt[r];
-    const int64_t delta = (r < M ? nprod_off[r] : 0) - cs;  // source - destination
-    const int64_t cbeg = __shfl_sync(0xffffffffu, cs, 0);
-    const int64_t cend = crpt[min(r0 + 32, M)];
-    constexpr int U = 4;  // four 32-element batches in flight
-    for (int64_t eb = cbeg; eb < cend; eb += 32 * U) {
-      int32_t cv[U];
-      double vv[U];
-      int64_t dst[U];
+  const int64_t nnz = crpt[M];
+  for (int64_t e0 = warp * kCompactChunk; e0 < nnz; e0 += nwarps * kCompactChunk) {
+    const int64_t e1 = min(e0 + kCompactChunk, nnz);
+    int64_t lo = 0, hi = M - 1;  // last row r with crpt[r] <= e0 (same on every lane)
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (crpt[mid] <= e0)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    int64_t r0 = lo;
+    int64_t eb0 = e0;
+    while (eb0 < e1) {
+      const int64_t r = min(r0 + lane, M);
+      const int64_t cs = crpt[r];
+      const int64_t delta = (r < M ? nprod_off[r] : 0) - cs;  // source - destination
+      const int64_t wend = min(e1, crpt[min(r0 + 32, M)]);
+      constexpr int U = 4;  // four 32-element batches in flight
+      for (int64_t eb = eb0; eb < wend; eb += 32 * U) {
+        int32_t cv[U];
+        double vv[U];
+        int64_t dst[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t e = eb + 32 * u + lane;
-        int lo = 0;  // row of element e: last lane whose C start <= e
+        for (int u = 0; u < U; ++u) {
+          const int64_t e = eb + 32 * u + lane;
+          int l = 0;  // row of element e: last lane whose C start <= e
 #pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const int64_t v = __shfl_sync(0xffffffffu, cs, lo + step);
-          if (v <= e) lo += step;
+          for (int step = 16; step > 0; step >>= 1) {
+            const int64_t v = __shfl_sync(0xffffffffu, cs, l + step);
+            if (v <= e) l += step;
+          }
+          const int64_t d = __shfl_sync(0xffffffffu, delta, l);
+          dst[u] = e < wend ? e : -1;
+          cv[u] = 0;
+          vv[u] = 0.0;
+          if (e < wend) {
+            cv[u] = cbar_col[e + d];
+            vv[u] = cbar_val[e + d];
+          }
         }
-        const int64_t d = __shfl_sync(0xffffffffu, delta, lo);
-        dst[u] = e < cend ? e : -1;
-        cv[u] = 0;
-        vv[u] = 0.0;
-        if (e < cend) {
-          cv[u] = cbar_col[e + d];
-          vv[u] = cbar_val[e + d];
-        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (dst[u] >= 0) {
+            ccol[dst[u]] = cv[u];
+            cval[dst[u]] = vv[u];
+          }
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (dst[u] >= 0) {
-          ccol[dst[u]] = cv[u];
-          cval[dst[u]] = vv[u];
-        }
+      eb0 = wend;
+      r0 += 32;
     }
   }
 }
@@ -750,6 +790,7 @@ static cudaError_t launch_tier_pk(const CsrView& A, const CsrView& B, const int3
   // (wrong values, no spills reported), so tiers keep NV <= 29
   static_assert(CAP <= 32 || (((CAP + LCAP + 1 + G - 1) / G) | 1) <= 29, "chunk tier NV must stay <= 29");
   static_assert(smem <= 232448, "tier shared memory exceeds 227 KB");
+  static_assert(G <= 32 || GPC == 1, "a group of more than 32 threads is the whole CTA");
   auto kern = k_tier<G, CAP, LCAP, GPC, VALS, OUT, PACK>;
   // one process drives one device, so per-instantiation caching is safe
   static int per_sm = 0;
@@ -778,6 +819,58 @@ static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, int64_t b_c
   return launch_tier_pk<G, CAP, LCAP, GPC, VALS, OUT, false>(A, B, rows, n, o, st);
 }
 
+template <int G, int CAP, int LCAP, bool VALS, int OUT, bool PACK>
+static cudaError_t launch_slab_pk(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
+                                  cudaStream_t st) {
+  constexpr int smem = rec_group_bytes<G, CAP, LCAP, RecT<VALS, PACK, CAP>>();
+  static_assert(smem <= 232448, "slab shared memory exceeds 227 KB");
+  static_assert((((CAP + LCAP + 1 + G - 1) / G) | 1) <= 29, "slab NV must stay <= 29");
+  auto kern = k_slab<G, CAP, LCAP, VALS, OUT, PACK>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t cap = (int64_t)per_sm * num_sms();
+  kern<<<(unsigned)(n < cap ? n : cap), G, smem, st>>>(A, B, rows, n, o);
+  return cudaGetLastError();
+}
+
+template <int G, int CAP, int LCAP, bool VALS, int OUT>
+static cudaError_t launch_slab_t(const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows, int64_t n,
+                                 const RowOut& o, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if constexpr (VALS) {
+    if (rec_pack_ok(CAP, b_cols)) return launch_slab_pk<G, CAP, LCAP, VALS, OUT, true>(A, B, rows, n, o, st);
+  }
+  return launch_slab_pk<G, CAP, LCAP, VALS, OUT, false>(A, B, rows, n, o, st);
+}
+
+template <int OUT>
+static cudaError_t launch_slab_k(int cls, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
+                                 int64_t n, const RowOut& o, cudaStream_t st) {
+  constexpr bool VALS = OUT != OUT_SYMBOLIC;
+  switch (cls) {
+    case 0: return launch_slab_t<BRM_SLAB0, VALS, OUT>(A, B, b_cols, rows, n, o, st);
+    case 1: return launch_slab_t<BRM_SLAB1, VALS, OUT>(A, B, b_cols, rows, n, o, st);
+    case 2: return launch_slab_t<BRM_SLAB2, VALS, OUT>(A, B, b_cols, rows, n, o, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_slab(int cls, int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
+                        int64_t n, const RowOut& o, cudaStream_t st) {
+  switch (out_kind) {
+    case OUT_SYMBOLIC: return launch_slab_k<OUT_SYMBOLIC>(cls, A, B, b_cols, rows, n, o, st);
+    case OUT_CBAR: return launch_slab_k<OUT_CBAR>(cls, A, B, b_cols, rows, n, o, st);
+    case OUT_C: return launch_slab_k<OUT_C>(cls, A, B, b_cols, rows, n, o, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <bool VALS, int OUT>
 static cudaError_t launch_tiny(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
                               cudaStream_t st) {
@@ -804,6 +897,7 @@ static cudaError_t launch_hash_t(const CsrView& A, const CsrView& B, const int32
   if (n <= 0) return cudaSuccess;
   constexpr int smem = hash_group_bytes<G, CAP, LCAP>() * GPC;
   static_assert(smem <= 232448, "hash tier shared memory exceeds 227 KB");
+  static_assert(G <= 32 || GPC == 1, "a group of more than 32 threads is the whole CTA");
   auto kern = k_hash_symbolic<G, CAP, LCAP, GPC>;
   static int per_sm = 0;
   if (!per_sm) {
@@ -824,10 +918,10 @@ static cudaError_t launch_tier_dispatch(int bin, const CsrView& A, const CsrView
                                         int64_t n, const RowOut& o, cudaStream_t st) {
   if constexpr (OUT == OUT_SYMBOLIC) {  // PRECISE step 3: hash counting on tiers 3-6
     switch (bin) {
-      case 3: return launch_hash_t<BRM_TIER3>(A, B, rows, n, o, st);
-      case 4: return launch_hash_t<BRM_TIER4>(A, B, rows, n, o, st);
-      case 5: return launch_hash_t<BRM_TIER5>(A, B, rows, n, o, st);
-      case 6: return launch_hash_t<BRM_TIER6>(A, B, rows, n, o, st);
+      case 3: return launch_hash_t<BRM_HASH3>(A, B, rows, n, o, st);
+      case 4: return launch_hash_t<BRM_HASH4>(A, B, rows, n, o, st);
+      case 5: return launch_hash_t<BRM_HASH5>(A, B, rows, n, o, st);
+      case 6: return launch_hash_t<BRM_HASH6>(A, B, rows, n, o, st);
       default: break;
     }
   }
@@ -871,10 +965,10 @@ cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B,
   return cudaGetLastError();
 }
 
-cudaError_t launch_compact(int64_t M, const int64_t* nprod_off, const int64_t* crpt, const int32_t* cbar_col,
+cudaError_t launch_compact(int64_t M, int64_t nnz, const int64_t* nprod_off, const int64_t* crpt, const int32_t* cbar_col,
                            const double* cbar_val, int32_t* ccol, double* cval, cudaStream_t st) {
-  if (M <= 0) return cudaSuccess;
-  int64_t blocks = (M + 255) / 256;  // one warp per 32 rows
+  if (M <= 0 || nnz <= 0) return cudaSuccess;
+  int64_t blocks = (nnz + 8 * kCompactChunk - 1) / (8 * kCompactChunk);  // one chunk per warp
   const int64_t cap = (int64_t)num_sms() * 16;
   if (blocks > cap) blocks = cap;
   k_compact<<<(unsigned)blocks, 256, 0, st>>>(M, nprod_off, crpt, cbar_col, cbar_val, ccol, cval);

@@ -50,6 +50,7 @@ def test_only_declared_symbols_exported(lib):
 
 
 def test_status_strings(lib):
+    assert lib.brm_set_heavy_route(None, 0) == 1  # BRM_ERR_INVALID
     assert lib.brm_status_string(0) == b"BRM_OK"
     assert lib.brm_status_string(5) == b"BRM_ERR_OVERFLOW"
 

@@ -18,7 +18,7 @@ def test_tier_table_matches_kernels():
             re.findall(r"t\.cap\[(\d)\] = (\d+);\s+t\.lcap\[\d\] = (\d+);", src)}
     for t in range(1, bench.NUM_BINS - 1):
         assert caps[t] == (bench.TIER_CAP[t], bench.TIER_LCAP[t]), t
-        m = re.search(rf"#define BRM_TIER{t} (\d+), (\d+), (\d+), (\d+)", src)
+        m = re.search(rf"#define BRM_TIER{t} (\w+), (\d+), (\d+), (\w+)", src)
         assert int(m.group(2)) == bench.TIER_CAP[t] and int(m.group(3)) == bench.TIER_LCAP[t]
     assert f"#define BRM_NUM_BINS {bench.NUM_BINS}" in (ROOT / "include" / "brmerge.h").read_text()
 

@@ -156,9 +156,85 @@ def test_many_empty_lists(ctx, oracle_mod, mode):
 
 
 @pytest.mark.parametrize("mode", MODES)
-def test_heavy_rows_global_tier(ctx, oracle_mod, mode):
-    """Rows far beyond the shared-memory tiers (n_prod up to ~200k)."""
+def test_heavy_rows(ctx, oracle_mod, mode):
+    """Rows far beyond the shared-memory tiers (n_prod up to ~200k): column
+    slabs (20 and 200 lists) and the global tier (1000 and 2000 long lists)."""
     A, B = _lists_matrix([200, 1000, 2000, 20], 100, 20000, seed=11)
+    compare(run(ctx, A, B, mode), A, B)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_heavy_rows_global_route(oracle_mod, mode):
+    """brm_set_heavy_route(BRM_HEAVY_GLOBAL): every heavy row on the
+    global-memory tier gives the same bits."""
+    from paper_2206_06611_b200 import Context
+    c = Context()
+    try:
+        c.brm_set_heavy_route(c.HEAVY_GLOBAL)
+        A, B = _lists_matrix([200, 1000, 2000, 20], 100, 20000, seed=11)
+        compare(run(c, A, B, mode), A, B)
+        A, B = _skewed_matrix([1, 2, 7, 64, 65, 300, 512, 513], 40000, seed=5)
+        compare(run(c, A, B, mode), A, B)
+    finally:
+        c.close()
+
+
+def _skewed_matrix(specs, ncols, seed, max_len=3000, identical=False):
+    """A row per nl in specs over a B of rows with lengths spread over
+    [0, max_len] (a tenth of them empty); identical=True gives every B row
+    the same columns (every column repeats in every list)."""
+    rng = np.random.default_rng(seed)
+    kb = max(specs)
+    lens = rng.integers(0, max_len + 1, size=kb)
+    lens[rng.random(kb) < 0.1] = 0
+    if identical:
+        lens[:] = max_len
+        base = np.sort(rng.choice(ncols, size=max_len, replace=False))
+    cols = [base if identical else np.sort(rng.choice(ncols, size=n, replace=False)) for n in lens]
+    rpt = np.zeros(kb + 1, np.int64)
+    np.cumsum(lens, out=rpt[1:])
+    bcol = np.concatenate(cols).astype(np.int32)
+    B = Csr(kb, ncols, rpt, bcol, rng.uniform(-1, 1, size=bcol.size))
+    arpt, acol = [0], []
+    for nl in specs:
+        acol.append(np.sort(rng.choice(kb, size=nl, replace=False)))
+        arpt.append(arpt[-1] + nl)
+    acol = np.concatenate(acol).astype(np.int32)
+    A = Csr(len(specs), kb, np.array(arpt, np.int64), acol, rng.uniform(-1, 1, size=acol.size))
+    return A, B
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("ncols", [40000, 1 << 21, 3_000_000])  # packed records up to 2^21 - 1 columns
+def test_slab_rows(ctx, oracle_mod, mode, ncols):
+    """Heavy rows of <= 512 lists merge in column slabs (k_slab): one list,
+    two, the class boundaries 64/65, 256/257 and 512, and 513 (global tier),
+    over lists of skewed lengths with empty ones."""
+    A, B = _skewed_matrix([1, 2, 7, 64, 65, 256, 257, 512, 513], ncols, seed=5)
+    compare(run(ctx, A, B, mode), A, B)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_slab_long_single_lists(ctx, oracle_mod, mode):
+    """Heavy rows of one list (20,000 products: Alg. 1 only scales it), of
+    two lists (20,000 + 5) and of three lists of which one is empty."""
+    rng = np.random.default_rng(8)
+    lens = np.array([20000, 5, 0, 9000])
+    cols = [np.sort(rng.choice(50000, size=n, replace=False)) for n in lens]
+    rpt = np.zeros(5, np.int64)
+    np.cumsum(lens, out=rpt[1:])
+    bcol = np.concatenate(cols).astype(np.int32)
+    B = Csr(4, 50000, rpt, bcol, rng.uniform(-1, 1, size=bcol.size))
+    acol = np.array([0, 0, 1, 0, 2, 3], np.int32)
+    A = Csr(3, 4, np.array([0, 1, 3, 6], np.int64), acol, rng.uniform(-1, 1, size=6))
+    compare(run(ctx, A, B, mode), A, B)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_slab_rows_identical_lists(ctx, oracle_mod, mode):
+    """Every list has the same 2,500 columns: each slab takes exactly q
+    products from every list, and every column sums nl products."""
+    A, B = _skewed_matrix([3, 40, 64, 200, 512], 10**6, seed=6, max_len=2500, identical=True)
     compare(run(ctx, A, B, mode), A, B)
 
 
