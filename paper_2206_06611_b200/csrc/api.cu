@@ -325,39 +325,43 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
   CK(cudaMemcpyAsync(ctx->h_rows.p, hrows, (size_t)nh * 4, cudaMemcpyDeviceToHost, ctx->stream), "copy heavy rows");
   CK(cudaStreamSynchronize(ctx->stream), "sync heavy rows");
   const int32_t* hr = static_cast<const int32_t*>(ctx->h_rows.p);
-  std::vector<int32_t> g_rows, s_rows, l_rows;
-  std::vector<int64_t> g_info, s_info, l_info;
-  // Routes: rows of at most 512 lists merge in column
-  // slabs in shared memory (k_slab, three classes by nl); rows of more, SHORT
-  // lists are split into aligned 32-list blocks (heavy_split: the blocks then
-  // fit the shared-memory tiers); the rest run on the global tier, as does
-  // every heavy row under BRM_HEAVY_GLOBAL.
-  std::vector<int64_t> order, slab[kSlabClasses];
+  std::vector<int32_t> g_rows, s_rows;
+  std::vector<int64_t> g_info, s_info;
+  // Routes: rows of at most kSlabLists lists merge in
+  // column slabs in shared memory (k_slab); rows of up to kSlab2Lists lists
+  // take two levels of column slabs over 64-list blocks (k_slab2, a small
+  // and a large shape) -- except rows of more than kSlab2SmallLists SHORT
+  // lists, which are split into aligned 32-list blocks (heavy_split: the
+  // blocks then fit the shared-memory tiers); the rest run on the global
+  // tier, as does every heavy row under BRM_HEAVY_GLOBAL. Workspace kinds:
+  // 0 = k_slab2 small, 1 = k_slab2 large, 2 = global tier.
+  std::vector<int64_t> order, slab;
+  std::vector<int> wkind(nh, 2);
+  const bool auto_route = ctx->heavy_route != BRM_HEAVY_GLOBAL;
   for (int64_t t = 0; t < nh; ++t) {
     const int64_t P = ctx->heavy[2 * t], nl = ctx->heavy[2 * t + 1];
-    int cls = -1;
-    if (ctx->heavy_route != BRM_HEAVY_GLOBAL)
-      for (int c = kSlabClasses - 1; c >= 0; --c)
-        if (nl <= kSlabLists[c]) cls = c;
-    if (cls >= 0) {
-      slab[cls].push_back(t);
-    } else if (ctx->heavy_route != BRM_HEAVY_GLOBAL && P <= nl * (int64_t)kSplitAvgLen) {
+    if (auto_route && nl <= kSlabLists) {
+      slab.push_back(t);
+    } else if (auto_route && nl <= kSlab2SmallLists) {
+      wkind[t] = 0;
+      order.push_back(t);
+    } else if (auto_route && P <= nl * (int64_t)kSplitAvgLen) {
       s_rows.push_back(hr[t]);
       s_info.push_back(P);
       s_info.push_back(nl);
-    } else if (ctx->heavy_route != BRM_HEAVY_GLOBAL && kSplitLong > 0) {
-      l_rows.push_back(hr[t]);
-      l_info.push_back(P);
-      l_info.push_back(nl);
     } else {
+      if (auto_route && nl <= kSlab2Lists) wkind[t] = 1;
       order.push_back(t);
     }
   }
-  // descending n_prod: a launch lasts as long as its heaviest rows, so they
-  // go first
+  // by workspace kind, then descending n_prod (a launch lasts as long as its
+  // heaviest rows, so they go first)
   auto by_nprod = [&](int64_t x, int64_t y) { return ctx->heavy[2 * x] > ctx->heavy[2 * y]; };
-  std::sort(order.begin(), order.end(), by_nprod);
-  for (auto& v : slab) std::sort(v.begin(), v.end(), by_nprod);
+  std::sort(order.begin(), order.end(),
+            [&](int64_t x, int64_t y) { return wkind[x] != wkind[y] ? wkind[x] < wkind[y] : by_nprod(x, y); });
+  std::sort(slab.begin(), slab.end(), by_nprod);
+  std::vector<int> gkind;
+  for (const int64_t t : order) gkind.push_back(wkind[t]);
   for (const int64_t t : order) {
     g_rows.push_back(hr[t]);
     g_info.push_back(ctx->heavy[2 * t]);
@@ -367,41 +371,34 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
     brm_status_t st = heavy_split(ctx, out, o, s_rows.data(), (int64_t)s_rows.size(), s_info.data(), kSplitShort);
     if (st != BRM_OK) return st;
   }
-  if (!l_rows.empty()) {
-    brm_status_t st = heavy_split(ctx, out, o, l_rows.data(), (int64_t)l_rows.size(), l_info.data(), kSplitLong);
-    if (st != BRM_OK) return st;
-  }
-  // one device list: [slab classes 0, 1, 2 | global tier]
-  int64_t nslab = 0;
-  for (const auto& v : slab) nslab += (int64_t)v.size();
+  // one device list: [slab rows | workspace rows]
+  const int64_t nslab = (int64_t)slab.size();
   const int64_t ng = (int64_t)g_rows.size();
   const int64_t nall = nslab + ng;
   if (nall > 0) {
     CK(ensure(ctx, ctx->glob_rows, (size_t)nall * 4), "alloc heavy rows");
     CK(ensure_host(ctx->h_split, (size_t)nall * 4), "alloc pinned heavy rows");
     int32_t* hs = static_cast<int32_t*>(ctx->h_split.p);
-    int64_t k = 0;
-    for (const auto& v : slab)
-      for (const int64_t t : v) hs[k++] = hr[t];
+    for (int64_t k = 0; k < nslab; ++k) hs[k] = hr[slab[k]];
     if (ng) memcpy(hs + nslab, g_rows.data(), (size_t)ng * 4);
     CK(cudaMemcpyAsync(ctx->glob_rows.p, hs, (size_t)nall * 4, cudaMemcpyHostToDevice, ctx->stream),
        "copy heavy rows");
   }
   const int32_t* srows = static_cast<const int32_t*>(ctx->glob_rows.p);
-  int64_t s0 = 0;
-  for (int c = 0; c < kSlabClasses; ++c) {
-    const int64_t n = (int64_t)slab[c].size();
-    if (!n) continue;
-    CK(launch_slab(c, out, ctx->A, ctx->B, ctx->N, srows + s0, n, o, ctx->stream), "k_slab");
+  if (nslab) {
+    CK(launch_slab(out, ctx->A, ctx->B, ctx->N, srows, nslab, o, ctx->stream), "k_slab");
     ++ctx->launches;
-    s0 += n;
   }
   if (ng > 0) {
     const int32_t* grows = srows + nslab;
     const bool vals = out != OUT_SYMBOLIC;
-    // batch the rows so their ping-pong slices fit the workspace budget
+    // batch the rows so their workspace slices fit the budget; a batch holds
+    // rows of one workspace kind
+    auto row_bytes = [&](int64_t t) {
+      return gkind[t] < 2 ? slab2_row_bytes(g_info[2 * t], vals) : global_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals);
+    };
     int64_t max_row = 0;
-    for (int64_t t = 0; t < ng; ++t) max_row = std::max(max_row, global_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals));
+    for (int64_t t = 0; t < ng; ++t) max_row = std::max(max_row, row_bytes(t));
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     // a workspace already held is reused as is; a new one takes at most half
@@ -414,8 +411,8 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
     std::vector<int64_t> cuts{0};
     int64_t acc = 0, need = 0;
     for (int64_t t = 0; t < ng; ++t) {
-      const int64_t bytes = global_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals);
-      if (acc + bytes > budget) {
+      const int64_t bytes = row_bytes(t);
+      if (t > 0 && (acc + bytes > budget || gkind[t] != gkind[t - 1])) {
         cuts.push_back(t);
         acc = 0;
       }
@@ -431,9 +428,13 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
     for (size_t c = 0; c + 1 < cuts.size(); ++c) {
       const int64_t b0 = cuts[c], n = cuts[c + 1] - b0;
       if (n <= 0) continue;
-      CK(launch_global_tier(out, ctx->A, ctx->B, grows + b0, n, static_cast<const int64_t*>(ctx->gws_off.p) + 2 * b0,
-                            static_cast<unsigned char*>(ctx->gws.p), o, ctx->stream),
-         "k_global_tier");
+      const int64_t* woff = static_cast<const int64_t*>(ctx->gws_off.p) + 2 * b0;
+      unsigned char* ws = static_cast<unsigned char*>(ctx->gws.p);
+      if (gkind[b0] < 2) {
+        CK(launch_slab2(gkind[b0], out, ctx->A, ctx->B, ctx->N, grows + b0, n, woff, ws, o, ctx->stream), "k_slab2");
+      } else {
+        CK(launch_global_tier(out, ctx->A, ctx->B, grows + b0, n, woff, ws, o, ctx->stream), "k_global_tier");
+      }
       ++ctx->launches;
     }
   }

@@ -80,8 +80,10 @@ struct TierBounds {
 #define BRM_HASH4 BRM_H4_G, 768, 64, BRM_H4_GPC
 #define BRM_HASH5 128, 3072, 256, 1
 #define BRM_HASH6 256, 6656, 512, 1
-// heavy rows of at most 512 lists, merged in column slabs (G, CAP, LCAP):
-// class c takes the rows of kSlabLists[c-1] < nl <= kSlabLists[c]
+// Heavy rows: rows of at most kSlabLists lists merge
+// in column slabs with shape BRM_SLAB0 (G, CAP, LCAP); rows of up to
+// kSlab2SmallLists / kSlab2Lists lists in two levels of slabs over aligned
+// kSlab2Block-list blocks with shape BRM_SLAB0 / BRM_SLAB1.
 #ifndef BRM_SLAB0
 #define BRM_SLAB0 128, 2048, 64
 #endif
@@ -92,9 +94,10 @@ struct TierBounds {
 #define BRM_S1_CAP 4096
 #endif
 #define BRM_SLAB1 BRM_S1_G, BRM_S1_CAP, 256
-#define BRM_SLAB2 256, 6656, 512
-constexpr int kSlabClasses = 3;
-constexpr int kSlabLists[kSlabClasses] = {64, 256, 512};
+constexpr int kSlabLists = 64;
+constexpr int kSlab2Block = 64;
+constexpr int kSlab2SmallLists = kSlab2Block * 64;  // BRM_SLAB0's LCAP blocks
+constexpr int kSlab2Lists = kSlab2Block * 256;      // BRM_SLAB1's LCAP blocks
 constexpr int kGlobalG = 1024;
 
 __host__ __device__ inline TierBounds tier_bounds() {

@@ -23,6 +23,8 @@ namespace brm {
 
 enum OutKind { OUT_SYMBOLIC = 0, OUT_CBAR = 1, OUT_C = 2 };
 
+constexpr int kHashEmpty = -1;  // empty slot of the shared hash tables (columns are >= 0)
+
 struct RowOut {
   const int64_t* base;  // OUT_CBAR: n_prod offsets; OUT_C: C.rpt
   int32_t* col;
@@ -571,9 +573,23 @@ __device__ __forceinline__ int merge_path_rec(const typename R::T* a, int la, co
 // off[0..nl]); same partition as chunk_round (G chunks of VT odd positions,
 // threads cross into the next pair when both sentinels merge). Outputs wait
 // in registers and overwrite `rec` compacted once the group has read it.
-template <int G, int NV, class R>
-__device__ __forceinline__ int rec_round(const Group<G>& g, typename R::T* rec, double* val, const int* off,
-                                         int* noff, int nl, int* scan_tmp) {
+// vote: the duplicate combine is skipped (one warp vote) when no lane of the
+// warp has a duplicate -- cheaper for rounds with few repeated columns.
+#ifndef BRM_VOTE_MODE
+#define BRM_VOTE_MODE 0
+#endif
+// 0: never vote; 1: vote chosen per round at run time; 2: per round, two
+// non-inlined specialisations (tuning switch). Measured on B200: mode 1 made
+// uniform1m_k16's tier 3 5 % faster and stencil27_64's tier 4 7 % slower (a
+// predicate test on every step), mode 2 doubled the registers; mode 0 stays.
+#if BRM_VOTE_MODE == 2
+#define BRM_ROUND_INLINE __noinline__
+#else
+#define BRM_ROUND_INLINE __forceinline__
+#endif
+template <int G, int NV, class R, int VOTE>  // VOTE: -1 run time (vote), 0 never, 1 always
+__device__ BRM_ROUND_INLINE int rec_round(const Group<G>& g, typename R::T* rec, double* val, const int* off,
+                                          int* noff, int nl, int* scan_tmp, bool vote) {
   constexpr bool VALS = R::kVals;
   using T = typename R::T;
   constexpr unsigned RB = R::kBytes;
@@ -640,10 +656,13 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, typename R::T* rec, 
     if (VALS) {
       // equal columns: val[left] = val[left] + val[right]
       const bool dup = ta && tb && !R::is_sent(ra);
-      double x = 0.0, y = 0.0;
-      lds_if(dup, valb + 8u * R::slot(ra), x);
-      lds_if(dup, valb + 8u * R::slot(rb), y);
-      if (dup) val[R::slot(ra)] = __dadd_rn(x, y);
+      const bool use_vote = VOTE < 0 ? vote : VOTE > 0;
+      if (!use_vote || __any_sync(G < 32 ? g.mask : 0xffffffffu, dup)) {  // a uniform branch
+        double x = 0.0, y = 0.0;
+        lds_if(dup, valb + 8u * R::slot(ra), x);
+        lds_if(dup, valb + 8u * R::slot(rb), y);
+        if (dup) val[R::slot(ra)] = __dadd_rn(x, y);
+      }
     }
     cnt += act;
     ia += ta;
@@ -685,7 +704,17 @@ __device__ __forceinline__ int rec_round(const Group<G>& g, typename R::T* rec, 
 // its P_l products then its sentinel), the sentinels written, rb.bst[l] = the
 // B index of list l's first product, rb.av[l] = its A value. Returns the
 // number T of merged records, left in rec[0..T).
-template <int G, int NV, class R>
+// source loads: read-only path (B) or plain coherent loads (a workspace this
+// kernel wrote earlier)
+template <bool NC, class T>
+__device__ __forceinline__ T src_ld(const T* p) {
+  if constexpr (NC)
+    return __ldg(p);
+  else
+    return *p;
+}
+
+template <int G, int NV, class R, bool NC = true>
 __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView& B, int nl, int P, int* off,
                                                int* noff, const RecBufs& rb) {
   constexpr bool VALS = R::kVals;
@@ -702,17 +731,32 @@ __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView&
     for (int e = rank; e < P; e += G) {
       const int l = owner[e];
       const int64_t src = rb.bst[l] + (e - (off[l] - l));
-      const int c = __ldg(B.col + src);
+      const int c = src_ld<NC>(B.col + src);
       rec[e + l] = R::make(c, e);
-      if (VALS) rb.val[e] = __dmul_rn(rb.av[l], __ldg(B.val + src));  // line 12: the product, rounded once
+      if (VALS) rb.val[e] = __dmul_rn(rb.av[l], src_ld<NC>(B.val + src));  // line 12: the product, rounded once
     }
   }
   g.sync();
   // accumulating phase (lines 21-35)
   int cur = nl;
   int end = P + nl;
+  // the combine of duplicates is voted away in rounds that follow a round
+  // with few of them (fewer than 1 in 8 positions): adapts per row and round
+  bool vote = false;
   while (cur > 1) {
-    end = rec_round<G, NV, R>(g, rec, rb.val, off, noff, cur, rb.scan_tmp);
+    const int npos = off[cur] + (cur & 1);
+#if BRM_VOTE_MODE == 0
+    end = rec_round<G, NV, R, 0>(g, rec, rb.val, off, noff, cur, rb.scan_tmp, false);
+#elif BRM_VOTE_MODE == 1
+    end = rec_round<G, NV, R, -1>(g, rec, rb.val, off, noff, cur, rb.scan_tmp, vote);
+#else
+    if (vote)
+      end = rec_round<G, NV, R, 1>(g, rec, rb.val, off, noff, cur, rb.scan_tmp, true);
+    else
+      end = rec_round<G, NV, R, 0>(g, rec, rb.val, off, noff, cur, rb.scan_tmp, false);
+#endif
+    const int dups = npos - end - ((cur + 1) >> 1);  // 2 positions -> 1 output: duplicates and sentinel pairs
+    vote = 8 * dups < npos;
     cur = (cur + 1) >> 1;
     int* t = off;  // lines 33-34
     off = noff;
@@ -783,28 +827,72 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
 // slab progresses). Quotas in proportion to what is left fill the slab when
 // the lists spread over the columns alike. A slab in which every list has at
 // most q_l products left is the last one.
-template <int G, int NV, int CAP, int LCAP, class R, int OUT>
-__device__ __forceinline__ void slab_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
-                                         const RowOut& o, const RecBufs& rb) {
+__host__ __device__ constexpr int pow2_floor(int x) {
+  int p = 1;
+  while (2 * p <= x) p <<= 1;
+  return p;
+}
+
+// Number of distinct columns among the P products of nl lists (product
+// offsets off[0..nl], list l's first product at S index rb.bst[l]): every
+// column goes into a shared hash table over the record buffer (H = the power
+// of two >= 3P/2, <= HMAX; multiplicative hash, linear probing, a plain load
+// before atomicCAS); the count is the number of first insertions.
+template <int G, bool NC, int HMAX>
+__device__ __forceinline__ int hash_count_lists(const Group<G>& g, const CsrView& S, int nl, int P, const int* off,
+                                                const RecBufs& rb) {
+  int* table = static_cast<int*>(rb.rec);
+  const int rank = g.rank;
+  int H = 64;
+  while (H < P + P / 2) H <<= 1;
+  H = min(H, HMAX);
+  for (int e = rank; e < H; e += G) table[e] = kHashEmpty;
+  unsigned short* owner = reinterpret_cast<unsigned short*>(rb.owner);
+  for (int l = rank; l < nl; l += G)
+    for (int e = off[l], e1 = off[l + 1]; e < e1; ++e) owner[e] = static_cast<unsigned short>(l);
+  g.sync();
+  int cnt = 0;
+  const volatile int* tv = table;
+  for (int e = rank; e < P; e += G) {
+    const int l = owner[e];
+    const int c = src_ld<NC>(S.col + rb.bst[l] + (e - off[l]));
+    unsigned h = (static_cast<unsigned>(c) * 2654435761u) & (H - 1);
+    while (true) {
+      int cur = tv[h];
+      if (cur == kHashEmpty) {
+        cur = atomicCAS(&table[h], kHashEmpty, c);
+        if (cur == kHashEmpty) {
+          ++cnt;
+          break;
+        }
+      }
+      if (cur == c) break;
+      h = (h + 1) & (H - 1);
+    }
+  }
+  return group_reduce<G, false>(g, cnt, rb.scan_tmp);
+}
+
+// The slab loop over nl lists of a source S: on entry rb.bst[l] = the start
+// of list l in S, bend[j] = the end of list rank + j*G, rb.av[l] = its scale.
+// Each slab's merged result is appended at ocol/oval (skipped when null);
+// returns the number of entries of the merged row. NC: S is read-only for
+// the kernel (B), else S is a workspace this CTA wrote (plain loads).
+template <int G, int NV, int CAP, int LCAP, class R, bool NC, bool COUNT = false>
+__device__ __forceinline__ int64_t slab_run(const Group<G>& g, const CsrView& S, int nl,
+                                            const int64_t (&bend)[(LCAP + G - 1) / G], int32_t* ocol, double* oval,
+                                            const RecBufs& rb) {
   constexpr bool VALS = R::kVals;
+  // COUNT (symbolic, no output wanted): each slab's distinct columns are
+  // counted in a shared hash table laid over the record buffer (HMAX slots,
+  // slabs of <= 2/3 HMAX products) instead of merged: the slab's columns
+  // are disjoint from every other slab's, so the counts add up to the row size
+  static_assert(!COUNT || !VALS, "COUNT is the symbolic pass");
+  constexpr int HMAX = pow2_floor(CAP + LCAP + 2);
+  constexpr int BUDGET = COUNT ? HMAX * 2 / 3 : CAP;
   constexpr int LPT = (LCAP + G - 1) / G;  // lists per thread: l = rank + j * G
   typename R::T* rec = static_cast<typename R::T*>(rb.rec);
   const int rank = g.rank;
-  const int64_t a0 = A.rpt[row];
-  const int nl = static_cast<int>(A.rpt[row + 1] - a0);
-  int64_t bend[LPT];  // end of each of this thread's lists in B; rb.bst[l] is its cursor
-#pragma unroll
-  for (int j = 0; j < LPT; ++j) {
-    const int l = rank + j * G;
-    bend[j] = 0;
-    if (l < nl) {
-      const int k = __ldg(A.col + a0 + l);
-      rb.bst[l] = __ldg(B.rpt + k);
-      bend[j] = __ldg(B.rpt + k + 1);
-      if (VALS) rb.av[l] = __ldg(A.val + a0 + l);
-    }
-  }
-  const int64_t ob = OUT != OUT_SYMBOLIC ? o.base[row] : 0;
   int64_t written = 0;
   while (true) {
     int rem[LPT], qloc[LPT];
@@ -820,8 +908,8 @@ __device__ __forceinline__ void slab_row(const Group<G>& g, const CsrView& A, co
 #pragma unroll
     for (int j = 0; j < LPT; ++j) {
       const int l = rank + j * G;
-      qloc[j] = max(1, static_cast<int>(static_cast<int64_t>(CAP - nl) * rem[j] / rsum));
-      if (l < nl && qloc[j] < rem[j]) cmin = min(cmin, __ldg(B.col + rb.bst[l] + qloc[j]));
+      qloc[j] = max(1, static_cast<int>(static_cast<int64_t>(BUDGET - nl) * rem[j] / max(rsum, 1)));
+      if (l < nl && qloc[j] < rem[j]) cmin = min(cmin, src_ld<NC>(S.col + rb.bst[l] + qloc[j]));
     }
     const int c1 = group_reduce<G, true>(g, cmin, rb.scan_tmp);  // INT_MAX: the last slab
     int* off = rb.off0;
@@ -841,7 +929,7 @@ __device__ __forceinline__ void slab_row(const Group<G>& g, const CsrView& A, co
           int lo = 0, hi = avail;
           while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (__ldg(B.col + st + mid) < c1)
+            if (src_ld<NC>(S.col + st + mid) < c1)
               lo = mid + 1;
             else
               hi = mid;
@@ -853,22 +941,34 @@ __device__ __forceinline__ void slab_row(const Group<G>& g, const CsrView& A, co
       int tot;
       const int ex = group_excl_scan<G>(g, n, tot, rb.scan_tmp);
       if (l < nl) {
-        off[l] = P + ex + l;
-        rec[P + ex + l + n] = R::sent();  // sentinel of list l
+        if (COUNT) {
+          off[l] = P + ex;  // product offsets
+        } else {
+          off[l] = P + ex + l;
+          rec[P + ex + l + n] = R::sent();  // sentinel of list l
+        }
       }
       P += tot;
     }
     if (rank == 0) {
-      off[nl] = P + nl;
-      rec[P + nl] = R::sent();  // lone partner sentinel if nl is odd
+      if (COUNT) {
+        off[nl] = P;
+      } else {
+        off[nl] = P + nl;
+        rec[P + nl] = R::sent();  // lone partner sentinel if nl is odd
+      }
     }
     g.sync();
-    const int T = rec_merge_lists<G, NV, R>(g, B, nl, P, off, noff, rb);
-    if (OUT != OUT_SYMBOLIC) {  // line 36, this slab's part of the row
+    int T;
+    if constexpr (COUNT)
+      T = hash_count_lists<G, NC, HMAX>(g, S, nl, P, off, rb);
+    else
+      T = rec_merge_lists<G, NV, R, NC>(g, S, nl, P, off, noff, rb);
+    if (!COUNT && ocol) {  // line 36, this slab's part of the row
       for (int e = rank; e < T; e += G) {
         const typename R::T r = rec[e];
-        o.col[ob + written + e] = R::col(r);
-        if (VALS) o.val[ob + written + e] = rb.val[R::slot(r)];
+        ocol[written + e] = R::col(r);
+        if (VALS && oval) oval[written + e] = rb.val[R::slot(r)];
       }
     }
     written += T;
@@ -880,7 +980,92 @@ __device__ __forceinline__ void slab_row(const Group<G>& g, const CsrView& A, co
     }
     if (c1 == INT_MAX) break;
   }
-  if (OUT != OUT_C && rank == 0) o.row_size[row] = written;
+  return written;
+}
+
+// A heavy row of nl <= LCAP lists in column slabs (slab_run over its B rows).
+template <int G, int NV, int CAP, int LCAP, class R, int OUT>
+__device__ __forceinline__ void slab_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
+                                         const RowOut& o, const RecBufs& rb) {
+  constexpr bool VALS = R::kVals;
+  constexpr int LPT = (LCAP + G - 1) / G;
+  const int rank = g.rank;
+  const int64_t a0 = A.rpt[row];
+  const int nl = static_cast<int>(A.rpt[row + 1] - a0);
+  int64_t bend[LPT];  // end of each of this thread's lists in B; rb.bst[l] is its cursor
+#pragma unroll
+  for (int j = 0; j < LPT; ++j) {
+    const int l = rank + j * G;
+    bend[j] = 0;
+    if (l < nl) {
+      const int k = __ldg(A.col + a0 + l);
+      rb.bst[l] = __ldg(B.rpt + k);
+      bend[j] = __ldg(B.rpt + k + 1);
+      if (VALS) rb.av[l] = __ldg(A.val + a0 + l);
+    }
+  }
+  const int64_t ob = OUT != OUT_SYMBOLIC ? o.base[row] : 0;
+  const int64_t n =
+      slab_run<G, NV, CAP, LCAP, R, true, OUT == OUT_SYMBOLIC>(g, B, nl, bend, OUT != OUT_SYMBOLIC ? o.col + ob : nullptr,
+                                                                VALS && OUT != OUT_SYMBOLIC ? o.val + ob : nullptr, rb);
+  if (OUT != OUT_C && rank == 0) o.row_size[row] = n;
+  g.sync();
+}
+
+// A heavy row of LCAP < nl <= SB * LCAP lists in two levels of column slabs.
+// Algorithm 1's tree over the nl lists splits into aligned sub-trees over
+// blocks of SB = 2^k consecutive lists (pairs are (2m, 2m+1) at every level,
+// so an aligned block -- a short last block included -- is merged exactly as
+// Algorithm 1 merges it on its own). Level 1 merges each block's B rows into
+// the row's workspace slice (ws_col / ws_val); level 2 merges the nb block
+// results, scale 1.0 (1.0 * v == v exactly), in the same tree order.
+template <int G, int NV, int CAP, int LCAP, int SB, class R, int OUT>
+__device__ __forceinline__ void slab2_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
+                                          const RowOut& o, const RecBufs& rb, int32_t* ws_col, double* ws_val,
+                                          int64_t* blk) {
+  constexpr bool VALS = R::kVals;
+  constexpr int LPT = (LCAP + G - 1) / G;
+  static_assert(SB <= LCAP, "a block must fit the slab list capacity");
+  const int rank = g.rank;
+  const int64_t a0 = A.rpt[row];
+  const int nl = static_cast<int>(A.rpt[row + 1] - a0);
+  const int nb = (nl + SB - 1) / SB;
+  int64_t bend[LPT];
+  int64_t wpos = 0;
+  for (int b = 0; b < nb; ++b) {  // level 1
+    const int l0 = b * SB, nlb = min(SB, nl - l0);
+#pragma unroll
+    for (int j = 0; j < LPT; ++j) {
+      const int l = rank + j * G;
+      bend[j] = 0;
+      if (l < nlb) {
+        const int k = __ldg(A.col + a0 + l0 + l);
+        rb.bst[l] = __ldg(B.rpt + k);
+        bend[j] = __ldg(B.rpt + k + 1);
+        if (VALS) rb.av[l] = __ldg(A.val + a0 + l0 + l);
+      }
+    }
+    if (rank == 0) blk[b] = wpos;
+    wpos += slab_run<G, NV, CAP, LCAP, R, true>(g, B, nlb, bend, ws_col + wpos, VALS ? ws_val + wpos : nullptr, rb);
+  }
+  if (rank == 0) blk[nb] = wpos;
+  g.sync();
+  const CsrView W{nullptr, ws_col, ws_val};  // level 2: the block results
+#pragma unroll
+  for (int j = 0; j < LPT; ++j) {
+    const int l = rank + j * G;
+    bend[j] = 0;
+    if (l < nb) {
+      rb.bst[l] = blk[l];
+      bend[j] = blk[l + 1];
+      if (VALS) rb.av[l] = 1.0;
+    }
+  }
+  const int64_t ob = OUT != OUT_SYMBOLIC ? o.base[row] : 0;
+  const int64_t n =
+      slab_run<G, NV, CAP, LCAP, R, false, OUT == OUT_SYMBOLIC>(g, W, nb, bend, OUT != OUT_SYMBOLIC ? o.col + ob : nullptr,
+                                                                 VALS && OUT != OUT_SYMBOLIC ? o.val + ob : nullptr, rb);
+  if (OUT != OUT_C && rank == 0) o.row_size[row] = n;
   g.sync();
 }
 
@@ -977,7 +1162,6 @@ namespace brm {
 // (linear probing, atomicCAS); the row size is the number of first
 // insertions. The table has H = the power of two >= 3P/2 slots (<= HCAP).
 // ===========================================================================
-constexpr int kHashEmpty = -1;
 
 template <int CAP>
 __host__ __device__ constexpr int hash_cap() {

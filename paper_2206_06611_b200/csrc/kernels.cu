@@ -456,6 +456,27 @@ __global__ void __launch_bounds__(G) k_slab(CsrView A, CsrView B, const int32_t*
     slab_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, CAP, LCAP, R, OUT>(g, A, B, rows[r], o, rb);
 }
 
+// Heavy rows of kSlabLists[last] < nl <= kSlab2Block * LCAP lists: one CTA
+// per row (rows sorted by n_prod descending), two levels of column slabs
+// (slab2_row) through the row's workspace slice (ws_off[2i] bytes into ws,
+// n_prod = ws_off[2i+1]; slab2_row_bytes).
+template <int G, int CAP, int LCAP, bool VALS, int OUT, bool PACK>
+__global__ void __launch_bounds__(G) k_slab2(CsrView A, CsrView B, const int32_t* __restrict__ rows,
+                                             const int64_t* __restrict__ ws_off, unsigned char* __restrict__ ws,
+                                             RowOut o) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using R = RecT<VALS, PACK, CAP>;
+  const Group<G> g = make_group<G>();
+  const RecBufs rb = rec_bufs<G, CAP, LCAP, R>(smem);
+  int64_t* blk = reinterpret_cast<int64_t*>(smem + rec_group_bytes<G, CAP, LCAP, R>());
+  const int64_t P = ws_off[2 * blockIdx.x + 1];
+  unsigned char* p = ws + ws_off[2 * blockIdx.x];
+  int32_t* ws_col = reinterpret_cast<int32_t*>(p);
+  double* ws_val = VALS ? reinterpret_cast<double*>(p + ((P * 4 + 15) & ~15ll)) : nullptr;
+  slab2_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, CAP, LCAP, kSlab2Block, R, OUT>(g, A, B, rows[blockIdx.x], o, rb,
+                                                                                   ws_col, ws_val, blk);
+}
+
 // PRECISE symbolic phase of tiers 3-6: hash_row per group (GPC groups of G).
 template <int G, int CAP, int LCAP, int GPC>
 __global__ void __launch_bounds__(G * GPC) k_hash_symbolic(CsrView A, CsrView B, const int32_t* __restrict__ rows,
@@ -849,24 +870,63 @@ static cudaError_t launch_slab_t(const CsrView& A, const CsrView& B, int64_t b_c
   return launch_slab_pk<G, CAP, LCAP, VALS, OUT, false>(A, B, rows, n, o, st);
 }
 
-template <int OUT>
-static cudaError_t launch_slab_k(int cls, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
-                                 int64_t n, const RowOut& o, cudaStream_t st) {
+template <int G, int CAP, int LCAP, bool VALS, int OUT, bool PACK>
+static cudaError_t launch_slab2_pk(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
+                                   const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st) {
+  constexpr int smem = rec_group_bytes<G, CAP, LCAP, RecT<VALS, PACK, CAP>>() + (LCAP + 1) * 8;
+  static_assert(smem <= 232448, "slab shared memory exceeds 227 KB");
+  auto kern = k_slab2<G, CAP, LCAP, VALS, OUT, PACK>;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  kern<<<(unsigned)n, G, smem, st>>>(A, B, rows, ws_off, ws, o);
+  return cudaGetLastError();
+}
+
+template <int G, int CAP, int LCAP, int OUT>
+static cudaError_t launch_slab2_t(const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows, int64_t n,
+                                  const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st) {
   constexpr bool VALS = OUT != OUT_SYMBOLIC;
-  switch (cls) {
-    case 0: return launch_slab_t<BRM_SLAB0, VALS, OUT>(A, B, b_cols, rows, n, o, st);
-    case 1: return launch_slab_t<BRM_SLAB1, VALS, OUT>(A, B, b_cols, rows, n, o, st);
-    case 2: return launch_slab_t<BRM_SLAB2, VALS, OUT>(A, B, b_cols, rows, n, o, st);
+  if (n <= 0) return cudaSuccess;
+  if constexpr (VALS) {
+    if (rec_pack_ok(CAP, b_cols))
+      return launch_slab2_pk<G, CAP, LCAP, VALS, OUT, true>(A, B, rows, n, ws_off, ws, o, st);
+  }
+  return launch_slab2_pk<G, CAP, LCAP, VALS, OUT, false>(A, B, rows, n, ws_off, ws, o, st);
+}
+
+template <int OUT>
+static cudaError_t launch_slab2_k(int shape, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
+                                  int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o,
+                                  cudaStream_t st) {
+  if (shape == 0) return launch_slab2_t<BRM_SLAB0, OUT>(A, B, b_cols, rows, n, ws_off, ws, o, st);
+  return launch_slab2_t<BRM_SLAB1, OUT>(A, B, b_cols, rows, n, ws_off, ws, o, st);
+}
+
+cudaError_t launch_slab2(int shape, int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols,
+                         const int32_t* rows, int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o,
+                         cudaStream_t st) {
+  switch (out_kind) {
+    case OUT_SYMBOLIC: return launch_slab2_k<OUT_SYMBOLIC>(shape, A, B, b_cols, rows, n, ws_off, ws, o, st);
+    case OUT_CBAR: return launch_slab2_k<OUT_CBAR>(shape, A, B, b_cols, rows, n, ws_off, ws, o, st);
+    case OUT_C: return launch_slab2_k<OUT_C>(shape, A, B, b_cols, rows, n, ws_off, ws, o, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_slab(int cls, int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
+int64_t slab2_row_bytes(int64_t nprod, bool vals) {
+  return ((nprod * 4 + 15) & ~15ll) + (vals ? ((nprod * 8 + 15) & ~15ll) : 0);
+}
+
+cudaError_t launch_slab(int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
                         int64_t n, const RowOut& o, cudaStream_t st) {
   switch (out_kind) {
-    case OUT_SYMBOLIC: return launch_slab_k<OUT_SYMBOLIC>(cls, A, B, b_cols, rows, n, o, st);
-    case OUT_CBAR: return launch_slab_k<OUT_CBAR>(cls, A, B, b_cols, rows, n, o, st);
-    case OUT_C: return launch_slab_k<OUT_C>(cls, A, B, b_cols, rows, n, o, st);
+    case OUT_SYMBOLIC: return launch_slab_t<BRM_SLAB0, false, OUT_SYMBOLIC>(A, B, b_cols, rows, n, o, st);
+    case OUT_CBAR: return launch_slab_t<BRM_SLAB0, true, OUT_CBAR>(A, B, b_cols, rows, n, o, st);
+    case OUT_C: return launch_slab_t<BRM_SLAB0, true, OUT_C>(A, B, b_cols, rows, n, o, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -32,10 +32,17 @@ cudaError_t launch_heavy_info(const CsrView& A, const int64_t* nprod_off, const 
 // bits when the columns fit)
 cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
                         int64_t n, const RowOut& o, cudaStream_t st);
-// heavy rows merged in column slabs, class cls (kSlabLists[cls - 1] < nl <=
-// kSlabLists[cls]); rows sorted by n_prod descending
-cudaError_t launch_slab(int cls, int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
+// heavy rows of <= kSlabLists lists merged in column slabs; rows sorted by
+// n_prod descending
+cudaError_t launch_slab(int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
                         int64_t n, const RowOut& o, cudaStream_t st);
+// heavy rows of kSlabLists < nl <= kSlab2Lists lists: two levels of column
+// slabs, one CTA per row, workspace slices like the global tier's
+// shape 0: class 0's (blocks of 64, <= 64 blocks), 1: class 1's (<= 256 blocks)
+cudaError_t launch_slab2(int shape, int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols,
+                         const int32_t* rows, int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o,
+                         cudaStream_t st);
+int64_t slab2_row_bytes(int64_t nprod, bool vals);
 int64_t global_row_bytes(int64_t nprod, int64_t nl, bool vals);
 cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
                                const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st);
@@ -47,12 +54,7 @@ cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, i
 // heavy-row decomposition (kernels.cu "Heavy-row decomposition")
 constexpr int kSplitShort = 32;   // block of lists for rows of short lists (mean length <= kSplitAvgLen)
 constexpr int kSplitAvgLen = 32;
-#ifndef BRM_SPLIT_LONG
-#define BRM_SPLIT_LONG 0
-#endif
-// block of lists for rows of > 512 LONG lists (0: those rows take the global
-// tier instead); a tuning switch, see DESIGN.md "Tier 7"
-constexpr int kSplitLong = BRM_SPLIT_LONG;
+
 cudaError_t launch_split_a1(const CsrView& A, const int32_t* rows, int n, const int64_t* ent_off,
                             const int64_t* blk_off, int bs, int64_t total, int64_t* a1_rpt, int32_t* a1_col,
                             double* a1_val, cudaStream_t st);

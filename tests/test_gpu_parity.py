@@ -207,9 +207,9 @@ def _skewed_matrix(specs, ncols, seed, max_len=3000, identical=False):
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("ncols", [40000, 1 << 21, 3_000_000])  # packed records up to 2^21 - 1 columns
 def test_slab_rows(ctx, oracle_mod, mode, ncols):
-    """Heavy rows of <= 512 lists merge in column slabs (k_slab): one list,
-    two, the class boundaries 64/65, 256/257 and 512, and 513 (global tier),
-    over lists of skewed lengths with empty ones."""
+    """Heavy rows in column slabs: one list, two, up to 64 (k_slab), then
+    two levels of slabs (k_slab2) at 65, 256, 257, 512 and 513, over lists of
+    skewed lengths with empty ones."""
     A, B = _skewed_matrix([1, 2, 7, 64, 65, 256, 257, 512, 513], ncols, seed=5)
     compare(run(ctx, A, B, mode), A, B)
 
@@ -227,6 +227,15 @@ def test_slab_long_single_lists(ctx, oracle_mod, mode):
     B = Csr(4, 50000, rpt, bcol, rng.uniform(-1, 1, size=bcol.size))
     acol = np.array([0, 0, 1, 0, 2, 3], np.int32)
     A = Csr(3, 4, np.array([0, 1, 3, 6], np.int64), acol, rng.uniform(-1, 1, size=6))
+    compare(run(ctx, A, B, mode), A, B)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_two_level_slab_rows(ctx, oracle_mod, mode):
+    """Rows of > 64 lists: two levels of column slabs over aligned 64-list
+    blocks (k_slab2; small shape up to 4,096 lists, large up to 16,384; short
+    last blocks at 700, 4,097 and 16,383), and the global tier at 16,385."""
+    A, B = _lists_matrix([700, 4096, 4097, 16383, 16384, 16385], 40, 200000, seed=17)
     compare(run(ctx, A, B, mode), A, B)
 
 
