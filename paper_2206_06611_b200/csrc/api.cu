@@ -329,12 +329,12 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
   std::vector<int64_t> g_info, s_info;
   // Routes: rows of at most kSlabLists lists merge in
   // column slabs in shared memory (k_slab); rows of up to kSlab2Lists lists
-  // take two levels of column slabs over 64-list blocks (k_slab2, a small
-  // and a large shape) -- except rows of more than kSlab2SmallLists SHORT
-  // lists, which are split into aligned 32-list blocks (heavy_split: the
-  // blocks then fit the shared-memory tiers); the rest run on the global
-  // tier, as does every heavy row under BRM_HEAVY_GLOBAL. Workspace kinds:
-  // 0 = k_slab2 small, 1 = k_slab2 large, 2 = global tier.
+  // take two or three levels of column slabs over 64-list blocks (k_slab2)
+  // -- except rows of more than 4096 SHORT lists, which are split into
+  // aligned 32-list blocks (heavy_split: the blocks then fit the
+  // shared-memory tiers); the rest run on the global tier, as does every
+  // heavy row under BRM_HEAVY_GLOBAL. Workspace kinds: 0 = k_slab2,
+  // 2 = global tier.
   std::vector<int64_t> order, slab;
   std::vector<int> wkind(nh, 2);
   const bool auto_route = ctx->heavy_route != BRM_HEAVY_GLOBAL;
@@ -342,15 +342,12 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
     const int64_t P = ctx->heavy[2 * t], nl = ctx->heavy[2 * t + 1];
     if (auto_route && nl <= kSlabLists) {
       slab.push_back(t);
-    } else if (auto_route && nl <= kSlab2SmallLists) {
-      wkind[t] = 0;
-      order.push_back(t);
-    } else if (auto_route && P <= nl * (int64_t)kSplitAvgLen) {
+    } else if (auto_route && nl > 4096 && P <= nl * (int64_t)kSplitAvgLen) {
       s_rows.push_back(hr[t]);
       s_info.push_back(P);
       s_info.push_back(nl);
     } else {
-      if (auto_route && nl <= kSlab2Lists) wkind[t] = 1;
+      if (auto_route && nl <= kSlab2Lists) wkind[t] = 0;
       order.push_back(t);
     }
   }
@@ -395,7 +392,8 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
     // batch the rows so their workspace slices fit the budget; a batch holds
     // rows of one workspace kind
     auto row_bytes = [&](int64_t t) {
-      return gkind[t] < 2 ? slab2_row_bytes(g_info[2 * t], vals) : global_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals);
+      return gkind[t] == 0 ? slab2_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals)
+                           : global_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals);
     };
     int64_t max_row = 0;
     for (int64_t t = 0; t < ng; ++t) max_row = std::max(max_row, row_bytes(t));
@@ -430,8 +428,8 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
       if (n <= 0) continue;
       const int64_t* woff = static_cast<const int64_t*>(ctx->gws_off.p) + 2 * b0;
       unsigned char* ws = static_cast<unsigned char*>(ctx->gws.p);
-      if (gkind[b0] < 2) {
-        CK(launch_slab2(gkind[b0], out, ctx->A, ctx->B, ctx->N, grows + b0, n, woff, ws, o, ctx->stream), "k_slab2");
+      if (gkind[b0] == 0) {
+        CK(launch_slab2(out, ctx->A, ctx->B, ctx->N, grows + b0, n, woff, ws, o, ctx->stream), "k_slab2");
       } else {
         CK(launch_global_tier(out, ctx->A, ctx->B, grows + b0, n, woff, ws, o, ctx->stream), "k_global_tier");
       }

@@ -82,22 +82,14 @@ struct TierBounds {
 #define BRM_HASH6 256, 6656, 512, 1
 // Heavy rows: rows of at most kSlabLists lists merge
 // in column slabs with shape BRM_SLAB0 (G, CAP, LCAP); rows of up to
-// kSlab2SmallLists / kSlab2Lists lists in two levels of slabs over aligned
-// kSlab2Block-list blocks with shape BRM_SLAB0 / BRM_SLAB1.
+// kSlab2Lists lists in two or three levels of slabs (same shape) over
+// aligned kSlab2Block-list blocks.
 #ifndef BRM_SLAB0
 #define BRM_SLAB0 128, 2048, 64
 #endif
-#ifndef BRM_S1_G
-#define BRM_S1_G 256
-#endif
-#ifndef BRM_S1_CAP
-#define BRM_S1_CAP 4096
-#endif
-#define BRM_SLAB1 BRM_S1_G, BRM_S1_CAP, 256
-constexpr int kSlabLists = 64;
+constexpr int kSlabLists = 64;                                    // = BRM_SLAB0's LCAP
 constexpr int kSlab2Block = 64;
-constexpr int kSlab2SmallLists = kSlab2Block * 64;  // BRM_SLAB0's LCAP blocks
-constexpr int kSlab2Lists = kSlab2Block * 256;      // BRM_SLAB1's LCAP blocks
+constexpr int kSlab2Lists = kSlab2Block * kSlab2Block * kSlabLists;  // three levels
 constexpr int kGlobalG = 1024;
 
 __host__ __device__ inline TierBounds tier_bounds() {

@@ -536,6 +536,7 @@ __host__ __device__ constexpr bool rec_pack_ok(int cap, int64_t b_cols) {
 
 struct RecBufs {
   void* rec;      // P + nl + 2 records (R::T): sentinel-terminated lists
+  longlong2* lst; // per list {S index of product 0 (B index - product offset), A value bits}
   double* val;    // P value slots (products, then partial sums)
   int* owner;     // P 16-bit entries: list of each product (multiplying phase)
   int* off0;
@@ -548,7 +549,7 @@ struct RecBufs {
 template <int G, int CAP, int LCAP, class R>
 __host__ __device__ constexpr int rec_group_bytes() {
   constexpr bool VALS = R::kVals;
-  return align16((CAP + LCAP + 2) * R::kBytes) + (VALS ? align16(CAP * 8) : 0) + align16(CAP * 2) + align16((LCAP + 2) * 4) * 2 +
+  return align16((CAP + LCAP + 2) * R::kBytes) + LCAP * 16 + (VALS ? align16(CAP * 8) : 0) + align16(CAP * 2) + align16((LCAP + 2) * 4) * 2 +
          align16(LCAP * 8) + (VALS ? align16(LCAP * 8) : 0) + (G > 32 ? align16((G / 32 + 2) * 4) : 0);
 }
 
@@ -724,16 +725,20 @@ __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView&
     // owner[e] = list of product e (16-bit table: nl <= 512 in these tiers),
     // filled by one thread per list; then the products are fetched coalesced
     unsigned short* owner = reinterpret_cast<unsigned short*>(rb.owner);
-    for (int l = rank; l < nl; l += G)
-      for (int e = off[l] - l, e1 = off[l + 1] - (l + 1); e < e1; ++e) owner[e] = static_cast<unsigned short>(l);
+    for (int l = rank; l < nl; l += G) {
+      const int e0 = off[l] - l, e1 = off[l + 1] - (l + 1);
+      rb.lst[l] = make_longlong2(rb.bst[l] - e0, VALS ? __double_as_longlong(rb.av[l]) : 0);  // one 16-byte load per product
+      for (int e = e0; e < e1; ++e) owner[e] = static_cast<unsigned short>(l);
+    }
     g.sync();
 #pragma unroll 2
     for (int e = rank; e < P; e += G) {
       const int l = owner[e];
-      const int64_t src = rb.bst[l] + (e - (off[l] - l));
+      const longlong2 d = rb.lst[l];
+      const int64_t src = d.x + e;
       const int c = src_ld<NC>(B.col + src);
       rec[e + l] = R::make(c, e);
-      if (VALS) rb.val[e] = __dmul_rn(rb.av[l], src_ld<NC>(B.val + src));  // line 12: the product, rounded once
+      if (VALS) rb.val[e] = __dmul_rn(__longlong_as_double(d.y), src_ld<NC>(B.val + src));  // line 12: the product, rounded once
     }
   }
   g.sync();
@@ -1012,27 +1017,33 @@ __device__ __forceinline__ void slab_row(const Group<G>& g, const CsrView& A, co
   g.sync();
 }
 
-// A heavy row of LCAP < nl <= SB * LCAP lists in two levels of column slabs.
-// Algorithm 1's tree over the nl lists splits into aligned sub-trees over
-// blocks of SB = 2^k consecutive lists (pairs are (2m, 2m+1) at every level,
-// so an aligned block -- a short last block included -- is merged exactly as
-// Algorithm 1 merges it on its own). Level 1 merges each block's B rows into
-// the row's workspace slice (ws_col / ws_val); level 2 merges the nb block
-// results, scale 1.0 (1.0 * v == v exactly), in the same tree order.
+// A heavy row of LCAP < nl <= SB * SB * LCAP lists in two or three levels
+// of column slabs. Algorithm 1's tree over the nl lists splits into aligned
+// sub-trees over blocks of SB = 2^k consecutive lists (pairs are (2m, 2m+1)
+// at every level, so an aligned block -- a short last block included -- is
+// merged exactly as Algorithm 1 merges it on its own). Level 1 merges each
+// block's B rows into the workspace ws1; if more than LCAP blocks result,
+// level 2 merges aligned groups of SB block results (an aligned block of
+// blocks is again a sub-tree) into ws2; the last level merges the <= LCAP
+// remaining lists into the output row. Levels above the first scale by 1.0
+// (1.0 * v == v exactly). Block-result offsets: smem `blk` (<= LCAP + 1) or,
+// for level 1 of a three-level row, the global table `tab1` (nb1 + 1).
 template <int G, int NV, int CAP, int LCAP, int SB, class R, int OUT>
 __device__ __forceinline__ void slab2_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
-                                          const RowOut& o, const RecBufs& rb, int32_t* ws_col, double* ws_val,
-                                          int64_t* blk) {
+                                          const RowOut& o, const RecBufs& rb, int32_t* ws1_col, double* ws1_val,
+                                          int32_t* ws2_col, double* ws2_val, int64_t* tab1, int64_t* blk) {
   constexpr bool VALS = R::kVals;
   constexpr int LPT = (LCAP + G - 1) / G;
   static_assert(SB <= LCAP, "a block must fit the slab list capacity");
   const int rank = g.rank;
   const int64_t a0 = A.rpt[row];
   const int nl = static_cast<int>(A.rpt[row + 1] - a0);
-  const int nb = (nl + SB - 1) / SB;
+  const int nb1 = (nl + SB - 1) / SB;
+  const bool three = nb1 > LCAP;
+  int64_t* t1 = three ? tab1 : blk;
   int64_t bend[LPT];
   int64_t wpos = 0;
-  for (int b = 0; b < nb; ++b) {  // level 1
+  for (int b = 0; b < nb1; ++b) {  // level 1: blocks of SB lists of B rows
     const int l0 = b * SB, nlb = min(SB, nl - l0);
 #pragma unroll
     for (int j = 0; j < LPT; ++j) {
@@ -1045,17 +1056,42 @@ __device__ __forceinline__ void slab2_row(const Group<G>& g, const CsrView& A, c
         if (VALS) rb.av[l] = __ldg(A.val + a0 + l0 + l);
       }
     }
-    if (rank == 0) blk[b] = wpos;
-    wpos += slab_run<G, NV, CAP, LCAP, R, true>(g, B, nlb, bend, ws_col + wpos, VALS ? ws_val + wpos : nullptr, rb);
+    if (rank == 0) t1[b] = wpos;
+    wpos += slab_run<G, NV, CAP, LCAP, R, true>(g, B, nlb, bend, ws1_col + wpos, VALS ? ws1_val + wpos : nullptr, rb);
   }
-  if (rank == 0) blk[nb] = wpos;
+  if (rank == 0) t1[nb1] = wpos;
   g.sync();
-  const CsrView W{nullptr, ws_col, ws_val};  // level 2: the block results
+  CsrView W{nullptr, ws1_col, ws1_val};
+  int nfin = nb1;
+  if (three) {  // level 2: aligned groups of SB block results
+    const int nb2 = (nb1 + SB - 1) / SB;
+    int64_t wpos2 = 0;
+    for (int c = 0; c < nb2; ++c) {
+      const int l0 = c * SB, nlc = min(SB, nb1 - l0);
 #pragma unroll
-  for (int j = 0; j < LPT; ++j) {
+      for (int j = 0; j < LPT; ++j) {
+        const int l = rank + j * G;
+        bend[j] = 0;
+        if (l < nlc) {
+          rb.bst[l] = t1[l0 + l];
+          bend[j] = t1[l0 + l + 1];
+          if (VALS) rb.av[l] = 1.0;
+        }
+      }
+      if (rank == 0) blk[c] = wpos2;
+      wpos2 += slab_run<G, NV, CAP, LCAP, R, false>(g, W, nlc, bend, ws2_col + wpos2, VALS ? ws2_val + wpos2 : nullptr,
+                                                    rb);
+    }
+    if (rank == 0) blk[nb2] = wpos2;
+    g.sync();
+    W = CsrView{nullptr, ws2_col, ws2_val};
+    nfin = nb2;
+  }
+#pragma unroll
+  for (int j = 0; j < LPT; ++j) {  // last level: the <= LCAP block results
     const int l = rank + j * G;
     bend[j] = 0;
-    if (l < nb) {
+    if (l < nfin) {
       rb.bst[l] = blk[l];
       bend[j] = blk[l + 1];
       if (VALS) rb.av[l] = 1.0;
@@ -1063,7 +1099,7 @@ __device__ __forceinline__ void slab2_row(const Group<G>& g, const CsrView& A, c
   }
   const int64_t ob = OUT != OUT_SYMBOLIC ? o.base[row] : 0;
   const int64_t n =
-      slab_run<G, NV, CAP, LCAP, R, false, OUT == OUT_SYMBOLIC>(g, W, nb, bend, OUT != OUT_SYMBOLIC ? o.col + ob : nullptr,
+      slab_run<G, NV, CAP, LCAP, R, false, OUT == OUT_SYMBOLIC>(g, W, nfin, bend, OUT != OUT_SYMBOLIC ? o.col + ob : nullptr,
                                                                  VALS && OUT != OUT_SYMBOLIC ? o.val + ob : nullptr, rb);
   if (OUT != OUT_C && rank == 0) o.row_size[row] = n;
   g.sync();

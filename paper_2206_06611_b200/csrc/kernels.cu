@@ -408,6 +408,7 @@ __device__ __forceinline__ RecBufs rec_bufs(unsigned char* p) {
   };
   RecBufs rb;
   rb.rec = take((CAP + LCAP + 2) * R::kBytes);
+  rb.lst = reinterpret_cast<longlong2*>(take(LCAP * 16));
   rb.val = R::kVals ? reinterpret_cast<double*>(take(CAP * 8)) : nullptr;
   rb.owner = reinterpret_cast<int*>(take(CAP * 2));
   rb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
@@ -456,10 +457,27 @@ __global__ void __launch_bounds__(G) k_slab(CsrView A, CsrView B, const int32_t*
     slab_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, CAP, LCAP, R, OUT>(g, A, B, rows[r], o, rb);
 }
 
-// Heavy rows of kSlabLists[last] < nl <= kSlab2Block * LCAP lists: one CTA
-// per row (rows sorted by n_prod descending), two levels of column slabs
+// Heavy rows of kSlabLists < nl <= kSlab2Lists lists: one CTA per row (rows
+// sorted by n_prod descending), two or three levels of column slabs
 // (slab2_row) through the row's workspace slice (ws_off[2i] bytes into ws,
-// n_prod = ws_off[2i+1]; slab2_row_bytes).
+// n_prod = ws_off[2i+1]; layout and size: slab2_layout / slab2_row_bytes).
+struct Slab2Layout {
+  int64_t col1, val1, col2, val2, tab1, bytes;  // byte offsets in the slice
+};
+__host__ __device__ inline Slab2Layout slab2_layout(int64_t P, int64_t nl, bool vals, int lcap) {
+  auto a = [](int64_t b) { return (b + 15) & ~15ll; };
+  const int64_t nb1 = (nl + kSlab2Block - 1) / kSlab2Block;
+  const bool three = nb1 > lcap;
+  Slab2Layout L{};
+  L.col1 = 0;
+  L.val1 = a(P * 4);
+  L.col2 = L.val1 + (vals ? a(P * 8) : 0);
+  L.val2 = L.col2 + (three ? a(P * 4) : 0);
+  L.tab1 = L.val2 + (three && vals ? a(P * 8) : 0);
+  L.bytes = L.tab1 + (three ? a((nb1 + 1) * 8) : 0);
+  return L;
+}
+
 template <int G, int CAP, int LCAP, bool VALS, int OUT, bool PACK>
 __global__ void __launch_bounds__(G) k_slab2(CsrView A, CsrView B, const int32_t* __restrict__ rows,
                                              const int64_t* __restrict__ ws_off, unsigned char* __restrict__ ws,
@@ -469,12 +487,14 @@ __global__ void __launch_bounds__(G) k_slab2(CsrView A, CsrView B, const int32_t
   const Group<G> g = make_group<G>();
   const RecBufs rb = rec_bufs<G, CAP, LCAP, R>(smem);
   int64_t* blk = reinterpret_cast<int64_t*>(smem + rec_group_bytes<G, CAP, LCAP, R>());
+  const int64_t row = rows[blockIdx.x];
   const int64_t P = ws_off[2 * blockIdx.x + 1];
+  const Slab2Layout L = slab2_layout(P, A.rpt[row + 1] - A.rpt[row], VALS, LCAP);
   unsigned char* p = ws + ws_off[2 * blockIdx.x];
-  int32_t* ws_col = reinterpret_cast<int32_t*>(p);
-  double* ws_val = VALS ? reinterpret_cast<double*>(p + ((P * 4 + 15) & ~15ll)) : nullptr;
-  slab2_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, CAP, LCAP, kSlab2Block, R, OUT>(g, A, B, rows[blockIdx.x], o, rb,
-                                                                                   ws_col, ws_val, blk);
+  slab2_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, CAP, LCAP, kSlab2Block, R, OUT>(
+      g, A, B, row, o, rb, reinterpret_cast<int32_t*>(p + L.col1), VALS ? reinterpret_cast<double*>(p + L.val1) : nullptr,
+      reinterpret_cast<int32_t*>(p + L.col2), VALS ? reinterpret_cast<double*>(p + L.val2) : nullptr,
+      reinterpret_cast<int64_t*>(p + L.tab1), blk);
 }
 
 // PRECISE symbolic phase of tiers 3-6: hash_row per group (GPC groups of G).
@@ -898,27 +918,19 @@ static cudaError_t launch_slab2_t(const CsrView& A, const CsrView& B, int64_t b_
   return launch_slab2_pk<G, CAP, LCAP, VALS, OUT, false>(A, B, rows, n, ws_off, ws, o, st);
 }
 
-template <int OUT>
-static cudaError_t launch_slab2_k(int shape, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
-                                  int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o,
-                                  cudaStream_t st) {
-  if (shape == 0) return launch_slab2_t<BRM_SLAB0, OUT>(A, B, b_cols, rows, n, ws_off, ws, o, st);
-  return launch_slab2_t<BRM_SLAB1, OUT>(A, B, b_cols, rows, n, ws_off, ws, o, st);
-}
-
-cudaError_t launch_slab2(int shape, int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols,
-                         const int32_t* rows, int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o,
-                         cudaStream_t st) {
+cudaError_t launch_slab2(int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
+                         int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st) {
   switch (out_kind) {
-    case OUT_SYMBOLIC: return launch_slab2_k<OUT_SYMBOLIC>(shape, A, B, b_cols, rows, n, ws_off, ws, o, st);
-    case OUT_CBAR: return launch_slab2_k<OUT_CBAR>(shape, A, B, b_cols, rows, n, ws_off, ws, o, st);
-    case OUT_C: return launch_slab2_k<OUT_C>(shape, A, B, b_cols, rows, n, ws_off, ws, o, st);
+    case OUT_SYMBOLIC: return launch_slab2_t<BRM_SLAB0, OUT_SYMBOLIC>(A, B, b_cols, rows, n, ws_off, ws, o, st);
+    case OUT_CBAR: return launch_slab2_t<BRM_SLAB0, OUT_CBAR>(A, B, b_cols, rows, n, ws_off, ws, o, st);
+    case OUT_C: return launch_slab2_t<BRM_SLAB0, OUT_C>(A, B, b_cols, rows, n, ws_off, ws, o, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-int64_t slab2_row_bytes(int64_t nprod, bool vals) {
-  return ((nprod * 4 + 15) & ~15ll) + (vals ? ((nprod * 8 + 15) & ~15ll) : 0);
+int64_t slab2_row_bytes(int64_t nprod, int64_t nl, bool vals) {
+  constexpr int kLcap = kSlab2Lists / (kSlab2Block * kSlab2Block);
+  return slab2_layout(nprod, nl, vals, kLcap).bytes;
 }
 
 cudaError_t launch_slab(int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,

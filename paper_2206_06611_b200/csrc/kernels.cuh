@@ -36,13 +36,11 @@ cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& 
 // n_prod descending
 cudaError_t launch_slab(int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
                         int64_t n, const RowOut& o, cudaStream_t st);
-// heavy rows of kSlabLists < nl <= kSlab2Lists lists: two levels of column
-// slabs, one CTA per row, workspace slices like the global tier's
-// shape 0: class 0's (blocks of 64, <= 64 blocks), 1: class 1's (<= 256 blocks)
-cudaError_t launch_slab2(int shape, int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols,
-                         const int32_t* rows, int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o,
-                         cudaStream_t st);
-int64_t slab2_row_bytes(int64_t nprod, bool vals);
+// heavy rows of kSlabLists < nl <= kSlab2Lists lists: two or three levels of
+// column slabs, one CTA per row, workspace slices like the global tier's
+cudaError_t launch_slab2(int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
+                         int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st);
+int64_t slab2_row_bytes(int64_t nprod, int64_t nl, bool vals);
 int64_t global_row_bytes(int64_t nprod, int64_t nl, bool vals);
 cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
                                const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st);

@@ -232,9 +232,9 @@ def test_slab_long_single_lists(ctx, oracle_mod, mode):
 
 @pytest.mark.parametrize("mode", MODES)
 def test_two_level_slab_rows(ctx, oracle_mod, mode):
-    """Rows of > 64 lists: two levels of column slabs over aligned 64-list
-    blocks (k_slab2; small shape up to 4,096 lists, large up to 16,384; short
-    last blocks at 700, 4,097 and 16,383), and the global tier at 16,385."""
+    """Rows of > 64 lists: levels of column slabs over aligned 64-list blocks
+    (k_slab2): two levels up to 4,096 lists, three beyond (short last blocks
+    and groups at 700, 4,097, 16,383 and 16,385)."""
     A, B = _lists_matrix([700, 4096, 4097, 16383, 16384, 16385], 40, 200000, seed=17)
     compare(run(ctx, A, B, mode), A, B)
 
