@@ -32,6 +32,55 @@ struct RowOut {
   int64_t* row_size;    // OUT_SYMBOLIC / OUT_CBAR: nnz of each output row
 };
 
+#ifndef BRM_OWNER_ROT
+#define BRM_OWNER_ROT 4
+#endif
+// owner[e * ostr] = l for the products e0..e1-1 of list l, one thread per
+// list. The fill starts at a different place in every list (rotation):
+// lists of equal length would otherwise hit one shared-memory bank together
+// (BRM_OWNER_ROT 0: no rotation, 1: by l mod n, 2: by l & 15 in two loops,
+// 3: by l & 15 (0 for shorter lists) in one loop, 4: by l mod n only for
+// lengths n that are multiples of 4; tuning switch). Measured (B200, same
+// box): 0 -> 1 made uniform1m_k16's tier 3 14 % faster and stencil27_64's
+// tier 4 2.8 % slower.
+__device__ __forceinline__ void owner_fill(unsigned short* owner, int ostr, int e0, int e1, int l) {
+  const unsigned short v = static_cast<unsigned short>(l);
+#if BRM_OWNER_ROT == 0
+  for (int e = e0; e < e1; ++e) owner[e * ostr] = v;
+#elif BRM_OWNER_ROT == 1
+  const int n = e1 - e0;
+  int e = n > 0 ? e0 + l % n : e0;
+  for (int i = 0; i < n; ++i) {
+    owner[e * ostr] = v;
+    if (++e == e1) e = e0;
+  }
+#elif BRM_OWNER_ROT == 3
+  const int n = e1 - e0;
+  int r = l & 15;
+  if (r >= n) r = 0;
+  int e = e0 + r;
+  for (int i = 0; i < n; ++i) {
+    owner[e * ostr] = v;
+    if (++e == e1) e = e0;
+  }
+#elif BRM_OWNER_ROT == 4
+  const int n = e1 - e0;
+  if ((n & 3) == 0 && n > 0) {  // lengths that line lists up on one bank
+    int e = e0 + l % n;
+    for (int i = 0; i < n; ++i) {
+      owner[e * ostr] = v;
+      if (++e == e1) e = e0;
+    }
+  } else {
+    for (int e = e0; e < e1; ++e) owner[e * ostr] = v;
+  }
+#else
+  const int em = min(e1, e0 + (l & 15));
+  for (int e = em; e < e1; ++e) owner[e * ostr] = v;
+  for (int e = e0; e < em; ++e) owner[e * ostr] = v;
+#endif
+}
+
 // Shared scratch of one register-tier (tier 2) group (G slots each).
 struct RegBufs {
   int* col;
@@ -538,7 +587,8 @@ struct RecBufs {
   void* rec;      // P + nl + 2 records (R::T): sentinel-terminated lists
   longlong2* lst; // per list {S index of product 0 (B index - product offset), A value bits}
   double* val;    // P value slots (products, then partial sums)
-  int* owner;     // P 16-bit entries: list of each product (multiplying phase)
+  unsigned short* owner;  // list of product e at owner[e * ostr] (multiplying phase);
+  int ostr;               // laid over val (ostr 4: product e's slot) when there are values
   int* off0;
   int* off1;
   int64_t* bst;
@@ -546,11 +596,14 @@ struct RecBufs {
   int* scan_tmp;
 };
 
-template <int G, int CAP, int LCAP, class R>
+// CUR: the per-list cursor arrays bst / av (column slabs); the record tiers
+// write the per-list table `lst` directly.
+template <int G, int CAP, int LCAP, class R, bool CUR>
 __host__ __device__ constexpr int rec_group_bytes() {
   constexpr bool VALS = R::kVals;
-  return align16((CAP + LCAP + 2) * R::kBytes) + LCAP * 16 + (VALS ? align16(CAP * 8) : 0) + align16(CAP * 2) + align16((LCAP + 2) * 4) * 2 +
-         align16(LCAP * 8) + (VALS ? align16(LCAP * 8) : 0) + (G > 32 ? align16((G / 32 + 2) * 4) : 0);
+  return align16((CAP + LCAP + 2) * R::kBytes) + LCAP * 16 + (VALS ? align16(CAP * 8) : align16(CAP * 2)) +
+         align16((LCAP + 2) * 4) * 2 + (CUR ? align16(LCAP * 8) + (VALS ? align16(LCAP * 8) : 0) : 0) +
+         (G > 32 ? align16((G / 32 + 2) * 4) : 0);
 }
 
 // merge path over the columns of two record lists (R::col_at reads only the
@@ -715,7 +768,7 @@ __device__ __forceinline__ T src_ld(const T* p) {
     return *p;
 }
 
-template <int G, int NV, class R, bool NC = true>
+template <int G, int NV, class R, bool NC = true, bool BUILD = true>
 __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView& B, int nl, int P, int* off,
                                                int* noff, const RecBufs& rb) {
   constexpr bool VALS = R::kVals;
@@ -724,16 +777,18 @@ __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView&
   {
     // owner[e] = list of product e (16-bit table: nl <= 512 in these tiers),
     // filled by one thread per list; then the products are fetched coalesced
-    unsigned short* owner = reinterpret_cast<unsigned short*>(rb.owner);
+    unsigned short* owner = rb.owner;
+    const int ostr = rb.ostr;
     for (int l = rank; l < nl; l += G) {
       const int e0 = off[l] - l, e1 = off[l + 1] - (l + 1);
-      rb.lst[l] = make_longlong2(rb.bst[l] - e0, VALS ? __double_as_longlong(rb.av[l]) : 0);  // one 16-byte load per product
-      for (int e = e0; e < e1; ++e) owner[e] = static_cast<unsigned short>(l);
+      if (BUILD)  // {product 0's source index, A value}: one 16-byte load per product below
+        rb.lst[l] = make_longlong2(rb.bst[l] - e0, VALS ? __double_as_longlong(rb.av[l]) : 0);
+      owner_fill(owner, ostr, e0, e1, l);
     }
     g.sync();
 #pragma unroll 2
     for (int e = rank; e < P; e += G) {
-      const int l = owner[e];
+      const int l = owner[e * ostr];  // (read before this thread overwrites val[e], which it may share)
       const longlong2 d = rb.lst[l];
       const int64_t src = d.x + e;
       const int c = src_ld<NC>(B.col + src);
@@ -786,18 +841,20 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
   for (int lb = 0; lb < nl; lb += G) {
     const int l = lb + rank;
     int n = 0;
+    int64_t st = 0;
+    double av = 0.0;
     if (l < nl) {
       const int k = __ldg(A.col + a0 + l);
-      const int64_t st = __ldg(B.rpt + k);
+      st = __ldg(B.rpt + k);
       n = static_cast<int>(__ldg(B.rpt + k + 1) - st);
-      rb.bst[l] = st;
-      if (VALS) rb.av[l] = __ldg(A.val + a0 + l);
+      if (VALS) av = __ldg(A.val + a0 + l);
     }
     int tot;
     const int ex = group_excl_scan<G>(g, n, tot, rb.scan_tmp);
     if (l < nl) {
       off[l] = P + ex + l;
       rec[P + ex + l + n] = R::sent();  // sentinel of list l
+      rb.lst[l] = make_longlong2(st - (P + ex), VALS ? __double_as_longlong(av) : 0);
     }
     P += tot;
   }
@@ -806,7 +863,7 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
     rec[P + nl] = R::sent();  // lone partner sentinel if nl is odd
   }
   g.sync();
-  const int T = rec_merge_lists<G, NV, R>(g, B, nl, P, off, noff, rb);
+  const int T = rec_merge_lists<G, NV, R, true, false>(g, B, nl, P, off, noff, rb);
   if (OUT != OUT_SYMBOLIC) {  // line 36
     const int64_t ob = o.base[row];
     for (int e = rank; e < T; e += G) {
@@ -852,9 +909,8 @@ __device__ __forceinline__ int hash_count_lists(const Group<G>& g, const CsrView
   while (H < P + P / 2) H <<= 1;
   H = min(H, HMAX);
   for (int e = rank; e < H; e += G) table[e] = kHashEmpty;
-  unsigned short* owner = reinterpret_cast<unsigned short*>(rb.owner);
-  for (int l = rank; l < nl; l += G)
-    for (int e = off[l], e1 = off[l + 1]; e < e1; ++e) owner[e] = static_cast<unsigned short>(l);
+  unsigned short* owner = rb.owner;  // no values in the symbolic pass: ostr == 1
+  for (int l = rank; l < nl; l += G) owner_fill(owner, 1, off[l], off[l + 1], l);
   g.sync();
   int cnt = 0;
   const volatile int* tv = table;
@@ -1242,19 +1298,19 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
     P += tot;
   }
   if (rank == 0) hb.off[nl] = P;
-  int H = 64;
-  while (H < P + P / 2) H <<= 1;
+  // H = 2P rounded up to 32 slots (load <= 1/2; a power of two would clear
+  // up to twice as many slots per row), at most the table's capacity
+  const int H = min((2 * P + 31) & ~31, hash_cap<CAP>());
   for (int e = rank; e < H; e += G) hb.table[e] = kHashEmpty;
   g.sync();
-  for (int l = rank; l < nl; l += G)
-    for (int e = hb.off[l], e1 = hb.off[l + 1]; e < e1; ++e) hb.owner[e] = static_cast<unsigned short>(l);
+  for (int l = rank; l < nl; l += G) owner_fill(hb.owner, 1, hb.off[l], hb.off[l + 1], l);
   g.sync();
   int cnt = 0;
 #pragma unroll 2
   for (int e = rank; e < P; e += G) {
     const int l = hb.owner[e];
     const int c = __ldg(B.col + hb.bst[l] + (e - hb.off[l]));
-    unsigned h = (static_cast<unsigned>(c) * 2654435761u) & (H - 1);
+    unsigned h = __umulhi(static_cast<unsigned>(c) * 2654435761u, static_cast<unsigned>(H));  // in [0, H)
     // a plain load first: most products repeat a column already inserted
     // (keys are never removed, so a non-empty slot read is final)
     const volatile int* tv = hb.table;
@@ -1268,7 +1324,7 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
         }
       }
       if (cur == c) break;
-      h = (h + 1) & (H - 1);
+      h = h + 1 == static_cast<unsigned>(H) ? 0u : h + 1;
     }
   }
   int total;

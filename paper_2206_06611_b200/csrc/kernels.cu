@@ -399,7 +399,7 @@ template <bool VALS, bool PACK, int CAP>
 using RecT = std::conditional_t<VALS, std::conditional_t<PACK, RecPacked<rec_slot_bits(CAP)>, RecWide>, RecCol>;
 
 // carve one record group's buffers (rec_group_bytes) out of shared memory
-template <int G, int CAP, int LCAP, class R>
+template <int G, int CAP, int LCAP, class R, bool CUR>
 __device__ __forceinline__ RecBufs rec_bufs(unsigned char* p) {
   auto take = [&](int n) {
     unsigned char* q = p;
@@ -409,12 +409,19 @@ __device__ __forceinline__ RecBufs rec_bufs(unsigned char* p) {
   RecBufs rb;
   rb.rec = take((CAP + LCAP + 2) * R::kBytes);
   rb.lst = reinterpret_cast<longlong2*>(take(LCAP * 16));
-  rb.val = R::kVals ? reinterpret_cast<double*>(take(CAP * 8)) : nullptr;
-  rb.owner = reinterpret_cast<int*>(take(CAP * 2));
+  if (R::kVals) {
+    rb.val = reinterpret_cast<double*>(take(CAP * 8));
+    rb.owner = reinterpret_cast<unsigned short*>(rb.val);  // laid over the value slots
+    rb.ostr = 4;
+  } else {
+    rb.val = nullptr;
+    rb.owner = reinterpret_cast<unsigned short*>(take(CAP * 2));
+    rb.ostr = 1;
+  }
   rb.off0 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
   rb.off1 = reinterpret_cast<int*>(take((LCAP + 2) * 4));
-  rb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
-  rb.av = R::kVals ? reinterpret_cast<double*>(take(LCAP * 8)) : nullptr;
+  rb.bst = CUR ? reinterpret_cast<int64_t*>(take(LCAP * 8)) : nullptr;
+  rb.av = CUR && R::kVals ? reinterpret_cast<double*>(take(LCAP * 8)) : nullptr;
   rb.scan_tmp = G > 32 ? reinterpret_cast<int*>(take((G / 32 + 2) * 4)) : nullptr;
   return rb;
 }
@@ -437,7 +444,7 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
       reg_row<G, VALS, OUT>(g, A, B, rows[r], o, rb);
   } else {
     using R = RecT<VALS, PACK, CAP>;
-    const RecBufs rb = rec_bufs<G, CAP, LCAP, R>(smem + gid * rec_group_bytes<G, CAP, LCAP, R>());
+    const RecBufs rb = rec_bufs<G, CAP, LCAP, R, false>(smem + gid * rec_group_bytes<G, CAP, LCAP, R, false>());
     for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
       rec_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, R, OUT>(g, A, B, rows[r], o, rb);
   }
@@ -452,7 +459,7 @@ __global__ void __launch_bounds__(G) k_slab(CsrView A, CsrView B, const int32_t*
   extern __shared__ __align__(16) unsigned char smem[];
   using R = RecT<VALS, PACK, CAP>;
   const Group<G> g = make_group<G>();
-  const RecBufs rb = rec_bufs<G, CAP, LCAP, R>(smem);
+  const RecBufs rb = rec_bufs<G, CAP, LCAP, R, true>(smem);
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x)
     slab_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, CAP, LCAP, R, OUT>(g, A, B, rows[r], o, rb);
 }
@@ -485,8 +492,8 @@ __global__ void __launch_bounds__(G) k_slab2(CsrView A, CsrView B, const int32_t
   extern __shared__ __align__(16) unsigned char smem[];
   using R = RecT<VALS, PACK, CAP>;
   const Group<G> g = make_group<G>();
-  const RecBufs rb = rec_bufs<G, CAP, LCAP, R>(smem);
-  int64_t* blk = reinterpret_cast<int64_t*>(smem + rec_group_bytes<G, CAP, LCAP, R>());
+  const RecBufs rb = rec_bufs<G, CAP, LCAP, R, true>(smem);
+  int64_t* blk = reinterpret_cast<int64_t*>(smem + rec_group_bytes<G, CAP, LCAP, R, true>());
   const int64_t row = rows[blockIdx.x];
   const int64_t P = ws_off[2 * blockIdx.x + 1];
   const Slab2Layout L = slab2_layout(P, A.rpt[row + 1] - A.rpt[row], VALS, LCAP);
@@ -825,7 +832,7 @@ template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT, bool PACK>
 static cudaError_t launch_tier_pk(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
                                   cudaStream_t st) {
   constexpr int per_group =
-      CAP <= 32 ? reg_group_bytes<G, VALS>() : rec_group_bytes<G, CAP, LCAP, RecT<VALS, PACK, CAP>>();
+      CAP <= 32 ? reg_group_bytes<G, VALS>() : rec_group_bytes<G, CAP, LCAP, RecT<VALS, PACK, CAP>, false>();
   constexpr int smem = per_group * GPC;
   // registers hold <= NV chunk outputs; NV = 31 (G = 256, CAP 7168) miscompiled
   // (wrong values, no spills reported), so tiers keep NV <= 29
@@ -863,7 +870,7 @@ static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, int64_t b_c
 template <int G, int CAP, int LCAP, bool VALS, int OUT, bool PACK>
 static cudaError_t launch_slab_pk(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
                                   cudaStream_t st) {
-  constexpr int smem = rec_group_bytes<G, CAP, LCAP, RecT<VALS, PACK, CAP>>();
+  constexpr int smem = rec_group_bytes<G, CAP, LCAP, RecT<VALS, PACK, CAP>, true>();
   static_assert(smem <= 232448, "slab shared memory exceeds 227 KB");
   static_assert((((CAP + LCAP + 1 + G - 1) / G) | 1) <= 29, "slab NV must stay <= 29");
   auto kern = k_slab<G, CAP, LCAP, VALS, OUT, PACK>;
@@ -893,7 +900,7 @@ static cudaError_t launch_slab_t(const CsrView& A, const CsrView& B, int64_t b_c
 template <int G, int CAP, int LCAP, bool VALS, int OUT, bool PACK>
 static cudaError_t launch_slab2_pk(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
                                    const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st) {
-  constexpr int smem = rec_group_bytes<G, CAP, LCAP, RecT<VALS, PACK, CAP>>() + (LCAP + 1) * 8;
+  constexpr int smem = rec_group_bytes<G, CAP, LCAP, RecT<VALS, PACK, CAP>, true>() + (LCAP + 1) * 8;
   static_assert(smem <= 232448, "slab shared memory exceeds 227 KB");
   auto kern = k_slab2<G, CAP, LCAP, VALS, OUT, PACK>;
   static bool init = false;
