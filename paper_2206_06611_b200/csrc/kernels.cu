@@ -687,6 +687,9 @@ cudaError_t launch_scatter_rows(const int32_t* rows, int n, const int64_t* rpt2,
 // found by a shuffle search over the window's row starts, its source is
 // nprod_off[row] + (e - crpt[row]). Stores are coalesced.
 constexpr int64_t kCompactChunk = 4096;
+#ifndef BRM_COMPACT_U
+#define BRM_COMPACT_U 4
+#endif
 
 __global__ void __launch_bounds__(256) k_compact(int64_t M, const int64_t* __restrict__ nprod_off,
                                                  const int64_t* __restrict__ crpt,
@@ -714,7 +717,7 @@ __global__ void __launch_bounds__(256) k_compact(int64_t M, const int64_t* __res
       const int64_t cs = crpt[r];
       const int64_t delta = (r < M ? nprod_off[r] : 0) - cs;  // source - destination
       const int64_t wend = min(e1, crpt[min(r0 + 32, M)]);
-      constexpr int U = 4;  // four 32-element batches in flight
+      constexpr int U = BRM_COMPACT_U;  // 32-element batches in flight per warp
       for (int64_t eb = eb0; eb < wend; eb += 32 * U) {
         int32_t cv[U];
         double vv[U];
