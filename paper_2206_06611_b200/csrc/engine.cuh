@@ -905,9 +905,11 @@ __device__ __forceinline__ int hash_count_lists(const Group<G>& g, const CsrView
                                                 const RecBufs& rb) {
   int* table = static_cast<int*>(rb.rec);
   const int rank = g.rank;
-  int H = 64;
-  while (H < P + P / 2) H <<= 1;
-  H = min(H, HMAX);
+  int H = 64, hb = 6;
+  while (H < P + P / 2 && H < HMAX) {
+    H <<= 1;
+    ++hb;
+  }
   for (int e = rank; e < H; e += G) table[e] = kHashEmpty;
   unsigned short* owner = rb.owner;  // no values in the symbolic pass: ostr == 1
   for (int l = rank; l < nl; l += G) owner_fill(owner, 1, off[l], off[l + 1], l);
@@ -917,7 +919,7 @@ __device__ __forceinline__ int hash_count_lists(const Group<G>& g, const CsrView
   for (int e = rank; e < P; e += G) {
     const int l = owner[e];
     const int c = src_ld<NC>(S.col + rb.bst[l] + (e - off[l]));
-    unsigned h = (static_cast<unsigned>(c) * 2654435761u) & (H - 1);
+    unsigned h = (static_cast<unsigned>(c) * 2654435761u) >> (32 - hb);  // the product's high bits
     while (true) {
       int cur = tv[h];
       if (cur == kHashEmpty) {
