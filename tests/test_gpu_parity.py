@@ -132,9 +132,9 @@ def test_record_packing_boundary(ctx, oracle_mod, mode, tier, slot_bits, list_le
 
 
 @pytest.mark.parametrize("mode", MODES)
-def test_misaligned_b_uses_cp_async_path(ctx, oracle_mod, mode):
-    """B arrays not 16-byte aligned: TMA windows are illegal, the kernels must
-    stage with cp.async instead and give the same bits."""
+def test_misaligned_b_arrays(ctx, oracle_mod, mode):
+    """B's col/val arrays at addresses that are not 16-byte aligned (views one
+    element into larger buffers): the gathers must give the same bits."""
     import torch
     from paper_2206_06611_b200 import TorchCsr
     A = uniform_random(3000, 3000, 13, seed=12)
