@@ -9,13 +9,17 @@
 // reg_row   (tier 2, P <= 32): one warp; lane e holds product e; each round
 //   merges list pairs in registers (shuffle rank search = warp-shuffle merge
 //   path, ballot arithmetic for positions, a 32-slot shared exchange).
-// rec_row   (tiers 3-6): a warp or CTA per row; rounds move 8-byte records
-//   {col, value slot} through one shared buffer, values stay in place and
-//   duplicates accumulate into the left slot; each round is one pass of G
-//   merge-path chunks of odd length VT; outputs wait in registers until the
-//   group scan gives their compacted positions.
-// chunk_row (tier 7): the same chunk partition over column/value ping-pong
-//   buffers in a global workspace, one 512-thread CTA per heavy row.
+// rec_row   (tiers 3-6): a warp or CTA per row; rounds move records
+//   {col, value slot} (32-bit packed or 8-byte) through one shared buffer,
+//   values stay in place and duplicates accumulate into the left slot; each
+//   round is one pass of G merge-path chunks of odd length VT; outputs wait
+//   in registers until the group scan gives their compacted positions.
+// slab_row / slab2_row (tier 7): heavy rows merged in column slabs with the
+//   record machinery (rec_merge_lists), in one level (<= 64 lists) or two or
+//   three levels over aligned 64-list blocks; the symbolic pass counts
+//   slabs in a shared hash table.
+// chunk_row (tier 7 fallback): the chunk partition over column/value
+//   ping-pong buffers in a global workspace, one 1024-thread CTA per row.
 #pragma once
 #include "brm_internal.cuh"
 

@@ -6,10 +6,13 @@
 //   k_bin_scatter    row binning by n_prod / list count into tiers.
 //   k_tiny           tier 1: one thread per row runs Algorithm 1 literally.
 //   k_tier<...>      tier 2: register BRMerge, one warp per row; tiers 3-6:
-//                    record BRMerge (warp / 64 / 128 / 256 threads per row).
+//                    record BRMerge (warp / warp / 128 / 256 threads per row).
 //   k_hash_symbolic  BRMerge-Precise step 3 on tiers 3-6: per-row shared
 //                    hash table counts the distinct columns.
-//   k_global_tier    tier 7: the heaviest rows, ping-pong buffers in a global
+//   k_slab           tier 7 rows of <= 64 lists: column slabs, CTA per row.
+//   k_slab2          tier 7 rows of 65-262,144 lists: two or three levels of
+//                    column slabs over aligned 64-list blocks.
+//   k_global_tier    tier 7 fallback: ping-pong buffers in a global
 //                    workspace, one 1024-thread CTA per row.
 //   k_split_a1/a2,   tier 7 heavy-row decomposition into aligned 32-list
 //   k_scatter_rows   blocks (sub-trees of Algorithm 1's tree).
