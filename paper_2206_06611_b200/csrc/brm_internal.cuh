@@ -84,9 +84,13 @@ struct TierBounds {
 // in column slabs with shape BRM_SLAB0 (G, CAP, LCAP); rows of up to
 // kSlab2Lists lists in two or three levels of slabs (same shape) over
 // aligned kSlab2Block-list blocks.
-#ifndef BRM_SLAB0
-#define BRM_SLAB0 128, 2048, 64
+#ifndef BRM_S0_G
+#define BRM_S0_G 128
 #endif
+#ifndef BRM_S0_CAP
+#define BRM_S0_CAP 2048
+#endif
+#define BRM_SLAB0 BRM_S0_G, BRM_S0_CAP, 64
 constexpr int kSlabLists = 64;                                    // = BRM_SLAB0's LCAP
 constexpr int kSlab2Block = 64;
 constexpr int kSlab2Lists = kSlab2Block * kSlab2Block * kSlabLists;  // three levels
