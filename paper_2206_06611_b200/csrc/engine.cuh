@@ -633,6 +633,9 @@ __device__ __forceinline__ int merge_path_rec(const typename R::T* a, int la, co
 // in registers and overwrite `rec` compacted once the group has read it.
 // vote: the duplicate combine is skipped (one warp vote) when no lane of the
 // warp has a duplicate -- cheaper for rounds with few repeated columns.
+#ifndef BRM_PLAIN_DUP
+#define BRM_PLAIN_DUP 0  // 1: plain combine in every record round (tuning switch)
+#endif
 #ifndef BRM_VOTE_MODE
 #define BRM_VOTE_MODE 0
 #endif
@@ -645,7 +648,11 @@ __device__ __forceinline__ int merge_path_rec(const typename R::T* a, int la, co
 #else
 #define BRM_ROUND_INLINE __forceinline__
 #endif
-template <int G, int NV, class R, int VOTE>  // VOTE: -1 run time (vote), 0 never, 1 always
+// PLAIN: the duplicate combine written as plain C++ (the compiler branches
+// around it) instead of predicated loads: faster on rows with few
+// duplicates, slower on rows with many (measured: uniform1m_k16's tier 3
+// -9 %, stencil27_64's tier 4 +3.4 %); the record tiers take it for tier 3.
+template <int G, int NV, class R, int VOTE, bool PLAIN = false>  // VOTE: -1 run time (vote), 0 never, 1 always
 __device__ BRM_ROUND_INLINE int rec_round(const Group<G>& g, typename R::T* rec, double* val, const int* off,
                                           int* noff, int nl, int* scan_tmp, bool vote) {
   constexpr bool VALS = R::kVals;
@@ -716,10 +723,14 @@ __device__ BRM_ROUND_INLINE int rec_round(const Group<G>& g, typename R::T* rec,
       const bool dup = ta && tb && !R::is_sent(ra);
       const bool use_vote = VOTE < 0 ? vote : VOTE > 0;
       if (!use_vote || __any_sync(G < 32 ? g.mask : 0xffffffffu, dup)) {  // a uniform branch
-        double x = 0.0, y = 0.0;
-        lds_if(dup, valb + 8u * R::slot(ra), x);
-        lds_if(dup, valb + 8u * R::slot(rb), y);
-        if (dup) val[R::slot(ra)] = __dadd_rn(x, y);
+        if constexpr (PLAIN || BRM_PLAIN_DUP) {
+          if (dup) val[R::slot(ra)] = __dadd_rn(val[R::slot(ra)], val[R::slot(rb)]);
+        } else {
+          double x = 0.0, y = 0.0;
+          lds_if(dup, valb + 8u * R::slot(ra), x);
+          lds_if(dup, valb + 8u * R::slot(rb), y);
+          if (dup) val[R::slot(ra)] = __dadd_rn(x, y);
+        }
       }
     }
     cnt += act;
@@ -772,7 +783,7 @@ __device__ __forceinline__ T src_ld(const T* p) {
     return *p;
 }
 
-template <int G, int NV, class R, bool NC = true, bool BUILD = true>
+template <int G, int NV, class R, bool NC = true, bool BUILD = true, bool PLAIN = false>
 __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView& B, int nl, int P, int* off,
                                                int* noff, const RecBufs& rb) {
   constexpr bool VALS = R::kVals;
@@ -810,7 +821,7 @@ __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView&
   while (cur > 1) {
     const int npos = off[cur] + (cur & 1);
 #if BRM_VOTE_MODE == 0
-    end = rec_round<G, NV, R, 0>(g, rec, rb.val, off, noff, cur, rb.scan_tmp, false);
+    end = rec_round<G, NV, R, 0, PLAIN>(g, rec, rb.val, off, noff, cur, rb.scan_tmp, false);
 #elif BRM_VOTE_MODE == 1
     end = rec_round<G, NV, R, -1>(g, rec, rb.val, off, noff, cur, rb.scan_tmp, vote);
 #else
@@ -829,7 +840,7 @@ __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView&
   return end - 1;  // list 0 = records [0, end - 1), then its sentinel
 }
 
-template <int G, int NV, class R, int OUT>
+template <int G, int NV, class R, int OUT, bool PLAIN = false>
 __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
                                         const RowOut& o, const RecBufs& rb) {
   constexpr bool VALS = R::kVals;
@@ -867,7 +878,7 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
     rec[P + nl] = R::sent();  // lone partner sentinel if nl is odd
   }
   g.sync();
-  const int T = rec_merge_lists<G, NV, R, true, false>(g, B, nl, P, off, noff, rb);
+  const int T = rec_merge_lists<G, NV, R, true, false, PLAIN>(g, B, nl, P, off, noff, rb);
   if (OUT != OUT_SYMBOLIC) {  // line 36
     const int64_t ob = o.base[row];
     for (int e = rank; e < T; e += G) {

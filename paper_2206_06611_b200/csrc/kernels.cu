@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
     using R = RecT<VALS, PACK, CAP>;
     const RecBufs rb = rec_bufs<G, CAP, LCAP, R, false>(smem + gid * rec_group_bytes<G, CAP, LCAP, R, false>());
     for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
-      rec_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, R, OUT>(g, A, B, rows[r], o, rb);
+      rec_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, R, OUT, (CAP <= 256)>(g, A, B, rows[r], o, rb);  // tier 3: plain combine
   }
 }
 
