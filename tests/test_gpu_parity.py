@@ -469,3 +469,15 @@ def test_host_form_large(ctx, oracle_mod, mode):
     Bh = TorchCsr.from_csr(B, pin=True)
     rows, cols, rpt, col, val = ctx.brmerge_spgemm_host(Ah, Bh, mode)
     compare((rpt.copy(), col.copy(), val.copy()), A, B)
+
+
+def test_alg1_pairing_order_hand_derived(ctx):
+    """The hand-derived Algorithm-1 trees of test_oracle_pins
+    straight against the CUDA path, no oracle in between."""
+    from test_oracle_pins import _TREE_CASES, _one_column_row
+    for vals, present, tree in _TREE_CASES:
+        A, B = _one_column_row(vals, present)
+        for mode in MODES:
+            rpt, col, val = run(ctx, A, B, mode)
+            assert rpt.tolist() == [0, 1] and col.tolist() == [0]
+            assert val[0] == tree(vals), (vals, mode, val[0], tree(vals))

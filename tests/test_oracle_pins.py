@@ -265,3 +265,145 @@ def test_table2_compression_ratios(oracle_mod):
     for r in rows:
         nprod, nnz, cr = int(r[6]), int(r[7]), float(r[8])
         assert abs(oracle_mod.compression_ratio(nprod, nnz) - cr) <= 0.005 + 1e-12, r[1]
+
+
+# ---------------------------------------------------------------------------
+# Pin of Algorithm 1's pairing ORDER (lines 21-35): each
+# round consumes the lists two at a time from the front of src_buffer --
+# (0,1), (2,3), ... -- and copies an odd trailing list (lines 28-29); the
+# next round pairs the results the same way. The value of a column is
+# therefore the tree sum below, written out by hand per case. fp64 addition
+# is not associative on these values (1e16 + 1 == 1e16), so a wrong pairing
+# -- k-order summation, (0,2)(1,3), the odd list copied first, pairing from
+# the back -- changes the bits. Every list is one B row with a single entry
+# in column 0, scaled by A_ik = 1.0 (exact), so the products are the values.
+# ---------------------------------------------------------------------------
+def _one_column_row(vals, present=None):
+    """One row of A with len(vals) nonzeros (all 1.0) over a B whose row k
+    holds vals[k] in column 0 (or is empty when present[k] is False)."""
+    k = len(vals)
+    present = [True] * k if present is None else present
+    lens = np.array([1 if p else 0 for p in present], np.int64)
+    rpt = np.zeros(k + 1, np.int64)
+    np.cumsum(lens, out=rpt[1:])
+    bval = np.array([v for v, p in zip(vals, present) if p], np.float64)
+    B = Csr(k, 1, rpt, np.zeros(bval.size, np.int32), bval)
+    A = Csr(1, k, np.array([0, k], np.int64), np.arange(k, dtype=np.int32), np.ones(k))
+    return A, B
+
+
+_BIG = 1e16  # spacing of fp64 at 1e16 is 2: 1e16 + 1 rounds back to 1e16
+
+# (values, present, the Algorithm-1 tree written out by hand)
+_TREE_CASES = [
+    # 3 lists: round 1 (0,1), 2 copied; round 2 (01, 2)
+    ([_BIG, 1.0, -_BIG], None, lambda v: (v[0] + v[1]) + v[2]),
+    ([1.0, -_BIG, _BIG], None, lambda v: (v[0] + v[1]) + v[2]),
+    # 4 lists: (0,1), (2,3); then (01, 23)
+    ([-_BIG, 1.0, _BIG, 1.0], None, lambda v: (v[0] + v[1]) + (v[2] + v[3])),
+    ([1.0, 1.0, _BIG, -_BIG], None, lambda v: (v[0] + v[1]) + (v[2] + v[3])),
+    # 5 lists: (0,1), (2,3), 4 copied; (01, 23), 4 copied; (0123, 4)
+    ([1.0, _BIG, -_BIG, 1.0, 1.0], None, lambda v: ((v[0] + v[1]) + (v[2] + v[3])) + v[4]),
+    ([_BIG, -_BIG, 1.0, 1.0, -_BIG], None, lambda v: ((v[0] + v[1]) + (v[2] + v[3])) + v[4]),
+    # 6 lists (Fig. 2's shape): (0,1),(2,3),(4,5); (01,23), 45 copied; (0123, 45)
+    ([1.0, _BIG, 1.0, -_BIG, 1.0, 1.0], None,
+     lambda v: ((v[0] + v[1]) + (v[2] + v[3])) + (v[4] + v[5])),
+    # 7 lists: (0,1),(2,3),(4,5), 6 copied; (01,23),(45,6); (0123, 456)
+    ([_BIG, 1.0, 1.0, 1.0, -_BIG, 1.0, 1.0], None,
+     lambda v: ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + v[6])),
+    # an empty list keeps its place in the tree (Alg. 1 line 14 records its
+    # offset): lists 1 and 4 lack the column, so pairs (0,1) and (4,5) pass
+    # one value through; the tree is (v0 + (v2 + v3)) + v5
+    ([1.0, 0.0, _BIG, 1.0, 0.0, -_BIG], [True, False, True, True, False, True],
+     lambda v: (v[0] + (v[2] + v[3])) + v[5]),
+    ([-_BIG, 0.0, 1.0, _BIG, 0.0, 1.0], [True, False, True, True, False, True],
+     lambda v: (v[0] + (v[2] + v[3])) + v[5]),
+]
+
+
+def _alt_orders(n):
+    """Plausible wrong orders (each must be refuted by some case)."""
+    def seq(v, pres):
+        s = None
+        for x, p in zip(v, pres):
+            if p:
+                s = x if s is None else s + x
+        return s
+
+    def rounds(v, pres, pair):
+        lists = [x if p else None for x, p in zip(v, pres)]
+        while len(lists) > 1:
+            lists = pair(lists)
+        return lists[0]
+
+    def add(a, b):
+        return a if b is None else (b if a is None else a + b)
+
+    def odd_first(ls):  # odd list copied FIRST, then (1,2), (3,4), ...
+        if len(ls) % 2:
+            return [ls[0]] + [add(ls[i], ls[i + 1]) for i in range(1, len(ls), 2)]
+        return [add(ls[i], ls[i + 1]) for i in range(0, len(ls), 2)]
+
+    def from_back(ls):  # pairs taken from the back: (n-2, n-1), ...
+        r = [add(ls[i - 1], ls[i]) for i in range(len(ls) - 1, 0, -2)]
+        if len(ls) % 2:
+            r.append(ls[0])
+        return r[::-1]
+
+    def strided(ls):  # (0, h), (1, h+1), ... with h = ceil(n/2)
+        h = (len(ls) + 1) // 2
+        return [add(ls[i], ls[i + h]) if i + h < len(ls) else ls[i] for i in range(h)]
+
+    return {"k-order": seq,
+            "odd list copied first": lambda v, p: rounds(v, p, odd_first),
+            "pairs from the back": lambda v, p: rounds(v, p, from_back),
+            "strided pairs (i, i+n/2)": lambda v, p: rounds(v, p, strided)}
+
+
+def test_alg1_pairing_order_pinned(oracle_mod):
+    """Algorithm 1's tree order, bit for bit, on hand-derived non-associative
+    cases; each plausible wrong order is refuted by at
+    least one case, so the pin discriminates."""
+    refuted = {name: False for name in _alt_orders(0)}
+    for vals, present, tree in _TREE_CASES:
+        pres = [True] * len(vals) if present is None else present
+        expect = tree(vals)
+        A, B = _one_column_row(vals, present)
+        C, rounds = oracle_mod.spgemm_brmerge(A, B)
+        assert C.nnz == 1 and C.col[0] == 0
+        assert C.val[0] == expect and np.signbit(C.val[0]) == np.signbit(expect), (vals, C.val[0], expect)
+        assert rounds[0] == math.ceil(math.log2(len(vals)))
+        for name, alt in _alt_orders(len(vals)).items():
+            if alt(vals, pres) != expect:
+                refuted[name] = True
+        # Gustavson (Eq. (2)) sums in k order: it must equal the k-order sum
+        G = oracle_mod.spgemm_gustavson(A, B)
+        assert G.val[0] == _alt_orders(0)["k-order"](vals, pres)
+    assert all(refuted.values()), refuted
+
+
+def test_alg1_pairing_order_multi_column(oracle_mod):
+    """The same tree per column when columns differ across lists: 5 lists over
+    2 columns; column 0 is in lists 0, 1, 3, 4 and column 1 in lists 1-4.
+    Hand-derived: col 0 = ((v0 + v1) + v3) + v4 per Alg. 1 (list 2 lacks it:
+    pair (2,3) passes v3 through), col 1 = (w1 + (w2 + w3)) + w4 (list 0
+    lacks it: pair (0,1) passes w1 through). (fp64 addition commutes, so
+    left + right vs right + left is not observable; grouping is.)"""
+    v = [1.0, _BIG, None, -_BIG, 1.0]        # column 0 entries of lists 0..4
+    w = [None, 1.0, 1.0, _BIG, -_BIG]        # column 1 entries
+    rpt, col, val = [0], [], []
+    for k in range(5):
+        for c, x in ((0, v[k]), (1, w[k])):
+            if x is not None:
+                col.append(c)
+                val.append(x)
+        rpt.append(len(col))
+    B = Csr(5, 2, np.array(rpt, np.int64), np.array(col, np.int32), np.array(val))
+    A = Csr(1, 5, np.array([0, 5], np.int64), np.arange(5, dtype=np.int32), np.ones(5))
+    C, _ = oracle_mod.spgemm_brmerge(A, B)
+    e0 = ((v[0] + v[1]) + v[3]) + v[4]
+    e1 = (w[1] + (w[2] + w[3])) + w[4]
+    assert list(C.col) == [0, 1]
+    assert C.val[0] == e0 and C.val[1] == e1
+    # column 1's tree differs from its k-order sum, so the case discriminates
+    assert e1 != ((w[1] + w[2]) + w[3]) + w[4]
