@@ -48,6 +48,10 @@ CONFIGS = {
     "uniform2k_k8": 0, "stencil27_64": 1, "uniform1m_k16": 2, "rmat20_ef16": 3, "amg_lap2048_agg2x2": 4,
 }
 DEFAULT_CONFIG = "stencil27_64"
+# stencil / uniform grow with the rank count (weak scaling); rmat20 and the AMG
+# product are the same problem at every N (strong scaling)
+SCALING = {"uniform2k_k8": "weak", "stencil27_64": "weak", "uniform1m_k16": "weak",
+           "rmat20_ef16": "strong", "amg_lap2048_agg2x2": "strong"}
 
 
 def build_workload(name: str, world: int):
@@ -214,7 +218,7 @@ def run_reference(args):
     v = 2.0 * sub_np / sec / 1e9
     line = {"impl": "reference", "metric": METRIC,
             "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": SCALING[args.config], "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "desc": desc, "mode": "oracle (Eq. (2), sorted-map Gustavson)",
                        "rows_sampled": int(rows.size)},
@@ -412,7 +416,7 @@ def main():
         line = {
             "metric": METRIC,
             "value": gflops, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": SCALING[args.config], "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "desc": desc, "mode": args.mode, "rows": A.rows,
                        "nnz_a": A.nnz, "nprod": nprod_all, "nnz_c": nnz_all,

@@ -49,6 +49,7 @@ struct brm_context {
   std::vector<int64_t> heavy;  // (n_prod, nl) per global-tier row
   brm_stats_t stats{};
   cudaEvent_t ev[32] = {};
+  cudaEvent_t handoff = nullptr;  // orders a stream switch after the old stream's work
   unsigned ev_mask = 0;  // events recorded since the last structure call
   int64_t launches = 0;  // kernels launched since the last structure call
   brm_context* sub = nullptr;  // heavy-row decomposition runs its sub-products here
@@ -598,6 +599,7 @@ brm_status_t brm_create(brm_context_t** out, int device, void* stream) {
   ctx->stream = static_cast<cudaStream_t>(stream);
   DeviceGuard g(device);
   for (auto& e : ctx->ev) cudaEventCreate(&e);
+  cudaEventCreateWithFlags(&ctx->handoff, cudaEventDisableTiming);
   *out = ctx;
   return BRM_OK;
 }
@@ -618,6 +620,7 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
       if (b->p) cudaFreeHost(b->p);
     for (auto& e : ctx->ev)
       if (e) cudaEventDestroy(e);
+    if (ctx->handoff) cudaEventDestroy(ctx->handoff);
   }
   if (ctx->sub) brm_destroy(ctx->sub);
   delete ctx;
@@ -626,7 +629,15 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
 
 brm_status_t brm_set_stream(brm_context_t* ctx, void* stream) {
   if (!ctx) return BRM_ERR_INVALID;
-  ctx->stream = static_cast<cudaStream_t>(stream);
+  cudaStream_t ns = static_cast<cudaStream_t>(stream);
+  if (ns == ctx->stream) return BRM_OK;
+  // the workspace (n_prod offsets, bins, C_bar, heavy-row plans) may still be
+  // read by kernels enqueued on the old stream: the new stream waits for them
+  DeviceGuard g(ctx->device);
+  CK(cudaEventRecord(ctx->handoff, ctx->stream), "record stream hand-off");
+  CK(cudaStreamWaitEvent(ns, ctx->handoff, 0), "wait for stream hand-off");
+  ctx->stream = ns;
+  if (ctx->sub) ctx->sub->stream = ns;
   return BRM_OK;
 }
 
@@ -683,7 +694,9 @@ brm_status_t brmerge_spgemm(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
                             brm_csr_t* C) {
   if (!ctx) return BRM_ERR_INVALID;
   if (!C) return fail(ctx, BRM_ERR_INVALID, "C is null");
-  if (!A) return fail(ctx, BRM_ERR_INVALID, "A is null");
+  brm_status_t s0;
+  if ((s0 = check_csr(ctx, A, "A")) != BRM_OK) return s0;  // before sizing C.rpt by A->rows
+  if ((s0 = check_csr(ctx, B, "B")) != BRM_OK) return s0;
   DeviceGuard g(ctx->device);
   memset(C, 0, sizeof(*C));
   int64_t* rpt = nullptr;

@@ -59,12 +59,22 @@ struct TierBounds {
 #ifndef BRM_T6_G
 #define BRM_T6_G 256
 #endif
-#define BRM_TIER1 8, 8, 8, 32
-#define BRM_TIER2 32, 32, 32, BRM_T2_GPC
-#define BRM_TIER3 BRM_T3_G, 256, 64, BRM_T3_GPC
-#define BRM_TIER4 BRM_T4_G, 768, 64, BRM_T4_GPC
-#define BRM_TIER5 BRM_T5_G, 3072, 256, 1
-#define BRM_TIER6 BRM_T6_G, 6656, 512, 1
+// PLAIN (5th field): the record round's duplicate combine as plain code the
+// compiler branches around (faster on rows with few duplicates) instead of
+// predicated loads. Measured on B200: tier 3 on uniform1m_k16 -9 % with it;
+// tier 4 on stencil27_64 +3.4 %, so only tier 3 takes it by default.
+#ifndef BRM_T3_PLAIN
+#define BRM_T3_PLAIN true
+#endif
+#ifndef BRM_T4_PLAIN
+#define BRM_T4_PLAIN false
+#endif
+#define BRM_TIER1 8, 8, 8, 32, false
+#define BRM_TIER2 32, 32, 32, BRM_T2_GPC, false
+#define BRM_TIER3 BRM_T3_G, 256, 64, BRM_T3_GPC, BRM_T3_PLAIN
+#define BRM_TIER4 BRM_T4_G, 768, 64, BRM_T4_GPC, BRM_T4_PLAIN
+#define BRM_TIER5 BRM_T5_G, 3072, 256, 1, false
+#define BRM_TIER6 BRM_T6_G, 6656, 512, 1, false
 // PRECISE symbolic (hash counting) launch shapes of tiers 3-6, tuned apart
 // from the merges: (G, CAP, LCAP, GPC)
 #ifndef BRM_H3_GPC

@@ -429,7 +429,7 @@ __device__ __forceinline__ RecBufs rec_bufs(unsigned char* p) {
   return rb;
 }
 
-template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT, bool PACK>
+template <int G, int CAP, int LCAP, int GPC, bool PLAIN, bool VALS, int OUT, bool PACK>
 __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const int32_t* __restrict__ rows,
                                                  int64_t nrows, RowOut o) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
     using R = RecT<VALS, PACK, CAP>;
     const RecBufs rb = rec_bufs<G, CAP, LCAP, R, false>(smem + gid * rec_group_bytes<G, CAP, LCAP, R, false>());
     for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
-      rec_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, R, OUT, (CAP <= 256)>(g, A, B, rows[r], o, rb);  // tier 3: plain combine
+      rec_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, R, OUT, PLAIN>(g, A, B, rows[r], o, rb);
   }
 }
 
@@ -791,15 +791,42 @@ __global__ void k_row_nprod(CsrView A, const int64_t* __restrict__ brpt, int64_t
 // ---------------------------------------------------------------------------
 // Host-side launchers.
 // ---------------------------------------------------------------------------
-static int g_num_sms = 0;
+// Launch setup is per DEVICE (the shared-memory attribute and the occupancy
+// apply to the current device only): cached per device ordinal.
+constexpr int kMaxDevices = 64;
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 || dev >= kMaxDevices ? 0 : dev;
+}
 static int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  static int n[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!n[dev]) {
+    cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (n[dev] <= 0) n[dev] = 148;
   }
-  return g_num_sms;
+  return n[dev];
+}
+
+// One kernel instantiation's setup on the current device: raise its dynamic
+// shared-memory limit to `smem` and return its resident CTAs per SM.
+struct LaunchSetup {
+  int per_sm[kMaxDevices] = {};
+};
+template <class K>
+static cudaError_t kernel_setup(LaunchSetup& ls, K kern, int threads, int smem, int& per_sm) {
+  const int dev = current_device();
+  if (!ls.per_sm[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int n = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem);
+    if (e != cudaSuccess) return e;
+    ls.per_sm[dev] = n < 1 ? 1 : n;
+  }
+  per_sm = ls.per_sm[dev];
+  return cudaSuccess;
 }
 
 int64_t scan_tiles(int64_t n) { return (n + kScanTile - 1) / kScanTile; }
@@ -834,7 +861,7 @@ cudaError_t launch_heavy_info(const CsrView& A, const int64_t* nprod_off, const 
   return cudaGetLastError();
 }
 
-template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT, bool PACK>
+template <int G, int CAP, int LCAP, int GPC, bool PLAIN, bool VALS, int OUT, bool PACK>
 static cudaError_t launch_tier_pk(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
                                   cudaStream_t st) {
   constexpr int per_group =
@@ -845,16 +872,10 @@ static cudaError_t launch_tier_pk(const CsrView& A, const CsrView& B, const int3
   static_assert(CAP <= 32 || (((CAP + LCAP + 1 + G - 1) / G) | 1) <= 29, "chunk tier NV must stay <= 29");
   static_assert(smem <= 232448, "tier shared memory exceeds 227 KB");
   static_assert(G <= 32 || GPC == 1, "a group of more than 32 threads is the whole CTA");
-  auto kern = k_tier<G, CAP, LCAP, GPC, VALS, OUT, PACK>;
-  // one process drives one device, so per-instantiation caching is safe
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G * GPC, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-  }
+  auto kern = k_tier<G, CAP, LCAP, GPC, PLAIN, VALS, OUT, PACK>;
+  static LaunchSetup ls;
+  int per_sm = 0;
+  if (cudaError_t e = kernel_setup(ls, kern, G * GPC, smem, per_sm); e != cudaSuccess) return e;
   const int64_t want = (n + GPC - 1) / GPC;
   const int64_t cap = (int64_t)per_sm * num_sms();
   const unsigned grid = (unsigned)(want < cap ? want : cap);
@@ -863,14 +884,14 @@ static cudaError_t launch_tier_pk(const CsrView& A, const CsrView& B, const int3
 }
 
 // numeric record tiers take packed records when B's columns fit beside the slot
-template <int G, int CAP, int LCAP, int GPC, bool VALS, int OUT>
+template <int G, int CAP, int LCAP, int GPC, bool PLAIN, bool VALS, int OUT>
 static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows, int64_t n,
                                  const RowOut& o, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if constexpr (VALS && CAP > 32) {
-    if (rec_pack_ok(CAP, b_cols)) return launch_tier_pk<G, CAP, LCAP, GPC, VALS, OUT, true>(A, B, rows, n, o, st);
+    if (rec_pack_ok(CAP, b_cols)) return launch_tier_pk<G, CAP, LCAP, GPC, PLAIN, VALS, OUT, true>(A, B, rows, n, o, st);
   }
-  return launch_tier_pk<G, CAP, LCAP, GPC, VALS, OUT, false>(A, B, rows, n, o, st);
+  return launch_tier_pk<G, CAP, LCAP, GPC, PLAIN, VALS, OUT, false>(A, B, rows, n, o, st);
 }
 
 template <int G, int CAP, int LCAP, bool VALS, int OUT, bool PACK>
@@ -880,14 +901,9 @@ static cudaError_t launch_slab_pk(const CsrView& A, const CsrView& B, const int3
   static_assert(smem <= 232448, "slab shared memory exceeds 227 KB");
   static_assert((((CAP + LCAP + 1 + G - 1) / G) | 1) <= 29, "slab NV must stay <= 29");
   auto kern = k_slab<G, CAP, LCAP, VALS, OUT, PACK>;
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-  }
+  static LaunchSetup ls;
+  int per_sm = 0;
+  if (cudaError_t e = kernel_setup(ls, kern, G, smem, per_sm); e != cudaSuccess) return e;
   const int64_t cap = (int64_t)per_sm * num_sms();
   kern<<<(unsigned)(n < cap ? n : cap), G, smem, st>>>(A, B, rows, n, o);
   return cudaGetLastError();
@@ -909,12 +925,9 @@ static cudaError_t launch_slab2_pk(const CsrView& A, const CsrView& B, const int
   constexpr int smem = rec_group_bytes<G, CAP, LCAP, RecT<VALS, PACK, CAP>, true>() + (LCAP + 1) * 8;
   static_assert(smem <= 232448, "slab shared memory exceeds 227 KB");
   auto kern = k_slab2<G, CAP, LCAP, VALS, OUT, PACK>;
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
+  static LaunchSetup ls;
+  int per_sm = 0;
+  if (cudaError_t e = kernel_setup(ls, kern, G, smem, per_sm); e != cudaSuccess) return e;
   kern<<<(unsigned)n, G, smem, st>>>(A, B, rows, ws_off, ws, o);
   return cudaGetLastError();
 }
@@ -962,14 +975,9 @@ static cudaError_t launch_tiny(const CsrView& A, const CsrView& B, const int32_t
   if (n <= 0) return cudaSuccess;
   constexpr int smem = tiny_block_bytes<kTinyNT, VALS>();
   auto kern = k_tiny<VALS, OUT>;
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTinyNT, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-  }
+  static LaunchSetup ls;
+  int per_sm = 0;
+  if (cudaError_t e = kernel_setup(ls, kern, kTinyNT, smem, per_sm); e != cudaSuccess) return e;
   const int64_t want = (n + kTinyNT - 1) / kTinyNT;
   const int64_t cap = (int64_t)per_sm * num_sms();
   kern<<<(unsigned)(want < cap ? want : cap), kTinyNT, smem, st>>>(A, B, rows, n, o);
@@ -984,14 +992,9 @@ static cudaError_t launch_hash_t(const CsrView& A, const CsrView& B, const int32
   static_assert(smem <= 232448, "hash tier shared memory exceeds 227 KB");
   static_assert(G <= 32 || GPC == 1, "a group of more than 32 threads is the whole CTA");
   auto kern = k_hash_symbolic<G, CAP, LCAP, GPC>;
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G * GPC, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-  }
+  static LaunchSetup ls;
+  int per_sm = 0;
+  if (cudaError_t e = kernel_setup(ls, kern, G * GPC, smem, per_sm); e != cudaSuccess) return e;
   const int64_t want = (n + GPC - 1) / GPC;
   const int64_t cap = (int64_t)per_sm * num_sms();
   kern<<<(unsigned)(want < cap ? want : cap), G * GPC, smem, st>>>(A, B, rows, n, o);
