@@ -6,6 +6,7 @@ path (paper_2206_06611_b200/) never imports it and shares no code with it.
 
 Functions and the PAPER.md passage each follows:
   row_nprod          §II.B.2, Alg. 1 line 1
+  row_sizes          Eq. (2)'s pattern: distinct columns per row
   spgemm_gustavson   Eq. (2), sorted-map accumulator
   spgemm_brmerge     Algorithm 1, literal, tree order
   brmerge_trace      Alg. 1 accumulating phase, live totals per round
@@ -55,6 +56,9 @@ def _load():
             f.restype = ctypes.c_void_p
             f.argtypes = [ctypes.c_int64, _i64p, _i32p, _f64p, _i64p, _i32p, _f64p,
                           _i64p, ctypes.c_int64]
+        lib.oracle_row_sizes.restype = None
+        lib.oracle_row_sizes.argtypes = [ctypes.c_int64, _i64p, _i32p, _i64p, _i32p, ctypes.c_int64,
+                                         _i64p, ctypes.c_int64, _i64p]
         lib.oracle_brmerge_trace.restype = ctypes.c_int64
         lib.oracle_brmerge_trace.argtypes = [_i64p, _i32p, _f64p, _i64p, _i32p, _f64p,
                                              ctypes.c_int64, _i64p, ctypes.c_int64]
@@ -90,6 +94,23 @@ def row_nprod(A, B) -> np.ndarray:
     out = np.zeros(A.rows, dtype=np.int64)
     _load().oracle_row_nprod(A.rows, _p(A.rpt, ctypes.c_int64), _p(A.col, ctypes.c_int32),
                              _p(B.rpt, ctypes.c_int64), _p(out, ctypes.c_int64))
+    return out
+
+
+def row_sizes(A, B, rows=None) -> np.ndarray:
+    """nnz of each output row (all rows, or `rows` in that order): the number
+    of distinct columns over the row's intermediate products -- Eq. (2)'s
+    pattern, structural zeros kept (R3). A set-membership count, no values."""
+    _check(A, B)
+    if rows is not None:
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        rp, nr, n = _p(rows, ctypes.c_int64), rows.size, rows.size
+    else:
+        rp, nr, n = None, 0, A.rows
+    out = np.zeros(n, np.int64)
+    _load().oracle_row_sizes(A.rows, _p(A.rpt, ctypes.c_int64), _p(A.col, ctypes.c_int32),
+                             _p(B.rpt, ctypes.c_int64), _p(B.col, ctypes.c_int32), B.cols,
+                             rp, nr, _p(out, ctypes.c_int64))
     return out
 
 

@@ -181,6 +181,32 @@ int64_t oracle_row_nprod(int64_t M, const int64_t* arpt, const int32_t* acol,
   return total;
 }
 
+// Row sizes only: nnz(C_i*) = |{ j : exists k in A_i* with j in B_k* }|, the
+// pattern of Eq. (2) with structural zeros kept (reading R3),
+// counted with a "last row seen" stamp per column (a plain set-membership
+// array of B.cols entries) -- the definition, without the values. For the
+// listed rows (all when null), out[t] = size of row rows[t].
+void oracle_row_sizes(int64_t M, const int64_t* arpt, const int32_t* acol, const int64_t* brpt,
+                      const int32_t* bcol, int64_t ncols, const int64_t* rows, int64_t nrows,
+                      int64_t* out) {
+  std::vector<int64_t> seen(ncols > 0 ? ncols : 1, -1);
+  const int64_t n = rows ? nrows : M;
+  for (int64_t t = 0; t < n; ++t) {
+    const int64_t i = rows ? rows[t] : t;
+    int64_t count = 0;
+    for (int64_t p = arpt[i]; p < arpt[i + 1]; ++p) {
+      const int32_t k = acol[p];
+      for (int64_t q = brpt[k]; q < brpt[k + 1]; ++q) {
+        if (seen[bcol[q]] != t) {
+          seen[bcol[q]] = t;
+          ++count;
+        }
+      }
+    }
+    out[t] = count;
+  }
+}
+
 // Eq. (2) with a sorted-map accumulator for the listed rows (all rows when
 // rows == nullptr). Result rows appear in the order of `rows`.
 void* oracle_gustavson(int64_t M, const int64_t* arpt, const int32_t* acol,

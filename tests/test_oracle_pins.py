@@ -407,3 +407,30 @@ def test_alg1_pairing_order_multi_column(oracle_mod):
     assert C.val[0] == e0 and C.val[1] == e1
     # column 1's tree differs from its k-order sum, so the case discriminates
     assert e1 != ((w[1] + w[2]) + w[3]) + w[4]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_row_sizes_definition(oracle_mod, seed):
+    """oracle.row_sizes = the per-row count of the boolean product's nonzeros
+    (dense pattern product, brute force), for all rows and for a row subset
+    given out of order."""
+    rng = np.random.default_rng(300 + seed)
+    m, k, n = (int(x) for x in rng.integers(1, 60, size=3))
+    A = random_sparse(m, k, float(rng.uniform(0.02, 0.4)), seed=seed)
+    B = random_sparse(k, n, float(rng.uniform(0.02, 0.4)), seed=seed + 7)
+    expect = ((_pattern(A) @ _pattern(B)) > 0).sum(axis=1)
+    np.testing.assert_array_equal(oracle_mod.row_sizes(A, B), expect)
+    rows = rng.permutation(m)[: max(1, m // 2)]
+    np.testing.assert_array_equal(oracle_mod.row_sizes(A, B, rows=rows), expect[rows])
+
+
+def test_row_sizes_closed_forms(oracle_mod):
+    """27-point stencil squared: rows of C are the 5x5x5 neighbourhoods
+    clipped to the grid, (5n-6)^3 nonzeros in total; identity: nnz(A_i*)."""
+    n = 7
+    S = stencil27(n, seed=1)
+    rs = oracle_mod.row_sizes(S, S)
+    assert rs.sum() == (5 * n - 6) ** 3
+    X = uniform_random(300, 300, 7, seed=3)
+    np.testing.assert_array_equal(oracle_mod.row_sizes(X, identity(300)), np.full(300, 7))
+    np.testing.assert_array_equal(oracle_mod.row_sizes(identity(300), X), np.full(300, 7))
