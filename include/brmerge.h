@@ -101,6 +101,10 @@ typedef struct {
   float ms_compact;                 /* UPPER: C_bar -> C compaction            */
   float ms_bin_numeric[BRM_NUM_BINS]; /* numeric merge per tier              */
   int64_t launches;                 /* kernels launched by the last structure+fill */
+  float ms_hv_plan;                 /* heavy rows of <= 1024 lists: window plan (k_hv_plan) */
+  float ms_hv_merge;                /* heavy rows of <= 1024 lists: windowed merge (k_hv_merge) */
+  int64_t hv_rows_one;              /* heavy rows merged in one level (<= 1024 lists)          */
+  int64_t hv_rows_multi;            /* heavy rows merged in levels of 1024-list blocks         */
 } brm_stats_t;
 
 typedef struct brm_context brm_context_t;

@@ -45,7 +45,9 @@ class brm_stats_t(ctypes.Structure):
                 ("ms_numeric", ctypes.c_float), ("ms_rowsize_scan", ctypes.c_float),
                 ("ms_compact", ctypes.c_float),
                 ("ms_bin_numeric", ctypes.c_float * BRM_NUM_BINS),
-                ("launches", ctypes.c_int64)]
+                ("launches", ctypes.c_int64),
+                ("ms_hv_plan", ctypes.c_float), ("ms_hv_merge", ctypes.c_float),
+                ("hv_rows_one", ctypes.c_int64), ("hv_rows_multi", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         d = {}

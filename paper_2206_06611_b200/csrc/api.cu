@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "brmerge.h"
+#include "heavy.cuh"
 #include "kernels.cuh"
 
 using namespace brm;
@@ -55,6 +56,17 @@ struct brm_context {
   brm_context* sub = nullptr;  // heavy-row decomposition runs its sub-products here
   DevBuf split_rows, split_off, glob_rows, a1_rpt, a1_col, a1_val, a2_rpt, a2_col, a2_val;
   HostBuf h_rows, h_split;
+  // windowed heavy rows (heavy.cuh): rows of <= kHvLists lists ("single",
+  // planned in structure, merged in fill under PRECISE) and the levels of
+  // rows of more lists ("multi", planned and merged within one call)
+  struct HvSet {
+    std::vector<HvRow> rows;
+    int64_t ntasks = 0;
+    DevBuf d_rows, cuts, wout, nwin, total;
+  } hv_single, hv_multi;
+  bool hv_single_planned = false;
+  DevBuf hv_lt[2], hv_ws_col[2], hv_ws_val[2], hv_tmp;
+  HostBuf h_hv;
 };
 
 namespace {
@@ -165,6 +177,8 @@ struct SmallDev {
   unsigned long long cursor[BRM_NUM_BINS];
   unsigned int counter[4];
   int64_t nnz_total;
+  unsigned int hv_err;  // heavy-row windows: inconsistency flags (heavy.cuh HvArgs::err)
+  unsigned int pad;
 };
 
 SmallDev* small_dev(brm_context_t* ctx) { return static_cast<SmallDev*>(ctx->small.p); }
@@ -173,6 +187,7 @@ SmallDev* small_dev(brm_context_t* ctx) { return static_cast<SmallDev*>(ctx->sma
 // 0/1 n_prod+scan+bin, 2/3 structure merge, 3/4 row_size scan, 5/6 fill,
 // 10+2b / 11+2b numeric merge of bin b.
 constexpr int kEvBin = 10;
+constexpr int kEvHv = 26;  // 26/27 heavy plan (single-level rows), 28/29 heavy merge
 void ev_record(brm_context_t* ctx, int i) {
   if (!ctx->timing) return;
   cudaEventRecord(ctx->ev[i], ctx->stream);
@@ -202,6 +217,264 @@ brm_status_t run_scan(brm_context_t* ctx, const int64_t* in, int64_t n, int64_t*
                      total_out, ctx->stream),
      "k_scan_i64");
   ++ctx->launches;
+  return BRM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Windowed heavy rows (heavy.cuh).
+// ---------------------------------------------------------------------------
+using HvSet = brm_context::HvSet;
+constexpr int kHvWch = 16;  // windows per merge task
+
+HvArgs hv_args(brm_context_t* ctx, HvSet& set) {
+  HvArgs a{};
+  a.A = ctx->A;
+  a.B = ctx->B;
+  a.ncols = ctx->N;
+  a.rows = static_cast<const HvRow*>(set.d_rows.p);
+  a.nrows = static_cast<int64_t>(set.rows.size());
+  a.cuts = static_cast<int32_t*>(set.cuts.p);
+  a.wout = static_cast<int32_t*>(set.wout.p);
+  a.nwin = static_cast<int32_t*>(set.nwin.p);
+  a.total = static_cast<int64_t*>(set.total.p);
+  a.err = &small_dev(ctx)->hv_err;
+  return a;
+}
+
+// Sort the virtual rows by n_prod (heaviest first: a launch lasts as long as
+// its heaviest rows), give each its plan slice and merge tasks, upload.
+brm_status_t hv_upload(brm_context_t* ctx, HvSet& set, bool sort) {
+  if (sort)
+    std::stable_sort(set.rows.begin(), set.rows.end(),
+                     [](const HvRow& x, const HvRow& y) { return x.nprod > y.nprod; });
+  int64_t plan = 0, task = 0;
+  for (HvRow& r : set.rows) {
+    r.maxwin = static_cast<int32_t>(hv_maxwin(r.nprod, ctx->N));
+    r.plan = plan;
+    plan += r.maxwin + 1;
+    r.wch = kHvWch;
+    r.task0 = task;
+    task += (r.maxwin + kHvWch - 1) / kHvWch;
+  }
+  set.ntasks = task;
+  const size_t n = set.rows.size();
+  CK(ensure(ctx, set.d_rows, n * sizeof(HvRow)), "alloc heavy rows");
+  CK(ensure(ctx, set.cuts, (size_t)plan * 4), "alloc heavy plan");
+  CK(ensure(ctx, set.wout, (size_t)plan * 4), "alloc heavy plan");
+  CK(ensure(ctx, set.nwin, n * 4), "alloc heavy plan");
+  CK(ensure(ctx, set.total, n * 8), "alloc heavy plan");
+  // pageable source: the copy is complete when the call returns
+  if (n) CK(cudaMemcpyAsync(set.d_rows.p, set.rows.data(), n * sizeof(HvRow), cudaMemcpyHostToDevice, ctx->stream),
+            "copy heavy rows");
+  return BRM_OK;
+}
+
+brm_status_t hv_check_err(brm_context_t* ctx) {
+  unsigned int e = 0;
+  CK(cudaMemcpyAsync(&e, &small_dev(ctx)->hv_err, 4, cudaMemcpyDeviceToHost, ctx->stream), "copy heavy flags");
+  CK(cudaStreamSynchronize(ctx->stream), "sync heavy flags");
+  if (e) return fail(ctx, BRM_ERR_CUDA, "heavy rows: internal inconsistency (flags " + std::to_string(e) + ")");
+  return BRM_OK;
+}
+
+// Rows of <= kHvLists lists: plan (bitmap + histogram windows; row sizes).
+brm_status_t hv_plan_single(brm_context_t* ctx, const std::vector<int32_t>& rows, const std::vector<int64_t>& info,
+                            int64_t* row_size) {
+  HvSet& set = ctx->hv_single;
+  set.rows.clear();
+  for (size_t i = 0; i < rows.size(); ++i) {
+    HvRow r{};
+    r.row = rows[i];
+    r.nprod = info[2 * i];
+    r.nl = static_cast<int32_t>(info[2 * i + 1]);
+    set.rows.push_back(r);
+  }
+  brm_status_t s = hv_upload(ctx, set, true);
+  if (s != BRM_OK) return s;
+  HvArgs a = hv_args(ctx, set);
+  a.row_size = row_size;
+  ev_record(ctx, kEvHv);
+  CK(launch_hv_plan(a, false, ctx->stream), "k_hv_plan");
+  ev_record(ctx, kEvHv + 1);
+  ++ctx->launches;
+  ctx->hv_single_planned = true;
+  return BRM_OK;
+}
+
+brm_status_t hv_merge_single(brm_context_t* ctx, int out, const RowOut& o) {
+  HvSet& set = ctx->hv_single;
+  if (set.rows.empty()) return BRM_OK;
+  if (!ctx->hv_single_planned) return fail(ctx, BRM_ERR_STATE, "heavy rows merged without a plan");
+  HvArgs a = hv_args(ctx, set);
+  ev_record(ctx, kEvHv + 2);
+  CK(launch_hv_merge(out, a, set.ntasks, o, ctx->stream), "k_hv_merge");
+  ev_record(ctx, kEvHv + 3);
+  ++ctx->launches;
+  return BRM_OK;
+}
+
+// Row sizes of rows of more than kHvLists lists (PRECISE symbolic): a bitmap
+// over all their lists.
+brm_status_t hv_count_multi(brm_context_t* ctx, const std::vector<int32_t>& rows, const std::vector<int64_t>& info,
+                            int64_t* row_size) {
+  if (rows.empty()) return BRM_OK;
+  HvSet& set = ctx->hv_multi;
+  set.rows.clear();
+  for (size_t i = 0; i < rows.size(); ++i) {
+    HvRow r{};
+    r.row = rows[i];
+    r.nprod = info[2 * i];
+    r.nl = static_cast<int32_t>(info[2 * i + 1]);
+    set.rows.push_back(r);
+  }
+  brm_status_t s = hv_upload(ctx, set, true);
+  if (s != BRM_OK) return s;
+  HvArgs a = hv_args(ctx, set);
+  a.row_size = row_size;
+  CK(launch_hv_plan(a, true, ctx->stream), "k_hv_plan (count)");
+  ++ctx->launches;
+  return BRM_OK;
+}
+
+// Rows of more than kHvLists lists, all levels: aligned blocks of kHvLists
+// lists (sub-trees of Algorithm 1's tree) merged into a workspace, whose
+// results are the next level's lists (scale 1.0), until a row has at most
+// kHvLists lists; that last level writes the output row. Rows are batched so
+// a level's workspace stays within a memory budget.
+brm_status_t hv_run_multi(brm_context_t* ctx, int out, const RowOut& o, const std::vector<int32_t>& rows,
+                          const std::vector<int64_t>& info) {
+  if (rows.empty()) return BRM_OK;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  int64_t maxP = 0;
+  for (size_t i = 0; i < rows.size(); ++i) maxP = std::max(maxP, info[2 * i]);
+  const int64_t budget = std::max<int64_t>(std::min<int64_t>((int64_t)(free_b / 4), 24ll << 30), maxP * 12);
+  HvSet& set = ctx->hv_multi;
+  size_t b0 = 0;
+  while (b0 < rows.size()) {
+    size_t b1 = b0;
+    int64_t bytes = 0;
+    while (b1 < rows.size() && (b1 == b0 || bytes + info[2 * b1] * 12 <= budget)) bytes += info[2 * b1++] * 12;
+    struct Cur {
+      int64_t row, first, nlist, P;
+      int src;
+    };
+    std::vector<Cur> cur;
+    for (size_t i = b0; i < b1; ++i) cur.push_back({rows[i], 0, info[2 * i + 1], info[2 * i], 0});
+    int lvl = 0;
+    while (!cur.empty()) {
+      set.rows.clear();
+      std::vector<int64_t> owner;  // the Cur entry of each virtual row
+      bool blocks = false;
+      for (size_t i = 0; i < cur.size(); ++i) {
+        const Cur& c = cur[i];
+        if (c.nlist <= kHvLists) {
+          HvRow r{};
+          r.row = c.row;
+          r.first = c.first;
+          r.nprod = c.P;
+          r.nl = static_cast<int32_t>(c.nlist);
+          r.src = c.src;
+          r.out = 0;
+          set.rows.push_back(r);
+          owner.push_back(static_cast<int64_t>(i));
+        } else {
+          blocks = true;
+          for (int64_t l0 = 0; l0 < c.nlist; l0 += kHvLists) {
+            HvRow r{};
+            r.row = c.row;
+            r.first = c.first + l0;
+            r.nprod = -1;
+            r.nl = static_cast<int32_t>(std::min<int64_t>(kHvLists, c.nlist - l0));
+            r.src = c.src;
+            r.out = 1;
+            set.rows.push_back(r);
+            owner.push_back(static_cast<int64_t>(i));
+          }
+        }
+      }
+      const size_t nv = set.rows.size();
+      const int in = (lvl + 1) & 1, outb = lvl & 1;  // workspace / list-table ping-pong
+      if (blocks) {  // products of each block
+        for (HvRow& r : set.rows) r.nprod = 0;
+        brm_status_t s = hv_upload(ctx, set, false);
+        if (s != BRM_OK) return s;
+        HvArgs a = hv_args(ctx, set);
+        a.lt = static_cast<const int64_t*>(ctx->hv_lt[in].p);
+        a.ws_col = static_cast<const int32_t*>(ctx->hv_ws_col[in].p);
+        CK(ensure(ctx, ctx->hv_tmp, nv * 8), "alloc heavy block sizes");
+        CK(launch_hv_vrow_nprod(a, static_cast<int64_t*>(ctx->hv_tmp.p), ctx->stream), "k_hv_vrow_nprod");
+        ++ctx->launches;
+        std::vector<int64_t> np(nv);
+        CK(cudaMemcpyAsync(np.data(), ctx->hv_tmp.p, nv * 8, cudaMemcpyDeviceToHost, ctx->stream), "copy block sizes");
+        CK(cudaStreamSynchronize(ctx->stream), "sync block sizes");
+        for (size_t v = 0; v < nv; ++v) set.rows[v].nprod = np[v];
+      }
+      // sort heaviest first, keeping each virtual row's Cur entry
+      std::vector<size_t> ord(nv);
+      for (size_t v = 0; v < nv; ++v) ord[v] = v;
+      std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) { return set.rows[x].nprod > set.rows[y].nprod; });
+      {
+        std::vector<HvRow> sr(nv);
+        std::vector<int64_t> so(nv);
+        for (size_t v = 0; v < nv; ++v) {
+          sr[v] = set.rows[ord[v]];
+          so[v] = owner[ord[v]];
+        }
+        set.rows.swap(sr);
+        owner.swap(so);
+      }
+      brm_status_t s = hv_upload(ctx, set, false);
+      if (s != BRM_OK) return s;
+      HvArgs a = hv_args(ctx, set);
+      a.lt = static_cast<const int64_t*>(ctx->hv_lt[in].p);
+      a.ws_col = static_cast<const int32_t*>(ctx->hv_ws_col[in].p);
+      a.ws_val = static_cast<const double*>(ctx->hv_ws_val[in].p);
+      a.row_size = out == OUT_C ? nullptr : o.row_size;
+      CK(launch_hv_plan(a, false, ctx->stream), "k_hv_plan");
+      ++ctx->launches;
+      std::vector<Cur> next;
+      if (blocks) {
+        // block results: contiguous per row, in block order
+        std::vector<int64_t> tot(nv);
+        CK(cudaMemcpyAsync(tot.data(), set.total.p, nv * 8, cudaMemcpyDeviceToHost, ctx->stream), "copy block totals");
+        CK(cudaStreamSynchronize(ctx->stream), "sync block totals");
+        std::vector<std::vector<size_t>> of(cur.size());  // block virtual rows of each Cur, in block order
+        for (size_t v = 0; v < nv; ++v)
+          if (set.rows[v].out == 1) of[owner[v]].push_back(v);
+        std::vector<int64_t> lt;
+        int64_t pos = 0;
+        for (size_t i = 0; i < cur.size(); ++i) {
+          if (of[i].empty()) continue;
+          std::sort(of[i].begin(), of[i].end(), [&](size_t x, size_t y) { return set.rows[x].first < set.rows[y].first; });
+          Cur nc{cur[i].row, static_cast<int64_t>(lt.size()), static_cast<int64_t>(of[i].size()), 0, 1};
+          for (size_t v : of[i]) {
+            set.rows[v].obase = pos;
+            lt.push_back(pos);
+            pos += tot[v];
+            nc.P += tot[v];
+          }
+          lt.push_back(pos);
+          next.push_back(nc);
+        }
+        CK(ensure(ctx, ctx->hv_ws_col[outb], (size_t)pos * 4), "alloc heavy workspace");
+        CK(ensure(ctx, ctx->hv_ws_val[outb], (size_t)pos * 8), "alloc heavy workspace");
+        CK(ensure(ctx, ctx->hv_lt[outb], lt.size() * 8), "alloc heavy list table");
+        CK(cudaMemcpyAsync(ctx->hv_lt[outb].p, lt.data(), lt.size() * 8, cudaMemcpyHostToDevice, ctx->stream),
+           "copy heavy list table");
+        CK(cudaMemcpyAsync(set.d_rows.p, set.rows.data(), nv * sizeof(HvRow), cudaMemcpyHostToDevice, ctx->stream),
+           "copy heavy rows");
+        a.wo_col = static_cast<int32_t*>(ctx->hv_ws_col[outb].p);
+        a.wo_val = static_cast<double*>(ctx->hv_ws_val[outb].p);
+      }
+      CK(launch_hv_merge(out == OUT_C ? OUT_C : OUT_CBAR, a, set.ntasks, o, ctx->stream), "k_hv_merge");
+      ++ctx->launches;
+      // the next level reads this level's workspace (ordered on the stream)
+      cur.swap(next);
+      ++lvl;
+    }
+    b0 = b1;
+  }
   return BRM_OK;
 }
 
@@ -326,6 +599,32 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
   CK(cudaMemcpyAsync(ctx->h_rows.p, hrows, (size_t)nh * 4, cudaMemcpyDeviceToHost, ctx->stream), "copy heavy rows");
   CK(cudaStreamSynchronize(ctx->stream), "sync heavy rows");
   const int32_t* hr = static_cast<const int32_t*>(ctx->h_rows.p);
+  if (ctx->heavy_route == BRM_HEAVY_AUTO) {
+    // windowed BRMerge (heavy.cuh): rows of <= kHvLists lists in one level,
+    // the rest in levels of aligned kHvLists-list blocks
+    std::vector<int32_t> r1, rm;
+    std::vector<int64_t> i1, im;
+    for (int64_t t = 0; t < nh; ++t) {
+      const int64_t P = ctx->heavy[2 * t], nl = ctx->heavy[2 * t + 1];
+      (nl <= kHvLists ? r1 : rm).push_back(hr[t]);
+      (nl <= kHvLists ? i1 : im).push_back(P);
+      (nl <= kHvLists ? i1 : im).push_back(nl);
+    }
+    ctx->stats.hv_rows_one = static_cast<int64_t>(r1.size());
+    ctx->stats.hv_rows_multi = static_cast<int64_t>(rm.size());
+    brm_status_t st = BRM_OK;
+    if (out == OUT_SYMBOLIC) {  // PRECISE step 3: row sizes (+ the windows of the one-level rows, kept for fill)
+      if ((st = hv_plan_single(ctx, r1, i1, o.row_size)) != BRM_OK) return st;
+      if ((st = hv_count_multi(ctx, rm, im, o.row_size)) != BRM_OK) return st;
+    } else {
+      if (out == OUT_CBAR && (st = hv_plan_single(ctx, r1, i1, o.row_size)) != BRM_OK) return st;
+      if ((st = hv_merge_single(ctx, out, o)) != BRM_OK) return st;
+      if ((st = hv_run_multi(ctx, out, o, rm, im)) != BRM_OK) return st;
+      if ((st = hv_check_err(ctx)) != BRM_OK) return st;
+    }
+    if (per_bin) ev_record(ctx, kEvBin + 2 * kBinGlobal + 1);
+    return BRM_OK;
+  }
   std::vector<int32_t> g_rows, s_rows;
   std::vector<int64_t> g_info, s_info;
   // Routes: rows of at most kSlabLists lists merge in
@@ -452,6 +751,8 @@ brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
   if (!c_rpt || !c_nnz) return fail(ctx, BRM_ERR_INVALID, "c_rpt / c_nnz is null");
   ctx->planned = false;
   ctx->heavy_loaded = false;
+  ctx->hv_single_planned = false;
+  ctx->hv_single.rows.clear();
   ctx->mode = mode;
   ctx->A = CsrView{A->rpt, A->col, A->val};
   ctx->B = CsrView{B->rpt, B->col, B->val};
@@ -613,7 +914,11 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
                       &ctx->cbar_val, &ctx->gws, &ctx->gws_off, &ctx->heavy_info, &ctx->stA_rpt, &ctx->stA_col,
                       &ctx->stA_val, &ctx->stB_rpt, &ctx->stB_col, &ctx->stB_val, &ctx->stC_rpt, &ctx->stC_col,
                       &ctx->stC_val, &ctx->split_rows, &ctx->split_off, &ctx->glob_rows, &ctx->a1_rpt, &ctx->a1_col,
-                      &ctx->a1_val, &ctx->a2_rpt, &ctx->a2_col, &ctx->a2_val})
+                      &ctx->a1_val, &ctx->a2_rpt, &ctx->a2_col, &ctx->a2_val, &ctx->hv_single.d_rows,
+                      &ctx->hv_single.cuts, &ctx->hv_single.wout, &ctx->hv_single.nwin, &ctx->hv_single.total,
+                      &ctx->hv_multi.d_rows, &ctx->hv_multi.cuts, &ctx->hv_multi.wout, &ctx->hv_multi.nwin,
+                      &ctx->hv_multi.total, &ctx->hv_lt[0], &ctx->hv_lt[1], &ctx->hv_ws_col[0], &ctx->hv_ws_col[1],
+                      &ctx->hv_ws_val[0], &ctx->hv_ws_val[1], &ctx->hv_tmp})
       free_dev(ctx, *b);
     cudaStreamSynchronize(ctx->stream);
     for (HostBuf* b : {&ctx->h_small, &ctx->h_heavy, &ctx->h_gws_off, &ctx->h_C, &ctx->h_rows, &ctx->h_split})
@@ -673,6 +978,8 @@ brm_status_t brm_get_stats(const brm_context_t* ctx, brm_stats_t* out) {
     }
     out->ms_rowsize_scan = ev_ms(ctx, 3, 4);
     for (int b = 0; b < BRM_NUM_BINS; ++b) out->ms_bin_numeric[b] = ev_ms(ctx, kEvBin + 2 * b, kEvBin + 2 * b + 1);
+    out->ms_hv_plan = ev_ms(ctx, kEvHv, kEvHv + 1);
+    out->ms_hv_merge = ev_ms(ctx, kEvHv + 2, kEvHv + 3);
   }
   return BRM_OK;
 }

@@ -783,9 +783,11 @@ __device__ __forceinline__ T src_ld(const T* p) {
     return *p;
 }
 
+// cbase: records carry col - cbase (the heavy-row windows pack columns
+// relative to the window start, so 20 column bits serve any B.cols).
 template <int G, int NV, class R, bool NC = true, bool BUILD = true, bool PLAIN = false>
 __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView& B, int nl, int P, int* off,
-                                               int* noff, const RecBufs& rb) {
+                                               int* noff, const RecBufs& rb, int cbase = 0) {
   constexpr bool VALS = R::kVals;
   typename R::T* rec = static_cast<typename R::T*>(rb.rec);
   const int rank = g.rank;
@@ -807,7 +809,7 @@ __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView&
       const longlong2 d = rb.lst[l];
       const int64_t src = d.x + e;
       const int c = src_ld<NC>(B.col + src);
-      rec[e + l] = R::make(c, e);
+      rec[e + l] = R::make(c - cbase, e);
       if (VALS) rb.val[e] = __dmul_rn(__longlong_as_double(d.y), src_ld<NC>(B.val + src));  // line 12: the product, rounded once
     }
   }

@@ -1,0 +1,607 @@
+// heavy.cu -- kernels of the windowed heavy-row path (heavy.cuh).
+#include <climits>
+
+#include "heavy.cuh"
+#include "kernels.cuh"
+
+namespace brm {
+
+namespace {
+
+// first index i in [0, n) with p[i] >= key (n if none); p is read-only here
+__device__ __forceinline__ int lower_bound_g(const int32_t* p, int n, int key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(p + mid) < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// Largest i in [lo, hi] with pred(i), pred monotone (true ... true false ...)
+// and pred(lo) true; evaluated by one warp, 32 probes per step.
+template <class Pred>
+__device__ __forceinline__ int warp_last_true(int lo, int hi, Pred pred) {
+  const int lane = threadIdx.x & 31;
+  while (lo < hi) {
+    const int step = (hi - lo + 31) / 32;
+    const int i = lo + (lane + 1) * step;
+    const bool p = i <= hi && pred(i);
+    const int k = __popc(__ballot_sync(0xffffffffu, p));  // probes 1..k hold
+    const int nlo = lo + k * step;
+    hi = min(hi, nlo + step - 1);
+    lo = nlo;
+  }
+  return lo;
+}
+
+// List j of virtual row r: its start in the column source and its length.
+struct ListRef {
+  int64_t start;
+  int len;
+};
+__device__ __forceinline__ ListRef hv_list(const HvArgs& a, const HvRow& r, int64_t a0, int64_t j) {
+  if (r.src == 0) {
+    const int k = __ldg(a.A.col + a0 + r.first + j);
+    const int64_t s = __ldg(a.B.rpt + k);
+    return {s, static_cast<int>(__ldg(a.B.rpt + k + 1) - s)};
+  }
+  const int64_t s = __ldg(a.lt + r.first + j);
+  return {s, static_cast<int>(__ldg(a.lt + r.first + j + 1) - s)};
+}
+
+// block-wide exclusive scan of n <= kHvLists ints in place (512 threads, two
+// entries each); returns the total. Ends synchronised.
+__device__ int plan_scan(int* x, int n, int* wtmp) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int i0 = 2 * t, i1 = 2 * t + 1;
+  const int v0 = i0 < n ? x[i0] : 0, v1 = i1 < n ? x[i1] : 0;
+  int s = v0 + v1, inc = s;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) wtmp[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    constexpr int NW = kHvPlanG / 32;
+    const int w = lane < NW ? wtmp[lane] : 0;
+    int wx = w;
+#pragma unroll
+    for (int d = 1; d < NW; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, wx, d);
+      if (lane >= d) wx += y;
+    }
+    if (lane < NW) wtmp[lane] = wx - w;
+    if (lane == NW - 1) wtmp[NW] = wx;
+  }
+  __syncthreads();
+  const int ex = wtmp[wid] + inc - s;
+  if (i0 < n) x[i0] = ex;
+  if (i1 < n) x[i1] = ex + v0;
+  const int total = wtmp[kHvPlanG / 32];
+  if (t == 0) x[n] = total;
+  __syncthreads();
+  return total;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Plan of one virtual row per CTA (see heavy.cuh). Columns are processed in
+// ranges of 2^20 (one range when B.cols <= 2^20); per range:
+//   1. bitmap of the product columns (atomicOr) and histogram of products per
+//      128-column bin (atomicAdd), one pass over the products;
+//   2. inclusive prefix of the histogram;
+//   3. windows, greedily: from x0, the largest cut x with
+//      count(x) <= count(x0) + kHvCap, at a bin boundary, or inside a bin of
+//      more than kHvCap products whose per-column counts were refined by an
+//      extra pass (64 such bins at a time); warp 0, 32 probes per step;
+//   4. each window's output size = bits set in [x0, x) (warp 0).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_only) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned* bm = reinterpret_cast<unsigned*>(smem);
+  unsigned* hist = bm + kHvRange / 32;
+  unsigned* fine = hist + kHvBins;
+  unsigned char* slot = reinterpret_cast<unsigned char*>(fine + kHvFine * 128);
+  int64_t* lstart = reinterpret_cast<int64_t*>(slot + kHvBins);
+  int* llen = reinterpret_cast<int*>(lstart + kHvLists);
+  int* loff = llen + kHvLists;
+  __shared__ int s_wtmp[kHvPlanG / 32 + 1];
+  __shared__ unsigned long long s_cnt;
+  __shared__ int s_cmin, s_cmax;
+  __shared__ int s_x0, s_nw, s_need, s_done, s_running;
+  __shared__ int s_refined_lo, s_refined_hi;  // bins [lo, hi] may hold refined slots
+
+  const HvRow r = a.rows[blockIdx.x];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t a0 = r.src == 0 ? a.A.rpt[r.row] : 0;
+  const int32_t* scol = r.src == 0 ? a.B.col : a.ws_col;
+  const int nl = r.nl;
+  // column span of the virtual row: first / last column of every list
+  if (t == 0) {
+    s_cmin = INT_MAX;
+    s_cmax = -1;
+    s_cnt = 0;
+    s_nw = 0;
+    s_running = 0;
+  }
+  __syncthreads();
+  {
+    int cmin = INT_MAX, cmax = -1;
+    for (int j = t; j < nl; j += kHvPlanG) {
+      const ListRef L = hv_list(a, r, a0, j);
+      if (L.len > 0) {
+        cmin = min(cmin, __ldg(scol + L.start));
+        cmax = max(cmax, __ldg(scol + L.start + L.len - 1));
+      }
+    }
+    cmin = __reduce_min_sync(0xffffffffu, cmin);
+    cmax = __reduce_max_sync(0xffffffffu, cmax);
+    if (lane == 0) {
+      atomicMin(&s_cmin, cmin);
+      atomicMax(&s_cmax, cmax);
+    }
+  }
+  __syncthreads();
+  const int cmin = s_cmin, cmax = s_cmax;
+  if (cmax < 0) {  // no products at all (a block of empty lists)
+    if (t == 0) {
+      if (!count_only) {
+        a.nwin[blockIdx.x] = 0;
+        a.wout[r.plan] = 0;
+        a.cuts[r.plan] = 0;
+      }
+      a.total[blockIdx.x] = 0;
+      if (r.out == 0 && a.row_size) a.row_size[r.row] = 0;
+    }
+    return;
+  }
+  const bool multi = (cmin >> kHvRangeBits) != (cmax >> kHvRangeBits);
+  const int nchunks = (nl + kHvLists - 1) / kHvLists;  // plan rows: nl <= kHvLists, one chunk
+  for (int rg = cmin >> kHvRangeBits; rg <= (cmax >> kHvRangeBits); ++rg) {
+    const int64_t rs0 = static_cast<int64_t>(rg) << kHvRangeBits;
+    const int rlen = static_cast<int>(min(static_cast<int64_t>(kHvRange), a.ncols - rs0));
+    const int lo_c = static_cast<int>(max(static_cast<int64_t>(cmin), rs0) - rs0);             // relative
+    const int hi_c = static_cast<int>(min(static_cast<int64_t>(cmax) + 1, rs0 + rlen) - rs0);  // relative, exclusive
+    // the whole range's bitmap (windows reach bin boundaries outside [lo_c, hi_c))
+    for (int w = t; w < (rlen + 31) >> 5; w += kHvPlanG) bm[w] = 0u;
+    if (!count_only) {
+      for (int b = t; b < kHvBins; b += kHvPlanG) {
+        hist[b] = 0u;
+        slot[b] = 0xff;
+      }
+    }
+    __syncthreads();
+    int prange = 0;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int j0 = ch * kHvLists, nc = min(kHvLists, nl - j0);
+      for (int j = t; j < nc; j += kHvPlanG) {
+        const ListRef L = hv_list(a, r, a0, j0 + j);
+        int lo = 0, hi = L.len;
+        if (multi) {
+          lo = lower_bound_g(scol + L.start, L.len, static_cast<int>(rs0));
+          hi = rs0 + kHvRange >= a.ncols ? L.len
+                                         : lower_bound_g(scol + L.start, L.len, static_cast<int>(rs0 + kHvRange));
+        }
+        lstart[j] = L.start + lo;
+        loff[j] = hi - lo;
+      }
+      __syncthreads();
+      const int pc = plan_scan(loff, nc, s_wtmp);
+      // one pass over the chunk's products (thread-strided; a thread's list
+      // index only moves forward)
+      int l = 0;
+      for (int e = t; e < pc; e += kHvPlanG) {
+        while (loff[l + 1] <= e) ++l;
+        const int rel = __ldg(scol + lstart[l] + (e - loff[l])) - static_cast<int>(rs0);
+        atomicOr(&bm[rel >> 5], 1u << (rel & 31));
+        if (!count_only) atomicAdd(&hist[rel >> kHvBinBits], 1u);
+      }
+      __syncthreads();
+      prange += pc;
+    }
+    if (count_only) {
+      unsigned long long c = 0;
+      for (int w = (lo_c >> 5) + t; w <= ((hi_c - 1) >> 5); w += kHvPlanG) c += __popc(bm[w]);
+      c = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(c));
+      if (lane == 0 && c) atomicAdd(&s_cnt, c);
+      __syncthreads();
+      continue;
+    }
+    if (prange == 0) continue;
+    // inclusive prefix of the histogram (16 bins per thread)
+    {
+      constexpr int PER = kHvBins / kHvPlanG;
+      unsigned v[PER];
+      unsigned s = 0;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        v[i] = hist[t * PER + i];
+        s += v[i];
+      }
+      unsigned inc = s;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
+      }
+      if (lane == 31) s_wtmp[wid] = static_cast<int>(inc);
+      __syncthreads();
+      if (wid == 0) {
+        constexpr int NW = kHvPlanG / 32;
+        const unsigned w = lane < NW ? static_cast<unsigned>(s_wtmp[lane]) : 0u;
+        unsigned wx = w;
+#pragma unroll
+        for (int d = 1; d < NW; d <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, wx, d);
+          if (lane >= d) wx += y;
+        }
+        if (lane < NW) s_wtmp[lane] = static_cast<int>(wx - w);
+      }
+      __syncthreads();
+      unsigned run = static_cast<unsigned>(s_wtmp[wid]) + inc - s;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        run += v[i];
+        v[i] = run;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < PER; ++i) hist[t * PER + i] = v[i];  // hist is now the inclusive prefix H
+      __syncthreads();
+    }
+    const unsigned* H = hist;
+    auto bin_count = [&](int b) { return H[b] - (b > 0 ? H[b - 1] : 0u); };
+    // greedy windows, with refinement passes as the walk meets bins of more
+    // than kHvCap products
+    if (t == 0) {
+      s_x0 = lo_c & ~((1 << kHvBinBits) - 1);  // a bin boundary: count 0
+      if (rg != (cmin >> kHvRangeBits)) s_x0 = 0;
+      s_need = -1;
+      s_done = 0;
+      s_refined_lo = 1;
+      s_refined_hi = 0;
+    }
+    __syncthreads();
+    const int nb = (rlen + (1 << kHvBinBits) - 1) >> kHvBinBits;
+    while (true) {
+      if (s_need >= 0) {
+        // refine the next kHvFine overflow bins from s_need on (whole CTA)
+        const int from = s_need;
+        if (wid == 0) {
+          for (int b = s_refined_lo + lane; b <= s_refined_hi; b += 32) slot[b] = 0xff;
+          __syncwarp();
+          int nsl = 0, last = from;
+          for (int b0 = from; b0 < nb && nsl < kHvFine; b0 += 32) {
+            const int b = b0 + lane;
+            const bool ov = b < nb && bin_count(b) > static_cast<unsigned>(kHvCap);
+            const unsigned m = __ballot_sync(0xffffffffu, ov);
+            const int rank = nsl + __popc(m & ((1u << lane) - 1u));
+            if (ov && rank < kHvFine) {
+              slot[b] = static_cast<unsigned char>(rank);
+              last = b;
+            }
+            nsl += __popc(m);
+            last = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(last));
+          }
+          if (lane == 0) {
+            s_refined_lo = from;
+            s_refined_hi = last;
+          }
+        }
+        for (int i = t; i < kHvFine * 128; i += kHvPlanG) fine[i] = 0u;
+        __syncthreads();
+        int l = 0;
+        const int pc = loff[nchunks == 1 ? nl : 0];  // plan rows have one chunk
+        for (int e = t; e < pc; e += kHvPlanG) {
+          while (loff[l + 1] <= e) ++l;
+          const int rel = __ldg(scol + lstart[l] + (e - loff[l])) - static_cast<int>(rs0);
+          const int sl = slot[rel >> kHvBinBits];
+          if (sl != 0xff) atomicAdd(&fine[sl * 128 + (rel & 127)], 1u);
+        }
+        __syncthreads();
+        // inclusive prefix per refined bin (a warp per bin)
+        for (int sl = wid; sl < kHvFine; sl += kHvPlanG / 32) {
+          unsigned* f = fine + sl * 128;
+          unsigned carry = 0;
+          for (int i0 = 0; i0 < 128; i0 += 32) {
+            unsigned x = f[i0 + lane];
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const unsigned y = __shfl_up_sync(0xffffffffu, x, d);
+              if (lane >= d) x += y;
+            }
+            f[i0 + lane] = x + carry;
+            carry += __shfl_sync(0xffffffffu, x, 31);
+          }
+        }
+        if (t == 0) s_need = -1;
+        __syncthreads();
+      }
+      if (wid == 0) {
+        int x0 = s_x0;
+        int nw = s_nw;
+        int running = s_running;
+        int need = -1;
+        // count(x): products of this range with relative column < x (x a bin
+        // boundary, or inside a refined bin)
+        auto count_at = [&](int x) -> unsigned {
+          const int b = x >> kHvBinBits, w = x & 127;
+          const unsigned base = b > 0 ? H[b - 1] : 0u;
+          if (w == 0) return base;
+          return base + fine[slot[b] * 128 + w - 1];
+        };
+        const unsigned ptot = H[nb - 1];
+        while (x0 < rlen && count_at(x0) < ptot) {
+          const unsigned T = count_at(x0) + kHvCap;
+          const int b0 = x0 >> kHvBinBits;
+          int cut;
+          if (H[b0] <= T) {  // the next bin boundary fits: the last one that does
+            const int B = warp_last_true(b0 + 1, nb, [&](int i) { return H[i - 1] <= T; });
+            cut = B << kHvBinBits;
+            if (B < nb && bin_count(B) > static_cast<unsigned>(kHvCap)) {  // continue inside bin B
+              if (slot[B] == 0xff) {
+                need = B;
+                break;
+              }
+              const int w = warp_last_true(0, 127, [&](int i) { return i == 0 || count_at(cut + i) <= T; });
+              cut += w;
+            }
+          } else {  // bin b0 alone holds too much: cut inside it (refined)
+            if (slot[b0] == 0xff) {
+              need = b0;
+              break;
+            }
+            const int w0 = x0 & 127;
+            const int w = warp_last_true(w0, 127, [&](int i) { return i == w0 || count_at((b0 << kHvBinBits) + i) <= T; });
+            cut = (b0 << kHvBinBits) + w;  // > x0: one column holds <= nl <= kHvCap products
+          }
+          if (cut - x0 > kHvSpan) cut = (x0 + kHvSpan) & ~((1 << kHvBinBits) - 1);
+          cut = min(cut, rlen);
+          // window [x0, cut): its output size = bits set
+          unsigned c = 0;
+          for (int wd = (x0 >> 5) + lane; wd <= ((cut - 1) >> 5); wd += 32) {
+            unsigned m = bm[wd];
+            if (wd == (x0 >> 5)) m &= ~0u << (x0 & 31);
+            if (wd == ((cut - 1) >> 5) && (cut & 31)) m &= (1u << (cut & 31)) - 1u;
+            c += __popc(m);
+          }
+          c = __reduce_add_sync(0xffffffffu, c);
+          if (nw >= r.maxwin) {
+            if (lane == 0) atomicOr(a.err, 1u);
+            need = -2;
+            break;
+          }
+          if (lane == 0) {
+            a.cuts[r.plan + nw] = static_cast<int>(rs0 + x0);
+            a.wout[r.plan + nw] = running;
+          }
+          running += static_cast<int>(c);
+          ++nw;
+          x0 = cut;
+        }
+        if (lane == 0) {
+          s_x0 = x0;
+          s_nw = nw;
+          s_running = running;
+          if (need >= 0) s_need = need; else s_done = 1;
+          if (need == -2) s_done = 2;
+          if (need == -1 && ptot > 0) s_cnt = static_cast<unsigned long long>(rs0 + x0);  // end of the last window
+        }
+      }
+      __syncthreads();
+      if (s_done) break;
+    }
+    if (s_done == 2) break;
+  }
+  __syncthreads();
+  if (t == 0) {
+    if (count_only) {
+      a.total[blockIdx.x] = static_cast<int64_t>(s_cnt);
+      if (r.out == 0 && a.row_size) a.row_size[r.row] = static_cast<int64_t>(s_cnt);
+    } else {
+      const int nw = s_nw;
+      a.cuts[r.plan + nw] = static_cast<int>(s_cnt);
+      a.wout[r.plan + nw] = s_running;
+      a.nwin[blockIdx.x] = nw;
+      a.total[blockIdx.x] = s_running;
+      if (r.out == 0 && a.row_size) a.row_size[r.row] = s_running;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Merge: one CTA per task = windows [w0, w1) of one virtual row.
+// ---------------------------------------------------------------------------
+template <int OUT>
+__global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
+  using R = RecPacked<kHvSB>;
+  constexpr int NV = ((kHvCap + kHvLists + 1 + kHvG - 1) / kHvG) | 1;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* p = smem;
+  auto take = [&](int n) {
+    unsigned char* q = p;
+    p += align16(n);
+    return q;
+  };
+  int64_t* S = reinterpret_cast<int64_t*>(take(kHvLists * 8));
+  double* AV = reinterpret_cast<double*>(take(kHvLists * 8));
+  int* L = reinterpret_cast<int*>(take(kHvLists * 4));
+  int* cur = reinterpret_cast<int*>(take(kHvLists * 4));
+  int* head = reinterpret_cast<int*>(take(kHvLists * 4));
+  int* cnt = reinterpret_cast<int*>(take(kHvLists * 4));
+  RecBufs rb;
+  rb.off0 = reinterpret_cast<int*>(take((kHvLists + 2) * 4));
+  rb.off1 = reinterpret_cast<int*>(take((kHvLists + 2) * 4));
+  rb.lst = reinterpret_cast<longlong2*>(take(kHvLists * 16));
+  rb.rec = take((kHvCap + kHvLists + 2) * 4);
+  rb.val = reinterpret_cast<double*>(take(kHvCap * 8));
+  rb.owner = reinterpret_cast<unsigned short*>(rb.val);
+  rb.ostr = 4;
+  rb.bst = nullptr;
+  rb.av = nullptr;
+  rb.scan_tmp = reinterpret_cast<int*>(take((kHvG / 32 + 2) * 4));
+  __shared__ int s_v;
+  const Group<kHvG> g = make_group<kHvG>();
+  const int rank = g.rank;
+  const int64_t t = blockIdx.x;
+  if (rank == 0) {  // the virtual row of this task: last v with rows[v].task0 <= t
+    int64_t lo = 0, hi = a.nrows - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (a.rows[mid].task0 <= t)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    s_v = static_cast<int>(lo);
+  }
+  g.sync();
+  const int v = s_v;
+  const HvRow r = a.rows[v];
+  const int nwin = a.nwin[v];
+  const int w0 = static_cast<int>(t - r.task0) * r.wch;
+  if (w0 >= nwin) return;
+  const int w1 = min(nwin, w0 + r.wch);
+  const int nl = r.nl;
+  const int64_t a0 = r.src == 0 ? a.A.rpt[r.row] : 0;
+  const CsrView Sv{nullptr, r.src == 0 ? a.B.col : a.ws_col, r.src == 0 ? a.B.val : a.ws_val};
+  const int cfirst = a.cuts[r.plan + w0];
+  for (int l = rank; l < nl; l += kHvG) {
+    const ListRef Lr = hv_list(a, r, a0, l);
+    const int c0 = w0 == 0 ? 0 : lower_bound_g(Sv.col + Lr.start, Lr.len, cfirst);
+    S[l] = Lr.start;
+    L[l] = Lr.len;
+    AV[l] = r.src == 0 ? __ldg(a.A.val + a0 + r.first + l) : 1.0;
+    cur[l] = c0;
+    head[l] = c0 < Lr.len ? __ldg(Sv.col + Lr.start + c0) : INT_MAX;
+  }
+  g.sync();
+  int32_t* ocol;
+  double* oval;
+  int64_t obase;
+  if (r.out == 0) {
+    ocol = o.col;
+    oval = o.val;
+    obase = o.base[r.row];
+  } else {
+    ocol = a.wo_col;
+    oval = a.wo_val;
+    obase = r.obase;
+  }
+  typename R::T* rec = static_cast<typename R::T*>(rb.rec);
+  for (int w = w0; w < w1; ++w) {
+    const int c0 = a.cuts[r.plan + w], c1 = a.cuts[r.plan + w + 1];
+    int* off = rb.off0;
+    int P = 0;
+    for (int lb = 0; lb < nl; lb += kHvG) {
+      const int l = lb + rank;
+      int n = 0;
+      if (l < nl && head[l] < c1) {  // list l's products in [c0, c1): a search from its cursor
+        const int cu = cur[l];
+        n = 1 + lower_bound_g(Sv.col + S[l] + cu + 1, min(L[l] - cu - 1, kHvCap), c1);
+      }
+      int tot;
+      const int ex = group_excl_scan<kHvG>(g, n, tot, rb.scan_tmp);
+      if (l < nl) {
+        off[l] = P + ex + l;
+        rec[P + ex + l + n] = R::sent();
+        rb.lst[l] = make_longlong2(S[l] + cur[l] - (P + ex), __double_as_longlong(AV[l]));
+        cnt[l] = n;
+      }
+      P += tot;
+    }
+    if (rank == 0) {
+      off[nl] = P + nl;
+      rec[P + nl] = R::sent();
+    }
+    g.sync();
+    const int T = rec_merge_lists<kHvG, NV, R, true, false>(g, Sv, nl, P, off, rb.off1, rb, c0);
+    const int ob = a.wout[r.plan + w];
+    if (rank == 0 && T != a.wout[r.plan + w + 1] - ob) atomicOr(a.err, 2u);
+    for (int e = rank; e < T; e += kHvG) {
+      const unsigned x = rec[e];
+      ocol[obase + ob + e] = R::col(x) + c0;
+      oval[obase + ob + e] = rb.val[R::slot(x)];
+    }
+    for (int l = rank; l < nl; l += kHvG) {
+      const int n = cnt[l];
+      if (n) {
+        const int cu = cur[l] + n;
+        cur[l] = cu;
+        head[l] = cu < L[l] ? __ldg(Sv.col + S[l] + cu) : INT_MAX;
+      }
+    }
+    g.sync();
+  }
+}
+
+// products of each (src 0) virtual row: one warp per row
+__global__ void k_hv_vrow_nprod(HvArgs a, int64_t* out) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= a.nrows) return;
+  const HvRow r = a.rows[w];
+  const int64_t a0 = r.src == 0 ? a.A.rpt[r.row] : 0;
+  int64_t s = 0;
+  for (int j = lane; j < r.nl; j += 32) s += hv_list(a, r, a0, j).len;
+#pragma unroll
+  for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+  if (lane == 0) out[w] = s;
+}
+
+cudaError_t launch_hv_plan(const HvArgs& a, bool count_only, cudaStream_t st) {
+  if (a.nrows <= 0) return cudaSuccess;
+  constexpr int smem = hv_plan_smem();
+  static_assert(smem <= 232448, "plan shared memory exceeds 227 KB");
+  static bool set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_hv_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    set[dev] = true;
+  }
+  k_hv_plan<<<static_cast<unsigned>(a.nrows), kHvPlanG, smem, st>>>(a, count_only ? 1 : 0);
+  return cudaGetLastError();
+}
+
+template <int OUT>
+static cudaError_t launch_hv_merge_t(const HvArgs& a, int64_t ntasks, const RowOut& o, cudaStream_t st) {
+  constexpr int smem = hv_merge_smem();
+  static_assert(smem <= 232448, "merge shared memory exceeds 227 KB");
+  static bool set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(k_hv_merge<OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    set[dev] = true;
+  }
+  k_hv_merge<OUT><<<static_cast<unsigned>(ntasks), kHvG, smem, st>>>(a, o);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hv_merge(int out_kind, const HvArgs& a, int64_t ntasks, const RowOut& o, cudaStream_t st) {
+  if (ntasks <= 0) return cudaSuccess;
+  switch (out_kind) {
+    case OUT_CBAR: return launch_hv_merge_t<OUT_CBAR>(a, ntasks, o, st);
+    case OUT_C: return launch_hv_merge_t<OUT_C>(a, ntasks, o, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_hv_vrow_nprod(const HvArgs& a, int64_t* out, cudaStream_t st) {
+  if (a.nrows <= 0) return cudaSuccess;
+  const int64_t threads = a.nrows * 32;
+  k_hv_vrow_nprod<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(a, out);
+  return cudaGetLastError();
+}
+
+}  // namespace brm

@@ -386,59 +386,6 @@ def _gather_rows(C, rows):
     return rpt.cpu().numpy(), C.col[idx].cpu().numpy(), C.val[idx].cpu().numpy()
 
 
-def _sample_rows(A, B, k=1500):
-    """Evenly strided rows plus the heaviest (largest n_prod) rows."""
-    import oracle
-    nprod = oracle.row_nprod(A, B)
-    strided = np.linspace(0, A.rows - 1, min(k, A.rows)).astype(np.int64)
-    heavy = np.argsort(nprod)[-64:]
-    return np.unique(np.concatenate([strided, heavy]))
-
-
-@pytest.mark.parametrize("mode", MODES)
-@pytest.mark.parametrize("name", ["stencil", "amg", "rmat", "uniform"])
-def test_workload_shapes_small(ctx, oracle_mod, mode, name):
-    """The paper-workload generators at sizes the oracle finishes in seconds
-    (several tiles of every tier they hit, ragged tails), every row."""
-    from inputs import aggregation_prolongator, laplace2d_5pt, rmat, stencil27
-    if name == "stencil":
-        A = B = stencil27(13, seed=2)
-    elif name == "amg":
-        A, B = laplace2d_5pt(96), aggregation_prolongator(96, seed=3)
-    elif name == "rmat":
-        A = B = rmat(11, 16, 0.57, 0.19, 0.19, 0.05, seed=4)
-    else:
-        A = B = uniform_random(20000, 20000, 16, seed=5)
-    compare(run(ctx, A, B, mode), A, B)
-
-
-FULL = ["uniform2k_k8", "stencil27_64", "uniform1m_k16", "amg_lap2048_agg2x2", "rmat20_ef16"]
-
-
-@pytest.mark.parametrize("name", FULL)
-def test_full_size_sampled(ctx, oracle_mod, name):
-    """BASELINE.json configs at full size, in the mode bench.py times
-    (PRECISE; UPPER too where C_bar fits), compared with the oracle on
-    sampled rows (strided + heaviest) and on global invariants."""
-    import torch
-    from inputs import workload
-    from paper_2206_06611_b200 import TorchCsr
-    A, B = workload(name)
-    rows = _sample_rows(A, B)
-    Ad, Bd = TorchCsr.from_csr(A), TorchCsr.from_csr(B)
-    modes = ["precise"] if name == "rmat20_ef16" else ["precise", "upper"]
-    for mode in modes:
-        C = ctx.spgemm(Ad, Bd, mode)
-        torch.cuda.synchronize()
-        rpt = C.rpt.cpu().numpy()
-        assert rpt[0] == 0 and np.all(np.diff(rpt) >= 0) and rpt[-1] == C.nnz
-        s = ctx.stats()
-        assert s["nnz_c"] == C.nnz
-        compare(_gather_rows(C, rows), A, B, rows=rows)
-        del C
-        torch.cuda.empty_cache()
-
-
 @pytest.mark.parametrize("mode", MODES)
 def test_heavy_row_recursive_split(ctx, oracle_mod, mode):
     """A row of 20,000 one-element lists over 50 columns: its 32-list blocks
