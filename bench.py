@@ -47,7 +47,7 @@ METRIC = _baseline_metric()
 CONFIGS = {
     "uniform2k_k8": 0, "stencil27_64": 1, "uniform1m_k16": 2, "rmat20_ef16": 3, "amg_lap2048_agg2x2": 4,
 }
-DEFAULT_CONFIG = "stencil27_64"
+DEFAULT_CONFIG = "rmat20_ef16"  # the largest single-GPU C = A*A config (BASELINE configs[3])
 # stencil / uniform grow with the rank count (weak scaling); rmat20 and the AMG
 # product are the same problem at every N (strong scaling)
 SCALING = {"uniform2k_k8": "weak", "stencil27_64": "weak", "uniform1m_k16": "weak",
@@ -104,6 +104,7 @@ def stencil27_box(nx, ny, nz, seed):
 TIER_CAP = [0, 8, 32, 256, 768, 3072, 6656]
 TIER_LCAP = [0, 8, 32, 64, 64, 256, 512]
 NUM_BINS = 8
+HV_LISTS = 1024  # heavy rows of at most this many lists merge in one level (csrc/heavy.cuh kHvLists)
 
 
 def tier_of(nprod: np.ndarray, nl: np.ndarray) -> np.ndarray:
@@ -123,7 +124,7 @@ def algorithmic_bytes(A, B, rows: np.ndarray, nnz_c_rows: int) -> int:
     a_bytes = int(rows.size) * 16 + int(lens.sum()) * 12
     idx = np.concatenate([np.arange(A.rpt[r], A.rpt[r + 1]) for r in rows]) if rows.size < 5000 else \
         np.repeat(A.rpt[rows], lens) + (np.arange(int(lens.sum())) - np.repeat(np.cumsum(lens) - lens, lens))
-    touched = np.unique(A.col[idx])
+    touched = gen.sorted_unique(A.col[idx])
     b_bytes = int(touched.size) * 16 + int((B.rpt[touched + 1] - B.rpt[touched]).sum()) * 12
     c_bytes = int(nnz_c_rows) * 12 + int(rows.size) * 8
     return a_bytes + b_bytes + c_bytes
@@ -183,14 +184,14 @@ def measured_peak_hbm():
         return 6650.0, "fallback"
 
 
-def measured_traffic(config: str, mode: str, bin_: int):
+def measured_traffic(config: str, mode: str, kernel: str):
     """DRAM bytes (read + write) per launch of the dominant kernel, from the
     `ncu --set full` capture recorded in profiles/traffic.json (None if this
     config/mode/kernel was not captured)."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
-        e = t.get(f"{config}/{mode}/bin{bin_}")
+        e = t.get(f"{config}/{mode}/{kernel.split()[0]}")
         return None if e is None else float(e["dram_bytes"])
     except Exception:
         return None
@@ -233,7 +234,7 @@ def _sample_rows(nprod, target_prod):
     total = int(nprod.sum())
     frac = min(1.0, target_prod / max(total, 1))
     n = max(1, int(M * frac))
-    rows = np.unique(np.linspace(0, M - 1, n).astype(np.int64))
+    rows = gen.sorted_unique(np.linspace(0, M - 1, n).astype(np.int64))
     return rows, f"{rows.size} of {M} rows (evenly strided), n_prod {int(nprod[rows].sum())} of {total}"
 
 
@@ -308,7 +309,7 @@ def main():
     ctx.set_timing(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     bin_ms = np.zeros(NUM_BINS)
-    sym_ms = num_ms = pre_ms = scan_ms = cmp_ms = 0.0
+    sym_ms = num_ms = pre_ms = scan_ms = cmp_ms = hv_plan_ms = hv_merge_ms = 0.0
     launches = 0
     if world > 1:
         dist.barrier()
@@ -327,6 +328,8 @@ def main():
             pre_ms += s["ms_nprod_scan"]
             scan_ms += s["ms_rowsize_scan"]
             cmp_ms += s["ms_compact"]
+            hv_plan_ms += s["ms_hv_plan"]
+            hv_merge_ms += s["ms_hv_merge"]
             launches += s["launches"]
         torch.cuda.synchronize(dev)
     ctx.set_timing(False)
@@ -346,17 +349,25 @@ def main():
     ms_step = total_ms / args.steps
     gflops = 2.0 * nprod_all / (ms_step * 1e-3) / 1e9
 
-    # roofline of the dominant kernel (numeric merge of the busiest tier)
+    # roofline of the dominant kernel: the single numeric-merge launch with the
+    # largest event time -- a shared-memory tier (k_tier / k_tiny, one launch
+    # per bin) or the windowed merge of the one-level heavy rows (k_hv_merge)
     peak, peak_kind = measured_peak_hbm()
-    dom = int(np.argmax(bin_ms))
     nl_loc = np.diff(Ablk.rpt)
     np_loc = nprod_h[r0:r1]
     tiers = tier_of(np_loc, nl_loc)
-    dom_rows = np.nonzero(tiers == dom)[0]
+    cand = {}
+    for b in range(1, NUM_BINS - 1):
+        cand[f"{'k_tiny' if b == 1 else 'k_tier'} (tier {b} numeric merge)"] = (
+            bin_ms[b] / args.steps, np.nonzero(tiers == b)[0])
+    if hv_merge_ms > 0:
+        cand["k_hv_merge (heavy rows of <= 1024 lists, windowed merge)"] = (
+            hv_merge_ms / args.steps, np.nonzero((tiers == NUM_BINS - 1) & (nl_loc <= HV_LISTS))[0])
+    dom_name = max(cand, key=lambda k: cand[k][0])
+    dom_ms, dom_rows = cand[dom_name]
     crpt = C.rpt.cpu().numpy()
     nnz_dom = int((crpt[dom_rows + 1] - crpt[dom_rows]).sum())
     dom_bytes = algorithmic_bytes(Ablk, B, dom_rows, nnz_dom)
-    dom_ms = bin_ms[dom] / args.steps
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
     all_rows = np.arange(Ablk.rows)
     step_bytes = algorithmic_bytes(Ablk, B, all_rows, nnz_local)
@@ -367,9 +378,15 @@ def main():
 
     # end to end through the host-buffer C entry (pinned H2D, D2H inside)
     e2e = None
-    if not args.no_e2e and nnz_local * 12 > (48 << 30):
-        e2e = {"value": None, "unit": "GFLOP/s", "skipped": f"C is {nnz_local * 12 / 2**30:.0f} GiB: not staged through pinned host memory"}
+    host_ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    c_bytes = nnz_local * 12 + (Ablk.rows + 1) * 8
+    if not args.no_e2e and c_bytes > 0.75 * host_ram:
+        e2e = {"value": None, "unit": "GFLOP/s",
+               "skipped": f"C is {c_bytes / 2**30:.0f} GiB, host RAM {host_ram / 2**30:.0f} GiB"}
     elif not args.no_e2e:
+        del C  # the host entry computes C again on the device: release this one first
+        C = None
+        torch.cuda.empty_cache()
         Ah = TorchCsr.from_csr(Ablk, pin=True)
         Bh = Ah if (B is A and world == 1) else TorchCsr.from_csr(B, pin=True)
         ctx.brmerge_spgemm_host(Ah, Bh, args.mode)  # warm
@@ -377,7 +394,7 @@ def main():
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        k_e2e = max(1, min(args.steps, 5))
+        k_e2e = max(1, min(args.steps, 5 if c_bytes < (8 << 30) else 2))  # rmat20: ~116 GB over PCIe per step
         e0.record(stream)
         for _ in range(k_e2e):
             out = ctx.brmerge_spgemm_host(Ah, Bh, args.mode)
@@ -424,13 +441,15 @@ def main():
                        "l2": "flushed (256 MiB write) between timed steps, outside the events",
                        "parallelism": f"dp{world} rows by balanced n_prod"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": measured_traffic(args.config, args.mode, dom),
-                         "kernel": f"k_tier bin {dom} (numeric merge)" if dom < NUM_BINS - 1 else "k_global_tier",
-                         "kernel_ms": dom_ms, "algorithmic_bytes": dom_bytes, "peak_kind": peak_kind},
+                         "frac": achieved / peak, "traffic": measured_traffic(args.config, args.mode, dom_name),
+                         "kernel": dom_name, "kernel_ms": dom_ms, "kernel_rows": int(dom_rows.size),
+                         "algorithmic_bytes": dom_bytes, "peak_kind": peak_kind},
             "hbm_step": {"achieved_gbs": step_gbs, "frac": step_gbs / peak, "algorithmic_bytes": int(b_all.item())},
             "phases_ms": {"nprod_scan_bin": pre_ms / args.steps, "symbolic": sym_ms / args.steps,
                           "numeric": num_ms / args.steps, "rowsize_scan": scan_ms / args.steps,
-                          "compact": cmp_ms / args.steps, "numeric_per_bin": (bin_ms / args.steps).tolist()},
+                          "compact": cmp_ms / args.steps, "numeric_per_bin": (bin_ms / args.steps).tolist(),
+                          "heavy_plan": hv_plan_ms / args.steps, "heavy_merge_one_level": hv_merge_ms / args.steps},
+            "heavy_rows": {"one_level": stats["hv_rows_one"], "levels_of_1024_list_blocks": stats["hv_rows_multi"]},
             "bin_rows": stats["bin_rows"],
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks,
