@@ -9,11 +9,15 @@ HBM. L2 is flushed (256 MiB write) between timed steps, outside the events.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME]
                   [--mode precise|upper] [--impl ours|reference]
 
-N > 1 (torchrun, NCCL): weak scaling -- the global workload grows with N
-(stencil: 64 x 64 x 64N grid; uniform: N x rows) and rows are partitioned
-across ranks by balanced n_prod (§III.D); B is NCCL-broadcast from rank 0 at
-setup; each step ends with an NCCL all-gather of the per-rank nnz(C) (the
-global row_ptr offsets of the C row blocks). Time = max over ranks.
+Default workload: rmat20_ef16 (BASELINE configs[3], the largest single-GPU
+C = A*A config), BRMerge-Precise (C_bar would need 251 GB).
+
+N > 1 (torchrun, NCCL): rows are partitioned across ranks by balanced n_prod
+(§III.D); B is NCCL-broadcast from rank 0 at setup; each timed step ends
+with the NCCL all-gather of the C row blocks' row pointers into the global
+row_ptr on every rank (--assemble full: the whole C). rmat20 / AMG are the
+same problem at every N (strong scaling); stencil / uniform grow with N
+(weak: 64 x 64 x 64N grid, N x rows). Time = max over ranks.
 `--impl reference` times the CPU oracle (test infrastructure) on a bounded
 row sample, rank 0 only.
 """
@@ -248,6 +252,9 @@ def main():
                     help="auto: BRMerge-Upper when its C_bar (12 B per intermediate product) fits in "
                          "half of the GPU memory, else BRMerge-Precise")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--assemble", default="rpt", choices=["rpt", "full"],
+                    help="N > 1: all-gather the global row_ptr (C's col/val stay row-distributed) "
+                         "or the whole C (row_ptr + col/val) on every rank, inside the timed step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-prod", type=float, default=2e6, help="probe sample (products)")
@@ -297,8 +304,11 @@ def main():
 
     def step():
         C = ctx.spgemm(Ad, Bd, args.mode)
-        if world > 1:  # row_ptr offsets of the C row blocks (all-gather)
-            bdist.block_nnz(C.nnz, dev)
+        if world > 1:  # C's row blocks assembled with all-gathers (NCCL)
+            if args.assemble == "full":  # row_ptr + col/val of every block on every rank
+                bdist.assemble_csr(C, A.rows)
+            else:  # the global row_ptr on every rank; col/val stay row-distributed
+                bdist.assemble_rpt(C, A.rows)
         return C
 
     C = None
@@ -439,7 +449,9 @@ def main():
                        "nnz_a": A.nnz, "nprod": nprod_all, "nnz_c": nnz_all,
                        "compression_ratio": nprod_all / max(nnz_all, 1),
                        "l2": "flushed (256 MiB write) between timed steps, outside the events",
-                       "parallelism": f"dp{world} rows by balanced n_prod"},
+                       "parallelism": f"dp{world} rows by balanced n_prod",
+                       "assembly": (("global row_ptr all-gathered, C row-distributed" if args.assemble == "rpt"
+                                     else "whole C all-gathered") if world > 1 else "n/a (one GPU)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": measured_traffic(args.config, args.mode, dom_name),
                          "kernel": dom_name, "kernel_ms": dom_ms, "kernel_rows": int(dom_rows.size),

@@ -128,6 +128,10 @@ class TorchCsr:
             return x.to(device)
         return cls(int(X.rows), int(X.cols), t(X.rpt), t(X.col), t(X.val))
 
+    def to(self, device) -> "TorchCsr":
+        """The same CSR with its tensors on `device`."""
+        return TorchCsr(self.rows, self.cols, self.rpt.to(device), self.col.to(device), self.val.to(device))
+
     def to_numpy(self):
         return (self.rpt.cpu().numpy(), self.col.cpu().numpy(), self.val.cpu().numpy())
 

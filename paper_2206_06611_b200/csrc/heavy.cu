@@ -89,6 +89,44 @@ __device__ int plan_scan(int* x, int n, int* wtmp) {
   return total;
 }
 
+// The products [0, pc) of a chunk of lists (list j at lstart[j], products
+// loff[j] .. loff[j+1]) visited by the CTA: warp w takes a contiguous span of
+// products, its lanes consecutive products (coalesced loads), each lane's list
+// index only moves forward; four loads in flight per lane. fn(col).
+template <class Fn>
+__device__ __forceinline__ void plan_for_products(const int32_t* scol, const int64_t* lstart, const int* loff, int nc,
+                                                  int pc, Fn fn) {
+  constexpr int NW = kHvPlanG / 32, U = 4;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int per = ((pc + NW - 1) / NW + 31) & ~31;
+  const int e0 = wid * per, e1 = min(pc, e0 + per);
+  if (e0 >= e1) return;
+  int lo = 0, hi = nc - 1;  // last list starting at or before e0
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (loff[mid] <= e0)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  int l = lo;
+  for (int eb = e0; eb < e1; eb += 32 * U) {
+    int c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = eb + 32 * u + lane;
+      c[u] = -1;
+      if (e < e1) {
+        while (loff[l + 1] <= e) ++l;
+        c[u] = __ldg(scol + lstart[l] + (e - loff[l]));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c[u] >= 0) fn(c[u]);
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -116,6 +154,7 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
   __shared__ unsigned long long s_cnt;
   __shared__ int s_cmin, s_cmax;
   __shared__ int s_x0, s_nw, s_need, s_done, s_running;
+  __shared__ int s_nwr;  // windows of the ranges done
   __shared__ int s_refined_lo, s_refined_hi;  // bins [lo, hi] may hold refined slots
 
   const HvRow r = a.rows[blockIdx.x];
@@ -129,6 +168,7 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
     s_cmax = -1;
     s_cnt = 0;
     s_nw = 0;
+    s_nwr = 0;
     s_running = 0;
   }
   __syncthreads();
@@ -194,14 +234,19 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
       }
       __syncthreads();
       const int pc = plan_scan(loff, nc, s_wtmp);
-      // one pass over the chunk's products (thread-strided; a thread's list
-      // index only moves forward)
-      int l = 0;
-      for (int e = t; e < pc; e += kHvPlanG) {
-        while (loff[l + 1] <= e) ++l;
-        const int rel = __ldg(scol + lstart[l] + (e - loff[l])) - static_cast<int>(rs0);
-        atomicOr(&bm[rel >> 5], 1u << (rel & 31));
-        if (!count_only) atomicAdd(&hist[rel >> kHvBinBits], 1u);
+      // one pass over the chunk's products
+      const int irs0 = static_cast<int>(rs0);
+      if (count_only) {
+        plan_for_products(scol, lstart, loff, nc, pc, [&](int c) {
+          const int rel = c - irs0;
+          atomicOr(&bm[rel >> 5], 1u << (rel & 31));
+        });
+      } else {
+        plan_for_products(scol, lstart, loff, nc, pc, [&](int c) {
+          const int rel = c - irs0;
+          atomicOr(&bm[rel >> 5], 1u << (rel & 31));
+          atomicAdd(&hist[rel >> kHvBinBits], 1u);
+        });
       }
       __syncthreads();
       prange += pc;
@@ -297,14 +342,12 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
         }
         for (int i = t; i < kHvFine * 128; i += kHvPlanG) fine[i] = 0u;
         __syncthreads();
-        int l = 0;
-        const int pc = loff[nchunks == 1 ? nl : 0];  // plan rows have one chunk
-        for (int e = t; e < pc; e += kHvPlanG) {
-          while (loff[l + 1] <= e) ++l;
-          const int rel = __ldg(scol + lstart[l] + (e - loff[l])) - static_cast<int>(rs0);
+        const int irs0 = static_cast<int>(rs0);
+        plan_for_products(scol, lstart, loff, nl, loff[nl], [&](int c) {  // plan rows: one chunk of lists
+          const int rel = c - irs0;
           const int sl = slot[rel >> kHvBinBits];
           if (sl != 0xff) atomicAdd(&fine[sl * 128 + (rel & 127)], 1u);
-        }
+        });
         __syncthreads();
         // inclusive prefix per refined bin (a warp per bin)
         for (int sl = wid; sl < kHvFine; sl += kHvPlanG / 32) {
@@ -327,7 +370,6 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
       if (wid == 0) {
         int x0 = s_x0;
         int nw = s_nw;
-        int running = s_running;
         int need = -1;
         // count(x): products of this range with relative column < x (x a bin
         // boundary, or inside a refined bin)
@@ -364,32 +406,18 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
           }
           if (cut - x0 > kHvSpan) cut = (x0 + kHvSpan) & ~((1 << kHvBinBits) - 1);
           cut = min(cut, rlen);
-          // window [x0, cut): its output size = bits set
-          unsigned c = 0;
-          for (int wd = (x0 >> 5) + lane; wd <= ((cut - 1) >> 5); wd += 32) {
-            unsigned m = bm[wd];
-            if (wd == (x0 >> 5)) m &= ~0u << (x0 & 31);
-            if (wd == ((cut - 1) >> 5) && (cut & 31)) m &= (1u << (cut & 31)) - 1u;
-            c += __popc(m);
-          }
-          c = __reduce_add_sync(0xffffffffu, c);
           if (nw >= r.maxwin) {
             if (lane == 0) atomicOr(a.err, 1u);
             need = -2;
             break;
           }
-          if (lane == 0) {
-            a.cuts[r.plan + nw] = static_cast<int>(rs0 + x0);
-            a.wout[r.plan + nw] = running;
-          }
-          running += static_cast<int>(c);
+          if (lane == 0) a.cuts[r.plan + nw] = static_cast<int>(rs0 + x0);
           ++nw;
           x0 = cut;
         }
         if (lane == 0) {
           s_x0 = x0;
           s_nw = nw;
-          s_running = running;
           if (need >= 0) s_need = need; else s_done = 1;
           if (need == -2) s_done = 2;
           if (need == -1 && ptot > 0) s_cnt = static_cast<unsigned long long>(rs0 + x0);  // end of the last window
@@ -399,6 +427,70 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
       if (s_done) break;
     }
     if (s_done == 2) break;
+    // output size of each window of this range = bits set in it: prefix
+    // popcounts of 32-word groups (hist is free now), then two partial
+    // prefixes per window (a warp per window)
+    {
+      const int nwords = (rlen + 31) >> 5, ngroups = (nwords + 31) >> 5;
+      unsigned* gp = hist;  // gp[g] = bits in groups < g
+      for (int g = t; g < ngroups; g += kHvPlanG) {
+        unsigned c = 0;
+        for (int i = 0; i < 32 && 32 * g + i < nwords; ++i) c += __popc(bm[32 * g + i]);
+        gp[g + 1] = c;
+      }
+      __syncthreads();
+      if (wid == 0) {
+        unsigned carry = 0;
+        if (lane == 0) gp[0] = 0;
+        for (int g0 = 1; g0 <= ngroups; g0 += 32) {
+          unsigned x = g0 + lane <= ngroups ? gp[g0 + lane] : 0u;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+          }
+          if (g0 + lane <= ngroups) gp[g0 + lane] = x + carry;
+          carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+      }
+      __syncthreads();
+      auto bits_below = [&](int x) -> unsigned {  // bits set in [0, x), by one warp
+        unsigned c = 0;
+        const int w = x >> 5, g = w >> 5;
+        const int wi = 32 * g + lane;
+        if (wi < w) c = __popc(bm[wi]);
+        else if (wi == w && (x & 31)) c = __popc(bm[wi] & ((1u << (x & 31)) - 1u));
+        return gp[g] + __reduce_add_sync(0xffffffffu, c);
+      };
+      const int nw1 = s_nw, nw0 = s_nwr;
+      for (int w = nw0 + wid; w < nw1; w += kHvPlanG / 32) {
+        const int x0 = a.cuts[r.plan + w] - static_cast<int>(rs0);
+        const int x1 = w + 1 < nw1 ? a.cuts[r.plan + w + 1] - static_cast<int>(rs0) : rlen;
+        const unsigned c = bits_below(x1) - bits_below(x0);
+        if (lane == 0) a.wout[r.plan + w] = static_cast<int>(c);  // a count for now
+      }
+      __syncthreads();
+      if (wid == 0) {  // counts -> output offsets (exclusive, continuing over ranges)
+        int carry = s_running;
+        for (int w0 = nw0; w0 < nw1; w0 += 32) {
+          const int w = w0 + lane;
+          const int c = w < nw1 ? a.wout[r.plan + w] : 0;
+          int x = c;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+          }
+          if (w < nw1) a.wout[r.plan + w] = carry + x - c;
+          carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) {
+          s_running = carry;
+          s_nwr = nw1;
+        }
+      }
+      __syncthreads();
+    }
   }
   __syncthreads();
   if (t == 0) {
@@ -418,11 +510,80 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
 
 // ---------------------------------------------------------------------------
 // Merge: one CTA per task = windows [w0, w1) of one virtual row.
+//
+// The window's rounds of Algorithm 1 run on 64-bit records
+//   key = (pair index q) << 32 | (col - c0) << kHvSB | slot
+// where list m of the current round belongs to pair q = m >> 1 (lines 22-29:
+// lists (2q, 2q+1) are consumed together; an odd trailing list has an empty
+// partner). The even lists are stored concatenated as sequence A, the odd
+// lists as sequence B; both are sorted by (q, col), so a whole round is ONE
+// merge of A with B: equal (q, col) keys are the duplicates of pair q and
+// combine as val[left] = val[left] + val[right] (A holds the left list).
+// An output of pair q is an element of list q of the next round: it goes to
+// A' if q is even, to B' if odd, with key q >> 1. Values never move (slots).
 // ---------------------------------------------------------------------------
+namespace {
+
+using Key = unsigned long long;
+constexpr Key kKeySent = ~0ull;
+constexpr Key kSlotMask = (1ull << kHvSB) - 1ull;
+
+// a before-or-equal b in (q, col) order (slot bits ignored)
+__device__ __forceinline__ bool key_le(Key a, Key b) { return a <= (b | kSlotMask); }
+__device__ __forceinline__ bool key_eq(Key a, Key b) { return (a | kSlotMask) == (b | kSlotMask); }
+
+// number of A elements among the first `diag` merged elements (a-first on ties)
+__device__ __forceinline__ int key_merge_path(const Key* A, int na, const Key* B, int nb, int diag) {
+  int lo = diag - nb > 0 ? diag - nb : 0;
+  int hi = diag < na ? diag : na;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (key_le(A[mid], B[diag - 1 - mid]))
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// inclusive max-scan of u16 owner marks over [0, n) by the CTA (n <= kHvCap)
+__device__ __forceinline__ void owner_max_scan(unsigned short* m, int n, int* wtmp) {
+  constexpr int PER = kHvCap / kHvG;  // 16 per thread
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int b0 = t * PER;
+  unsigned short v[PER];
+  unsigned run = 0;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    v[i] = b0 + i < n ? m[b0 + i] : 0;
+    run = max(run, static_cast<unsigned>(v[i]));
+  }
+  unsigned inc = run;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc = max(inc, y);
+  }
+  if (lane == 31) wtmp[wid] = static_cast<int>(inc);
+  __syncthreads();
+  unsigned pre = 0;
+  for (int w = 0; w < wid; ++w) pre = max(pre, static_cast<unsigned>(wtmp[w]));
+  unsigned ex = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) ex = 0;
+  run = max(pre, ex);
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    run = max(run, static_cast<unsigned>(v[i]));
+    if (b0 + i < n) m[b0 + i] = static_cast<unsigned short>(run);
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
 template <int OUT>
 __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
-  using R = RecPacked<kHvSB>;
-  constexpr int NV = ((kHvCap + kHvLists + 1 + kHvG - 1) / kHvG) | 1;
+  constexpr int NV = (kHvCap + kHvG - 1) / kHvG;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* p = smem;
   auto take = [&](int n) {
@@ -430,26 +591,18 @@ __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
     p += align16(n);
     return q;
   };
+  longlong2* lst = reinterpret_cast<longlong2*>(take(kHvLists * 16));  // {src of layout position 0, A value}
   int64_t* S = reinterpret_cast<int64_t*>(take(kHvLists * 8));
-  double* AV = reinterpret_cast<double*>(take(kHvLists * 8));
   int* L = reinterpret_cast<int*>(take(kHvLists * 4));
   int* cur = reinterpret_cast<int*>(take(kHvLists * 4));
   int* head = reinterpret_cast<int*>(take(kHvLists * 4));
   int* cnt = reinterpret_cast<int*>(take(kHvLists * 4));
-  RecBufs rb;
-  rb.off0 = reinterpret_cast<int*>(take((kHvLists + 2) * 4));
-  rb.off1 = reinterpret_cast<int*>(take((kHvLists + 2) * 4));
-  rb.lst = reinterpret_cast<longlong2*>(take(kHvLists * 16));
-  rb.rec = take((kHvCap + kHvLists + 2) * 4);
-  rb.val = reinterpret_cast<double*>(take(kHvCap * 8));
-  rb.owner = reinterpret_cast<unsigned short*>(rb.val);
-  rb.ostr = 4;
-  rb.bst = nullptr;
-  rb.av = nullptr;
-  rb.scan_tmp = reinterpret_cast<int*>(take((kHvG / 32 + 2) * 4));
-  __shared__ int s_v;
-  const Group<kHvG> g = make_group<kHvG>();
-  const int rank = g.rank;
+  Key* rec = reinterpret_cast<Key*>(take((kHvCap + 2) * 8));
+  double* val = reinterpret_cast<double*>(take(kHvCap * 8));
+  unsigned short* own = reinterpret_cast<unsigned short*>(take(kHvCap * 2));
+  int* wtmp = reinterpret_cast<int*>(take(64));
+  __shared__ int s_v, s_na;
+  const int rank = threadIdx.x;
   const int64_t t = blockIdx.x;
   if (rank == 0) {  // the virtual row of this task: last v with rows[v].task0 <= t
     int64_t lo = 0, hi = a.nrows - 1;
@@ -462,7 +615,7 @@ __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
     }
     s_v = static_cast<int>(lo);
   }
-  g.sync();
+  __syncthreads();
   const int v = s_v;
   const HvRow r = a.rows[v];
   const int nwin = a.nwin[v];
@@ -470,19 +623,21 @@ __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
   if (w0 >= nwin) return;
   const int w1 = min(nwin, w0 + r.wch);
   const int nl = r.nl;
+  const int ne = (nl + 1) >> 1;  // even lists: layout ranks [0, ne), odd lists: [ne, nl)
   const int64_t a0 = r.src == 0 ? a.A.rpt[r.row] : 0;
-  const CsrView Sv{nullptr, r.src == 0 ? a.B.col : a.ws_col, r.src == 0 ? a.B.val : a.ws_val};
+  const int32_t* scol = r.src == 0 ? a.B.col : a.ws_col;
+  const double* sval = r.src == 0 ? a.B.val : a.ws_val;
   const int cfirst = a.cuts[r.plan + w0];
   for (int l = rank; l < nl; l += kHvG) {
     const ListRef Lr = hv_list(a, r, a0, l);
-    const int c0 = w0 == 0 ? 0 : lower_bound_g(Sv.col + Lr.start, Lr.len, cfirst);
+    const int c0 = w0 == 0 ? 0 : lower_bound_g(scol + Lr.start, Lr.len, cfirst);
     S[l] = Lr.start;
     L[l] = Lr.len;
-    AV[l] = r.src == 0 ? __ldg(a.A.val + a0 + r.first + l) : 1.0;
+    lst[l].y = __double_as_longlong(r.src == 0 ? __ldg(a.A.val + a0 + r.first + l) : 1.0);
     cur[l] = c0;
-    head[l] = c0 < Lr.len ? __ldg(Sv.col + Lr.start + c0) : INT_MAX;
+    head[l] = c0 < Lr.len ? __ldg(scol + Lr.start + c0) : INT_MAX;
   }
-  g.sync();
+  __syncthreads();
   int32_t* ocol;
   double* oval;
   int64_t obase;
@@ -495,50 +650,156 @@ __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
     oval = a.wo_val;
     obase = r.obase;
   }
-  typename R::T* rec = static_cast<typename R::T*>(rb.rec);
   for (int w = w0; w < w1; ++w) {
     const int c0 = a.cuts[r.plan + w], c1 = a.cuts[r.plan + w + 1];
-    int* off = rb.off0;
-    int P = 0;
-    for (int lb = 0; lb < nl; lb += kHvG) {
-      const int l = lb + rank;
+    // (1) each list's share of [c0, c1): 8 probes past the cursor (one
+    // latency), then a binary search only if the list goes on inside; the
+    // first column >= c1 becomes the list's new head
+    for (int l = rank; l < nl; l += kHvG) {
       int n = 0;
-      if (l < nl && head[l] < c1) {  // list l's products in [c0, c1): a search from its cursor
+      if (head[l] < c1) {
         const int cu = cur[l];
-        n = 1 + lower_bound_g(Sv.col + S[l] + cu + 1, min(L[l] - cu - 1, kHvCap), c1);
+        const int rem = L[l] - cu;  // >= 1
+        const int32_t* q = scol + S[l] + cu;
+        int pr[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pr[k] = k + 1 < rem ? __ldg(q + k + 1) : INT_MAX;
+        n = 1;
+        int nh = INT_MAX;
+        bool more = true;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (more) {
+            if (pr[k] < c1) {
+              ++n;
+            } else {
+              nh = pr[k];
+              more = false;
+            }
+          }
+        }
+        if (more && n < rem) {  // all 8 probes inside the window: search on
+          const int lim = min(rem, kHvCap + 1);
+          n += lower_bound_g(q + n, lim - n, c1);
+          nh = n < rem ? __ldg(q + n) : INT_MAX;
+        }
+        head[l] = nh;
       }
+      cnt[l] = n;
+    }
+    __syncthreads();
+    // (2) layout: even lists (A) then odd lists (B), in list order; owner
+    // marks at each non-empty list's first position
+    for (int i = rank; i < kHvCap / 8; i += kHvG) reinterpret_cast<uint4*>(own)[i] = make_uint4(0, 0, 0, 0);
+    int P = 0;
+    for (int vb = 0; vb < nl; vb += kHvG) {
+      const int vr = vb + rank;
+      const int m = vr < ne ? 2 * vr : 2 * (vr - ne) + 1;
+      const int n = vr < nl ? cnt[m] : 0;
       int tot;
-      const int ex = group_excl_scan<kHvG>(g, n, tot, rb.scan_tmp);
-      if (l < nl) {
-        off[l] = P + ex + l;
-        rec[P + ex + l + n] = R::sent();
-        rb.lst[l] = make_longlong2(S[l] + cur[l] - (P + ex), __double_as_longlong(AV[l]));
-        cnt[l] = n;
+      const int ex = group_excl_scan<kHvG>(Group<kHvG>{rank, 0xffffffffu, 0}, n, tot, wtmp);
+      if (vr < nl) {
+        const int pos = P + ex;
+        lst[m].x = S[m] + cur[m] - pos;
+        if (n) own[pos] = static_cast<unsigned short>(vr);
+        if (vr == ne - 1) s_na = pos + n;  // nA: the even lists' products
       }
       P += tot;
     }
-    if (rank == 0) {
-      off[nl] = P + nl;
-      rec[P + nl] = R::sent();
+    __syncthreads();
+    const int nA0 = s_na;
+    owner_max_scan(own, P, wtmp);
+    // (3) gather: product at layout position e, record key (m >> 1, col - c0, slot e)
+    // A occupies rec[0, nA), a sentinel at nA, B at [nA + 1, P + 1), a sentinel at P + 1
+#pragma unroll 2
+    for (int e = rank; e < P; e += kHvG) {
+      const int vr = own[e];
+      const int m = vr < ne ? 2 * vr : 2 * (vr - ne) + 1;
+      const longlong2 d = lst[m];
+      const int64_t src = d.x + e;
+      const int c = __ldg(scol + src);
+      val[e] = __dmul_rn(__longlong_as_double(d.y), __ldg(sval + src));  // line 12: the product, rounded once
+      rec[e + (e >= nA0 ? 1 : 0)] =
+          (static_cast<Key>(m >> 1) << 32) | (static_cast<Key>(c - c0) << kHvSB) | static_cast<Key>(e);
     }
-    g.sync();
-    const int T = rec_merge_lists<kHvG, NV, R, true, false>(g, Sv, nl, P, off, rb.off1, rb, c0);
+    if (rank == 0) {
+      rec[nA0] = kKeySent;
+      rec[P + 1] = kKeySent;
+    }
+    __syncthreads();
+    // (4) accumulating phase: ceil(log2 nl) rounds (lines 21-35)
+    int nA = nA0, nB = P - nA0, lists = nl;
+    while (lists > 1) {
+      const Key* A = rec;
+      const Key* B = rec + nA + 1;
+      const int n = nA + nB;
+      const int VT = (n + kHvG - 1) / kHvG;
+      const int g0 = min(rank * VT, n), g1 = min(g0 + VT, n);
+      Key orec[NV];
+      int cntv = 0, cntE = 0;
+      if (g0 < g1) {
+        const int i = key_merge_path(A, nA, B, nB, g0);
+        int j = g0 - i;
+        if (i > 0 && j < nB && key_eq(A[i - 1], B[j])) ++j;  // B[j] was combined on the left
+        int ia = i, ib = j;
+        Key ra = A[ia], rb = B[ib];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          if (k >= VT) break;
+          const bool act = ia + ib < g1;
+          const bool ta = act && key_le(ra, rb);
+          const bool tb = act && key_le(rb, ra);
+          const Key out = ta ? ra : rb;
+          if (ta && tb) {  // a duplicate column of pair q: left + right (Fig. 2)
+            const int sa = static_cast<int>(ra & kSlotMask), sb = static_cast<int>(rb & kSlotMask);
+            val[sa] = __dadd_rn(val[sa], val[sb]);
+          }
+          orec[k] = out;
+          cntv += act;
+          cntE += act && !((out >> 32) & 1ull);
+          ia += ta;
+          ib += tb;
+          if (ta) ra = A[ia];
+          if (tb) rb = B[ib];
+        }
+      }
+      // outputs of even pairs go to A', odd pairs to B' (packed 16 | 16 scan)
+      int tot;
+      const int packed = group_excl_scan<kHvG>(Group<kHvG>{rank, 0xffffffffu, 0}, cntE | ((cntv - cntE) << 16), tot, wtmp);
+      const int nA2 = tot & 0xffff, nB2 = tot >> 16;
+      int pe = packed & 0xffff, po = nA2 + 1 + (packed >> 16);
+      // every thread has read its inputs (group_excl_scan ends synchronised)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        if (k >= cntv) break;
+        const Key x = orec[k];
+        const Key q = x >> 32;
+        const Key y = ((q >> 1) << 32) | (x & 0xffffffffull);
+        if (q & 1ull)
+          rec[po++] = y;
+        else
+          rec[pe++] = y;
+      }
+      if (rank == 0) {
+        rec[nA2] = kKeySent;
+        rec[nA2 + 1 + nB2] = kKeySent;
+      }
+      __syncthreads();
+      nA = nA2;
+      nB = nB2;
+      lists = (lists + 1) >> 1;
+    }
+    // (5) line 36: the window's part of the row (list 0 = A)
+    const int T = nA;
     const int ob = a.wout[r.plan + w];
     if (rank == 0 && T != a.wout[r.plan + w + 1] - ob) atomicOr(a.err, 2u);
     for (int e = rank; e < T; e += kHvG) {
-      const unsigned x = rec[e];
-      ocol[obase + ob + e] = R::col(x) + c0;
-      oval[obase + ob + e] = rb.val[R::slot(x)];
+      const Key x = rec[e];
+      ocol[obase + ob + e] = static_cast<int>((x & 0xffffffffull) >> kHvSB) + c0;
+      oval[obase + ob + e] = val[x & kSlotMask];
     }
-    for (int l = rank; l < nl; l += kHvG) {
-      const int n = cnt[l];
-      if (n) {
-        const int cu = cur[l] + n;
-        cur[l] = cu;
-        head[l] = cu < L[l] ? __ldg(Sv.col + S[l] + cu) : INT_MAX;
-      }
-    }
-    g.sync();
+    for (int l = rank; l < nl; l += kHvG) cur[l] += cnt[l];
+    __syncthreads();
   }
 }
 

@@ -74,6 +74,23 @@ def _all_gather_varlen(x: torch.Tensor, counts: list[int], group=None) -> torch.
     return torch.cat([p[:c] for p, c in zip(parts, counts)])
 
 
+def assemble_rpt(C_blk: TorchCsr, total_rows: int, group=None) -> torch.Tensor:
+    """Global row_ptr of C on every rank (int64[total_rows + 1]) from the row
+    blocks' row pointers: block g's entries shifted by the nnz of blocks < g.
+    C's col/val stay row-distributed (each rank owns its rows)."""
+    dev = C_blk.device
+    world = dist.get_world_size(group)
+    nnz = block_nnz(C_blk.nnz, dev, group).tolist()
+    rows = block_nnz(C_blk.rows, dev, group).tolist()
+    if sum(rows) != total_rows:
+        raise ValueError(f"row blocks cover {sum(rows)} rows, expected {total_rows}")
+    rp = _all_gather_varlen(C_blk.rpt[1:], rows, group)  # drop each block's leading 0
+    shift = torch.repeat_interleave(
+        torch.tensor([sum(nnz[:g]) for g in range(world)], dtype=torch.int64, device=dev),
+        torch.tensor(rows, dtype=torch.int64, device=dev))
+    return torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), rp + shift])
+
+
 def assemble_csr(C_blk: TorchCsr, total_rows: int, group=None) -> TorchCsr:
     """Whole C on every rank from the row blocks (rank order = row order).
     rpt of block g is shifted by the nnz of blocks < g."""

@@ -1,0 +1,85 @@
+"""Two ranks on one GPU (gloo for the collectives), each running the C ABI on
+its n_prod-balanced row block (§III.D): the partition comes from
+the library's own kernels (brm_row_nprod -> brm_exclusive_scan_i64 ->
+brm_partition_rows), B is broadcast from rank 0, each rank computes its block
+of C on cuda:0, and dist.assemble_csr all-gathers the row blocks and row_ptr
+offsets. The assembled C must equal the oracle's bit for bit (columns, row
+pointers, Algorithm-1 values). This is the multi-GPU path of bench.py with
+both ranks' kernels on one device (they never wait on each other's kernels)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case, mode, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from inputs import rmat, uniform_random
+        from paper_2206_06611_b200 import Context, TorchCsr
+        from paper_2206_06611_b200 import dist as bd
+        if case == "rmat":  # heavy rows (windowed path) land on both ranks
+            A = rmat(13, 16, 0.57, 0.19, 0.19, 0.05, seed=9)
+        else:
+            A = uniform_random(30001, 30001, 9, seed=10)
+        B = A
+        ctx = Context(torch.device("cuda", 0))
+        Bd = TorchCsr.from_csr(B) if rank == 0 else None
+        Bc = bd.broadcast_csr(Bd.to("cpu") if rank == 0 else None, src=0, device="cpu")  # gloo: host tensors
+        Bd = Bc.to("cuda")
+        Ad = TorchCsr.from_csr(A)
+        nprod = ctx.brm_row_nprod(Ad, Bd)
+        bounds = ctx.brm_partition_rows(ctx.brm_exclusive_scan_i64(nprod), world).cpu().tolist()
+        assert bounds == oracle.balance_by_nprod(oracle.row_nprod(A, B), world)
+        blk = bd.row_block(Ad, bounds[rank], bounds[rank + 1])
+        Cb = ctx.spgemm(blk, Bd, mode)
+        torch.cuda.synchronize()
+        C = bd.assemble_csr(Cb.to("cpu"), A.rows)
+        ref, _ = oracle.spgemm_brmerge(A, B)
+        ok = (np.array_equal(C.rpt.numpy(), ref.rpt) and np.array_equal(C.col.numpy(), ref.col)
+              and np.array_equal(C.val.numpy(), ref.val))
+        q.put((rank, ok, bounds))
+        ctx.close()
+    except Exception as e:  # surface in the parent
+        import traceback
+        q.put((rank, traceback.format_exc(), None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,mode", [("uniform", "precise"), ("uniform", "upper"), ("rmat", "precise"),
+                                       ("rmat", "upper")])
+def test_two_ranks_one_gpu(case, mode, oracle_mod):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, _ in res:
+        assert ok is True, (rank, ok)
+    assert res[0][2] == res[1][2]

@@ -7,6 +7,7 @@ from collections import defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+by_inst = len(sys.argv) > 3 and sys.argv[3] == "inst"
 agg = defaultdict(lambda: [0, 0, ""])
 fname = "?"
 hdr = None
@@ -37,5 +38,5 @@ for r in rows:
 tot_i = sum(v[0] for v in agg.values()) or 1
 tot_s = sum(v[1] for v in agg.values()) or 1
 print(f"total instr {tot_i:.3g}  samples {tot_s:.3g}")
-for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
+for k, v in sorted(agg.items(), key=lambda x: -x[1][0 if by_inst else 1])[:top]:
     print(f"{100*v[1]/tot_s:5.1f}% stall {100*v[0]/tot_i:5.1f}% inst  {k[0]}:{k[1]}  {v[2].strip()}")
