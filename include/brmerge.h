@@ -79,10 +79,12 @@ typedef struct {
 } brm_csr_t;
 
 /* Number of row bins (tiers) the binning pass sorts rows into; see DESIGN.md
- * "Kernels": 0 = empty rows (n_prod == 0), 1-2 = register tiers (8-lane
- * group, warp), 3-6 = shared-memory record tiers (warp, warp, 128 and
- * 256 threads), 7 = heavy rows (column slabs, list-block decomposition or
- * the global-memory tier; see brm_set_heavy_route).                       */
+ * "Kernels": 0 = empty rows (n_prod == 0), 1 = one thread per row (Alg. 1
+ * literally, P <= 8), 2 = one warp per row in registers (P <= 32), 3-6 =
+ * shared-memory record tiers (warp, warp, 128 and 256 threads per row),
+ * 7 = heavy rows (windowed BRMerge in column windows, in levels of
+ * 1024-list blocks beyond 1024 lists; or the global-memory tier, see
+ * brm_set_heavy_route).                                                     */
 #define BRM_NUM_BINS 8
 
 typedef struct {
@@ -120,10 +122,14 @@ BRM_API brm_status_t brm_set_stream(brm_context_t* ctx, void* stream);
 /* Record per-phase CUDA-event times into brm_stats_t (adds syncs; off by default). */
 BRM_API brm_status_t brm_set_timing(brm_context_t* ctx, int enable);
 /* Route of the heavy rows (bin 7): BRM_HEAVY_AUTO (0,
- * default): rows of <= 512 lists merge in column slabs in shared memory,
- * rows of more lists are split into aligned list blocks; BRM_HEAVY_GLOBAL
- * (1): every heavy row runs on the global-memory tier (testing and
- * comparison). Results are identical. Errors: BRM_ERR_INVALID.            */
+ * default): each row is merged in column windows of <= 4096 products in
+ * shared memory (k_hv_plan picks the windows, k_hv_merge merges them); a
+ * row of more than 1024 lists first merges aligned 1024-list blocks into a
+ * workspace (sub-trees of Algorithm 1's tree) whose results are the next
+ * level's lists. BRM_HEAVY_GLOBAL (1): every heavy row runs on the
+ * global-memory tier instead (one 1024-thread CTA per row, ping-pong
+ * buffers in global memory; testing and comparison). Results are identical,
+ * bit for bit. Errors: BRM_ERR_INVALID.                                     */
 #define BRM_HEAVY_AUTO 0
 #define BRM_HEAVY_GLOBAL 1
 BRM_API brm_status_t brm_set_heavy_route(brm_context_t* ctx, int route);

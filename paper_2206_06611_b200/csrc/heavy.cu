@@ -111,7 +111,7 @@ __device__ __forceinline__ void plan_for_products(const int32_t* scol, const int
   }
   int l = lo;
   for (int eb = e0; eb < e1; eb += 32 * U) {
-    int c[U];
+    int c[U], li[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = eb + 32 * u + lane;
@@ -120,10 +120,26 @@ __device__ __forceinline__ void plan_for_products(const int32_t* scol, const int
         while (loff[l + 1] <= e) ++l;
         c[u] = __ldg(scol + lstart[l] + (e - loff[l]));
       }
+      li[u] = l;
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (c[u] >= 0) fn(c[u]);
+    for (int u = 0; u < U; ++u) fn(c[u], li[u]);  // every lane (warp-level aggregation); c < 0: none
+  }
+}
+
+// Warp-aggregated shared-memory add of 1 per lane to counter[key]: the lanes
+// hold consecutive products, so equal keys of one list are runs of lanes;
+// the last lane of a run adds the run length (one atomic per run instead of
+// one per lane on the same address). key < 0: no product.
+__device__ __forceinline__ void warp_run_add(unsigned* counter, int key, int list) {
+  const int lane = threadIdx.x & 31;
+  const int kp = __shfl_up_sync(0xffffffffu, key, 1), lp = __shfl_up_sync(0xffffffffu, list, 1);
+  const bool start = lane == 0 || kp != key || lp != list;
+  const unsigned starts = __ballot_sync(0xffffffffu, start);
+  const bool end = lane == 31 || ((starts >> (lane + 1)) & 1u);
+  if (end && key >= 0) {
+    const int rs = 31 - __clz(starts & ((2u << lane) - 1u));
+    atomicAdd(&counter[key], static_cast<unsigned>(lane - rs + 1));
   }
 }
 
@@ -237,15 +253,17 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
       // one pass over the chunk's products
       const int irs0 = static_cast<int>(rs0);
       if (count_only) {
-        plan_for_products(scol, lstart, loff, nc, pc, [&](int c) {
-          const int rel = c - irs0;
-          atomicOr(&bm[rel >> 5], 1u << (rel & 31));
+        plan_for_products(scol, lstart, loff, nc, pc, [&](int c, int) {
+          if (c >= 0) {
+            const int rel = c - irs0;
+            atomicOr(&bm[rel >> 5], 1u << (rel & 31));
+          }
         });
       } else {
-        plan_for_products(scol, lstart, loff, nc, pc, [&](int c) {
+        plan_for_products(scol, lstart, loff, nc, pc, [&](int c, int li) {
           const int rel = c - irs0;
-          atomicOr(&bm[rel >> 5], 1u << (rel & 31));
-          atomicAdd(&hist[rel >> kHvBinBits], 1u);
+          if (c >= 0) atomicOr(&bm[rel >> 5], 1u << (rel & 31));
+          warp_run_add(hist, c >= 0 ? rel >> kHvBinBits : -1, li);
         });
       }
       __syncthreads();
@@ -343,10 +361,12 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
         for (int i = t; i < kHvFine * 128; i += kHvPlanG) fine[i] = 0u;
         __syncthreads();
         const int irs0 = static_cast<int>(rs0);
-        plan_for_products(scol, lstart, loff, nl, loff[nl], [&](int c) {  // plan rows: one chunk of lists
-          const int rel = c - irs0;
-          const int sl = slot[rel >> kHvBinBits];
-          if (sl != 0xff) atomicAdd(&fine[sl * 128 + (rel & 127)], 1u);
+        plan_for_products(scol, lstart, loff, nl, loff[nl], [&](int c, int) {  // plan rows: one chunk of lists
+          if (c >= 0) {
+            const int rel = c - irs0;
+            const int sl = slot[rel >> kHvBinBits];
+            if (sl != 0xff) atomicAdd(&fine[sl * 128 + (rel & 127)], 1u);
+          }
         });
         __syncthreads();
         // inclusive prefix per refined bin (a warp per bin)
@@ -528,6 +548,12 @@ using Key = unsigned long long;
 constexpr Key kKeySent = ~0ull;
 constexpr Key kSlotMask = (1ull << kHvSB) - 1ull;
 
+__device__ __forceinline__ void lds_if(bool p, unsigned addr, unsigned long long& v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.b64 %0, [%1];\n\t}"
+               : "+l"(v)
+               : "r"(addr), "r"((unsigned)p));
+}
+
 // a before-or-equal b in (q, col) order (slot bits ignored)
 __device__ __forceinline__ bool key_le(Key a, Key b) { return a <= (b | kSlotMask); }
 __device__ __forceinline__ bool key_eq(Key a, Key b) { return (a | kSlotMask) == (b | kSlotMask); }
@@ -583,7 +609,7 @@ __device__ __forceinline__ void owner_max_scan(unsigned short* m, int n, int* wt
 
 template <int OUT>
 __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
-  constexpr int NV = (kHvCap + kHvG - 1) / kHvG;
+  constexpr int NV = ((kHvCap + kHvG - 1) / kHvG) | 1;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* p = smem;
   auto take = [&](int n) {
@@ -655,37 +681,68 @@ __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
     // (1) each list's share of [c0, c1): 8 probes past the cursor (one
     // latency), then a binary search only if the list goes on inside; the
     // first column >= c1 becomes the list's new head
-    for (int l = rank; l < nl; l += kHvG) {
-      int n = 0;
-      if (head[l] < c1) {
-        const int cu = cur[l];
-        const int rem = L[l] - cu;  // >= 1
-        const int32_t* q = scol + S[l] + cu;
-        int pr[8];
+    {
+      // a thread's lists l = rank + j * kHvG: the probes of all of them are
+      // issued before any is resolved (one memory latency for the batch)
+      constexpr int LPT = kHvLists / kHvG;
+      int pr[LPT][8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) pr[k] = k + 1 < rem ? __ldg(q + k + 1) : INT_MAX;
-        n = 1;
-        int nh = INT_MAX;
-        bool more = true;
+      for (int j = 0; j < LPT; ++j) {
+        const int l = rank + j * kHvG;
+        const bool live = l < nl && head[l] < c1;
+        const int cu = live ? cur[l] : 0;
+        const int rem = live ? L[l] - cu : 0;
+        const int32_t* q = scol + (live ? S[l] + cu : 0);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (more) {
-            if (pr[k] < c1) {
-              ++n;
-            } else {
-              nh = pr[k];
-              more = false;
+        for (int k = 0; k < 8; ++k) pr[j][k] = k + 1 < rem ? __ldg(q + k + 1) : INT_MAX;
+      }
+#pragma unroll
+      for (int j = 0; j < LPT; ++j) {
+        const int l = rank + j * kHvG;
+        if (l >= nl) break;
+        int n = 0;
+        if (head[l] < c1) {
+          const int cu = cur[l];
+          const int rem = L[l] - cu;  // >= 1
+          n = 1;
+          int nh = INT_MAX;
+          bool more = true;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (more) {
+              if (pr[j][k] < c1) {
+                ++n;
+              } else {
+                nh = pr[j][k];
+                more = false;
+              }
             }
           }
+          if (more && n < rem) {  // all 8 probes inside the window: 16-ary search on
+            const int32_t* q = scol + S[l] + cu;
+            int lo = n, hi = min(rem, kHvCap + 1);  // first index >= c1 lies in [lo, hi]
+            while (hi - lo > 16) {
+              const int st = (hi - lo + 15) / 16;
+              int k = 0;
+              int pv[16];
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const int ix = lo + (u + 1) * st - 1;
+                pv[u] = ix < hi ? __ldg(q + ix) : INT_MAX;
+              }
+#pragma unroll
+              for (int u = 0; u < 16; ++u) k += pv[u] < c1;
+              const int nlo = lo + k * st;
+              hi = min(hi, nlo + st - 1);
+              lo = nlo;
+            }
+            n = lo + lower_bound_g(q + lo, hi - lo, c1);
+            nh = n < rem ? __ldg(q + n) : INT_MAX;
+          }
+          head[l] = nh;
         }
-        if (more && n < rem) {  // all 8 probes inside the window: search on
-          const int lim = min(rem, kHvCap + 1);
-          n += lower_bound_g(q + n, lim - n, c1);
-          nh = n < rem ? __ldg(q + n) : INT_MAX;
-        }
-        head[l] = nh;
+        cnt[l] = n;
       }
-      cnt[l] = n;
     }
     __syncthreads();
     // (2) layout: even lists (A) then odd lists (B), in list order; owner
@@ -711,16 +768,41 @@ __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
     owner_max_scan(own, P, wtmp);
     // (3) gather: product at layout position e, record key (m >> 1, col - c0, slot e)
     // A occupies rec[0, nA), a sentinel at nA, B at [nA + 1, P + 1), a sentinel at P + 1
-#pragma unroll 2
-    for (int e = rank; e < P; e += kHvG) {
-      const int vr = own[e];
-      const int m = vr < ne ? 2 * vr : 2 * (vr - ne) + 1;
-      const longlong2 d = lst[m];
-      const int64_t src = d.x + e;
-      const int c = __ldg(scol + src);
-      val[e] = __dmul_rn(__longlong_as_double(d.y), __ldg(sval + src));  // line 12: the product, rounded once
-      rec[e + (e >= nA0 ? 1 : 0)] =
-          (static_cast<Key>(m >> 1) << 32) | (static_cast<Key>(c - c0) << kHvSB) | static_cast<Key>(e);
+    {
+      // a batch of a thread's loads is issued before its products are formed
+      constexpr int PPT = kHvCap / kHvG / 2;
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+      int cg[PPT], mq[PPT];
+      double bv[PPT], av[PPT];
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const int e = rank + (k + half * PPT) * kHvG;
+        cg[k] = 0;
+        bv[k] = 0.0;
+        av[k] = 0.0;
+        mq[k] = 0;
+        if (e < P) {
+          const int vr = own[e];
+          const int m = vr < ne ? 2 * vr : 2 * (vr - ne) + 1;
+          const longlong2 d = lst[m];
+          const int64_t src = d.x + e;
+          cg[k] = __ldg(scol + src);
+          bv[k] = __ldg(sval + src);
+          av[k] = __longlong_as_double(d.y);
+          mq[k] = m >> 1;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const int e = rank + (k + half * PPT) * kHvG;
+        if (e < P) {
+          val[e] = __dmul_rn(av[k], bv[k]);  // line 12: the product, rounded once
+          rec[e + (e >= nA0 ? 1 : 0)] =
+              (static_cast<Key>(mq[k]) << 32) | (static_cast<Key>(cg[k] - c0) << kHvSB) | static_cast<Key>(e);
+        }
+      }
+      }
     }
     if (rank == 0) {
       rec[nA0] = kKeySent;
@@ -733,7 +815,7 @@ __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
       const Key* A = rec;
       const Key* B = rec + nA + 1;
       const int n = nA + nB;
-      const int VT = (n + kHvG - 1) / kHvG;
+      const int VT = min(((n + kHvG - 1) / kHvG) | 1, NV);  // odd: 8-byte strided accesses spread over the banks
       const int g0 = min(rank * VT, n), g1 = min(g0 + VT, n);
       Key orec[NV];
       int cntv = 0, cntE = 0;
@@ -743,6 +825,7 @@ __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
         if (i > 0 && j < nB && key_eq(A[i - 1], B[j])) ++j;  // B[j] was combined on the left
         int ia = i, ib = j;
         Key ra = A[ia], rb = B[ib];
+        const unsigned recb = smem_u32(rec), valb = smem_u32(val);
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
           if (k >= VT) break;
@@ -750,20 +833,27 @@ __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
           const bool ta = act && key_le(ra, rb);
           const bool tb = act && key_le(rb, ra);
           const Key out = ta ? ra : rb;
-          if (ta && tb) {  // a duplicate column of pair q: left + right (Fig. 2)
-            const int sa = static_cast<int>(ra & kSlotMask), sb = static_cast<int>(rb & kSlotMask);
-            val[sa] = __dadd_rn(val[sa], val[sb]);
+          {  // a duplicate column of pair q: val[left] = val[left] + val[right] (Fig. 2), predicated
+            const bool dup = ta && tb;
+            const unsigned sa = valb + 8u * static_cast<unsigned>(ra & kSlotMask);
+            const unsigned sb = valb + 8u * static_cast<unsigned>(rb & kSlotMask);
+            double x = 0.0, y = 0.0;
+            lds_if(dup, sa, x);
+            lds_if(dup, sb, y);
+            if (dup) val[ra & kSlotMask] = __dadd_rn(x, y);
           }
           orec[k] = out;
           cntv += act;
-          cntE += act && !((out >> 32) & 1ull);
           ia += ta;
           ib += tb;
-          if (ta) ra = A[ia];
-          if (tb) rb = B[ib];
+          lds_if(ta, recb + 8u * ia, ra);
+          lds_if(tb, recb + 8u * (nA + 1 + ib), rb);
         }
       }
       // outputs of even pairs go to A', odd pairs to B' (packed 16 | 16 scan)
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        if (k < cntv) cntE += 1 - (static_cast<int>(orec[k] >> 32) & 1);
       int tot;
       const int packed = group_excl_scan<kHvG>(Group<kHvG>{rank, 0xffffffffu, 0}, cntE | ((cntv - cntE) << 16), tot, wtmp);
       const int nA2 = tot & 0xffff, nB2 = tot >> 16;
@@ -772,13 +862,12 @@ __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         if (k >= cntv) break;
-        const Key x = orec[k];
-        const Key q = x >> 32;
-        const Key y = ((q >> 1) << 32) | (x & 0xffffffffull);
-        if (q & 1ull)
-          rec[po++] = y;
-        else
-          rec[pe++] = y;
+        const unsigned q = static_cast<unsigned>(orec[k] >> 32);
+        const unsigned odd = q & 1u;
+        const int dst = odd ? po : pe;
+        po += odd;
+        pe += 1 - odd;
+        rec[dst] = (static_cast<Key>(q >> 1) << 32) | (orec[k] & 0xffffffffull);
       }
       if (rank == 0) {
         rec[nA2] = kKeySent;
