@@ -53,9 +53,8 @@ struct brm_context {
   cudaEvent_t handoff = nullptr;  // orders a stream switch after the old stream's work
   unsigned ev_mask = 0;  // events recorded since the last structure call
   int64_t launches = 0;  // kernels launched since the last structure call
-  brm_context* sub = nullptr;  // heavy-row decomposition runs its sub-products here
-  DevBuf split_rows, split_off, glob_rows, a1_rpt, a1_col, a1_val, a2_rpt, a2_col, a2_val;
-  HostBuf h_rows, h_split;
+  DevBuf glob_rows;
+  HostBuf h_rows;
   // windowed heavy rows (heavy.cuh): rows of <= kHvLists lists ("single",
   // planned in structure, merged in fill under PRECISE) and the levels of
   // rows of more lists ("multi", planned and merged within one call)
@@ -68,15 +67,6 @@ struct brm_context {
   DevBuf hv_lt[2], hv_ws_col[2], hv_ws_val[2], hv_tmp;
   HostBuf h_hv;
 };
-
-namespace {
-brm_status_t heavy_split_impl(brm_context_t* ctx, int out, const RowOut& o, const int32_t* rows, int64_t n,
-                              const int64_t* info, int bs);
-brm_status_t heavy_split(brm_context_t* ctx, int out, const RowOut& o, const int32_t* rows, int64_t n,
-                         const int64_t* info, int bs) {
-  return heavy_split_impl(ctx, out, o, rows, n, info, bs);
-}
-}  // namespace
 
 namespace {
 
@@ -478,93 +468,6 @@ brm_status_t hv_run_multi(brm_context_t* ctx, int out, const RowOut& o, const st
   return BRM_OK;
 }
 
-// Heavy-row decomposition (kernels.cu): the rows (host ids `rows`, host
-// (n_prod, nl) pairs `info`) are processed in batches bounded by free memory;
-// per batch C1 = A1 * B over blocks of bs lists, C2 = A2 * C1
-// over the block results (both through the sub-context, recursively), and C2's
-// rows are scattered into this context's output.
-brm_status_t heavy_split_impl(brm_context_t* ctx, int out, const RowOut& o, const int32_t* rows, int64_t n,
-                              const int64_t* info, int bs) {
-  if (!ctx->sub) {
-    brm_status_t st = brm_create(&ctx->sub, ctx->device, ctx->stream);
-    if (st != BRM_OK) return fail(ctx, st, "heavy rows: cannot create the sub-context");
-  }
-  brm_context_t* sub = ctx->sub;
-  sub->stream = ctx->stream;
-  size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
-  const int64_t budget = std::max<int64_t>((int64_t)(free_b / 3), 256ll << 20);
-  int64_t t0 = 0;
-  while (t0 < n) {
-    // batch [t0, t1): ~5 x 12 B per product (A1, C_bar and C of both sub-products)
-    int64_t t1 = t0, bytes = 0;
-    while (t1 < n && (t1 == t0 || bytes + info[2 * t1] * 60 <= budget)) bytes += info[2 * t1++] * 60;
-    const int nb = (int)(t1 - t0);
-    std::vector<int64_t> hoff(2 * (nb + 1));
-    int64_t* ent = hoff.data();
-    int64_t* blk = hoff.data() + nb + 1;
-    ent[0] = blk[0] = 0;
-    for (int r = 0; r < nb; ++r) {
-      const int64_t nl = info[2 * (t0 + r) + 1];
-      ent[r + 1] = ent[r] + nl;
-      blk[r + 1] = blk[r] + (nl + bs - 1) / bs;
-    }
-    const int64_t ne = ent[nb], nblk = blk[nb];
-    CK(ensure(ctx, ctx->split_rows, (size_t)nb * 4), "alloc split rows");
-    CK(ensure(ctx, ctx->split_off, hoff.size() * 8), "alloc split offsets");
-    CK(ensure_host(ctx->h_split, (size_t)nb * 4 + hoff.size() * 8), "alloc pinned split info");
-    unsigned char* hs = static_cast<unsigned char*>(ctx->h_split.p);
-    memcpy(hs, rows + t0, (size_t)nb * 4);
-    memcpy(hs + (size_t)nb * 4, hoff.data(), hoff.size() * 8);
-    CK(cudaMemcpyAsync(ctx->split_rows.p, hs, (size_t)nb * 4, cudaMemcpyHostToDevice, ctx->stream), "copy split rows");
-    CK(cudaMemcpyAsync(ctx->split_off.p, hs + (size_t)nb * 4, hoff.size() * 8, cudaMemcpyHostToDevice, ctx->stream),
-       "copy split offsets");
-    const int32_t* drows = static_cast<const int32_t*>(ctx->split_rows.p);
-    const int64_t* dent = static_cast<const int64_t*>(ctx->split_off.p);
-    const int64_t* dblk = dent + nb + 1;
-    // level 1: C1 = A1 * B
-    CK(ensure(ctx, ctx->a1_rpt, (size_t)(nblk + 1) * 8), "alloc A1.rpt");
-    CK(ensure(ctx, ctx->a1_col, (size_t)ne * 4), "alloc A1.col");
-    CK(ensure(ctx, ctx->a1_val, (size_t)ne * 8), "alloc A1.val");
-    CK(launch_split_a1(ctx->A, drows, nb, dent, dblk, bs, ne + nblk + 1, static_cast<int64_t*>(ctx->a1_rpt.p),
-                       static_cast<int32_t*>(ctx->a1_col.p), static_cast<double*>(ctx->a1_val.p), ctx->stream),
-       "k_split_a1");
-    ++ctx->launches;
-    const brm_csr_t A1{nblk, ctx->K, ne, static_cast<int64_t*>(ctx->a1_rpt.p), static_cast<int32_t*>(ctx->a1_col.p),
-                       static_cast<double*>(ctx->a1_val.p)};
-    const brm_csr_t Bc{ctx->K, ctx->N, ctx->bnnz, const_cast<int64_t*>(ctx->B.rpt), const_cast<int32_t*>(ctx->B.col),
-                       const_cast<double*>(ctx->B.val)};
-    brm_csr_t C1{};
-    brm_status_t st = brmerge_spgemm(sub, &A1, &Bc, BRM_UPPER, &C1);
-    ctx->launches += sub->launches;
-    if (st != BRM_OK) return fail(ctx, st, std::string("heavy rows, level 1: ") + sub->err);
-    // level 2: C2 = A2 * C1 (A2 = the blocks of each row, value 1.0)
-    CK(ensure(ctx, ctx->a2_rpt, (size_t)(nb + 1) * 8), "alloc A2.rpt");
-    CK(ensure(ctx, ctx->a2_col, (size_t)nblk * 4), "alloc A2.col");
-    CK(ensure(ctx, ctx->a2_val, (size_t)nblk * 8), "alloc A2.val");
-    CK(launch_split_a2(nb, dblk, nblk + nb + 1, static_cast<int64_t*>(ctx->a2_rpt.p),
-                       static_cast<int32_t*>(ctx->a2_col.p), static_cast<double*>(ctx->a2_val.p), ctx->stream),
-       "k_split_a2");
-    ++ctx->launches;
-    const brm_csr_t A2{nb, nblk, nblk, static_cast<int64_t*>(ctx->a2_rpt.p), static_cast<int32_t*>(ctx->a2_col.p),
-                       static_cast<double*>(ctx->a2_val.p)};
-    brm_csr_t C2{};
-    st = brmerge_spgemm(sub, &A2, &C1, BRM_UPPER, &C2);
-    ctx->launches += sub->launches;
-    brm_csr_free(sub, &C1);
-    if (st != BRM_OK) return fail(ctx, st, std::string("heavy rows, level 2: ") + sub->err);
-    CK(launch_scatter_rows(drows, nb, C2.rpt, C2.col, C2.val, out, o, ctx->stream), "k_scatter_rows");
-    ++ctx->launches;
-    brm_csr_free(sub, &C2);
-    t0 = t1;
-  }
-  // the sub-context's grow-only workspace (C_bar of the sub-products) can be
-  // large: release it before the global tier sizes its own workspace
-  brm_destroy(ctx->sub);
-  ctx->sub = nullptr;
-  return BRM_OK;
-}
-
 // Launch the merge of every non-empty bin with output kind `out`.
 brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bin) {
   const int32_t* bins = static_cast<const int32_t*>(ctx->bins.p);
@@ -625,76 +528,28 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
     if (per_bin) ev_record(ctx, kEvBin + 2 * kBinGlobal + 1);
     return BRM_OK;
   }
-  std::vector<int32_t> g_rows, s_rows;
-  std::vector<int64_t> g_info, s_info;
-  // Routes: rows of at most kSlabLists lists merge in
-  // column slabs in shared memory (k_slab); rows of up to kSlab2Lists lists
-  // take two or three levels of column slabs over 64-list blocks (k_slab2)
-  // -- except rows of more than 4096 SHORT lists, which are split into
-  // aligned 32-list blocks (heavy_split: the blocks then fit the
-  // shared-memory tiers); the rest run on the global tier, as does every
-  // heavy row under BRM_HEAVY_GLOBAL. Workspace kinds: 0 = k_slab2,
-  // 2 = global tier.
-  std::vector<int64_t> order, slab;
-  std::vector<int> wkind(nh, 2);
-  const bool auto_route = ctx->heavy_route != BRM_HEAVY_GLOBAL;
-  for (int64_t t = 0; t < nh; ++t) {
-    const int64_t P = ctx->heavy[2 * t], nl = ctx->heavy[2 * t + 1];
-    if (auto_route && nl <= kSlabLists) {
-      slab.push_back(t);
-    } else if (auto_route && nl > 4096 && P <= nl * (int64_t)kSplitAvgLen) {
-      s_rows.push_back(hr[t]);
-      s_info.push_back(P);
-      s_info.push_back(nl);
-    } else {
-      if (auto_route && nl <= kSlab2Lists) wkind[t] = 0;
-      order.push_back(t);
-    }
-  }
-  // by workspace kind, then descending n_prod (a launch lasts as long as its
-  // heaviest rows, so they go first)
-  auto by_nprod = [&](int64_t x, int64_t y) { return ctx->heavy[2 * x] > ctx->heavy[2 * y]; };
+  // BRM_HEAVY_GLOBAL: every heavy row on the global-memory tier, heaviest
+  // first (a launch lasts as long as its heaviest rows)
+  std::vector<int64_t> order(nh);
+  for (int64_t t = 0; t < nh; ++t) order[t] = t;
   std::sort(order.begin(), order.end(),
-            [&](int64_t x, int64_t y) { return wkind[x] != wkind[y] ? wkind[x] < wkind[y] : by_nprod(x, y); });
-  std::sort(slab.begin(), slab.end(), by_nprod);
-  std::vector<int> gkind;
-  for (const int64_t t : order) gkind.push_back(wkind[t]);
+            [&](int64_t x, int64_t y) { return ctx->heavy[2 * x] > ctx->heavy[2 * y]; });
+  std::vector<int32_t> g_rows;
+  std::vector<int64_t> g_info;
   for (const int64_t t : order) {
     g_rows.push_back(hr[t]);
     g_info.push_back(ctx->heavy[2 * t]);
     g_info.push_back(ctx->heavy[2 * t + 1]);
   }
-  if (!s_rows.empty()) {
-    brm_status_t st = heavy_split(ctx, out, o, s_rows.data(), (int64_t)s_rows.size(), s_info.data(), kSplitShort);
-    if (st != BRM_OK) return st;
-  }
-  // one device list: [slab rows | workspace rows]
-  const int64_t nslab = (int64_t)slab.size();
   const int64_t ng = (int64_t)g_rows.size();
-  const int64_t nall = nslab + ng;
-  if (nall > 0) {
-    CK(ensure(ctx, ctx->glob_rows, (size_t)nall * 4), "alloc heavy rows");
-    CK(ensure_host(ctx->h_split, (size_t)nall * 4), "alloc pinned heavy rows");
-    int32_t* hs = static_cast<int32_t*>(ctx->h_split.p);
-    for (int64_t k = 0; k < nslab; ++k) hs[k] = hr[slab[k]];
-    if (ng) memcpy(hs + nslab, g_rows.data(), (size_t)ng * 4);
-    CK(cudaMemcpyAsync(ctx->glob_rows.p, hs, (size_t)nall * 4, cudaMemcpyHostToDevice, ctx->stream),
-       "copy heavy rows");
-  }
-  const int32_t* srows = static_cast<const int32_t*>(ctx->glob_rows.p);
-  if (nslab) {
-    CK(launch_slab(out, ctx->A, ctx->B, ctx->N, srows, nslab, o, ctx->stream), "k_slab");
-    ++ctx->launches;
-  }
+  CK(ensure(ctx, ctx->glob_rows, (size_t)ng * 4), "alloc heavy rows");
+  CK(cudaMemcpyAsync(ctx->glob_rows.p, g_rows.data(), (size_t)ng * 4, cudaMemcpyHostToDevice, ctx->stream),
+     "copy heavy rows");  // pageable source: copied when the call returns
   if (ng > 0) {
-    const int32_t* grows = srows + nslab;
+    const int32_t* grows = static_cast<const int32_t*>(ctx->glob_rows.p);
     const bool vals = out != OUT_SYMBOLIC;
-    // batch the rows so their workspace slices fit the budget; a batch holds
-    // rows of one workspace kind
-    auto row_bytes = [&](int64_t t) {
-      return gkind[t] == 0 ? slab2_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals)
-                           : global_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals);
-    };
+    // batch the rows so their workspace slices fit the budget
+    auto row_bytes = [&](int64_t t) { return global_row_bytes(g_info[2 * t], g_info[2 * t + 1], vals); };
     int64_t max_row = 0;
     for (int64_t t = 0; t < ng; ++t) max_row = std::max(max_row, row_bytes(t));
     size_t free_b = 0, total_b = 0;
@@ -710,7 +565,7 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
     int64_t acc = 0, need = 0;
     for (int64_t t = 0; t < ng; ++t) {
       const int64_t bytes = row_bytes(t);
-      if (t > 0 && (acc + bytes > budget || gkind[t] != gkind[t - 1])) {
+      if (t > 0 && acc + bytes > budget) {
         cuts.push_back(t);
         acc = 0;
       }
@@ -728,11 +583,7 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
       if (n <= 0) continue;
       const int64_t* woff = static_cast<const int64_t*>(ctx->gws_off.p) + 2 * b0;
       unsigned char* ws = static_cast<unsigned char*>(ctx->gws.p);
-      if (gkind[b0] == 0) {
-        CK(launch_slab2(out, ctx->A, ctx->B, ctx->N, grows + b0, n, woff, ws, o, ctx->stream), "k_slab2");
-      } else {
-        CK(launch_global_tier(out, ctx->A, ctx->B, grows + b0, n, woff, ws, o, ctx->stream), "k_global_tier");
-      }
+      CK(launch_global_tier(out, ctx->A, ctx->B, grows + b0, n, woff, ws, o, ctx->stream), "k_global_tier");
       ++ctx->launches;
     }
   }
@@ -913,21 +764,19 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
     for (DevBuf* b : {&ctx->nprod_off, &ctx->row_size, &ctx->bins, &ctx->status, &ctx->small, &ctx->cbar_col,
                       &ctx->cbar_val, &ctx->gws, &ctx->gws_off, &ctx->heavy_info, &ctx->stA_rpt, &ctx->stA_col,
                       &ctx->stA_val, &ctx->stB_rpt, &ctx->stB_col, &ctx->stB_val, &ctx->stC_rpt, &ctx->stC_col,
-                      &ctx->stC_val, &ctx->split_rows, &ctx->split_off, &ctx->glob_rows, &ctx->a1_rpt, &ctx->a1_col,
-                      &ctx->a1_val, &ctx->a2_rpt, &ctx->a2_col, &ctx->a2_val, &ctx->hv_single.d_rows,
+                      &ctx->stC_val, &ctx->glob_rows, &ctx->hv_single.d_rows,
                       &ctx->hv_single.cuts, &ctx->hv_single.wout, &ctx->hv_single.nwin, &ctx->hv_single.total,
                       &ctx->hv_multi.d_rows, &ctx->hv_multi.cuts, &ctx->hv_multi.wout, &ctx->hv_multi.nwin,
                       &ctx->hv_multi.total, &ctx->hv_lt[0], &ctx->hv_lt[1], &ctx->hv_ws_col[0], &ctx->hv_ws_col[1],
                       &ctx->hv_ws_val[0], &ctx->hv_ws_val[1], &ctx->hv_tmp})
       free_dev(ctx, *b);
     cudaStreamSynchronize(ctx->stream);
-    for (HostBuf* b : {&ctx->h_small, &ctx->h_heavy, &ctx->h_gws_off, &ctx->h_C, &ctx->h_rows, &ctx->h_split})
+    for (HostBuf* b : {&ctx->h_small, &ctx->h_heavy, &ctx->h_gws_off, &ctx->h_C, &ctx->h_rows})
       if (b->p) cudaFreeHost(b->p);
     for (auto& e : ctx->ev)
       if (e) cudaEventDestroy(e);
     if (ctx->handoff) cudaEventDestroy(ctx->handoff);
   }
-  if (ctx->sub) brm_destroy(ctx->sub);
   delete ctx;
   return BRM_OK;
 }
@@ -942,7 +791,6 @@ brm_status_t brm_set_stream(brm_context_t* ctx, void* stream) {
   CK(cudaEventRecord(ctx->handoff, ctx->stream), "record stream hand-off");
   CK(cudaStreamWaitEvent(ns, ctx->handoff, 0), "wait for stream hand-off");
   ctx->stream = ns;
-  if (ctx->sub) ctx->sub->stream = ns;
   return BRM_OK;
 }
 

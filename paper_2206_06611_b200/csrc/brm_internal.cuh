@@ -93,20 +93,6 @@ struct TierBounds {
 #define BRM_HASH4 BRM_H4_G, 768, 64, BRM_H4_GPC
 #define BRM_HASH5 128, 3072, 256, 1
 #define BRM_HASH6 256, 6656, 512, 1
-// Heavy rows: rows of at most kSlabLists lists merge
-// in column slabs with shape BRM_SLAB0 (G, CAP, LCAP); rows of up to
-// kSlab2Lists lists in two or three levels of slabs (same shape) over
-// aligned kSlab2Block-list blocks.
-#ifndef BRM_S0_G
-#define BRM_S0_G 128
-#endif
-#ifndef BRM_S0_CAP
-#define BRM_S0_CAP 2048
-#endif
-#define BRM_SLAB0 BRM_S0_G, BRM_S0_CAP, 64
-constexpr int kSlabLists = 64;                                    // = BRM_SLAB0's LCAP
-constexpr int kSlab2Block = 64;
-constexpr int kSlab2Lists = kSlab2Block * kSlab2Block * kSlabLists;  // three levels
 constexpr int kGlobalG = 1024;
 
 __host__ __device__ inline TierBounds tier_bounds() {

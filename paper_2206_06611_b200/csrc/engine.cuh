@@ -14,12 +14,9 @@
 //   values stay in place and duplicates accumulate into the left slot; each
 //   round is one pass of G merge-path chunks of odd length VT; outputs wait
 //   in registers until the group scan gives their compacted positions.
-// slab_row / slab2_row (tier 7): heavy rows merged in column slabs with the
-//   record machinery (rec_merge_lists), in one level (<= 64 lists) or two or
-//   three levels over aligned 64-list blocks; the symbolic pass counts
-//   slabs in a shared hash table.
-// chunk_row (tier 7 fallback): the chunk partition over column/value
-//   ping-pong buffers in a global workspace, one 1024-thread CTA per row.
+// chunk_row (tier 7 under BRM_HEAVY_GLOBAL): the chunk partition over
+//   column/value ping-pong buffers in a global workspace, one 1024-thread CTA
+//   per row. (The default heavy-row path is heavy.cuh.)
 #pragma once
 #include "brm_internal.cuh"
 
@@ -890,293 +887,6 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
     }
   }
   if (OUT != OUT_C && rank == 0) o.row_size[row] = T;
-  g.sync();
-}
-
-// Column slabs of a heavy row (nl <= LCAP lists, any n_prod). Restricting
-// every list to a column range [c0, c1) keeps the number of lists and the
-// pairing of every round (empty lists keep their place in the tree), so each
-// column receives exactly Algorithm 1's additions in Algorithm 1's order; the
-// row is merged slab by slab in shared memory (rec_merge_lists) and the slab
-// results, already in column order, are concatenated. Slab end: every list
-// with r_l products left gets a quota q_l = max(1, (CAP - nl) r_l / sum r)
-// (so sum q_l <= CAP), and c1 = the smallest column found q_l places past a
-// list's cursor: no list contributes more than q_l products (the slab fits
-// CAP) and the list attaining the minimum contributes exactly q_l >= 1 (every
-// slab progresses). Quotas in proportion to what is left fill the slab when
-// the lists spread over the columns alike. A slab in which every list has at
-// most q_l products left is the last one.
-__host__ __device__ constexpr int pow2_floor(int x) {
-  int p = 1;
-  while (2 * p <= x) p <<= 1;
-  return p;
-}
-
-// Number of distinct columns among the P products of nl lists (product
-// offsets off[0..nl], list l's first product at S index rb.bst[l]): every
-// column goes into a shared hash table over the record buffer (H = the power
-// of two >= 3P/2, <= HMAX; multiplicative hash, linear probing, a plain load
-// before atomicCAS); the count is the number of first insertions.
-template <int G, bool NC, int HMAX>
-__device__ __forceinline__ int hash_count_lists(const Group<G>& g, const CsrView& S, int nl, int P, const int* off,
-                                                const RecBufs& rb) {
-  int* table = static_cast<int*>(rb.rec);
-  const int rank = g.rank;
-  int H = 64, hb = 6;
-  while (H < P + P / 2 && H < HMAX) {
-    H <<= 1;
-    ++hb;
-  }
-  for (int e = rank; e < H; e += G) table[e] = kHashEmpty;
-  unsigned short* owner = rb.owner;  // no values in the symbolic pass: ostr == 1
-  for (int l = rank; l < nl; l += G) owner_fill(owner, 1, off[l], off[l + 1], l);
-  g.sync();
-  int cnt = 0;
-  const volatile int* tv = table;
-  for (int e = rank; e < P; e += G) {
-    const int l = owner[e];
-    const int c = src_ld<NC>(S.col + rb.bst[l] + (e - off[l]));
-    unsigned h = (static_cast<unsigned>(c) * 2654435761u) >> (32 - hb);  // the product's high bits
-    while (true) {
-      int cur = tv[h];
-      if (cur == kHashEmpty) {
-        cur = atomicCAS(&table[h], kHashEmpty, c);
-        if (cur == kHashEmpty) {
-          ++cnt;
-          break;
-        }
-      }
-      if (cur == c) break;
-      h = (h + 1) & (H - 1);
-    }
-  }
-  return group_reduce<G, false>(g, cnt, rb.scan_tmp);
-}
-
-// The slab loop over nl lists of a source S: on entry rb.bst[l] = the start
-// of list l in S, bend[j] = the end of list rank + j*G, rb.av[l] = its scale.
-// Each slab's merged result is appended at ocol/oval (skipped when null);
-// returns the number of entries of the merged row. NC: S is read-only for
-// the kernel (B), else S is a workspace this CTA wrote (plain loads).
-template <int G, int NV, int CAP, int LCAP, class R, bool NC, bool COUNT = false>
-__device__ __forceinline__ int64_t slab_run(const Group<G>& g, const CsrView& S, int nl,
-                                            const int64_t (&bend)[(LCAP + G - 1) / G], int32_t* ocol, double* oval,
-                                            const RecBufs& rb) {
-  constexpr bool VALS = R::kVals;
-  // COUNT (symbolic, no output wanted): each slab's distinct columns are
-  // counted in a shared hash table laid over the record buffer (HMAX slots,
-  // slabs of <= 2/3 HMAX products) instead of merged: the slab's columns
-  // are disjoint from every other slab's, so the counts add up to the row size
-  static_assert(!COUNT || !VALS, "COUNT is the symbolic pass");
-  constexpr int HMAX = pow2_floor(CAP + LCAP + 2);
-  constexpr int BUDGET = COUNT ? HMAX * 2 / 3 : CAP;
-  constexpr int LPT = (LCAP + G - 1) / G;  // lists per thread: l = rank + j * G
-  typename R::T* rec = static_cast<typename R::T*>(rb.rec);
-  const int rank = g.rank;
-  int64_t written = 0;
-  while (true) {
-    int rem[LPT], qloc[LPT];
-    int rsum = 0;
-#pragma unroll
-    for (int j = 0; j < LPT; ++j) {
-      const int l = rank + j * G;
-      rem[j] = l < nl ? static_cast<int>(bend[j] - rb.bst[l]) : 0;  // r_l (a row has n_prod < 2^31)
-      rsum += rem[j];
-    }
-    rsum = group_reduce<G, false>(g, rsum, rb.scan_tmp);
-    int cmin = INT_MAX;
-#pragma unroll
-    for (int j = 0; j < LPT; ++j) {
-      const int l = rank + j * G;
-      qloc[j] = max(1, static_cast<int>(static_cast<int64_t>(BUDGET - nl) * rem[j] / max(rsum, 1)));
-      if (l < nl && qloc[j] < rem[j]) cmin = min(cmin, src_ld<NC>(S.col + rb.bst[l] + qloc[j]));
-    }
-    const int c1 = group_reduce<G, true>(g, cmin, rb.scan_tmp);  // INT_MAX: the last slab
-    int* off = rb.off0;
-    int* noff = rb.off1;
-    int nloc[LPT];
-    int P = 0;
-#pragma unroll
-    for (int j = 0; j < LPT; ++j) {
-      const int l = rank + j * G;
-      int n = 0;
-      if (l < nl) {
-        const int64_t st = rb.bst[l];
-        const int avail = min(qloc[j], rem[j]);
-        if (c1 == INT_MAX) {
-          n = avail;
-        } else {  // products of list l with column < c1 (lower bound within its next q)
-          int lo = 0, hi = avail;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (src_ld<NC>(S.col + st + mid) < c1)
-              lo = mid + 1;
-            else
-              hi = mid;
-          }
-          n = lo;
-        }
-      }
-      nloc[j] = n;
-      int tot;
-      const int ex = group_excl_scan<G>(g, n, tot, rb.scan_tmp);
-      if (l < nl) {
-        if (COUNT) {
-          off[l] = P + ex;  // product offsets
-        } else {
-          off[l] = P + ex + l;
-          rec[P + ex + l + n] = R::sent();  // sentinel of list l
-        }
-      }
-      P += tot;
-    }
-    if (rank == 0) {
-      if (COUNT) {
-        off[nl] = P;
-      } else {
-        off[nl] = P + nl;
-        rec[P + nl] = R::sent();  // lone partner sentinel if nl is odd
-      }
-    }
-    g.sync();
-    int T;
-    if constexpr (COUNT)
-      T = hash_count_lists<G, NC, HMAX>(g, S, nl, P, off, rb);
-    else
-      T = rec_merge_lists<G, NV, R, NC>(g, S, nl, P, off, noff, rb);
-    if (!COUNT && ocol) {  // line 36, this slab's part of the row
-      for (int e = rank; e < T; e += G) {
-        const typename R::T r = rec[e];
-        ocol[written + e] = R::col(r);
-        if (VALS && oval) oval[written + e] = rb.val[R::slot(r)];
-      }
-    }
-    written += T;
-    g.sync();
-#pragma unroll
-    for (int j = 0; j < LPT; ++j) {
-      const int l = rank + j * G;
-      if (l < nl) rb.bst[l] += nloc[j];
-    }
-    if (c1 == INT_MAX) break;
-  }
-  return written;
-}
-
-// A heavy row of nl <= LCAP lists in column slabs (slab_run over its B rows).
-template <int G, int NV, int CAP, int LCAP, class R, int OUT>
-__device__ __forceinline__ void slab_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
-                                         const RowOut& o, const RecBufs& rb) {
-  constexpr bool VALS = R::kVals;
-  constexpr int LPT = (LCAP + G - 1) / G;
-  const int rank = g.rank;
-  const int64_t a0 = A.rpt[row];
-  const int nl = static_cast<int>(A.rpt[row + 1] - a0);
-  int64_t bend[LPT];  // end of each of this thread's lists in B; rb.bst[l] is its cursor
-#pragma unroll
-  for (int j = 0; j < LPT; ++j) {
-    const int l = rank + j * G;
-    bend[j] = 0;
-    if (l < nl) {
-      const int k = __ldg(A.col + a0 + l);
-      rb.bst[l] = __ldg(B.rpt + k);
-      bend[j] = __ldg(B.rpt + k + 1);
-      if (VALS) rb.av[l] = __ldg(A.val + a0 + l);
-    }
-  }
-  const int64_t ob = OUT != OUT_SYMBOLIC ? o.base[row] : 0;
-  const int64_t n =
-      slab_run<G, NV, CAP, LCAP, R, true, OUT == OUT_SYMBOLIC>(g, B, nl, bend, OUT != OUT_SYMBOLIC ? o.col + ob : nullptr,
-                                                                VALS && OUT != OUT_SYMBOLIC ? o.val + ob : nullptr, rb);
-  if (OUT != OUT_C && rank == 0) o.row_size[row] = n;
-  g.sync();
-}
-
-// A heavy row of LCAP < nl <= SB * SB * LCAP lists in two or three levels
-// of column slabs. Algorithm 1's tree over the nl lists splits into aligned
-// sub-trees over blocks of SB = 2^k consecutive lists (pairs are (2m, 2m+1)
-// at every level, so an aligned block -- a short last block included -- is
-// merged exactly as Algorithm 1 merges it on its own). Level 1 merges each
-// block's B rows into the workspace ws1; if more than LCAP blocks result,
-// level 2 merges aligned groups of SB block results (an aligned block of
-// blocks is again a sub-tree) into ws2; the last level merges the <= LCAP
-// remaining lists into the output row. Levels above the first scale by 1.0
-// (1.0 * v == v exactly). Block-result offsets: smem `blk` (<= LCAP + 1) or,
-// for level 1 of a three-level row, the global table `tab1` (nb1 + 1).
-template <int G, int NV, int CAP, int LCAP, int SB, class R, int OUT>
-__device__ __forceinline__ void slab2_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
-                                          const RowOut& o, const RecBufs& rb, int32_t* ws1_col, double* ws1_val,
-                                          int32_t* ws2_col, double* ws2_val, int64_t* tab1, int64_t* blk) {
-  constexpr bool VALS = R::kVals;
-  constexpr int LPT = (LCAP + G - 1) / G;
-  static_assert(SB <= LCAP, "a block must fit the slab list capacity");
-  const int rank = g.rank;
-  const int64_t a0 = A.rpt[row];
-  const int nl = static_cast<int>(A.rpt[row + 1] - a0);
-  const int nb1 = (nl + SB - 1) / SB;
-  const bool three = nb1 > LCAP;
-  int64_t* t1 = three ? tab1 : blk;
-  int64_t bend[LPT];
-  int64_t wpos = 0;
-  for (int b = 0; b < nb1; ++b) {  // level 1: blocks of SB lists of B rows
-    const int l0 = b * SB, nlb = min(SB, nl - l0);
-#pragma unroll
-    for (int j = 0; j < LPT; ++j) {
-      const int l = rank + j * G;
-      bend[j] = 0;
-      if (l < nlb) {
-        const int k = __ldg(A.col + a0 + l0 + l);
-        rb.bst[l] = __ldg(B.rpt + k);
-        bend[j] = __ldg(B.rpt + k + 1);
-        if (VALS) rb.av[l] = __ldg(A.val + a0 + l0 + l);
-      }
-    }
-    if (rank == 0) t1[b] = wpos;
-    wpos += slab_run<G, NV, CAP, LCAP, R, true>(g, B, nlb, bend, ws1_col + wpos, VALS ? ws1_val + wpos : nullptr, rb);
-  }
-  if (rank == 0) t1[nb1] = wpos;
-  g.sync();
-  CsrView W{nullptr, ws1_col, ws1_val};
-  int nfin = nb1;
-  if (three) {  // level 2: aligned groups of SB block results
-    const int nb2 = (nb1 + SB - 1) / SB;
-    int64_t wpos2 = 0;
-    for (int c = 0; c < nb2; ++c) {
-      const int l0 = c * SB, nlc = min(SB, nb1 - l0);
-#pragma unroll
-      for (int j = 0; j < LPT; ++j) {
-        const int l = rank + j * G;
-        bend[j] = 0;
-        if (l < nlc) {
-          rb.bst[l] = t1[l0 + l];
-          bend[j] = t1[l0 + l + 1];
-          if (VALS) rb.av[l] = 1.0;
-        }
-      }
-      if (rank == 0) blk[c] = wpos2;
-      wpos2 += slab_run<G, NV, CAP, LCAP, R, false>(g, W, nlc, bend, ws2_col + wpos2, VALS ? ws2_val + wpos2 : nullptr,
-                                                    rb);
-    }
-    if (rank == 0) blk[nb2] = wpos2;
-    g.sync();
-    W = CsrView{nullptr, ws2_col, ws2_val};
-    nfin = nb2;
-  }
-#pragma unroll
-  for (int j = 0; j < LPT; ++j) {  // last level: the <= LCAP block results
-    const int l = rank + j * G;
-    bend[j] = 0;
-    if (l < nfin) {
-      rb.bst[l] = blk[l];
-      bend[j] = blk[l + 1];
-      if (VALS) rb.av[l] = 1.0;
-    }
-  }
-  const int64_t ob = OUT != OUT_SYMBOLIC ? o.base[row] : 0;
-  const int64_t n =
-      slab_run<G, NV, CAP, LCAP, R, false, OUT == OUT_SYMBOLIC>(g, W, nfin, bend, OUT != OUT_SYMBOLIC ? o.col + ob : nullptr,
-                                                                 VALS && OUT != OUT_SYMBOLIC ? o.val + ob : nullptr, rb);
-  if (OUT != OUT_C && rank == 0) o.row_size[row] = n;
   g.sync();
 }
 

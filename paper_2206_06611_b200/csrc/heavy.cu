@@ -90,40 +90,42 @@ __device__ int plan_scan(int* x, int n, int* wtmp) {
 }
 
 // The products [0, pc) of a chunk of lists (list j at lstart[j], products
-// loff[j] .. loff[j+1]) visited by the CTA: warp w takes a contiguous span of
-// products, its lanes consecutive products (coalesced loads), each lane's list
-// index only moves forward; four loads in flight per lane. fn(col).
+// loff[j] .. loff[j+1]) visited by the CTA in items of <= 1024 consecutive
+// products of ONE list (item offsets ioff, built here): a warp takes items
+// round-robin, its lanes read consecutive columns (coalesced, four loads in
+// flight per lane); no per-product list search. fn(col, list) on every lane
+// (col < 0: none).
 template <class Fn>
 __device__ __forceinline__ void plan_for_products(const int32_t* scol, const int64_t* lstart, const int* loff, int nc,
-                                                  int pc, Fn fn) {
-  constexpr int NW = kHvPlanG / 32, U = 4;
+                                                  int pc, int* ioff, int* wtmp, Fn fn) {
+  constexpr int NW = kHvPlanG / 32, U = 4, ITEM = 1024;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int per = ((pc + NW - 1) / NW + 31) & ~31;
-  const int e0 = wid * per, e1 = min(pc, e0 + per);
-  if (e0 >= e1) return;
-  int lo = 0, hi = nc - 1;  // last list starting at or before e0
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (loff[mid] <= e0)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  int l = lo;
-  for (int eb = e0; eb < e1; eb += 32 * U) {
-    int c[U], li[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = eb + 32 * u + lane;
-      c[u] = -1;
-      if (e < e1) {
-        while (loff[l + 1] <= e) ++l;
-        c[u] = __ldg(scol + lstart[l] + (e - loff[l]));
-      }
-      li[u] = l;
+  for (int j = threadIdx.x; j < nc; j += kHvPlanG) ioff[j] = (loff[j + 1] - loff[j] + ITEM - 1) / ITEM;
+  __syncthreads();
+  const int nitems = plan_scan(ioff, nc, wtmp);
+  for (int it = wid; it < nitems; it += NW) {
+    int lo = 0, hi = nc - 1;  // the list of item it: last j with ioff[j] <= it
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ioff[mid] <= it)
+        lo = mid;
+      else
+        hi = mid - 1;
     }
+    const int l = lo;
+    const int b0 = (it - ioff[l]) * ITEM;
+    const int n = min(ITEM, loff[l + 1] - loff[l] - b0);
+    const int32_t* base = scol + lstart[l] + b0;
+    for (int i0 = 0; i0 < n; i0 += 32 * U) {
+      int c[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) fn(c[u], li[u]);  // every lane (warp-level aggregation); c < 0: none
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + 32 * u + lane;
+        c[u] = i < n ? __ldg(base + i) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) fn(c[u], l);
+    }
   }
 }
 
@@ -164,8 +166,8 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
   unsigned* fine = hist + kHvBins;
   unsigned char* slot = reinterpret_cast<unsigned char*>(fine + kHvFine * 128);
   int64_t* lstart = reinterpret_cast<int64_t*>(slot + kHvBins);
-  int* llen = reinterpret_cast<int*>(lstart + kHvLists);
-  int* loff = llen + kHvLists;
+  int* ioff = reinterpret_cast<int*>(lstart + kHvLists);  // items of each list (plan_for_products)
+  int* loff = ioff + kHvLists + 4;
   __shared__ int s_wtmp[kHvPlanG / 32 + 1];
   __shared__ unsigned long long s_cnt;
   __shared__ int s_cmin, s_cmax;
@@ -253,17 +255,19 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
       // one pass over the chunk's products
       const int irs0 = static_cast<int>(rs0);
       if (count_only) {
-        plan_for_products(scol, lstart, loff, nc, pc, [&](int c, int) {
+        plan_for_products(scol, lstart, loff, nc, pc, ioff, s_wtmp, [&](int c, int) {
           if (c >= 0) {
             const int rel = c - irs0;
             atomicOr(&bm[rel >> 5], 1u << (rel & 31));
           }
         });
       } else {
-        plan_for_products(scol, lstart, loff, nc, pc, [&](int c, int li) {
-          const int rel = c - irs0;
-          if (c >= 0) atomicOr(&bm[rel >> 5], 1u << (rel & 31));
-          warp_run_add(hist, c >= 0 ? rel >> kHvBinBits : -1, li);
+        plan_for_products(scol, lstart, loff, nc, pc, ioff, s_wtmp, [&](int c, int) {
+          if (c >= 0) {
+            const int rel = c - irs0;
+            atomicOr(&bm[rel >> 5], 1u << (rel & 31));
+            atomicAdd(&hist[rel >> kHvBinBits], 1u);
+          }
         });
       }
       __syncthreads();
@@ -361,7 +365,7 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
         for (int i = t; i < kHvFine * 128; i += kHvPlanG) fine[i] = 0u;
         __syncthreads();
         const int irs0 = static_cast<int>(rs0);
-        plan_for_products(scol, lstart, loff, nl, loff[nl], [&](int c, int) {  // plan rows: one chunk of lists
+        plan_for_products(scol, lstart, loff, nl, loff[nl], ioff, s_wtmp, [&](int c, int) {  // plan rows: one chunk of lists
           if (c >= 0) {
             const int rel = c - irs0;
             const int sl = slot[rel >> kHvBinBits];

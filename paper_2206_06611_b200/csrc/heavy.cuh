@@ -80,7 +80,7 @@ struct HvArgs {
 
 // plan shared memory: bitmap, histogram, fine counts, bin slots, list table
 constexpr int hv_plan_smem() {
-  return kHvRange / 8 + kHvBins * 4 + kHvFine * 128 * 4 + kHvBins + kHvLists * 8 + kHvLists * 4 +
+  return kHvRange / 8 + kHvBins * 4 + kHvFine * 128 * 4 + kHvBins + kHvLists * 8 + (kHvLists + 4) * 4 +
          align16((kHvLists + 1) * 4) + 256;
 }
 // merge shared memory

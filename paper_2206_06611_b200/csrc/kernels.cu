@@ -9,13 +9,9 @@
 //                    record BRMerge (warp / warp / 128 / 256 threads per row).
 //   k_hash_symbolic  BRMerge-Precise step 3 on tiers 3-6: per-row shared
 //                    hash table counts the distinct columns.
-//   k_slab           tier 7 rows of <= 64 lists: column slabs, CTA per row.
-//   k_slab2          tier 7 rows of 65-262,144 lists: two or three levels of
-//                    column slabs over aligned 64-list blocks.
-//   k_global_tier    tier 7 fallback: ping-pong buffers in a global
-//                    workspace, one 1024-thread CTA per row.
-//   k_split_a1/a2,   tier 7 heavy-row decomposition into aligned 32-list
-//   k_scatter_rows   blocks (sub-trees of Algorithm 1's tree).
+//   (heavy.cu)       tier 7: k_hv_plan / k_hv_merge, windowed BRMerge.
+//   k_global_tier    tier 7 under BRM_HEAVY_GLOBAL: ping-pong buffers in a
+//                    global workspace, one 1024-thread CTA per row.
 //   k_scan_i64       exclusive scan (row_size -> rpt; generic).
 //   k_compact        Step 6 of Fig. 4a: C_bar -> C copy (BRMerge-Upper).
 //   k_partition      §III.D row partition by balanced n_prod (multi-GPU).
@@ -453,60 +449,6 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
   }
 }
 
-// Heavy rows of at most LCAP lists: one CTA of G threads per row, merged in
-// column slabs of <= CAP products (slab_row); rows sorted by n_prod
-// descending, taken grid-stride.
-template <int G, int CAP, int LCAP, bool VALS, int OUT, bool PACK>
-__global__ void __launch_bounds__(G) k_slab(CsrView A, CsrView B, const int32_t* __restrict__ rows, int64_t nrows,
-                                            RowOut o) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  using R = RecT<VALS, PACK, CAP>;
-  const Group<G> g = make_group<G>();
-  const RecBufs rb = rec_bufs<G, CAP, LCAP, R, true>(smem);
-  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x)
-    slab_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, CAP, LCAP, R, OUT>(g, A, B, rows[r], o, rb);
-}
-
-// Heavy rows of kSlabLists < nl <= kSlab2Lists lists: one CTA per row (rows
-// sorted by n_prod descending), two or three levels of column slabs
-// (slab2_row) through the row's workspace slice (ws_off[2i] bytes into ws,
-// n_prod = ws_off[2i+1]; layout and size: slab2_layout / slab2_row_bytes).
-struct Slab2Layout {
-  int64_t col1, val1, col2, val2, tab1, bytes;  // byte offsets in the slice
-};
-__host__ __device__ inline Slab2Layout slab2_layout(int64_t P, int64_t nl, bool vals, int lcap) {
-  auto a = [](int64_t b) { return (b + 15) & ~15ll; };
-  const int64_t nb1 = (nl + kSlab2Block - 1) / kSlab2Block;
-  const bool three = nb1 > lcap;
-  Slab2Layout L{};
-  L.col1 = 0;
-  L.val1 = a(P * 4);
-  L.col2 = L.val1 + (vals ? a(P * 8) : 0);
-  L.val2 = L.col2 + (three ? a(P * 4) : 0);
-  L.tab1 = L.val2 + (three && vals ? a(P * 8) : 0);
-  L.bytes = L.tab1 + (three ? a((nb1 + 1) * 8) : 0);
-  return L;
-}
-
-template <int G, int CAP, int LCAP, bool VALS, int OUT, bool PACK>
-__global__ void __launch_bounds__(G) k_slab2(CsrView A, CsrView B, const int32_t* __restrict__ rows,
-                                             const int64_t* __restrict__ ws_off, unsigned char* __restrict__ ws,
-                                             RowOut o) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  using R = RecT<VALS, PACK, CAP>;
-  const Group<G> g = make_group<G>();
-  const RecBufs rb = rec_bufs<G, CAP, LCAP, R, true>(smem);
-  int64_t* blk = reinterpret_cast<int64_t*>(smem + rec_group_bytes<G, CAP, LCAP, R, true>());
-  const int64_t row = rows[blockIdx.x];
-  const int64_t P = ws_off[2 * blockIdx.x + 1];
-  const Slab2Layout L = slab2_layout(P, A.rpt[row + 1] - A.rpt[row], VALS, LCAP);
-  unsigned char* p = ws + ws_off[2 * blockIdx.x];
-  slab2_row<G, ((CAP + LCAP + 1 + G - 1) / G) | 1, CAP, LCAP, kSlab2Block, R, OUT>(
-      g, A, B, row, o, rb, reinterpret_cast<int32_t*>(p + L.col1), VALS ? reinterpret_cast<double*>(p + L.val1) : nullptr,
-      reinterpret_cast<int32_t*>(p + L.col2), VALS ? reinterpret_cast<double*>(p + L.val2) : nullptr,
-      reinterpret_cast<int64_t*>(p + L.tab1), blk);
-}
-
 // PRECISE symbolic phase of tiers 3-6: hash_row per group (GPC groups of G).
 template <int G, int CAP, int LCAP, int GPC>
 __global__ void __launch_bounds__(G * GPC) k_hash_symbolic(CsrView A, CsrView B, const int32_t* __restrict__ rows,
@@ -573,112 +515,6 @@ __global__ void __launch_bounds__(kGlobalG) k_global_tier(CsrView A, CsrView B, 
   cb.av = VALS ? reinterpret_cast<double*>(take(nl * 8)) : nullptr;
   cb.scan_tmp = scan_tmp;
   chunk_row<kGlobalG, VALS, OUT>(g, A, B, row, o, cb);
-}
-
-// ---------------------------------------------------------------------------
-// Heavy-row decomposition (tier 7 rows of more lists than the column slabs
-// take). Algorithm 1's tree over a row's nl lists splits into aligned
-// sub-trees over blocks of bs = 2^k consecutive lists (32 for rows of short
-// lists, 512 for long ones; pairs are (2m, 2m+1) at every level,
-// so an aligned block is merged exactly as Algorithm 1 would merge it on its
-// own, a short last block included). Level 1: every block becomes a row of
-// A1 (a copy of the block's A entries) and C1 = A1 * B runs through the
-// ordinary tiers. Level 2: row i of A2 lists its blocks' rows of C1 with
-// value 1.0 (1.0 * v == v exactly), so C2 = A2 * C1 merges the block results
-// in the same tree order; C2 may itself be heavy and split again.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int upper_row(const int64_t* off, int n, int64_t e) {  // last r with off[r] <= e
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= e)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  return lo;
-}
-
-// A1: rows = blocks; ent_off / blk_off = exclusive prefix sums over the
-// batch rows of nl_i and ceil(nl_i / kSplitLists).
-__global__ void k_split_a1(CsrView A, const int32_t* __restrict__ rows, int n, const int64_t* __restrict__ ent_off,
-                           const int64_t* __restrict__ blk_off, int bs, int64_t* __restrict__ a1_rpt,
-                           int32_t* __restrict__ a1_col, double* __restrict__ a1_val) {
-  const int64_t ne = ent_off[n], nb = blk_off[n];
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ne + nb + 1;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    if (t < ne) {
-      const int r = upper_row(ent_off, n, t);
-      const int64_t src = A.rpt[rows[r]] + (t - ent_off[r]);
-      a1_col[t] = A.col[src];
-      a1_val[t] = A.val[src];
-    } else if (t < ne + nb) {
-      const int64_t b = t - ne;
-      const int r = upper_row(blk_off, n, b);
-      a1_rpt[b] = ent_off[r] + (int64_t)bs * (b - blk_off[r]);
-    } else {
-      a1_rpt[nb] = ne;
-    }
-  }
-}
-
-// A2: row r lists blocks blk_off[r] .. blk_off[r+1]-1 of C1 with value 1.0.
-__global__ void k_split_a2(int n, const int64_t* __restrict__ blk_off, int64_t* __restrict__ a2_rpt,
-                           int32_t* __restrict__ a2_col, double* __restrict__ a2_val) {
-  const int64_t nb = blk_off[n];
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= nb + n; t += (int64_t)gridDim.x * blockDim.x) {
-    if (t < nb) {
-      a2_col[t] = (int32_t)t;
-      a2_val[t] = 1.0;
-    } else {
-      a2_rpt[t - nb] = blk_off[t - nb];
-    }
-  }
-}
-
-// Row r of C2 (rpt2/col2/val2) is output row rows[r]: its size goes to
-// row_size (OUT_SYMBOLIC / OUT_CBAR), its entries to the output at base[row].
-__global__ void k_scatter_rows(const int32_t* __restrict__ rows, int n, const int64_t* __restrict__ rpt2,
-                               const int32_t* __restrict__ col2, const double* __restrict__ val2, int out_kind,
-                               RowOut o) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = w; r < n; r += nw) {
-    const int64_t row = rows[r];
-    const int64_t s = rpt2[r], len = rpt2[r + 1] - s;
-    if (out_kind != OUT_C && lane == 0) o.row_size[row] = len;
-    if (out_kind == OUT_SYMBOLIC) continue;
-    const int64_t d = o.base[row];
-    for (int64_t e = lane; e < len; e += 32) {
-      o.col[d + e] = col2[s + e];
-      o.val[d + e] = val2[s + e];
-    }
-  }
-}
-
-cudaError_t launch_split_a1(const CsrView& A, const int32_t* rows, int n, const int64_t* ent_off,
-                            const int64_t* blk_off, int bs, int64_t total, int64_t* a1_rpt, int32_t* a1_col,
-                            double* a1_val, cudaStream_t st) {
-  const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
-  k_split_a1<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(A, rows, n, ent_off, blk_off, bs, a1_rpt, a1_col,
-                                                                      a1_val);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_split_a2(int n, const int64_t* blk_off, int64_t total, int64_t* a2_rpt, int32_t* a2_col,
-                            double* a2_val, cudaStream_t st) {
-  const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
-  k_split_a2<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(n, blk_off, a2_rpt, a2_col, a2_val);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_scatter_rows(const int32_t* rows, int n, const int64_t* rpt2, const int32_t* col2,
-                                const double* val2, int out_kind, const RowOut& o, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  const int64_t blocks = std::min<int64_t>(((int64_t)n * 32 + 255) / 256, (int64_t)num_sms() * 16);
-  k_scatter_rows<<<(unsigned)blocks, 256, 0, st>>>(rows, n, rpt2, col2, val2, out_kind, o);
-  return cudaGetLastError();
 }
 
 // Step 6 of Fig. 4a: copy each row of C_bar (at its n_prod offset) to C.
@@ -892,81 +728,6 @@ static cudaError_t launch_tier_t(const CsrView& A, const CsrView& B, int64_t b_c
     if (rec_pack_ok(CAP, b_cols)) return launch_tier_pk<G, CAP, LCAP, GPC, PLAIN, VALS, OUT, true>(A, B, rows, n, o, st);
   }
   return launch_tier_pk<G, CAP, LCAP, GPC, PLAIN, VALS, OUT, false>(A, B, rows, n, o, st);
-}
-
-template <int G, int CAP, int LCAP, bool VALS, int OUT, bool PACK>
-static cudaError_t launch_slab_pk(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
-                                  cudaStream_t st) {
-  constexpr int smem = rec_group_bytes<G, CAP, LCAP, RecT<VALS, PACK, CAP>, true>();
-  static_assert(smem <= 232448, "slab shared memory exceeds 227 KB");
-  static_assert((((CAP + LCAP + 1 + G - 1) / G) | 1) <= 29, "slab NV must stay <= 29");
-  auto kern = k_slab<G, CAP, LCAP, VALS, OUT, PACK>;
-  static LaunchSetup ls;
-  int per_sm = 0;
-  if (cudaError_t e = kernel_setup(ls, kern, G, smem, per_sm); e != cudaSuccess) return e;
-  const int64_t cap = (int64_t)per_sm * num_sms();
-  kern<<<(unsigned)(n < cap ? n : cap), G, smem, st>>>(A, B, rows, n, o);
-  return cudaGetLastError();
-}
-
-template <int G, int CAP, int LCAP, bool VALS, int OUT>
-static cudaError_t launch_slab_t(const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows, int64_t n,
-                                 const RowOut& o, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  if constexpr (VALS) {
-    if (rec_pack_ok(CAP, b_cols)) return launch_slab_pk<G, CAP, LCAP, VALS, OUT, true>(A, B, rows, n, o, st);
-  }
-  return launch_slab_pk<G, CAP, LCAP, VALS, OUT, false>(A, B, rows, n, o, st);
-}
-
-template <int G, int CAP, int LCAP, bool VALS, int OUT, bool PACK>
-static cudaError_t launch_slab2_pk(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
-                                   const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st) {
-  constexpr int smem = rec_group_bytes<G, CAP, LCAP, RecT<VALS, PACK, CAP>, true>() + (LCAP + 1) * 8;
-  static_assert(smem <= 232448, "slab shared memory exceeds 227 KB");
-  auto kern = k_slab2<G, CAP, LCAP, VALS, OUT, PACK>;
-  static LaunchSetup ls;
-  int per_sm = 0;
-  if (cudaError_t e = kernel_setup(ls, kern, G, smem, per_sm); e != cudaSuccess) return e;
-  kern<<<(unsigned)n, G, smem, st>>>(A, B, rows, ws_off, ws, o);
-  return cudaGetLastError();
-}
-
-template <int G, int CAP, int LCAP, int OUT>
-static cudaError_t launch_slab2_t(const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows, int64_t n,
-                                  const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st) {
-  constexpr bool VALS = OUT != OUT_SYMBOLIC;
-  if (n <= 0) return cudaSuccess;
-  if constexpr (VALS) {
-    if (rec_pack_ok(CAP, b_cols))
-      return launch_slab2_pk<G, CAP, LCAP, VALS, OUT, true>(A, B, rows, n, ws_off, ws, o, st);
-  }
-  return launch_slab2_pk<G, CAP, LCAP, VALS, OUT, false>(A, B, rows, n, ws_off, ws, o, st);
-}
-
-cudaError_t launch_slab2(int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
-                         int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st) {
-  switch (out_kind) {
-    case OUT_SYMBOLIC: return launch_slab2_t<BRM_SLAB0, OUT_SYMBOLIC>(A, B, b_cols, rows, n, ws_off, ws, o, st);
-    case OUT_CBAR: return launch_slab2_t<BRM_SLAB0, OUT_CBAR>(A, B, b_cols, rows, n, ws_off, ws, o, st);
-    case OUT_C: return launch_slab2_t<BRM_SLAB0, OUT_C>(A, B, b_cols, rows, n, ws_off, ws, o, st);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
-int64_t slab2_row_bytes(int64_t nprod, int64_t nl, bool vals) {
-  constexpr int kLcap = kSlab2Lists / (kSlab2Block * kSlab2Block);
-  return slab2_layout(nprod, nl, vals, kLcap).bytes;
-}
-
-cudaError_t launch_slab(int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
-                        int64_t n, const RowOut& o, cudaStream_t st) {
-  switch (out_kind) {
-    case OUT_SYMBOLIC: return launch_slab_t<BRM_SLAB0, false, OUT_SYMBOLIC>(A, B, b_cols, rows, n, o, st);
-    case OUT_CBAR: return launch_slab_t<BRM_SLAB0, true, OUT_CBAR>(A, B, b_cols, rows, n, o, st);
-    case OUT_C: return launch_slab_t<BRM_SLAB0, true, OUT_C>(A, B, b_cols, rows, n, o, st);
-    default: return cudaErrorInvalidValue;
-  }
 }
 
 template <bool VALS, int OUT>

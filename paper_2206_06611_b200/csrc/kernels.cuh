@@ -32,15 +32,6 @@ cudaError_t launch_heavy_info(const CsrView& A, const int64_t* nprod_off, const 
 // bits when the columns fit)
 cudaError_t launch_tier(int bin, int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
                         int64_t n, const RowOut& o, cudaStream_t st);
-// heavy rows of <= kSlabLists lists merged in column slabs; rows sorted by
-// n_prod descending
-cudaError_t launch_slab(int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
-                        int64_t n, const RowOut& o, cudaStream_t st);
-// heavy rows of kSlabLists < nl <= kSlab2Lists lists: two or three levels of
-// column slabs, one CTA per row, workspace slices like the global tier's
-cudaError_t launch_slab2(int out_kind, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
-                         int64_t n, const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st);
-int64_t slab2_row_bytes(int64_t nprod, int64_t nl, bool vals);
 int64_t global_row_bytes(int64_t nprod, int64_t nl, bool vals);
 cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
                                const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st);
@@ -48,17 +39,5 @@ cudaError_t launch_compact(int64_t M, int64_t nnz, const int64_t* nprod_off, con
                            const double* cbar_val, int32_t* ccol, double* cval, cudaStream_t st);
 cudaError_t launch_partition(const int64_t* nprod_off, int64_t M, int p, int64_t* bounds, cudaStream_t st);
 cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod, cudaStream_t st);
-
-// heavy-row decomposition (kernels.cu "Heavy-row decomposition")
-constexpr int kSplitShort = 32;   // block of lists for rows of short lists (mean length <= kSplitAvgLen)
-constexpr int kSplitAvgLen = 32;
-
-cudaError_t launch_split_a1(const CsrView& A, const int32_t* rows, int n, const int64_t* ent_off,
-                            const int64_t* blk_off, int bs, int64_t total, int64_t* a1_rpt, int32_t* a1_col,
-                            double* a1_val, cudaStream_t st);
-cudaError_t launch_split_a2(int n, const int64_t* blk_off, int64_t total, int64_t* a2_rpt, int32_t* a2_col,
-                            double* a2_val, cudaStream_t st);
-cudaError_t launch_scatter_rows(const int32_t* rows, int n, const int64_t* rpt2, const int32_t* col2,
-                                const double* val2, int out_kind, const RowOut& o, cudaStream_t st);
 
 }  // namespace brm
