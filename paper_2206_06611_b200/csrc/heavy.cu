@@ -578,7 +578,7 @@ __device__ __forceinline__ int key_merge_path(const Key* A, int na, const Key* B
 
 // inclusive max-scan of u16 owner marks over [0, n) by the CTA (n <= kHvCap)
 __device__ __forceinline__ void owner_max_scan(unsigned short* m, int n, int* wtmp) {
-  constexpr int PER = kHvCap / kHvG;  // 16 per thread
+  constexpr int PER = (kHvCap + kHvG - 1) / kHvG;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int b0 = t * PER;
   unsigned short v[PER];
@@ -612,7 +612,7 @@ __device__ __forceinline__ void owner_max_scan(unsigned short* m, int n, int* wt
 }  // namespace
 
 template <int OUT>
-__global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
+__global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOut o) {
   constexpr int NV = ((kHvCap + kHvG - 1) / kHvG) | 1;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* p = smem;
@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
     {
       // a thread's lists l = rank + j * kHvG: the probes of all of them are
       // issued before any is resolved (one memory latency for the batch)
-      constexpr int LPT = kHvLists / kHvG;
+      constexpr int LPT = (kHvLists + kHvG - 1) / kHvG;
       int pr[LPT][8];
 #pragma unroll
       for (int j = 0; j < LPT; ++j) {
@@ -774,7 +774,7 @@ __global__ void __launch_bounds__(kHvG, 2) k_hv_merge(HvArgs a, RowOut o) {
     // A occupies rec[0, nA), a sentinel at nA, B at [nA + 1, P + 1), a sentinel at P + 1
     {
       // a batch of a thread's loads is issued before its products are formed
-      constexpr int PPT = kHvCap / kHvG / 2;
+      constexpr int PPT = ((kHvCap + kHvG - 1) / kHvG + 1) / 2;
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
       int cg[PPT], mq[PPT];

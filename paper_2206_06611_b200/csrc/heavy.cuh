@@ -29,10 +29,24 @@
 
 namespace brm {
 
-constexpr int kHvCap = 4096;       // products per window
-constexpr int kHvSB = 12;          // slot bits of a packed record (rec_slot_bits(kHvCap))
-constexpr int kHvLists = 1024;     // lists per virtual row: an aligned 2^10-list sub-tree
-constexpr int kHvG = 256;          // merge CTA
+// (tuning overrides: BRM_NVCC_FLAGS="-DBRM_HV_CAP=3072 -DBRM_HV_MINB=3", tools/variants.sh)
+#ifndef BRM_HV_CAP
+#define BRM_HV_CAP 4096
+#endif
+#ifndef BRM_HV_LISTS
+#define BRM_HV_LISTS 1024
+#endif
+#ifndef BRM_HV_G
+#define BRM_HV_G 256
+#endif
+#ifndef BRM_HV_MINB
+#define BRM_HV_MINB 2
+#endif
+constexpr int kHvCap = BRM_HV_CAP;      // products per window
+constexpr int kHvSB = 12;               // slot bits of a record (slots 0 .. kHvCap - 1)
+constexpr int kHvLists = BRM_HV_LISTS;  // lists per virtual row: an aligned 2^k-list sub-tree
+constexpr int kHvG = BRM_HV_G;          // merge CTA
+constexpr int kHvMinBlocks = BRM_HV_MINB;  // merge CTAs per SM (launch bounds)
 constexpr int kHvPlanG = 512;      // plan CTA
 constexpr int kHvRangeBits = 20;   // bitmap over 2^20 columns per pass ("range")
 constexpr int kHvRange = 1 << kHvRangeBits;
@@ -42,7 +56,8 @@ constexpr int kHvFine = 64;        // bins refined to single columns per refinem
 // records pack col - c0 into 32 - kHvSB bits; the all-ones word (column
 // 2^20 - 1) is the sentinel, so a window spans at most 2^20 - 1 columns
 constexpr int kHvSpan = (1 << (32 - kHvSB)) - 1;
-static_assert((1 << kHvSB) == kHvCap, "slot bits");
+static_assert(kHvCap <= (1 << kHvSB), "slot bits");
+static_assert((kHvLists & (kHvLists - 1)) == 0, "a block of lists must be an aligned power-of-two sub-tree");
 static_assert(kHvLists <= kHvCap, "a column holds at most one product per list: a single column fits a window");
 
 struct HvRow {
