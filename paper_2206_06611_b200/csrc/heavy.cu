@@ -442,7 +442,9 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
         if (lane == 0) {
           s_x0 = x0;
           s_nw = nw;
-          if (need >= 0) s_need = need; else s_done = 1;
+          // a window start inside a refined bin keeps that bin refined: the
+          // next group of refined bins starts at x0's bin
+          if (need >= 0) s_need = (x0 & 127) ? min(need, x0 >> kHvBinBits) : need; else s_done = 1;
           if (need == -2) s_done = 2;
           if (need == -1 && ptot > 0) s_cnt = static_cast<unsigned long long>(rs0 + x0);  // end of the last window
         }

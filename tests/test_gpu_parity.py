@@ -428,3 +428,33 @@ def test_alg1_pairing_order_hand_derived(ctx):
             rpt, col, val = run(ctx, A, B, mode)
             assert rpt.tolist() == [0, 1] and col.tolist() == [0]
             assert val[0] == tree(vals), (vals, mode, val[0], tree(vals))
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_heavy_dense_refined_windows(ctx, oracle_mod, mode):
+    """Heavy rows whose lists are dense over the same columns: every
+    128-column histogram bin holds more products than a window (> 4096), so
+    the windows are cut inside bins from per-column counts, in several
+    refinement passes (> 64 such bins), with window starts inside refined
+    bins; plus a row mixing dense and sparse lists and one of > 1024 lists."""
+    rng = np.random.default_rng(41)
+    ncols = 40000
+    rows_b = []
+    for k in range(100):  # 100 dense lists over columns [0, 10000) with a few gaps
+        c = np.arange(10000)
+        c = c[rng.random(c.size) > 0.02]
+        rows_b.append(c)
+    for k in range(1100):  # sparse lists over the whole range
+        rows_b.append(np.sort(rng.choice(ncols, size=int(rng.integers(0, 60)), replace=False)))
+    lens = np.array([r.size for r in rows_b])
+    rpt = np.zeros(lens.size + 1, np.int64)
+    np.cumsum(lens, out=rpt[1:])
+    bcol = np.concatenate(rows_b).astype(np.int32)
+    B = Csr(lens.size, ncols, rpt, bcol, rng.uniform(-1, 1, size=bcol.size))
+    specs = [np.arange(100), np.concatenate([np.arange(0, 100, 3), np.arange(100, 600)]),
+             np.arange(0, 1200)]
+    acol = [np.sort(s).astype(np.int32) for s in specs]
+    arpt = np.concatenate([[0], np.cumsum([a.size for a in acol])]).astype(np.int64)
+    acol = np.concatenate(acol)
+    A = Csr(len(specs), B.rows, arpt, acol, rng.uniform(-1, 1, size=acol.size))
+    compare(run(ctx, A, B, mode), A, B)
