@@ -108,7 +108,7 @@ def stencil27_box(nx, ny, nz, seed):
 TIER_CAP = [0, 8, 32, 256, 768, 3072, 6656]
 TIER_LCAP = [0, 8, 32, 64, 64, 256, 512]
 NUM_BINS = 8
-HV_LISTS = 1024  # heavy rows of at most this many lists merge in one level (csrc/heavy.cuh kHvLists)
+HV_LISTS = 512  # heavy rows of at most this many lists merge in one level (csrc/heavy.cuh kHvLists)
 
 
 def tier_of(nprod: np.ndarray, nl: np.ndarray) -> np.ndarray:
@@ -371,7 +371,7 @@ def main():
         cand[f"{'k_tiny' if b == 1 else 'k_tier'} (tier {b} numeric merge)"] = (
             bin_ms[b] / args.steps, np.nonzero(tiers == b)[0])
     if hv_merge_ms > 0:
-        cand["k_hv_merge (heavy rows of <= 1024 lists, windowed merge)"] = (
+        cand[f"k_hv_merge (heavy rows of <= {HV_LISTS} lists, windowed merge)"] = (
             hv_merge_ms / args.steps, np.nonzero((tiers == NUM_BINS - 1) & (nl_loc <= HV_LISTS))[0])
     dom_name = max(cand, key=lambda k: cand[k][0])
     dom_ms, dom_rows = cand[dom_name]
@@ -461,7 +461,7 @@ def main():
                           "numeric": num_ms / args.steps, "rowsize_scan": scan_ms / args.steps,
                           "compact": cmp_ms / args.steps, "numeric_per_bin": (bin_ms / args.steps).tolist(),
                           "heavy_plan": hv_plan_ms / args.steps, "heavy_merge_one_level": hv_merge_ms / args.steps},
-            "heavy_rows": {"one_level": stats["hv_rows_one"], "levels_of_1024_list_blocks": stats["hv_rows_multi"]},
+            "heavy_rows": {"one_level": stats["hv_rows_one"], f"levels_of_{HV_LISTS}_list_blocks": stats["hv_rows_multi"]},
             "bin_rows": stats["bin_rows"],
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks,

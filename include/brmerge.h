@@ -83,7 +83,7 @@ typedef struct {
  * literally, P <= 8), 2 = one warp per row in registers (P <= 32), 3-6 =
  * shared-memory record tiers (warp, warp, 128 and 256 threads per row),
  * 7 = heavy rows (windowed BRMerge in column windows, in levels of
- * 1024-list blocks beyond 1024 lists; or the global-memory tier, see
+ * 512-list blocks beyond 512 lists; or the global-memory tier, see
  * brm_set_heavy_route).                                                     */
 #define BRM_NUM_BINS 8
 
@@ -103,10 +103,10 @@ typedef struct {
   float ms_compact;                 /* UPPER: C_bar -> C compaction            */
   float ms_bin_numeric[BRM_NUM_BINS]; /* numeric merge per tier              */
   int64_t launches;                 /* kernels launched by the last structure+fill */
-  float ms_hv_plan;                 /* heavy rows of <= 1024 lists: window plan (k_hv_plan) */
-  float ms_hv_merge;                /* heavy rows of <= 1024 lists: windowed merge (k_hv_merge) */
-  int64_t hv_rows_one;              /* heavy rows merged in one level (<= 1024 lists)          */
-  int64_t hv_rows_multi;            /* heavy rows merged in levels of 1024-list blocks         */
+  float ms_hv_plan;                 /* heavy rows of <= 512 lists: window plan (k_hv_plan)  */
+  float ms_hv_merge;                /* heavy rows of <= 512 lists: windowed merge (k_hv_merge)  */
+  int64_t hv_rows_one;              /* heavy rows merged in one level (<= 512 lists)           */
+  int64_t hv_rows_multi;            /* heavy rows merged in levels of 512-list blocks          */
 } brm_stats_t;
 
 typedef struct brm_context brm_context_t;
@@ -124,7 +124,7 @@ BRM_API brm_status_t brm_set_timing(brm_context_t* ctx, int enable);
 /* Route of the heavy rows (bin 7): BRM_HEAVY_AUTO (0,
  * default): each row is merged in column windows of <= 4096 products in
  * shared memory (k_hv_plan picks the windows, k_hv_merge merges them); a
- * row of more than 1024 lists first merges aligned 1024-list blocks into a
+ * row of more than 512 lists first merges aligned 512-list blocks into a
  * workspace (sub-trees of Algorithm 1's tree) whose results are the next
  * level's lists. BRM_HEAVY_GLOBAL (1): every heavy row runs on the
  * global-memory tier instead (one 1024-thread CTA per row, ping-pong

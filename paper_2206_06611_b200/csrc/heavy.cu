@@ -632,9 +632,8 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
   Key* rec = reinterpret_cast<Key*>(take((kHvCap + 2) * 8));
   double* val = reinterpret_cast<double*>(take(kHvCap * 8));
   unsigned short* own = reinterpret_cast<unsigned short*>(take(kHvCap * 2));
-  int* qlist = reinterpret_cast<int*>(take(kHvLists * 4));  // lists whose share needs a search
   int* wtmp = reinterpret_cast<int*>(take(64));
-  __shared__ int s_v, s_na, s_nq;
+  __shared__ int s_v, s_na;
   const int rank = threadIdx.x;
   const int64_t t = blockIdx.x;
   if (rank == 0) {  // the virtual row of this task: last v with rows[v].task0 <= t
@@ -650,7 +649,6 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
   }
   __syncthreads();
   const int v = s_v;
-  if (rank == 0) s_nq = 0;
   const HvRow r = a.rows[v];
   const int nwin = a.nwin[v];
   const int w0 = static_cast<int>(t - r.task0) * r.wch;
@@ -726,55 +724,33 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
               }
             }
           }
-          if (more && n < rem) {  // all 8 probes inside the window: searched below
-            const int slot = atomicAdd(&s_nq, 1);
-            qlist[slot] = l;
-            nh = n;  // the searched range starts here
+          if (more && n < rem) {  // all 8 probes inside the window: 16-ary search on
+            const int32_t* q = scol + S[l] + cu;
+            int lo = n, hi = min(rem, kHvCap + 1);  // first index >= c1 lies in [lo, hi]
+            while (hi - lo > 16) {
+              const int st = (hi - lo + 15) / 16;
+              int k = 0;
+              int pv[16];
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const int ix = lo + (u + 1) * st - 1;
+                pv[u] = ix < hi ? __ldg(q + ix) : INT_MAX;
+              }
+#pragma unroll
+              for (int u = 0; u < 16; ++u) k += pv[u] < c1;
+              const int nlo = lo + k * st;
+              hi = min(hi, nlo + st - 1);
+              lo = nlo;
+            }
+            n = lo + lower_bound_g(q + lo, hi - lo, c1);
+            nh = n < rem ? __ldg(q + n) : INT_MAX;
           }
           head[l] = nh;
         }
         cnt[l] = n;
       }
-      __syncthreads();
-      // lists that go on past the probes: one per thread (not one after
-      // another), 16-ary search with 16 loads in flight per level; the
-      // last level's probe at the answer is the list's new head
-      const int nq = s_nq;
-      for (int qi = rank; qi < nq; qi += kHvG) {
-        const int l = qlist[qi];
-        const int cu = cur[l];
-        const int rem = L[l] - cu;
-        const int32_t* q = scol + S[l] + cu;
-        int lo = head[l], hi = min(rem, kHvCap + 1);  // first index >= c1 lies in [lo, hi]
-        int nh = INT_MAX;
-        while (lo < hi) {
-          const int st = (hi - lo + 15) / 16;
-          int pv[16];
-#pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            const int ix = lo + (u + 1) * st - 1;
-            pv[u] = ix < hi ? __ldg(q + ix) : INT_MAX;
-          }
-          int k = 0;
-#pragma unroll
-          for (int u = 0; u < 16; ++u) k += pv[u] < c1;
-          if (st == 1) {  // probes at lo .. lo + 15: the answer is lo + k
-            nh = k < 16 ? pv[k] : INT_MAX;
-            lo += k;
-            hi = lo;
-          } else {
-            const int nlo = lo + k * st;
-            hi = min(hi, nlo + st - 1);
-            lo = nlo;
-          }
-        }
-        if (nh == INT_MAX && lo < rem) nh = __ldg(q + lo);
-        cnt[l] = lo;
-        head[l] = nh;
-      }
     }
     __syncthreads();
-    if (rank == 0) s_nq = 0;  // (every thread has read it before the barrier above)
     // (2) layout: even lists (A) then odd lists (B), in list order; owner
     // marks at each non-empty list's first position
     for (int i = rank; i < kHvCap / 8; i += kHvG) reinterpret_cast<uint4*>(own)[i] = make_uint4(0, 0, 0, 0);

@@ -7,7 +7,7 @@
 // PAPER.md:190), so each column receives exactly Algorithm 1's additions in
 // Algorithm 1's order and the windows' results, in column
 // order, concatenate to the row. A row of more than kHvLists lists is first
-// cut into aligned blocks of kHvLists = 2^10 consecutive lists -- sub-trees
+// cut into aligned blocks of kHvLists = 2^9 consecutive lists -- sub-trees
 // of Algorithm 1's tree (pairs are (2m, 2m+1) at every level) -- whose
 // results, scaled by 1.0 (exact), are the lists of the next level.
 //
@@ -34,7 +34,7 @@ namespace brm {
 #define BRM_HV_CAP 4096
 #endif
 #ifndef BRM_HV_LISTS
-#define BRM_HV_LISTS 1024
+#define BRM_HV_LISTS 512
 #endif
 #ifndef BRM_HV_G
 #define BRM_HV_G 256
@@ -101,8 +101,7 @@ constexpr int hv_plan_smem() {
 // merge shared memory
 constexpr int hv_merge_smem() {
   return kHvLists * 16 /*lst*/ + kHvLists * 8 /*S*/ + kHvLists * 4 * 4 /*L, cur, head, cnt*/ +
-         align16((kHvCap + 2) * 8) /*rec*/ + kHvCap * 8 /*val*/ + kHvCap * 2 /*owner*/ + kHvLists * 4 /*queue*/ +
-         64 /*scan tmp*/;
+         align16((kHvCap + 2) * 8) /*rec*/ + kHvCap * 8 /*val*/ + kHvCap * 2 /*owner*/ + 64 /*scan tmp*/;
 }
 
 // upper bound of the windows of a virtual row of P products whose columns

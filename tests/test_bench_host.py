@@ -21,6 +21,8 @@ def test_tier_table_matches_kernels():
         m = re.search(rf"#define BRM_TIER{t} (\w+), (\d+), (\d+), (\w+)", src)
         assert int(m.group(2)) == bench.TIER_CAP[t] and int(m.group(3)) == bench.TIER_LCAP[t]
     assert f"#define BRM_NUM_BINS {bench.NUM_BINS}" in (ROOT / "include" / "brmerge.h").read_text()
+    hv = (ROOT / "paper_2206_06611_b200" / "csrc" / "heavy.cuh").read_text()
+    assert f"#define BRM_HV_LISTS {bench.HV_LISTS}" in hv  # one-level heavy rows (roofline rows)
 
 
 def test_algorithmic_bytes_brute_force():

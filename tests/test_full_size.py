@@ -49,7 +49,7 @@ def test_full_size_rmat20(ctx, oracle_mod):
     * every row of tiers 1-6 (~800k rows) against Eq. (2) (columns, tolerance)
       and Algorithm 1 (bits);
     * every heavy row (245k rows, 97 % of the products) -- one-level windowed
-      rows (<= 1024 lists) and two-level rows (> 1024 lists) -- against
+      rows (<= 512 lists, bench.HV_LISTS) and rows of levels (> 512 lists) -- against
       Algorithm 1's oracle: columns exact, values bit-identical;
     * the Eq. (2) tolerance on heavy rows for the 16 heaviest one-level rows,
       16 two-level rows spread over their list counts, and 256 random heavy
@@ -67,8 +67,8 @@ def test_full_size_rmat20(ctx, oracle_mod):
     np.testing.assert_array_equal(np.diff(C.rpt.cpu().numpy()), sizes)
     light = np.nonzero((tiers >= 1) & (tiers <= 6))[0]
     heavy = np.nonzero(tiers == 7)[0]
-    one = heavy[nl[heavy] <= 1024]
-    two = heavy[nl[heavy] > 1024]
+    one = heavy[nl[heavy] <= bench.HV_LISTS]
+    two = heavy[nl[heavy] > bench.HV_LISTS]
     assert one.size > 100_000 and two.size > 1000  # both heavy routes are exercised
     res = compare_rows(C, A, B, light, nprod)
     assert res["rows"] == light.size
