@@ -560,6 +560,25 @@ __device__ __forceinline__ void lds_if(bool p, unsigned addr, unsigned long long
                : "r"(addr), "r"((unsigned)p));
 }
 
+// 32-bit keys (q << kColBits | col - c0), values moving with them
+constexpr int kColBits = 20;
+constexpr unsigned kColMask = (1u << kColBits) - 1u;
+constexpr unsigned kKey32Sent = 0xffffffffu;
+static_assert(kHvLists / 2 <= (1 << (32 - kColBits)) - 2, "pair indices fit the key's high bits");
+
+__device__ __forceinline__ int key32_merge_path(const unsigned* A, int na, const unsigned* B, int nb, int diag) {
+  int lo = diag - nb > 0 ? diag - nb : 0;
+  int hi = diag < na ? diag : na;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (A[mid] <= B[diag - 1 - mid])
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
 // a before-or-equal b in (q, col) order (slot bits ignored)
 __device__ __forceinline__ bool key_le(Key a, Key b) { return a <= (b | kSlotMask); }
 __device__ __forceinline__ bool key_eq(Key a, Key b) { return (a | kSlotMask) == (b | kSlotMask); }
@@ -629,8 +648,8 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
   int* cur = reinterpret_cast<int*>(take(kHvLists * 4));
   int* head = reinterpret_cast<int*>(take(kHvLists * 4));
   int* cnt = reinterpret_cast<int*>(take(kHvLists * 4));
-  Key* rec = reinterpret_cast<Key*>(take((kHvCap + 2) * 8));
-  double* val = reinterpret_cast<double*>(take(kHvCap * 8));
+  unsigned* rk = reinterpret_cast<unsigned*>(take((kHvCap + 2) * 4));  // keys (q, col - c0)
+  double* rv = reinterpret_cast<double*>(take((kHvCap + 2) * 8));     // their values (move with them)
   unsigned short* own = reinterpret_cast<unsigned short*>(take(kHvCap * 2));
   int* wtmp = reinterpret_cast<int*>(take(64));
   __shared__ int s_v, s_na;
@@ -803,63 +822,60 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
       for (int k = 0; k < PPT; ++k) {
         const int e = rank + (k + half * PPT) * kHvG;
         if (e < P) {
-          val[e] = __dmul_rn(av[k], bv[k]);  // line 12: the product, rounded once
-          rec[e + (e >= nA0 ? 1 : 0)] =
-              (static_cast<Key>(mq[k]) << 32) | (static_cast<Key>(cg[k] - c0) << kHvSB) | static_cast<Key>(e);
+          const int pos = e + (e >= nA0 ? 1 : 0);
+          rv[pos] = __dmul_rn(av[k], bv[k]);  // line 12: the product, rounded once
+          rk[pos] = (static_cast<unsigned>(mq[k]) << kColBits) | static_cast<unsigned>(cg[k] - c0);
         }
       }
       }
     }
     if (rank == 0) {
-      rec[nA0] = kKeySent;
-      rec[P + 1] = kKeySent;
+      rk[nA0] = kKey32Sent;
+      rk[P + 1] = kKey32Sent;
     }
     __syncthreads();
     // (4) accumulating phase: ceil(log2 nl) rounds (lines 21-35)
     int nA = nA0, nB = P - nA0, lists = nl;
     while (lists > 1) {
-      const Key* A = rec;
-      const Key* B = rec + nA + 1;
+      const unsigned* A = rk;
+      const unsigned* B = rk + nA + 1;
       const int n = nA + nB;
-      const int VT = min(((n + kHvG - 1) / kHvG) | 1, NV);  // odd: 8-byte strided accesses spread over the banks
+      const int VT = min(((n + kHvG - 1) / kHvG) | 1, NV);  // odd: strided accesses spread over the banks
       const int g0 = min(rank * VT, n), g1 = min(g0 + VT, n);
-      Key orec[NV];
+      unsigned ok[NV];
+      double ov[NV];
       int cntv = 0, cntE = 0;
       if (g0 < g1) {
-        const int i = key_merge_path(A, nA, B, nB, g0);
+        const int i = key32_merge_path(A, nA, B, nB, g0);
         int j = g0 - i;
-        if (i > 0 && j < nB && key_eq(A[i - 1], B[j])) ++j;  // B[j] was combined on the left
-        int ia = i, ib = j;
-        Key ra = A[ia], rb = B[ib];
-        const unsigned recb = smem_u32(rec), valb = smem_u32(val);
+        if (i > 0 && j < nB && A[i - 1] == B[j]) ++j;  // B[j] was combined on the left
+        int ia = i, ib = nA + 1 + j;  // ib indexes rk / rv directly
+        unsigned ra = A[ia], rb = rk[ib];
+        double va = rv[ia], vb = rv[ib];
+        const int lim = g1 + nA + 1;  // ia + ib < lim <=> positions consumed < g1
+        const unsigned kb = smem_u32(rk), vbase = smem_u32(rv);
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
           if (k >= VT) break;
-          const bool act = ia + ib < g1;
-          const bool ta = act && key_le(ra, rb);
-          const bool tb = act && key_le(rb, ra);
-          const Key out = ta ? ra : rb;
-          {  // a duplicate column of pair q: val[left] = val[left] + val[right] (Fig. 2), predicated
-            const bool dup = ta && tb;
-            const unsigned sa = valb + 8u * static_cast<unsigned>(ra & kSlotMask);
-            const unsigned sb = valb + 8u * static_cast<unsigned>(rb & kSlotMask);
-            double x = 0.0, y = 0.0;
-            lds_if(dup, sa, x);
-            lds_if(dup, sb, y);
-            if (dup) val[ra & kSlotMask] = __dadd_rn(x, y);
-          }
-          orec[k] = out;
+          const bool act = ia + ib < lim;
+          const bool ta = act && ra <= rb;
+          const bool tb = act && rb <= ra;
+          ok[k] = ta ? ra : rb;
+          // equal keys: a duplicate column of pair q, left + right (Fig. 2)
+          ov[k] = ta ? (tb ? __dadd_rn(va, vb) : va) : vb;
           cntv += act;
           ia += ta;
           ib += tb;
-          lds_if(ta, recb + 8u * ia, ra);
-          lds_if(tb, recb + 8u * (nA + 1 + ib), rb);
+          lds_if(ta, kb + 4u * ia, ra);
+          lds_if(ta, vbase + 8u * ia, va);
+          lds_if(tb, kb + 4u * ib, rb);
+          lds_if(tb, vbase + 8u * ib, vb);
         }
       }
       // outputs of even pairs go to A', odd pairs to B' (packed 16 | 16 scan)
 #pragma unroll
       for (int k = 0; k < NV; ++k)
-        if (k < cntv) cntE += 1 - (static_cast<int>(orec[k] >> 32) & 1);
+        if (k < cntv) cntE += 1 - static_cast<int>((ok[k] >> kColBits) & 1u);
       int tot;
       const int packed = group_excl_scan<kHvG>(Group<kHvG>{rank, 0xffffffffu, 0}, cntE | ((cntv - cntE) << 16), tot, wtmp);
       const int nA2 = tot & 0xffff, nB2 = tot >> 16;
@@ -868,16 +884,17 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         if (k >= cntv) break;
-        const unsigned q = static_cast<unsigned>(orec[k] >> 32);
+        const unsigned q = ok[k] >> kColBits;
         const unsigned odd = q & 1u;
         const int dst = odd ? po : pe;
         po += odd;
         pe += 1 - odd;
-        rec[dst] = (static_cast<Key>(q >> 1) << 32) | (orec[k] & 0xffffffffull);
+        rk[dst] = ((q >> 1) << kColBits) | (ok[k] & kColMask);
+        rv[dst] = ov[k];
       }
       if (rank == 0) {
-        rec[nA2] = kKeySent;
-        rec[nA2 + 1 + nB2] = kKeySent;
+        rk[nA2] = kKey32Sent;
+        rk[nA2 + 1 + nB2] = kKey32Sent;
       }
       __syncthreads();
       nA = nA2;
@@ -889,9 +906,8 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
     const int ob = a.wout[r.plan + w];
     if (rank == 0 && T != a.wout[r.plan + w + 1] - ob) atomicOr(a.err, 2u);
     for (int e = rank; e < T; e += kHvG) {
-      const Key x = rec[e];
-      ocol[obase + ob + e] = static_cast<int>((x & 0xffffffffull) >> kHvSB) + c0;
-      oval[obase + ob + e] = val[x & kSlotMask];
+      ocol[obase + ob + e] = static_cast<int>(rk[e] & kColMask) + c0;
+      oval[obase + ob + e] = rv[e];
     }
     for (int l = rank; l < nl; l += kHvG) cur[l] += cnt[l];
     __syncthreads();

@@ -101,7 +101,8 @@ constexpr int hv_plan_smem() {
 // merge shared memory
 constexpr int hv_merge_smem() {
   return kHvLists * 16 /*lst*/ + kHvLists * 8 /*S*/ + kHvLists * 4 * 4 /*L, cur, head, cnt*/ +
-         align16((kHvCap + 2) * 8) /*rec*/ + kHvCap * 8 /*val*/ + kHvCap * 2 /*owner*/ + 64 /*scan tmp*/;
+         align16((kHvCap + 2) * 4) /*keys*/ + align16((kHvCap + 2) * 8) /*values*/ + kHvCap * 2 /*owner*/ +
+         64 /*scan tmp*/;
 }
 
 // upper bound of the windows of a virtual row of P products whose columns
