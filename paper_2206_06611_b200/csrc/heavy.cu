@@ -129,22 +129,6 @@ __device__ __forceinline__ void plan_for_products(const int32_t* scol, const int
   }
 }
 
-// Warp-aggregated shared-memory add of 1 per lane to counter[key]: the lanes
-// hold consecutive products, so equal keys of one list are runs of lanes;
-// the last lane of a run adds the run length (one atomic per run instead of
-// one per lane on the same address). key < 0: no product.
-__device__ __forceinline__ void warp_run_add(unsigned* counter, int key, int list) {
-  const int lane = threadIdx.x & 31;
-  const int kp = __shfl_up_sync(0xffffffffu, key, 1), lp = __shfl_up_sync(0xffffffffu, list, 1);
-  const bool start = lane == 0 || kp != key || lp != list;
-  const unsigned starts = __ballot_sync(0xffffffffu, start);
-  const bool end = lane == 31 || ((starts >> (lane + 1)) & 1u);
-  if (end && key >= 0) {
-    const int rs = 31 - __clz(starts & ((2u << lane) - 1u));
-    atomicAdd(&counter[key], static_cast<unsigned>(lane - rs + 1));
-  }
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -537,28 +521,18 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
 // ---------------------------------------------------------------------------
 // Merge: one CTA per task = windows [w0, w1) of one virtual row.
 //
-// The window's rounds of Algorithm 1 run on 64-bit records
-//   key = (pair index q) << 32 | (col - c0) << kHvSB | slot
-// where list m of the current round belongs to pair q = m >> 1 (lines 22-29:
-// lists (2q, 2q+1) are consumed together; an odd trailing list has an empty
-// partner). The even lists are stored concatenated as sequence A, the odd
-// lists as sequence B; both are sorted by (q, col), so a whole round is ONE
-// merge of A with B: equal (q, col) keys are the duplicates of pair q and
-// combine as val[left] = val[left] + val[right] (A holds the left list).
-// An output of pair q is an element of list q of the next round: it goes to
-// A' if q is even, to B' if odd, with key q >> 1. Values never move (slots).
+// The window's rounds of Algorithm 1 run on 32-bit keys
+//   key = (pair index q) << 20 | (col - c0)
+// with the values moving alongside: list m of the current round belongs to
+// pair q = m >> 1 (lines 22-29: lists (2q, 2q+1) are consumed together; an
+// odd trailing list has an empty partner). The even lists are stored
+// concatenated as sequence A, the odd lists as sequence B; both are sorted by
+// (q, col), so a whole round is ONE merge of A with B: equal keys are the
+// duplicate columns of pair q and combine as left + right (A holds the left
+// list). An output of pair q is an element of list q of the next round: it
+// goes to A' if q is even, to B' if odd, with key q >> 1.
 // ---------------------------------------------------------------------------
 namespace {
-
-using Key = unsigned long long;
-constexpr Key kKeySent = ~0ull;
-constexpr Key kSlotMask = (1ull << kHvSB) - 1ull;
-
-__device__ __forceinline__ void lds_if(bool p, unsigned addr, unsigned long long& v) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.b64 %0, [%1];\n\t}"
-               : "+l"(v)
-               : "r"(addr), "r"((unsigned)p));
-}
 
 // 32-bit keys (q << kColBits | col - c0), values moving with them
 constexpr int kColBits = 20;
@@ -572,24 +546,6 @@ __device__ __forceinline__ int key32_merge_path(const unsigned* A, int na, const
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (A[mid] <= B[diag - 1 - mid])
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
-}
-
-// a before-or-equal b in (q, col) order (slot bits ignored)
-__device__ __forceinline__ bool key_le(Key a, Key b) { return a <= (b | kSlotMask); }
-__device__ __forceinline__ bool key_eq(Key a, Key b) { return (a | kSlotMask) == (b | kSlotMask); }
-
-// number of A elements among the first `diag` merged elements (a-first on ties)
-__device__ __forceinline__ int key_merge_path(const Key* A, int na, const Key* B, int nb, int diag) {
-  int lo = diag - nb > 0 ? diag - nb : 0;
-  int hi = diag < na ? diag : na;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (key_le(A[mid], B[diag - 1 - mid]))
       lo = mid + 1;
     else
       hi = mid;
@@ -792,7 +748,7 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
     const int nA0 = s_na;
     owner_max_scan(own, P, wtmp);
     // (3) gather: product at layout position e, record key (m >> 1, col - c0, slot e)
-    // A occupies rec[0, nA), a sentinel at nA, B at [nA + 1, P + 1), a sentinel at P + 1
+    // A occupies rk/rv[0, nA), a sentinel at nA, B at [nA + 1, P + 1), a sentinel at P + 1
     {
       // a batch of a thread's loads is issued before its products are formed
       constexpr int PPT = ((kHvCap + kHvG - 1) / kHvG + 1) / 2;

@@ -20,10 +20,10 @@
 //               PAPER.md:298). count_only: the bitmap alone, any number of
 //               lists (row sizes of rows that take several levels).
 //   k_hv_merge  one CTA per task (a run of consecutive windows of one
-//               virtual row): per window, each list's share by a search from
+//               virtual row): per window, each list's share by probes from
 //               its cursor, the products gathered into shared memory, the
-//               record rounds of Algorithm 1 (rec_merge_lists), the result
-//               written at the window's output offset.
+//               rounds of Algorithm 1 as one A-with-B merge per round (heavy.cu),
+//               the result written at the window's output offset.
 #pragma once
 #include "engine.cuh"
 
