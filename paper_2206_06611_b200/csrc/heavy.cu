@@ -560,10 +560,25 @@ __device__ __forceinline__ void owner_max_scan(unsigned short* m, int n, int* wt
   const int b0 = t * PER;
   unsigned short v[PER];
   unsigned run = 0;
+  if constexpr (PER % 8 == 0) {  // 16-byte loads: a thread's 2*PER bytes (u16 loads at a 2*PER-byte stride conflict)
 #pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    v[i] = b0 + i < n ? m[b0 + i] : 0;
-    run = max(run, static_cast<unsigned>(v[i]));
+    for (int i = 0; i < PER; i += 8) {
+      const uint4 x = *reinterpret_cast<const uint4*>(m + b0 + i);
+      const unsigned w4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        v[i + 2 * h] = static_cast<unsigned short>(w4[h] & 0xffffu);
+        v[i + 2 * h + 1] = static_cast<unsigned short>(w4[h] >> 16);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) run = max(run, static_cast<unsigned>(v[i]));
+  } else {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      v[i] = b0 + i < n ? m[b0 + i] : 0;
+      run = max(run, static_cast<unsigned>(v[i]));
+    }
   }
   unsigned inc = run;
 #pragma unroll
@@ -581,7 +596,22 @@ __device__ __forceinline__ void owner_max_scan(unsigned short* m, int n, int* wt
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     run = max(run, static_cast<unsigned>(v[i]));
-    if (b0 + i < n) m[b0 + i] = static_cast<unsigned short>(run);
+    v[i] = static_cast<unsigned short>(run);
+  }
+  if constexpr (PER % 8 == 0) {  // (positions >= n get values too: the marks are cleared per window)
+#pragma unroll
+    for (int i = 0; i < PER; i += 8) {
+      uint4 x;
+      x.x = v[i] | (static_cast<unsigned>(v[i + 1]) << 16);
+      x.y = v[i + 2] | (static_cast<unsigned>(v[i + 3]) << 16);
+      x.z = v[i + 4] | (static_cast<unsigned>(v[i + 5]) << 16);
+      x.w = v[i + 6] | (static_cast<unsigned>(v[i + 7]) << 16);
+      *reinterpret_cast<uint4*>(m + b0 + i) = x;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
+      if (b0 + i < n) m[b0 + i] = v[i];
   }
   __syncthreads();
 }
