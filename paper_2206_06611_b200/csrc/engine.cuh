@@ -800,14 +800,40 @@ __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView&
       owner_fill(owner, ostr, e0, e1, l);
     }
     g.sync();
-#pragma unroll 2
-    for (int e = rank; e < P; e += G) {
-      const int l = owner[e * ostr];  // (read before this thread overwrites val[e], which it may share)
-      const longlong2 d = rb.lst[l];
-      const int64_t src = d.x + e;
-      const int c = src_ld<NC>(B.col + src);
-      rec[e + l] = R::make(c - cbase, e);
-      if (VALS) rb.val[e] = __dmul_rn(__longlong_as_double(d.y), src_ld<NC>(B.val + src));  // line 12: the product, rounded once
+    // BRM_GATHER_BATCH products' loads in flight per thread (tuning switch)
+#ifndef BRM_GATHER_BATCH
+#define BRM_GATHER_BATCH 2
+#endif
+    constexpr int GB = BRM_GATHER_BATCH;
+    for (int eb = rank; eb < P; eb += G * GB) {
+      int cg[GB], lg[GB];
+      double vg[GB], ag[GB];
+#pragma unroll
+      for (int u = 0; u < GB; ++u) {
+        const int e = eb + u * G;
+        lg[u] = -1;
+        cg[u] = 0;
+        vg[u] = ag[u] = 0.0;
+        if (e < P) {
+          const int l = owner[e * ostr];  // (read before this thread overwrites val[e], which it may share)
+          const longlong2 d = rb.lst[l];
+          const int64_t src = d.x + e;
+          lg[u] = l;
+          cg[u] = src_ld<NC>(B.col + src);
+          if (VALS) {
+            vg[u] = src_ld<NC>(B.val + src);
+            ag[u] = __longlong_as_double(d.y);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < GB; ++u) {
+        const int e = eb + u * G;
+        if (lg[u] >= 0) {
+          rec[e + lg[u]] = R::make(cg[u] - cbase, e);
+          if (VALS) rb.val[e] = __dmul_rn(ag[u], vg[u]);  // line 12: the product, rounded once
+        }
+      }
     }
   }
   g.sync();
@@ -1041,25 +1067,43 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
   for (int l = rank; l < nl; l += G) owner_fill(hb.owner, 1, hb.off[l], hb.off[l + 1], l);
   g.sync();
   int cnt = 0;
-#pragma unroll 2
-  for (int e = rank; e < P; e += G) {
-    const int l = hb.owner[e];
-    const int c = __ldg(B.col + hb.bst[l] + (e - hb.off[l]));
-    unsigned h = (static_cast<unsigned>(c) * 2654435761u) >> (32 - hbits);
-    // a plain load first: most products repeat a column already inserted
-    // (keys are never removed, so a non-empty slot read is final)
-    const volatile int* tv = hb.table;
-    while (true) {
-      int cur = tv[h];
-      if (cur == kHashEmpty) {
-        cur = atomicCAS(&hb.table[h], kHashEmpty, c);
-        if (cur == kHashEmpty) {
-          ++cnt;
-          break;
-        }
+  // BRM_HASH_BATCH column loads in flight per thread before they are hashed
+  // (tuning switch; 1 = one load at a time)
+#ifndef BRM_HASH_BATCH
+#define BRM_HASH_BATCH 8
+#endif
+  constexpr int HB = BRM_HASH_BATCH;
+  for (int eb = rank; eb < P; eb += G * HB) {
+    int cc[HB];
+#pragma unroll
+    for (int u = 0; u < HB; ++u) {
+      const int e = eb + u * G;
+      cc[u] = -1;
+      if (e < P) {
+        const int l = hb.owner[e];
+        cc[u] = __ldg(B.col + hb.bst[l] + (e - hb.off[l]));
       }
-      if (cur == c) break;
-      h = (h + 1) & (H - 1);
+    }
+#pragma unroll
+    for (int u = 0; u < HB; ++u) {
+      const int c = cc[u];
+      if (c < 0) continue;
+      unsigned h = (static_cast<unsigned>(c) * 2654435761u) >> (32 - hbits);
+      // a plain load first: most products repeat a column already inserted
+      // (keys are never removed, so a non-empty slot read is final)
+      const volatile int* tv = hb.table;
+      while (true) {
+        int cur = tv[h];
+        if (cur == kHashEmpty) {
+          cur = atomicCAS(&hb.table[h], kHashEmpty, c);
+          if (cur == kHashEmpty) {
+            ++cnt;
+            break;
+          }
+        }
+        if (cur == c) break;
+        h = (h + 1) & (H - 1);
+      }
     }
   }
   int total;
