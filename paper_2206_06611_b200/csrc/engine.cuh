@@ -1031,7 +1031,7 @@ __host__ __device__ constexpr int hash_group_bytes() {
          (G > 32 ? align16((G / 32 + 2) * 4) : 0);
 }
 
-template <int G, int CAP>
+template <int G, int CAP, int HB>
 __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
                                          const RowOut& o, const HashBufs& hb) {
   const int rank = g.rank;
@@ -1067,12 +1067,7 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
   for (int l = rank; l < nl; l += G) owner_fill(hb.owner, 1, hb.off[l], hb.off[l + 1], l);
   g.sync();
   int cnt = 0;
-  // BRM_HASH_BATCH column loads in flight per thread before they are hashed
-  // (tuning switch; 1 = one load at a time)
-#ifndef BRM_HASH_BATCH
-#define BRM_HASH_BATCH 8
-#endif
-  constexpr int HB = BRM_HASH_BATCH;
+  // HB column loads in flight per thread before they are hashed
   for (int eb = rank; eb < P; eb += G * HB) {
     int cc[HB];
 #pragma unroll
