@@ -338,7 +338,11 @@ brm_status_t hv_run_multi(brm_context_t* ctx, int out, const RowOut& o, const st
   cudaMemGetInfo(&free_b, &total_b);
   int64_t maxP = 0;
   for (size_t i = 0; i < rows.size(); ++i) maxP = std::max(maxP, info[2 * i]);
-  const int64_t budget = std::max<int64_t>(std::min<int64_t>((int64_t)(free_b / 4), 24ll << 30), maxP * 12);
+#ifndef BRM_HV_BUDGET_DIV
+#define BRM_HV_BUDGET_DIV 4  // a batch's level-1 workspace takes at most 1/4 of the free memory (tuning switch)
+#endif
+  const int64_t budget =
+      std::max<int64_t>(std::min<int64_t>((int64_t)(free_b / BRM_HV_BUDGET_DIV), 48ll << 30), maxP * 12);
   HvSet& set = ctx->hv_multi;
   size_t b0 = 0;
   while (b0 < rows.size()) {
