@@ -779,6 +779,33 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
     owner_max_scan(own, P, wtmp);
     // (3) gather: product at layout position e, record key (m >> 1, col - c0, slot e)
     // A occupies rk/rv[0, nA), a sentinel at nA, B at [nA + 1, P + 1), a sentinel at P + 1
+#ifndef BRM_HV_CPASYNC
+#define BRM_HV_CPASYNC 0  // 1: the gather by cp.async straight into the key/value arrays (A/B switch)
+#endif
+#if BRM_HV_CPASYNC
+    {
+      // every product's column and value copied by cp.async (4 + 8 bytes) to
+      // its layout position, all in flight at once; then keys and products
+      // formed in place
+      for (int e = rank; e < P; e += kHvG) {
+        const int vr = own[e];
+        const int m = vr < ne ? 2 * vr : 2 * (vr - ne) + 1;
+        const int64_t src = lst[m].x + e;
+        const int pos = e + (e >= nA0 ? 1 : 0);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(rk + pos)), "l"(scol + src) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(rv + pos)), "l"(sval + src) : "memory");
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      for (int e = rank; e < P; e += kHvG) {  // (each thread converts the entries it copied)
+        const int vr = own[e];
+        const int m = vr < ne ? 2 * vr : 2 * (vr - ne) + 1;
+        const int pos = e + (e >= nA0 ? 1 : 0);
+        rv[pos] = __dmul_rn(__longlong_as_double(lst[m].y), rv[pos]);  // line 12: the product, rounded once
+        rk[pos] = (static_cast<unsigned>(m >> 1) << kColBits) | (rk[pos] - static_cast<unsigned>(c0));
+      }
+    }
+#else
     {
       // a batch of a thread's loads is issued before its products are formed
       constexpr int PPT = ((kHvCap + kHvG - 1) / kHvG + 1) / 2;
@@ -815,6 +842,7 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
       }
       }
     }
+#endif
     if (rank == 0) {
       rk[nA0] = kKey32Sent;
       rk[P + 1] = kKey32Sent;
