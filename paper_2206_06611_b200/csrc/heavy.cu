@@ -266,45 +266,30 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
       continue;
     }
     if (prange == 0) continue;
-    // inclusive prefix of the histogram (16 bins per thread)
+    // inclusive prefix of the histogram: warp w owns bins [w * 512, w * 512 +
+    // 512); its lanes read consecutive bins (a thread reading 16 consecutive
+    // bins would put lanes t and t + 2 on one bank)
     {
-      constexpr int PER = kHvBins / kHvPlanG;
-      unsigned v[PER];
-      unsigned s = 0;
+      constexpr int SPAN = kHvBins / (kHvPlanG / 32), ITER = SPAN / 32;
+      unsigned v[ITER];
+      unsigned carry = 0;
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        v[i] = hist[t * PER + i];
-        s += v[i];
-      }
-      unsigned inc = s;
+      for (int i = 0; i < ITER; ++i) {
+        unsigned x = hist[wid * SPAN + i * 32 + lane];
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += y;
-      }
-      if (lane == 31) s_wtmp[wid] = static_cast<int>(inc);
-      __syncthreads();
-      if (wid == 0) {
-        constexpr int NW = kHvPlanG / 32;
-        const unsigned w = lane < NW ? static_cast<unsigned>(s_wtmp[lane]) : 0u;
-        unsigned wx = w;
-#pragma unroll
-        for (int d = 1; d < NW; d <<= 1) {
-          const unsigned y = __shfl_up_sync(0xffffffffu, wx, d);
-          if (lane >= d) wx += y;
+        for (int d = 1; d < 32; d <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, x, d);
+          if (lane >= d) x += y;
         }
-        if (lane < NW) s_wtmp[lane] = static_cast<int>(wx - w);
+        v[i] = x + carry;
+        carry += __shfl_sync(0xffffffffu, x, 31);
       }
+      if (lane == 0) s_wtmp[wid] = static_cast<int>(carry);
       __syncthreads();
-      unsigned run = static_cast<unsigned>(s_wtmp[wid]) + inc - s;
+      unsigned pre = 0;
+      for (int w = 0; w < wid; ++w) pre += static_cast<unsigned>(s_wtmp[w]);
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        run += v[i];
-        v[i] = run;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int i = 0; i < PER; ++i) hist[t * PER + i] = v[i];  // hist is now the inclusive prefix H
+      for (int i = 0; i < ITER; ++i) hist[wid * SPAN + i * 32 + lane] = v[i] + pre;  // hist is now the inclusive prefix H
       __syncthreads();
     }
     const unsigned* H = hist;
@@ -443,10 +428,12 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
     {
       const int nwords = (rlen + 31) >> 5, ngroups = (nwords + 31) >> 5;
       unsigned* gp = hist;  // gp[g] = bits in groups < g
-      for (int g = t; g < ngroups; g += kHvPlanG) {
-        unsigned c = 0;
-        for (int i = 0; i < 32 && 32 * g + i < nwords; ++i) c += __popc(bm[32 * g + i]);
-        gp[g + 1] = c;
+      // a warp per group of 32 words: lane i reads word i (a thread reading
+      // its own 32 words would put all 32 lanes on one bank)
+      for (int g = wid; g < ngroups; g += kHvPlanG / 32) {
+        const int w = 32 * g + lane;
+        const unsigned c = __reduce_add_sync(0xffffffffu, w < nwords ? __popc(bm[w]) : 0u);
+        if (lane == 0) gp[g + 1] = c;
       }
       __syncthreads();
       if (wid == 0) {
