@@ -66,11 +66,6 @@ struct brm_context {
   bool hv_single_planned = false;
   DevBuf hv_lt[2], hv_ws_col[2], hv_ws_val[2], hv_tmp;
   HostBuf h_hv;
-  // host-buffer form, row-blocked: two pipeline contexts on their own streams
-  brm_context* pipe[2] = {nullptr, nullptr};
-  cudaStream_t pipe_st[2] = {nullptr, nullptr};
-  cudaEvent_t up_done = nullptr;
-  DevBuf hb_nprod, hb_off;
 };
 
 namespace {
@@ -730,88 +725,6 @@ brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
   return BRM_OK;
 }
 
-// Host-buffer form for large A, row-blocked: C's row sizes first (a PRECISE
-// structure pass over all of A gives C.rpt and nnz(C), so the pinned output
-// is allocated once, exactly), then A's rows in blocks of balanced n_prod on
-// two pipeline contexts with their own streams: the device-to-host copy of
-// block k's col/val overlaps the SpGEMM of block k+1. A row block is a view
-// of the uploaded A (its rpt values stay absolute offsets into A's col/val).
-constexpr int64_t kPipeMinRows = 65536;
-constexpr int kPipeMaxBlocks = 8;
-
-brm_status_t host_blocked(brm_context_t* ctx, const brm_csr_t* Ah, const brm_csr_t* Bh, const brm_csr_t* Ad,
-                          const brm_csr_t* Bd, brm_mode_t mode, brm_csr_t* Ch) {
-  const int64_t M = Ah->rows;
-  brm_status_t s;
-  // (1) C's row sizes, rpt and nnz(C): a PRECISE structure pass over all rows
-  int64_t nnz = 0;
-  int64_t* drpt = static_cast<int64_t*>(ctx->stC_rpt.p);
-  if ((s = structure_impl(ctx, Ad, Bd, BRM_PRECISE, drpt, &nnz)) != BRM_OK) return s;
-  const int64_t launches0 = ctx->launches;
-  const size_t brpt = (size_t)(M + 1) * 8, bcol = (size_t)nnz * 4, bval = (size_t)nnz * 8;
-  CK(ensure_host(ctx->h_C, brpt + bcol + bval + 32), "alloc pinned C");
-  unsigned char* h = static_cast<unsigned char*>(ctx->h_C.p);
-  int64_t* hrpt = reinterpret_cast<int64_t*>(h);
-  double* hv = reinterpret_cast<double*>(h + ((brpt + 15) & ~size_t(15)));
-  int32_t* hc = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(hv) + ((bval + 15) & ~size_t(15)));
-  CK(cudaMemcpyAsync(hrpt, drpt, brpt, cudaMemcpyDeviceToHost, ctx->stream), "D2H C.rpt");
-  // (2) row blocks of about equal n_prod (the structure pass left n_prod offsets)
-  std::vector<int64_t> noff(M + 1);
-  CK(cudaMemcpyAsync(noff.data(), ctx->nprod_off.p, brpt, cudaMemcpyDeviceToHost, ctx->stream), "D2H n_prod offsets");
-  CK(cudaEventRecord(ctx->up_done, ctx->stream), "record uploads");
-  CK(cudaStreamSynchronize(ctx->stream), "sync sizes");
-  const int64_t total = noff[M];
-  const int nblk = (int)std::max<int64_t>(2, std::min<int64_t>(kPipeMaxBlocks, (total * 12 >> 28) + 1));
-  std::vector<int64_t> bounds{0};
-  for (int b = 1; b < nblk; ++b) {
-    const int64_t target = total / nblk * b;
-    const int64_t r = std::lower_bound(noff.begin(), noff.end(), target) - noff.begin();
-    if (r > bounds.back() && r < M) bounds.push_back(r);
-  }
-  bounds.push_back(M);
-  for (int j = 0; j < 2; ++j) {
-    if (!ctx->pipe_st[j]) CK(cudaStreamCreateWithFlags(&ctx->pipe_st[j], cudaStreamNonBlocking), "create stream");
-    if (!ctx->pipe[j]) {
-      if ((s = brm_create(&ctx->pipe[j], ctx->device, ctx->pipe_st[j])) != BRM_OK)
-        return fail(ctx, s, "cannot create a pipeline context");
-    }
-    ctx->pipe[j]->heavy_route = ctx->heavy_route;
-    CK(cudaStreamWaitEvent(ctx->pipe_st[j], ctx->up_done, 0), "wait uploads");
-  }
-  // (3) blocks: structure + fill on alternating contexts, col/val copied back
-  // on the block's stream while the next block computes on the other
-  for (size_t b = 0; b + 1 < bounds.size(); ++b) {
-    brm_context_t* pc = ctx->pipe[b & 1];
-    const int64_t r0 = bounds[b], r1 = bounds[b + 1];
-    const brm_csr_t Ab{r1 - r0, Ad->cols, Ah->rpt[r1] - Ah->rpt[r0], Ad->rpt + r0, Ad->col, Ad->val};
-    CK(ensure(pc, pc->stC_rpt, (size_t)(r1 - r0 + 1) * 8), "alloc block C.rpt");
-    int64_t nb = 0;
-    s = structure_impl(pc, &Ab, Bd, mode, static_cast<int64_t*>(pc->stC_rpt.p), &nb);
-    ctx->launches += pc->launches;
-    if (s != BRM_OK) return fail(ctx, s, std::string("row block: ") + pc->err);
-    if (nb != hrpt[r1] - hrpt[r0]) return fail(ctx, BRM_ERR_CUDA, "row block: nnz differs from the sizing pass");
-    CK(ensure(pc, pc->stC_col, (size_t)std::max<int64_t>(nb, 1) * 4), "alloc block C.col");
-    CK(ensure(pc, pc->stC_val, (size_t)std::max<int64_t>(nb, 1) * 8), "alloc block C.val");
-    brm_csr_t Cb{0, 0, 0, static_cast<int64_t*>(pc->stC_rpt.p), static_cast<int32_t*>(pc->stC_col.p),
-                 static_cast<double*>(pc->stC_val.p)};
-    if ((s = fill_impl(pc, &Cb)) != BRM_OK) return fail(ctx, s, std::string("row block: ") + pc->err);
-    ctx->launches += pc->launches;
-    if (nb) {
-      CK(cudaMemcpyAsync(hv + hrpt[r0], Cb.val, (size_t)nb * 8, cudaMemcpyDeviceToHost, pc->stream), "D2H block val");
-      CK(cudaMemcpyAsync(hc + hrpt[r0], Cb.col, (size_t)nb * 4, cudaMemcpyDeviceToHost, pc->stream), "D2H block col");
-    }
-  }
-  for (int j = 0; j < 2; ++j) CK(cudaStreamSynchronize(ctx->pipe_st[j]), "sync pipeline");
-  (void)launches0;
-  Ch->rows = M;
-  Ch->cols = Bh->cols;
-  Ch->nnz = nnz;
-  Ch->rpt = hrpt;
-  Ch->val = hv;
-  Ch->col = hc;
-  return BRM_OK;
-}
-
 }  // namespace
 
 extern "C" {
@@ -843,7 +756,6 @@ brm_status_t brm_create(brm_context_t** out, int device, void* stream) {
   DeviceGuard g(device);
   for (auto& e : ctx->ev) cudaEventCreate(&e);
   cudaEventCreateWithFlags(&ctx->handoff, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&ctx->up_done, cudaEventDisableTiming);
   *out = ctx;
   return BRM_OK;
 }
@@ -860,7 +772,7 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
                       &ctx->hv_single.cuts, &ctx->hv_single.wout, &ctx->hv_single.nwin, &ctx->hv_single.total,
                       &ctx->hv_multi.d_rows, &ctx->hv_multi.cuts, &ctx->hv_multi.wout, &ctx->hv_multi.nwin,
                       &ctx->hv_multi.total, &ctx->hv_lt[0], &ctx->hv_lt[1], &ctx->hv_ws_col[0], &ctx->hv_ws_col[1],
-                      &ctx->hv_ws_val[0], &ctx->hv_ws_val[1], &ctx->hv_tmp, &ctx->hb_nprod, &ctx->hb_off})
+                      &ctx->hv_ws_val[0], &ctx->hv_ws_val[1], &ctx->hv_tmp})
       free_dev(ctx, *b);
     cudaStreamSynchronize(ctx->stream);
     for (HostBuf* b : {&ctx->h_small, &ctx->h_heavy, &ctx->h_gws_off, &ctx->h_C, &ctx->h_rows})
@@ -869,11 +781,6 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
       if (e) cudaEventDestroy(e);
     if (ctx->handoff) cudaEventDestroy(ctx->handoff);
   }
-  for (int j = 0; j < 2; ++j) {
-    if (ctx->pipe[j]) brm_destroy(ctx->pipe[j]);
-    if (ctx->pipe_st[j]) cudaStreamDestroy(ctx->pipe_st[j]);
-  }
-  if (ctx->up_done) cudaEventDestroy(ctx->up_done);
   delete ctx;
   return BRM_OK;
 }
@@ -1018,7 +925,6 @@ brm_status_t brmerge_spgemm_host(brm_context_t* ctx, const brm_csr_t* Ah, const 
   brm_csr_t Bd{Bh->rows, Bh->cols, Bh->nnz, static_cast<int64_t*>(br.p), static_cast<int32_t*>(bc.p),
                static_cast<double*>(bv.p)};
   CK(ensure(ctx, ctx->stC_rpt, (size_t)(Ah->rows + 1) * 8), "alloc C.rpt");
-  if (Ah->rows >= kPipeMinRows) return host_blocked(ctx, Ah, Bh, &Ad, &Bd, mode, Ch);
   int64_t nnz = 0;
   if ((s = structure_impl(ctx, &Ad, &Bd, mode, static_cast<int64_t*>(ctx->stC_rpt.p), &nnz)) != BRM_OK) return s;
   CK(ensure(ctx, ctx->stC_col, (size_t)nnz * 4), "alloc C.col");
