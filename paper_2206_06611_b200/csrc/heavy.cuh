@@ -43,7 +43,6 @@ namespace brm {
 #define BRM_HV_MINB 2
 #endif
 constexpr int kHvCap = BRM_HV_CAP;      // products per window
-constexpr int kHvSB = 12;               // slot bits of a record (slots 0 .. kHvCap - 1)
 constexpr int kHvLists = BRM_HV_LISTS;  // lists per virtual row: an aligned 2^k-list sub-tree
 constexpr int kHvG = BRM_HV_G;          // merge CTA
 constexpr int kHvMinBlocks = BRM_HV_MINB;  // merge CTAs per SM (launch bounds)
@@ -53,10 +52,10 @@ constexpr int kHvRange = 1 << kHvRangeBits;
 constexpr int kHvBinBits = 7;      // histogram bins of 128 columns
 constexpr int kHvBins = kHvRange >> kHvBinBits;
 constexpr int kHvFine = 64;        // bins refined to single columns per refinement pass
-// records pack col - c0 into 32 - kHvSB bits; the all-ones word (column
-// 2^20 - 1) is the sentinel, so a window spans at most 2^20 - 1 columns
-constexpr int kHvSpan = (1 << (32 - kHvSB)) - 1;
-static_assert(kHvCap <= (1 << kHvSB), "slot bits");
+// merge keys hold col - c0 in their low 20 bits (heavy.cu kColBits): a
+// window spans at most 2^20 - 1 columns
+constexpr int kHvSpan = (1 << 20) - 1;
+static_assert(kHvCap <= 65535, "owner marks and the packed 16|16 round scan");
 static_assert((kHvLists & (kHvLists - 1)) == 0, "a block of lists must be an aligned power-of-two sub-tree");
 static_assert(kHvLists <= kHvCap, "a column holds at most one product per list: a single column fits a window");
 
