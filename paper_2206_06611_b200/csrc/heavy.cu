@@ -607,7 +607,11 @@ __device__ __forceinline__ void owner_max_scan(unsigned short* m, int n, int* wt
 
 template <int OUT>
 __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOut o) {
-  constexpr int NV = ((kHvCap + kHvG - 1) / kHvG) | 1;
+#ifndef BRM_HV_ILP
+#define BRM_HV_ILP 1  // merge chunks per thread and round (tuning switch)
+#endif
+  constexpr int CH = BRM_HV_ILP;
+  constexpr int NVC = ((kHvCap + CH * kHvG - 1) / (CH * kHvG)) | 1;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* p = smem;
   auto take = [&](int n) {
@@ -841,57 +845,85 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
       const unsigned* A = rk;
       const unsigned* B = rk + nA + 1;
       const int n = nA + nB;
-      const int VT = min(((n + kHvG - 1) / kHvG) | 1, NV);  // odd: strided accesses spread over the banks
-      const int g0 = min(rank * VT, n), g1 = min(g0 + VT, n);
-      unsigned ok[NV];
-      double ov[NV];
-      int cntv = 0, cntE = 0;
-      if (g0 < g1) {
+      // CH chunks per thread (virtual threads rank + c * kHvG): independent
+      // merges stepped together, so one chunk's shared-memory latency hides
+      // behind the other's work
+      const int VT = min(((n + CH * kHvG - 1) / (CH * kHvG)) | 1, NVC);  // odd: strided accesses spread over the banks
+      unsigned ok[CH][NVC];
+      double ov[CH][NVC];
+      int cntv[CH], cntE[CH], ia[CH], ib[CH], lim[CH];
+      unsigned ra[CH], rb[CH];
+      double va[CH], vb[CH];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int g0 = min((rank + c * kHvG) * VT, n), g1 = min(g0 + VT, n);
+        cntv[c] = cntE[c] = 0;
         const int i = key32_merge_path(A, nA, B, nB, g0);
         int j = g0 - i;
         if (i > 0 && j < nB && A[i - 1] == B[j]) ++j;  // B[j] was combined on the left
-        int ia = i, ib = nA + 1 + j;  // ib indexes rk / rv directly
-        unsigned ra = A[ia], rb = rk[ib];
-        double va = rv[ia], vb = rv[ib];
-        const int lim = g1 + nA + 1;  // ia + ib < lim <=> positions consumed < g1
-        const unsigned kb = smem_u32(rk), vbase = smem_u32(rv);
+        ia[c] = i;
+        ib[c] = nA + 1 + j;  // ib indexes rk / rv directly
+        lim[c] = g0 < g1 ? g1 + nA + 1 : 0;  // ia + ib < lim <=> positions consumed < g1
+        ra[c] = A[ia[c]];
+        rb[c] = rk[ib[c]];
+        va[c] = rv[ia[c]];
+        vb[c] = rv[ib[c]];
+      }
+      const unsigned kb = smem_u32(rk), vbase = smem_u32(rv);
 #pragma unroll
-        for (int k = 0; k < NV; ++k) {
-          if (k >= VT) break;
-          const bool act = ia + ib < lim;
-          const bool ta = act && ra <= rb;
-          const bool tb = act && rb <= ra;
-          ok[k] = ta ? ra : rb;
+      for (int k = 0; k < NVC; ++k) {
+        if (k >= VT) break;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const bool act = ia[c] + ib[c] < lim[c];
+          const bool ta = act && ra[c] <= rb[c];
+          const bool tb = act && rb[c] <= ra[c];
+          ok[c][k] = ta ? ra[c] : rb[c];
           // equal keys: a duplicate column of pair q, left + right (Fig. 2)
-          ov[k] = ta ? (tb ? __dadd_rn(va, vb) : va) : vb;
-          cntv += act;
-          ia += ta;
-          ib += tb;
-          lds_if(ta, kb + 4u * ia, ra);
-          lds_if(ta, vbase + 8u * ia, va);
-          lds_if(tb, kb + 4u * ib, rb);
-          lds_if(tb, vbase + 8u * ib, vb);
+          ov[c][k] = ta ? (tb ? __dadd_rn(va[c], vb[c]) : va[c]) : vb[c];
+          cntv[c] += act;
+          ia[c] += ta;
+          ib[c] += tb;
+          lds_if(ta, kb + 4u * ia[c], ra[c]);
+          lds_if(ta, vbase + 8u * ia[c], va[c]);
+          lds_if(tb, kb + 4u * ib[c], rb[c]);
+          lds_if(tb, vbase + 8u * ib[c], vb[c]);
         }
       }
-      // outputs of even pairs go to A', odd pairs to B' (packed 16 | 16 scan)
+      // outputs of even pairs go to A', odd pairs to B' (packed 16 | 16
+      // scans, one per chunk: virtual thread order is chunk 0 of every
+      // thread, then chunk 1)
+      int pe[CH], po[CH];
+      int totE = 0, totO = 0;
 #pragma unroll
-      for (int k = 0; k < NV; ++k)
-        if (k < cntv) cntE += 1 - static_cast<int>((ok[k] >> kColBits) & 1u);
-      int tot;
-      const int packed = group_excl_scan<kHvG>(Group<kHvG>{rank, 0xffffffffu, 0}, cntE | ((cntv - cntE) << 16), tot, wtmp);
-      const int nA2 = tot & 0xffff, nB2 = tot >> 16;
-      int pe = packed & 0xffff, po = nA2 + 1 + (packed >> 16);
+      for (int c = 0; c < CH; ++c) {
+#pragma unroll
+        for (int k = 0; k < NVC; ++k)
+          if (k < cntv[c]) cntE[c] += 1 - static_cast<int>((ok[c][k] >> kColBits) & 1u);
+        int tot;
+        const int packed =
+            group_excl_scan<kHvG>(Group<kHvG>{rank, 0xffffffffu, 0}, cntE[c] | ((cntv[c] - cntE[c]) << 16), tot, wtmp);
+        pe[c] = totE + (packed & 0xffff);
+        po[c] = totO + (packed >> 16);
+        totE += tot & 0xffff;
+        totO += tot >> 16;
+      }
+      const int nA2 = totE, nB2 = totO;
       // every thread has read its inputs (group_excl_scan ends synchronised)
 #pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        if (k >= cntv) break;
-        const unsigned q = ok[k] >> kColBits;
-        const unsigned odd = q & 1u;
-        const int dst = odd ? po : pe;
-        po += odd;
-        pe += 1 - odd;
-        rk[dst] = ((q >> 1) << kColBits) | (ok[k] & kColMask);
-        rv[dst] = ov[k];
+      for (int c = 0; c < CH; ++c) {
+        int e_ = pe[c], o_ = nA2 + 1 + po[c];
+#pragma unroll
+        for (int k = 0; k < NVC; ++k) {
+          if (k >= cntv[c]) break;
+          const unsigned q = ok[c][k] >> kColBits;
+          const unsigned odd = q & 1u;
+          const int dst = odd ? o_ : e_;
+          o_ += odd;
+          e_ += 1 - odd;
+          rk[dst] = ((q >> 1) << kColBits) | (ok[c][k] & kColMask);
+          rv[dst] = ov[c][k];
+        }
       }
       if (rank == 0) {
         rk[nA2] = kKey32Sent;
