@@ -201,32 +201,78 @@ def measured_traffic(config: str, mode: str, kernel: str):
         return None
 
 
+def workload_config(name, desc, mode, A, nprod, nnz_c, world=1, assemble="rpt"):
+    """`config` of a bench line (both arms: the same workload gives the same dict)."""
+    return {"workload": name, "desc": desc, "mode": mode, "rows": A.rows,
+            "nnz_a": A.nnz, "nprod": nprod, "nnz_c": nnz_c,
+            "compression_ratio": nprod / max(nnz_c, 1),
+            "l2": "flushed (256 MiB write) between timed steps, outside the events",
+            "parallelism": f"dp{world} rows by balanced n_prod",
+            "assembly": (("global row_ptr all-gathered, C row-distributed" if assemble == "rpt"
+                          else "whole C all-gathered") if world > 1 else "n/a (one GPU)")}
+
+
+def resolve_mode(mode, nprod, total_mem):
+    """auto: BRMerge-Upper when C_bar (12 B per intermediate product) fits in half the GPU memory."""
+    if mode != "auto":
+        return mode
+    return "upper" if nprod * 12 < total_mem // 2 else "precise"
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle (Eq. (2) Gustavson, single thread) on
-    a bounded row sample of the same workload, rank 0 only."""
+    the same workload, rank 0 only: the whole matrix when the K + W steps
+    fit in about --ref-budget-s seconds (then `config` equals the GPU arm's),
+    else an evenly strided row sample per step sized to that budget."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
     A, B, desc = build_workload(args.config, 1)
     nprod = oracle.row_nprod(A, B)
-    rows, sample = _sample_rows(nprod, target_prod=args.ref_sample_prod)
-    sub_np = int(nprod[rows].sum())
+    total = int(nprod.sum())
+    # probe: the oracle's rate on a small sample
+    prow, _ = _sample_rows(nprod, target_prod=args.cpu_sample_prod)
+    t0 = time.perf_counter()
+    oracle.spgemm_gustavson(A, B, rows=prow)
+    rate = max(float(nprod[prow].sum()), 1.0) / max(time.perf_counter() - t0, 1e-6)
+    per_step = args.ref_budget_s / (args.steps + args.warmup)
+    whole = total / rate <= per_step
+    if whole:
+        rows = None
+        sample = f"whole matrix ({A.rows} rows, n_prod {total})"
+        sub_np = total
+    else:
+        rows, sample = _sample_rows(nprod, target_prod=rate * per_step)
+        sub_np = int(nprod[rows].sum())
     times = []
+    C = None
     for it in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        oracle.spgemm_gustavson(A, B, rows=rows)
+        C = oracle.spgemm_gustavson(A, B, rows=rows) if rows is not None else oracle.spgemm_gustavson(A, B)
         dt = time.perf_counter() - t0
         if it >= args.warmup:
             times.append(dt)
     sec = float(np.mean(times))
     v = 2.0 * sub_np / sec / 1e9
+    try:
+        import torch
+        mem = torch.cuda.get_device_properties(0).total_memory if torch.cuda.is_available() else 0
+    except Exception:
+        mem = 0
+    mode = resolve_mode(args.mode, total, mem or (178 << 30))
+    if whole:
+        nnz_c = int(C.nnz) if hasattr(C, "nnz") else int(C.rpt[-1])
+        cfg = workload_config(args.config, desc, mode, A, total, nnz_c)
+    else:
+        cfg = {"workload": args.config, "desc": desc, "mode": mode, "rows": A.rows, "nnz_a": A.nnz,
+               "nprod": total, "rows_sampled": int(rows.size)}
     line = {"impl": "reference", "metric": METRIC,
             "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": SCALING[args.config], "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "desc": desc, "mode": "oracle (Eq. (2), sorted-map Gustavson)",
-                       "rows_sampled": int(rows.size)},
+            "dtype": "f64", "data": "synthetic", "config": cfg,
+            "reference": "CPU oracle: Eq. (2) Gustavson with a sorted-map accumulator (oracle/oracle.cpp), "
+                         "single thread; there is no reference implementation to install (the reference is a paper)",
             "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -259,7 +305,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-prod", type=float, default=2e6, help="probe sample (products)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target oracle time of the cpu_baseline")
-    ap.add_argument("--ref-sample-prod", type=float, default=1.5e7)
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="--impl reference: oracle seconds for the whole K + W run")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -295,9 +342,7 @@ def main():
     Ablk = gen.Csr(r1 - r0, A.cols, (A.rpt[r0:r1 + 1] - a0).astype(np.int64), A.col[a0:a1].copy(), A.val[a0:a1].copy())
     Ad = TorchCsr.from_csr(Ablk)
     local_nprod = int(nprod_h[r0:r1].sum())
-    if args.mode == "auto":
-        fits = local_nprod * 12 < torch.cuda.get_device_properties(dev).total_memory // 2
-        args.mode = "upper" if fits else "precise"
+    args.mode = resolve_mode(args.mode, local_nprod, torch.cuda.get_device_properties(dev).total_memory)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -445,13 +490,7 @@ def main():
             "value": gflops, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": SCALING[args.config], "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "desc": desc, "mode": args.mode, "rows": A.rows,
-                       "nnz_a": A.nnz, "nprod": nprod_all, "nnz_c": nnz_all,
-                       "compression_ratio": nprod_all / max(nnz_all, 1),
-                       "l2": "flushed (256 MiB write) between timed steps, outside the events",
-                       "parallelism": f"dp{world} rows by balanced n_prod",
-                       "assembly": (("global row_ptr all-gathered, C row-distributed" if args.assemble == "rpt"
-                                     else "whole C all-gathered") if world > 1 else "n/a (one GPU)")},
+            "config": workload_config(args.config, desc, args.mode, A, nprod_all, nnz_all, world, args.assemble),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": measured_traffic(args.config, args.mode, dom_name),
                          "kernel": dom_name, "kernel_ms": dom_ms, "kernel_rows": int(dom_rows.size),

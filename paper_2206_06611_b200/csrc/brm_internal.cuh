@@ -25,7 +25,7 @@ struct CsrView {
 //   5  record BRMerge, 128 threads      P <= 3072, nl <= 256  (smem records)
 //   6  record BRMerge, 256 threads      P <= 6656, nl <= 512  (smem records)
 //   7  heavy rows: windowed BRMerge (heavy.cuh; column windows of <= 4096
-//      products, levels of 1024-list blocks), or under BRM_HEAVY_GLOBAL the
+//      products, levels of 512-list blocks), or under BRM_HEAVY_GLOBAL the
 //      chunked BRMerge on 1024 threads with ping-pong buffers in a global
 //      workspace
 // ---------------------------------------------------------------------------

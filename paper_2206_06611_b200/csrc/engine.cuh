@@ -800,12 +800,42 @@ __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView&
       owner_fill(owner, ostr, e0, e1, l);
     }
     g.sync();
+#ifndef BRM_REC_CPASYNC
+#define BRM_REC_CPASYNC 0  // 1: block-per-row tiers (G > 32) stage B by cp.async (A/B switch)
+#endif
+    if constexpr (BRM_REC_CPASYNC && G > 32 && VALS) {
+      // every product's column (4 bytes) and value (8 bytes) copied by
+      // cp.async straight into its record / value slot, all in flight at
+      // once; then each list's entries become records {col, slot} and
+      // products A_ik * B_kj (one rounding, line 12), a warp per list
+      for (int e = rank; e < P; e += G) {
+        const int l = owner[e * ostr];  // (read before the copy into val[e] lands on it)
+        const int64_t src = rb.lst[l].x + e;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(rec + e + l)), "l"(B.col + src)
+                     : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(rb.val + e)), "l"(B.val + src)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      g.sync();
+      const int lane = rank & 31;
+      for (int l = rank >> 5; l < nl; l += G / 32) {
+        const int e0 = off[l] - l, e1 = off[l + 1] - (l + 1);
+        const double a = __longlong_as_double(rb.lst[l].y);
+        for (int e = e0 + lane; e < e1; e += 32) {
+          const int c = *reinterpret_cast<const int*>(rec + e + l);  // the raw column (first 4 bytes)
+          rec[e + l] = R::make(c - cbase, e);
+          rb.val[e] = __dmul_rn(a, rb.val[e]);
+        }
+      }
+    } else {
     // BRM_GATHER_BATCH products' loads in flight per thread (tuning switch)
 #ifndef BRM_GATHER_BATCH
 #define BRM_GATHER_BATCH 2
 #endif
-    constexpr int GB = BRM_GATHER_BATCH;
-    for (int eb = rank; eb < P; eb += G * GB) {
+    for (int eb = rank; eb < P; eb += G * BRM_GATHER_BATCH) {
+      constexpr int GB = BRM_GATHER_BATCH;
       int cg[GB], lg[GB];
       double vg[GB], ag[GB];
 #pragma unroll
@@ -834,6 +864,7 @@ __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView&
           if (VALS) rb.val[e] = __dmul_rn(ag[u], vg[u]);  // line 12: the product, rounded once
         }
       }
+    }
     }
   }
   g.sync();

@@ -882,6 +882,7 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
           // equal keys: a duplicate column of pair q, left + right (Fig. 2)
           ov[c][k] = ta ? (tb ? __dadd_rn(va[c], vb[c]) : va[c]) : vb[c];
           cntv[c] += act;
+          cntE[c] += act && !((ok[c][k] >> kColBits) & 1u);  // outputs of even pairs (-> A')
           ia[c] += ta;
           ib[c] += tb;
           lds_if(ta, kb + 4u * ia[c], ra[c]);
@@ -897,9 +898,6 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
       int totE = 0, totO = 0;
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
-#pragma unroll
-        for (int k = 0; k < NVC; ++k)
-          if (k < cntv[c]) cntE[c] += 1 - static_cast<int>((ok[c][k] >> kColBits) & 1u);
         int tot;
         const int packed =
             group_excl_scan<kHvG>(Group<kHvG>{rank, 0xffffffffu, 0}, cntE[c] | ((cntv[c] - cntE[c]) << 16), tot, wtmp);
