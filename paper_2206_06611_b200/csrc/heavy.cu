@@ -607,11 +607,7 @@ __device__ __forceinline__ void owner_max_scan(unsigned short* m, int n, int* wt
 
 template <int OUT>
 __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOut o) {
-#ifndef BRM_HV_ILP
-#define BRM_HV_ILP 1  // merge chunks per thread and round (tuning switch)
-#endif
-  constexpr int CH = BRM_HV_ILP;
-  constexpr int NVC = ((kHvCap + CH * kHvG - 1) / (CH * kHvG)) | 1;
+  constexpr int NVC = ((kHvCap + kHvG - 1) / kHvG) | 1;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* p = smem;
   auto take = [&](int n) {
@@ -827,8 +823,9 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
         const int e = rank + (k + half * PPT) * kHvG;
         if (e < P) {
           const int pos = e + (e >= nA0 ? 1 : 0);
+          const unsigned key = (static_cast<unsigned>(mq[k]) << kColBits) | static_cast<unsigned>(cg[k] - c0);
           rv[pos] = __dmul_rn(av[k], bv[k]);  // line 12: the product, rounded once
-          rk[pos] = (static_cast<unsigned>(mq[k]) << kColBits) | static_cast<unsigned>(cg[k] - c0);
+          rk[pos] = key;
         }
       }
       }
@@ -845,83 +842,56 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
       const unsigned* A = rk;
       const unsigned* B = rk + nA + 1;
       const int n = nA + nB;
-      // CH chunks per thread (virtual threads rank + c * kHvG): independent
-      // merges stepped together, so one chunk's shared-memory latency hides
-      // behind the other's work
-      const int VT = min(((n + CH * kHvG - 1) / (CH * kHvG)) | 1, NVC);  // odd: strided accesses spread over the banks
-      unsigned ok[CH][NVC];
-      double ov[CH][NVC];
-      int cntv[CH], cntE[CH], ia[CH], ib[CH], lim[CH];
-      unsigned ra[CH], rb[CH];
-      double va[CH], vb[CH];
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const int g0 = min((rank + c * kHvG) * VT, n), g1 = min(g0 + VT, n);
-        cntv[c] = cntE[c] = 0;
-        const int i = key32_merge_path(A, nA, B, nB, g0);
-        int j = g0 - i;
-        if (i > 0 && j < nB && A[i - 1] == B[j]) ++j;  // B[j] was combined on the left
-        ia[c] = i;
-        ib[c] = nA + 1 + j;  // ib indexes rk / rv directly
-        lim[c] = g0 < g1 ? g1 + nA + 1 : 0;  // ia + ib < lim <=> positions consumed < g1
-        ra[c] = A[ia[c]];
-        rb[c] = rk[ib[c]];
-        va[c] = rv[ia[c]];
-        vb[c] = rv[ib[c]];
-      }
+      const int VT = min(((n + kHvG - 1) / kHvG) | 1, NVC);  // odd: strided accesses spread over the banks
+      const int g0 = min(rank * VT, n), g1 = min(g0 + VT, n);
+      int cntv = 0, cntE = 0;
+      const int i = key32_merge_path(A, nA, B, nB, g0);
+      int j = g0 - i;
+      if (i > 0 && j < nB && A[i - 1] == B[j]) ++j;  // B[j] was combined on the left
+      int ia = i;
+      int ib = nA + 1 + j;  // ib indexes rk directly
+      const int lim = g0 < g1 ? g1 + nA + 1 : 0;  // ia + ib < lim <=> positions consumed < g1
+      unsigned ra = A[ia], rb = rk[ib];
+      unsigned ok[NVC];
+      double ov[NVC];
+      double va = rv[ia], vb = rv[ib];
       const unsigned kb = smem_u32(rk), vbase = smem_u32(rv);
 #pragma unroll
       for (int k = 0; k < NVC; ++k) {
         if (k >= VT) break;
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          const bool act = ia[c] + ib[c] < lim[c];
-          const bool ta = act && ra[c] <= rb[c];
-          const bool tb = act && rb[c] <= ra[c];
-          ok[c][k] = ta ? ra[c] : rb[c];
-          // equal keys: a duplicate column of pair q, left + right (Fig. 2)
-          ov[c][k] = ta ? (tb ? __dadd_rn(va[c], vb[c]) : va[c]) : vb[c];
-          cntv[c] += act;
-          cntE[c] += act && !((ok[c][k] >> kColBits) & 1u);  // outputs of even pairs (-> A')
-          ia[c] += ta;
-          ib[c] += tb;
-          lds_if(ta, kb + 4u * ia[c], ra[c]);
-          lds_if(ta, vbase + 8u * ia[c], va[c]);
-          lds_if(tb, kb + 4u * ib[c], rb[c]);
-          lds_if(tb, vbase + 8u * ib[c], vb[c]);
-        }
+        const bool act = ia + ib < lim;
+        const bool ta = act && ra <= rb;
+        const bool tb = act && rb <= ra;
+        ok[k] = ta ? ra : rb;
+        // equal keys: a duplicate column of pair q, left + right (Fig. 2)
+        ov[k] = ta ? (tb ? __dadd_rn(va, vb) : va) : vb;
+        cntv += act;
+        cntE += act && !((ok[k] >> kColBits) & 1u);  // outputs of even pairs (-> A')
+        ia += ta;
+        ib += tb;
+        lds_if(ta, kb + 4u * ia, ra);
+        lds_if(ta, vbase + 8u * ia, va);
+        lds_if(tb, kb + 4u * ib, rb);
+        lds_if(tb, vbase + 8u * ib, vb);
       }
-      // outputs of even pairs go to A', odd pairs to B' (packed 16 | 16
-      // scans, one per chunk: virtual thread order is chunk 0 of every
-      // thread, then chunk 1)
-      int pe[CH], po[CH];
-      int totE = 0, totO = 0;
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        int tot;
-        const int packed =
-            group_excl_scan<kHvG>(Group<kHvG>{rank, 0xffffffffu, 0}, cntE[c] | ((cntv[c] - cntE[c]) << 16), tot, wtmp);
-        pe[c] = totE + (packed & 0xffff);
-        po[c] = totO + (packed >> 16);
-        totE += tot & 0xffff;
-        totO += tot >> 16;
-      }
-      const int nA2 = totE, nB2 = totO;
+      // outputs of even pairs go to A', odd pairs to B' (one packed 16 | 16 scan)
+      int tot;
+      const int packed = group_excl_scan<kHvG>(Group<kHvG>{rank, 0xffffffffu, 0}, cntE | ((cntv - cntE) << 16), tot, wtmp);
+      const int nA2 = tot & 0xffff, nB2 = tot >> 16;
       // every thread has read its inputs (group_excl_scan ends synchronised)
+      int e_ = packed & 0xffff, o_ = nA2 + 1 + (packed >> 16);
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        int e_ = pe[c], o_ = nA2 + 1 + po[c];
-#pragma unroll
-        for (int k = 0; k < NVC; ++k) {
-          if (k >= cntv[c]) break;
-          const unsigned q = ok[c][k] >> kColBits;
-          const unsigned odd = q & 1u;
-          const int dst = odd ? o_ : e_;
-          o_ += odd;
-          e_ += 1 - odd;
-          rk[dst] = ((q >> 1) << kColBits) | (ok[c][k] & kColMask);
-          rv[dst] = ov[c][k];
-        }
+      for (int k = 0; k < NVC; ++k) {
+        if (k >= cntv) break;
+        const unsigned key = ok[k];
+        const unsigned q = key >> kColBits;
+        const unsigned odd = q & 1u;
+        const int dst = odd ? o_ : e_;
+        o_ += odd;
+        e_ += 1 - odd;
+        const unsigned nkey = ((q >> 1) << kColBits) | (key & kColMask);
+        rk[dst] = nkey;
+        rv[dst] = ov[k];
       }
       if (rank == 0) {
         rk[nA2] = kKey32Sent;

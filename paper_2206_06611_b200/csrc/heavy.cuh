@@ -100,7 +100,8 @@ constexpr int hv_plan_smem() {
 // merge shared memory
 constexpr int hv_merge_smem() {
   return kHvLists * 16 /*lst*/ + kHvLists * 8 /*S*/ + kHvLists * 4 * 4 /*L, cur, head, cnt*/ +
-         align16((kHvCap + 2) * 4) /*keys*/ + align16((kHvCap + 2) * 8) /*values*/ + kHvCap * 2 /*owner*/ +
+         align16((kHvCap + 2) * 4) /*keys*/ + align16((kHvCap + 2) * 8) /*values*/ +
+         kHvCap * 2 /*owner*/ +
          64 /*scan tmp*/;
 }
 
