@@ -92,10 +92,31 @@ struct TierBounds {
 // 5th field: column loads in flight per thread before they are hashed.
 // Measured on B200 (same box): tier 3 (uniform1m_k16) 2.45 ms with 1 vs
 // 3.12 ms with 8 (registers); tier 4 (stencil27_64) 0.67 ms with 8 vs 0.78.
-#define BRM_HASH3 32, 256, 64, BRM_H3_GPC, 1
-#define BRM_HASH4 BRM_H4_G, 768, 64, BRM_H4_GPC, 8
-#define BRM_HASH5 128, 3072, 256, 1, 8
-#define BRM_HASH6 256, 6656, 512, 1, 8
+// 6th field: table slots per product x 4 (HQ: H = pow2 >= P * HQ / 4).
+// 7th field: direct atomicCAS inserts (no read of the slot first).
+// Measured on B200 (same box): stencil27_64's tier-4 symbolic 0.670 ms with
+// HQ 6 -> 0.617 with HQ 5 (a smaller table to clear); uniform1m_k16's tier 3
+// 2.43 ms with a read first vs 2.56 with direct CAS, and 2.43 / 1.82 / 2.42 ms
+// with HQ 8 / 16 / 32 (uniform1m_k16 PRECISE 81.5 -> 90.0 GFLOP/s at 16).
+#ifndef BRM_H3_HB
+#define BRM_H3_HB 1
+#endif
+#ifndef BRM_H3_HQ
+#define BRM_H3_HQ 16
+#endif
+#ifndef BRM_H3_DIRECT
+#define BRM_H3_DIRECT false
+#endif
+#define BRM_HASH3 32, 256, 64, BRM_H3_GPC, BRM_H3_HB, BRM_H3_HQ, BRM_H3_DIRECT
+#ifndef BRM_H4_HB
+#define BRM_H4_HB 8
+#endif
+#ifndef BRM_H4_HQ
+#define BRM_H4_HQ 5
+#endif
+#define BRM_HASH4 BRM_H4_G, 768, 64, BRM_H4_GPC, BRM_H4_HB, BRM_H4_HQ, false
+#define BRM_HASH5 128, 3072, 256, 1, 8, 5, false
+#define BRM_HASH6 256, 6656, 512, 1, 8, 5, false
 constexpr int kGlobalG = 1024;
 
 __host__ __device__ inline TierBounds tier_bounds() {

@@ -1038,13 +1038,16 @@ namespace brm {
 // row_size of the C matrix by the hashing method"), tiers 3-6: every product
 // column of the row is inserted into a per-row shared-memory hash table
 // (linear probing, atomicCAS); the row size is the number of first
-// insertions. The table has H = the power of two >= 3P/2 slots (<= HCAP).
+// insertions. The table has H = the power of two >= P * HQ / 4 slots (per tier).
 // ===========================================================================
 
-template <int CAP>
+// table of H = the power of two >= P * HQ / 4 slots (>= 64): HQ = 5 keeps the
+// load factor <= 0.8 for the tiers whose rows repeat their columns; rows of
+// mostly distinct columns take a sparser table (fewer, shorter probe chains)
+template <int CAP, int HQ>
 __host__ __device__ constexpr int hash_cap() {
   int h = 64;
-  while (h < CAP + CAP / 2) h <<= 1;
+  while (h < CAP * HQ / 4) h <<= 1;
   return h;
 }
 
@@ -1056,13 +1059,16 @@ struct HashBufs {
   int* scan_tmp;
 };
 
-template <int G, int CAP, int LCAP>
+template <int G, int CAP, int LCAP, int HQ>
 __host__ __device__ constexpr int hash_group_bytes() {
-  return align16(hash_cap<CAP>() * 4) + align16(CAP * 2) + align16((LCAP + 1) * 4) + align16(LCAP * 8) +
+  return align16(hash_cap<CAP, HQ>() * 4) + align16(CAP * 2) + align16((LCAP + 1) * 4) + align16(LCAP * 8) +
          (G > 32 ? align16((G / 32 + 2) * 4) : 0);
 }
 
-template <int G, int CAP, int HB>
+// DIRECT: insert by atomicCAS straight away; else read the slot first and
+// CAS only an empty one (most products of rows that repeat their columns find
+// their column already inserted)
+template <int G, int CAP, int HB, int HQ, bool DIRECT>
 __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
                                          const RowOut& o, const HashBufs& hb) {
   const int rank = g.rank;
@@ -1084,16 +1090,16 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
     P += tot;
   }
   if (rank == 0) hb.off[nl] = P;
-  // H = the power of two >= 1.5P; a column's slot is the HIGH bits of its
-  // multiplicative hash (the low bits of c * K follow c's low bits, which
-  // cluster for structured rows: the stencil's symbolic pass ran 2.7x slower
-  // with them)
+  // a column's slot is the HIGH bits of its multiplicative hash (the low bits
+  // of c * K follow c's low bits, which cluster for structured rows: the
+  // stencil's symbolic pass ran 2.7x slower with them)
   int H = 64, hbits = 6;
-  while (H < P + P / 2) {
+  while (H < P * HQ / 4) {
     H <<= 1;
     ++hbits;
   }
-  for (int e = rank; e < H; e += G) hb.table[e] = kHashEmpty;
+  for (int e = rank; e < (H >> 2); e += G)
+    reinterpret_cast<int4*>(hb.table)[e] = make_int4(kHashEmpty, kHashEmpty, kHashEmpty, kHashEmpty);
   g.sync();
   for (int l = rank; l < nl; l += G) owner_fill(hb.owner, 1, hb.off[l], hb.off[l + 1], l);
   g.sync();
@@ -1115,20 +1121,31 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
       const int c = cc[u];
       if (c < 0) continue;
       unsigned h = (static_cast<unsigned>(c) * 2654435761u) >> (32 - hbits);
-      // a plain load first: most products repeat a column already inserted
-      // (keys are never removed, so a non-empty slot read is final)
-      const volatile int* tv = hb.table;
-      while (true) {
-        int cur = tv[h];
-        if (cur == kHashEmpty) {
-          cur = atomicCAS(&hb.table[h], kHashEmpty, c);
+      if constexpr (DIRECT) {
+        while (true) {
+          const int cur = atomicCAS(&hb.table[h], kHashEmpty, c);
           if (cur == kHashEmpty) {
             ++cnt;
             break;
           }
+          if (cur == c) break;
+          h = (h + 1) & (H - 1);
         }
-        if (cur == c) break;
-        h = (h + 1) & (H - 1);
+      } else {
+        // a plain load first (keys are never removed, so a non-empty slot read is final)
+        const volatile int* tv = hb.table;
+        while (true) {
+          int cur = tv[h];
+          if (cur == kHashEmpty) {
+            cur = atomicCAS(&hb.table[h], kHashEmpty, c);
+            if (cur == kHashEmpty) {
+              ++cnt;
+              break;
+            }
+          }
+          if (cur == c) break;
+          h = (h + 1) & (H - 1);
+        }
       }
     }
   }

@@ -450,26 +450,26 @@ __global__ void __launch_bounds__(G * GPC) k_tier(CsrView A, CsrView B, const in
 }
 
 // PRECISE symbolic phase of tiers 3-6: hash_row per group (GPC groups of G).
-template <int G, int CAP, int LCAP, int GPC, int HB>
+template <int G, int CAP, int LCAP, int GPC, int HB, int HQ, bool DIRECT>
 __global__ void __launch_bounds__(G * GPC) k_hash_symbolic(CsrView A, CsrView B, const int32_t* __restrict__ rows,
                                                           int64_t nrows, RowOut o) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Group<G> g = make_group<G>();
   const int gid = threadIdx.x / G;
-  unsigned char* p = smem + gid * hash_group_bytes<G, CAP, LCAP>();
+  unsigned char* p = smem + gid * hash_group_bytes<G, CAP, LCAP, HQ>();
   auto take = [&](int n) {
     unsigned char* q = p;
     p += align16(n);
     return q;
   };
   HashBufs hb;
-  hb.table = reinterpret_cast<int*>(take(hash_cap<CAP>() * 4));
+  hb.table = reinterpret_cast<int*>(take(hash_cap<CAP, HQ>() * 4));
   hb.owner = reinterpret_cast<unsigned short*>(take(CAP * 2));
   hb.off = reinterpret_cast<int*>(take((LCAP + 1) * 4));
   hb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
   hb.scan_tmp = G > 32 ? reinterpret_cast<int*>(take((G / 32 + 2) * 4)) : nullptr;
   for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
-    hash_row<G, CAP, HB>(g, A, B, rows[r], o, hb);
+    hash_row<G, CAP, HB, HQ, DIRECT>(g, A, B, rows[r], o, hb);
 }
 
 // Tier 1: one thread per row (tiny_row), NT threads per CTA.
@@ -745,14 +745,14 @@ static cudaError_t launch_tiny(const CsrView& A, const CsrView& B, const int32_t
   return cudaGetLastError();
 }
 
-template <int G, int CAP, int LCAP, int GPC, int HB>
+template <int G, int CAP, int LCAP, int GPC, int HB, int HQ, bool DIRECT>
 static cudaError_t launch_hash_t(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
                                  cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  constexpr int smem = hash_group_bytes<G, CAP, LCAP>() * GPC;
+  constexpr int smem = hash_group_bytes<G, CAP, LCAP, HQ>() * GPC;
   static_assert(smem <= 232448, "hash tier shared memory exceeds 227 KB");
   static_assert(G <= 32 || GPC == 1, "a group of more than 32 threads is the whole CTA");
-  auto kern = k_hash_symbolic<G, CAP, LCAP, GPC, HB>;
+  auto kern = k_hash_symbolic<G, CAP, LCAP, GPC, HB, HQ, DIRECT>;
   static LaunchSetup ls;
   int per_sm = 0;
   if (cudaError_t e = kernel_setup(ls, kern, G * GPC, smem, per_sm); e != cudaSuccess) return e;
