@@ -84,10 +84,10 @@ struct TierBounds {
 #define BRM_H3_GPC 4
 #endif
 #ifndef BRM_H4_G
-#define BRM_H4_G 64
+#define BRM_H4_G 32
 #endif
 #ifndef BRM_H4_GPC
-#define BRM_H4_GPC 1
+#define BRM_H4_GPC 2
 #endif
 // 5th field: column loads in flight per thread before they are hashed.
 // Measured on B200 (same box): tier 3 (uniform1m_k16) 2.45 ms with 1 vs
@@ -97,7 +97,10 @@ struct TierBounds {
 // Measured on B200 (same box): stencil27_64's tier-4 symbolic 0.670 ms with
 // HQ 6 -> 0.617 with HQ 5 (a smaller table to clear); uniform1m_k16's tier 3
 // 2.43 ms with a read first vs 2.56 with direct CAS, and 2.43 / 1.82 / 2.42 ms
-// with HQ 8 / 16 / 32 (uniform1m_k16 PRECISE 81.5 -> 90.0 GFLOP/s at 16).
+// with HQ 8 / 16 / 32 (uniform1m_k16 PRECISE 81.5 -> 90.0 GFLOP/s at 16);
+// tier 4 on stencil27_64: 0.617 ms on 64 threads per row, 0.529 on one warp
+// per row (2 rows per CTA; 4 per CTA 0.538), 8 loads in flight (4: 0.636,
+// 2: 0.841), HQ 5 (4: 0.621, 8: 0.674) -- profiles/r02c_hash.
 #ifndef BRM_H3_HB
 #define BRM_H3_HB 1
 #endif
