@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
   int64_t* lstart = reinterpret_cast<int64_t*>(slot + kHvBins);
   int* ioff = reinterpret_cast<int*>(lstart + kHvLists);  // items of each list (plan_for_products)
   int* loff = ioff + kHvLists + 4;
+  unsigned* gp = reinterpret_cast<unsigned*>(loff + kHvLists + 4);  // gp[g] = bits set in groups < g
   __shared__ int s_wtmp[kHvPlanG / 32 + 1];
   __shared__ unsigned long long s_cnt;
   __shared__ int s_cmin, s_cmax;
@@ -212,12 +213,11 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
     const int lo_c = static_cast<int>(max(static_cast<int64_t>(cmin), rs0) - rs0);             // relative
     const int hi_c = static_cast<int>(min(static_cast<int64_t>(cmax) + 1, rs0 + rlen) - rs0);  // relative, exclusive
     // the whole range's bitmap (windows reach bin boundaries outside [lo_c, hi_c))
-    for (int w = t; w < (rlen + 31) >> 5; w += kHvPlanG) bm[w] = 0u;
+    for (int w = t; w < (((rlen + 31) >> 5) + 3) >> 2; w += kHvPlanG) reinterpret_cast<uint4*>(bm)[w] = make_uint4(0, 0, 0, 0);
     if (!count_only) {
-      for (int b = t; b < kHvBins; b += kHvPlanG) {
-        hist[b] = 0u;
-        slot[b] = 0xff;
-      }
+      for (int b = t; b < kHvBins / 4; b += kHvPlanG) reinterpret_cast<uint4*>(hist)[b] = make_uint4(0, 0, 0, 0);
+      for (int b = t; b < kHvBins / 16; b += kHvPlanG)
+        reinterpret_cast<uint4*>(slot)[b] = make_uint4(~0u, ~0u, ~0u, ~0u);
     }
     __syncthreads();
     int prange = 0;
@@ -306,6 +306,8 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
     }
     __syncthreads();
     const int nb = (rlen + (1 << kHvBinBits) - 1) >> kHvBinBits;
+    const int nwords = (rlen + 31) >> 5, ngroups = (nwords + 31) >> 5;
+    bool gp_done = false;
     while (true) {
       if (s_need >= 0) {
         // refine the next kHvFine overflow bins from s_need on (whole CTA)
@@ -417,40 +419,50 @@ __global__ void __launch_bounds__(kHvPlanG, 1) k_hv_plan(HvArgs a, int count_onl
           if (need == -2) s_done = 2;
           if (need == -1 && ptot > 0) s_cnt = static_cast<unsigned long long>(rs0 + x0);  // end of the last window
         }
+      } else if (!gp_done) {
+        // while warp 0 cuts the windows, the other warps count the bits of
+        // every group of 32 bitmap words (16-byte loads: 8 lanes per group)
+        // and warp 1 turns the counts into the exclusive prefix gp
+        gp_done = true;
+        constexpr int NWK = kHvPlanG / 32 - 1;
+        const int sub = lane >> 3, part = lane & 7;
+        for (int g0 = 4 * (wid - 1); g0 < ngroups; g0 += 4 * NWK) {
+          const int g = g0 + sub;
+          const int w = 32 * g + 4 * part;
+          unsigned c = 0;
+          if (g < ngroups && w < nwords) {
+            const uint4 x = *reinterpret_cast<const uint4*>(bm + w);  // (words past nwords are cleared)
+            c = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+          }
+          c += __shfl_xor_sync(0xffffffffu, c, 4);
+          c += __shfl_xor_sync(0xffffffffu, c, 2);
+          c += __shfl_xor_sync(0xffffffffu, c, 1);
+          if (part == 0 && g < ngroups) gp[g + 1] = c;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kHvPlanG - 32) : "memory");  // warps 1.. only
+        if (wid == 1) {
+          unsigned carry = 0;
+          if (lane == 0) gp[0] = 0;
+          for (int g0 = 1; g0 <= ngroups; g0 += 32) {
+            unsigned x = g0 + lane <= ngroups ? gp[g0 + lane] : 0u;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const unsigned y = __shfl_up_sync(0xffffffffu, x, d);
+              if (lane >= d) x += y;
+            }
+            if (g0 + lane <= ngroups) gp[g0 + lane] = x + carry;
+            carry += __shfl_sync(0xffffffffu, x, 31);
+          }
+        }
       }
       __syncthreads();
       if (s_done) break;
     }
     if (s_done == 2) break;
-    // output size of each window of this range = bits set in it: prefix
-    // popcounts of 32-word groups (hist is free now), then two partial
+    // output size of each window of this range = bits set in it: the group
+    // prefix gp (made above, beside the window cutting), then two partial
     // prefixes per window (a warp per window)
     {
-      const int nwords = (rlen + 31) >> 5, ngroups = (nwords + 31) >> 5;
-      unsigned* gp = hist;  // gp[g] = bits in groups < g
-      // a warp per group of 32 words: lane i reads word i (a thread reading
-      // its own 32 words would put all 32 lanes on one bank)
-      for (int g = wid; g < ngroups; g += kHvPlanG / 32) {
-        const int w = 32 * g + lane;
-        const unsigned c = __reduce_add_sync(0xffffffffu, w < nwords ? __popc(bm[w]) : 0u);
-        if (lane == 0) gp[g + 1] = c;
-      }
-      __syncthreads();
-      if (wid == 0) {
-        unsigned carry = 0;
-        if (lane == 0) gp[0] = 0;
-        for (int g0 = 1; g0 <= ngroups; g0 += 32) {
-          unsigned x = g0 + lane <= ngroups ? gp[g0 + lane] : 0u;
-#pragma unroll
-          for (int d = 1; d < 32; d <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += y;
-          }
-          if (g0 + lane <= ngroups) gp[g0 + lane] = x + carry;
-          carry += __shfl_sync(0xffffffffu, x, 31);
-        }
-      }
-      __syncthreads();
       auto bits_below = [&](int x) -> unsigned {  // bits set in [0, x), by one warp
         unsigned c = 0;
         const int w = x >> 5, g = w >> 5;

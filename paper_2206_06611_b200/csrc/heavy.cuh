@@ -93,9 +93,10 @@ struct HvArgs {
 };
 
 // plan shared memory: bitmap, histogram, fine counts, bin slots, list table
+constexpr int kHvGroups = kHvRange / 1024;  // popcount groups of 32 bitmap words
 constexpr int hv_plan_smem() {
   return kHvRange / 8 + kHvBins * 4 + kHvFine * 128 * 4 + kHvBins + kHvLists * 8 + (kHvLists + 4) * 4 +
-         align16((kHvLists + 1) * 4) + 256;
+         align16((kHvLists + 4) * 4) + (kHvGroups + 4) * 4 + 256;
 }
 // merge shared memory
 constexpr int hv_merge_smem() {
