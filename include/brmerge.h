@@ -81,7 +81,7 @@ typedef struct {
 /* Number of row bins (tiers) the binning pass sorts rows into; see DESIGN.md
  * "Kernels": 0 = empty rows (n_prod == 0), 1 = one thread per row (Alg. 1
  * literally, P <= 8), 2 = one warp per row in registers (P <= 32), 3-6 =
- * shared-memory record tiers (warp, warp, 128 and 256 threads per row),
+ * shared-memory record tiers (warp, warp, 256 and 512 threads per row),
  * 7 = heavy rows (windowed BRMerge in column windows, in levels of
  * 512-list blocks beyond 512 lists; or the global-memory tier, see
  * brm_set_heavy_route).                                                     */

@@ -22,8 +22,8 @@ struct CsrView {
 //   2  register BRMerge, one warp       P <= 32,   nl <= 32
 //   3  record BRMerge, one warp         P <= 256,  nl <= 64   (smem records)
 //   4  record BRMerge, one warp         P <= 768,  nl <= 64   (smem records)
-//   5  record BRMerge, 128 threads      P <= 3072, nl <= 256  (smem records)
-//   6  record BRMerge, 256 threads      P <= 6656, nl <= 512  (smem records)
+//   5  record BRMerge, 256 threads      P <= 3072, nl <= 256  (smem records)
+//   6  record BRMerge, 512 threads      P <= 6656, nl <= 512  (smem records)
 //   7  heavy rows: windowed BRMerge (heavy.cuh; column windows of <= 4096
 //      products, levels of 512-list blocks), or under BRM_HEAVY_GLOBAL the
 //      chunked BRMerge on 1024 threads with ping-pong buffers in a global
@@ -56,11 +56,13 @@ struct TierBounds {
 #ifndef BRM_T4_GPC
 #define BRM_T4_GPC 2
 #endif
+// tiers 5-6 on 256 / 512 threads: 3.93 / 14.12 ms numeric on rmat20_ef16
+// against 4.37 / 15.47 on 128 / 256 (profiles/r02c_scale/README.md)
 #ifndef BRM_T5_G
-#define BRM_T5_G 128
+#define BRM_T5_G 256
 #endif
 #ifndef BRM_T6_G
-#define BRM_T6_G 256
+#define BRM_T6_G 512
 #endif
 // PLAIN (5th field): the record round's duplicate combine as plain code the
 // compiler branches around (faster on rows with few duplicates) instead of
@@ -118,8 +120,14 @@ struct TierBounds {
 #define BRM_H4_HQ 5
 #endif
 #define BRM_HASH4 BRM_H4_G, 768, 64, BRM_H4_GPC, BRM_H4_HB, BRM_H4_HQ, false
-#define BRM_HASH5 128, 3072, 256, 1, 8, 5, false
-#define BRM_HASH6 256, 6656, 512, 1, 8, 5, false
+#ifndef BRM_H5_G
+#define BRM_H5_G 128
+#endif
+#ifndef BRM_H6_G
+#define BRM_H6_G 256
+#endif
+#define BRM_HASH5 BRM_H5_G, 3072, 256, 1, 8, 5, false
+#define BRM_HASH6 BRM_H6_G, 6656, 512, 1, 8, 5, false
 constexpr int kGlobalG = 1024;
 
 __host__ __device__ inline TierBounds tier_bounds() {
