@@ -66,6 +66,13 @@ struct brm_context {
   bool hv_single_planned = false;
   DevBuf hv_lt[2], hv_ws_col[2], hv_ws_val[2], hv_tmp;
   HostBuf h_hv;
+  // host-buffer form for large A: row blocks, C copied back per block on a
+  // copy stream (brmerge_spgemm_host, "pipelined")
+  static constexpr int kPipeBlocks = 8;
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t ev_blk[kPipeBlocks] = {};
+  DevBuf blk_rpt[kPipeBlocks], blk_col[kPipeBlocks], blk_val[kPipeBlocks], hb_nprod, hb_off, hb_bounds;
+  HostBuf h_prpt, h_pcol, h_pval, h_bounds;
 };
 
 namespace {
@@ -725,6 +732,110 @@ brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
   return BRM_OK;
 }
 
+// Host-buffer form for large A, pipelined: the rows are cut into
+// kPipeBlocks blocks of balanced n_prod (the §III.D rule, by the library's
+// own n_prod / scan / partition kernels), and each block runs structure +
+// fill on the context stream into its own device C slice; an event then
+// lets a separate copy stream bring the block's rpt / col / val back to
+// pinned host memory while the next block computes. The compute stream never
+// waits for a copy (every block has its own slice), so the device-to-host
+// copies of C -- the e2e step's bound on large outputs -- overlap all but the
+// first block's SpGEMM. A row block is a view of the uploaded A (its rpt
+// values stay absolute offsets into A's col/val); block-local C.rpt values
+// are rebased on the host after the copies.
+constexpr int64_t kPipeMinRows = 65536;
+
+brm_status_t host_pipelined(brm_context_t* ctx, const brm_csr_t* Ah, const brm_csr_t* Bh, const brm_csr_t* Ad,
+                            const brm_csr_t* Bd, brm_mode_t mode, brm_csr_t* Ch) {
+  constexpr int K = brm_context::kPipeBlocks;
+  const int64_t M = Ah->rows;
+  brm_status_t s;
+  if (Ad->cols != Bd->rows) return fail(ctx, BRM_ERR_DIM, "A.cols != B.rows");
+  // (1) row blocks of balanced n_prod
+  CK(ensure(ctx, ctx->hb_nprod, (size_t)M * 8), "alloc n_prod");
+  CK(ensure(ctx, ctx->hb_off, (size_t)(M + 1) * 8), "alloc n_prod offsets");
+  CK(ensure(ctx, ctx->hb_bounds, (size_t)(K + 1) * 8), "alloc block bounds");
+  CK(ensure(ctx, ctx->small, sizeof(SmallDev)), "alloc small");
+  CK(launch_row_nprod(CsrView{Ad->rpt, Ad->col, Ad->val}, Bd->rpt, M, static_cast<int64_t*>(ctx->hb_nprod.p),
+                      ctx->stream), "k_row_nprod");
+  if ((s = run_scan(ctx, static_cast<const int64_t*>(ctx->hb_nprod.p), M, static_cast<int64_t*>(ctx->hb_off.p),
+                    nullptr)) != BRM_OK)
+    return s;
+  CK(launch_partition(static_cast<const int64_t*>(ctx->hb_off.p), M, K, static_cast<int64_t*>(ctx->hb_bounds.p),
+                      ctx->stream), "k_partition");
+  CK(ensure_host(ctx->h_bounds, (size_t)(K + 1) * 8), "alloc pinned bounds");
+  int64_t* bounds = static_cast<int64_t*>(ctx->h_bounds.p);
+  CK(cudaMemcpyAsync(bounds, ctx->hb_bounds.p, (size_t)(K + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream),
+     "D2H block bounds");
+  CK(cudaStreamSynchronize(ctx->stream), "sync block bounds");
+  // the blocks hold C: release the one-shot form's C buffers
+  free_dev(ctx, ctx->stC_col);
+  free_dev(ctx, ctx->stC_val);
+  if (!ctx->copy_st) CK(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking), "create copy stream");
+  for (auto& e : ctx->ev_blk)
+    if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "create block event");
+  CK(ensure_host(ctx->h_prpt, (size_t)(M + 1) * 8), "alloc pinned C.rpt");
+  int64_t* hrpt = static_cast<int64_t*>(ctx->h_prpt.p);
+  // (2) the blocks: compute on the context stream, copies on the copy stream
+  int64_t boff[K + 1] = {};
+  bool fits = true;
+  auto copy_block = [&](int k) -> cudaError_t {
+    const int64_t r0 = bounds[k], r1 = bounds[k + 1], nb = boff[k + 1] - boff[k];
+    cudaError_t e = cudaSuccess;
+    if (r1 > r0)
+      e = cudaMemcpyAsync(hrpt + r0, ctx->blk_rpt[k].p, (size_t)(r1 - r0) * 8, cudaMemcpyDeviceToHost, ctx->copy_st);
+    if (e == cudaSuccess && nb)
+      e = cudaMemcpyAsync(static_cast<double*>(ctx->h_pval.p) + boff[k], ctx->blk_val[k].p, (size_t)nb * 8,
+                          cudaMemcpyDeviceToHost, ctx->copy_st);
+    if (e == cudaSuccess && nb)
+      e = cudaMemcpyAsync(static_cast<int32_t*>(ctx->h_pcol.p) + boff[k], ctx->blk_col[k].p, (size_t)nb * 4,
+                          cudaMemcpyDeviceToHost, ctx->copy_st);
+    return e;
+  };
+  for (int k = 0; k < K; ++k) {
+    const int64_t r0 = bounds[k], r1 = bounds[k + 1];
+    int64_t nb = 0;
+    if (r1 > r0) {
+      const brm_csr_t Ab{r1 - r0, Ad->cols, Ah->rpt[r1] - Ah->rpt[r0], Ad->rpt + r0, Ad->col, Ad->val};
+      CK(ensure(ctx, ctx->blk_rpt[k], (size_t)(r1 - r0 + 1) * 8), "alloc block C.rpt");
+      if ((s = structure_impl(ctx, &Ab, Bd, mode, static_cast<int64_t*>(ctx->blk_rpt[k].p), &nb)) != BRM_OK)
+        return s;
+      CK(ensure(ctx, ctx->blk_col[k], (size_t)nb * 4), "alloc block C.col");
+      CK(ensure(ctx, ctx->blk_val[k], (size_t)nb * 8), "alloc block C.val");
+      brm_csr_t Cb{0, 0, 0, static_cast<int64_t*>(ctx->blk_rpt[k].p), static_cast<int32_t*>(ctx->blk_col[k].p),
+                   static_cast<double*>(ctx->blk_val[k].p)};
+      if ((s = fill_impl(ctx, &Cb)) != BRM_OK) return s;
+    }
+    boff[k + 1] = boff[k] + nb;
+    CK(cudaEventRecord(ctx->ev_blk[k], ctx->stream), "record block event");
+    fits = fits && ctx->h_pcol.cap >= (size_t)boff[k + 1] * 4 && ctx->h_pval.cap >= (size_t)boff[k + 1] * 8;
+    if (fits) {
+      CK(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_blk[k], 0), "copy waits for block");
+      CK(copy_block(k), "D2H block");
+    }
+  }
+  const int64_t nnz = boff[K];
+  if (!fits) {  // first call at this size: grow the pinned output, then copy every block
+    CK(cudaStreamSynchronize(ctx->copy_st), "sync copies");
+    CK(ensure_host(ctx->h_pcol, (size_t)nnz * 4), "alloc pinned C.col");
+    CK(ensure_host(ctx->h_pval, (size_t)nnz * 8), "alloc pinned C.val");
+    CK(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_blk[K - 1], 0), "copy waits for the blocks");
+    for (int k = 0; k < K; ++k) CK(copy_block(k), "D2H block");
+  }
+  CK(cudaStreamSynchronize(ctx->copy_st), "sync copies");
+  CK(cudaStreamSynchronize(ctx->stream), "sync blocks");
+  for (int k = 0; k < K; ++k)
+    for (int64_t r = bounds[k]; r < bounds[k + 1]; ++r) hrpt[r] += boff[k];
+  hrpt[M] = nnz;
+  Ch->rows = M;
+  Ch->cols = Bh->cols;
+  Ch->nnz = nnz;
+  Ch->rpt = hrpt;
+  Ch->val = static_cast<double*>(ctx->h_pval.p);
+  Ch->col = static_cast<int32_t*>(ctx->h_pcol.p);
+  return BRM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -772,12 +883,22 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
                       &ctx->hv_single.cuts, &ctx->hv_single.wout, &ctx->hv_single.nwin, &ctx->hv_single.total,
                       &ctx->hv_multi.d_rows, &ctx->hv_multi.cuts, &ctx->hv_multi.wout, &ctx->hv_multi.nwin,
                       &ctx->hv_multi.total, &ctx->hv_lt[0], &ctx->hv_lt[1], &ctx->hv_ws_col[0], &ctx->hv_ws_col[1],
-                      &ctx->hv_ws_val[0], &ctx->hv_ws_val[1], &ctx->hv_tmp})
+                      &ctx->hv_ws_val[0], &ctx->hv_ws_val[1], &ctx->hv_tmp, &ctx->hb_nprod, &ctx->hb_off,
+                      &ctx->hb_bounds})
       free_dev(ctx, *b);
+    for (int k = 0; k < brm_context::kPipeBlocks; ++k)
+      for (DevBuf* b : {&ctx->blk_rpt[k], &ctx->blk_col[k], &ctx->blk_val[k]}) free_dev(ctx, *b);
     cudaStreamSynchronize(ctx->stream);
-    for (HostBuf* b : {&ctx->h_small, &ctx->h_heavy, &ctx->h_gws_off, &ctx->h_C, &ctx->h_rows})
+    if (ctx->copy_st) {
+      cudaStreamSynchronize(ctx->copy_st);
+      cudaStreamDestroy(ctx->copy_st);
+    }
+    for (HostBuf* b : {&ctx->h_small, &ctx->h_heavy, &ctx->h_gws_off, &ctx->h_C, &ctx->h_rows, &ctx->h_prpt,
+                       &ctx->h_pcol, &ctx->h_pval, &ctx->h_bounds})
       if (b->p) cudaFreeHost(b->p);
     for (auto& e : ctx->ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->ev_blk)
       if (e) cudaEventDestroy(e);
     if (ctx->handoff) cudaEventDestroy(ctx->handoff);
   }
@@ -924,6 +1045,7 @@ brm_status_t brmerge_spgemm_host(brm_context_t* ctx, const brm_csr_t* Ah, const 
   const DevBuf& bv = same ? ctx->stA_val : ctx->stB_val;
   brm_csr_t Bd{Bh->rows, Bh->cols, Bh->nnz, static_cast<int64_t*>(br.p), static_cast<int32_t*>(bc.p),
                static_cast<double*>(bv.p)};
+  if (Ah->rows >= kPipeMinRows) return host_pipelined(ctx, Ah, Bh, &Ad, &Bd, mode, Ch);
   CK(ensure(ctx, ctx->stC_rpt, (size_t)(Ah->rows + 1) * 8), "alloc C.rpt");
   int64_t nnz = 0;
   if ((s = structure_impl(ctx, &Ad, &Bd, mode, static_cast<int64_t*>(ctx->stC_rpt.p), &nnz)) != BRM_OK) return s;

@@ -471,3 +471,34 @@ def test_host_form_heavy_rows(ctx, oracle_mod, mode):
     rows, cols, rpt, col, val = ctx.brmerge_spgemm_host(Ah, Ah, mode)
     assert (rows, cols) == (A.rows, A.cols)
     compare((rpt.copy(), col.copy(), val.copy()), A, A)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_host_form_pipelined_heavy_rows(ctx, oracle_mod, mode):
+    """The host-buffer entry's row-blocked pipeline (A of >= 65,536 rows: 8
+    blocks of balanced n_prod, C copied back per block on a copy stream) on a
+    matrix whose heavy rows (one level and 512-list blocks) sit in different
+    blocks, plus empty rows; two calls (pinned output grown, then reused)."""
+    from paper_2206_06611_b200 import TorchCsr
+    rng = np.random.default_rng(77)
+    M = 70001
+    base = uniform_random(M, M, 3, seed=78)
+    heavy = {5: 700, 20000: 300, 45000: 1100, 69999: 520}
+    empty = {100, 30000}
+    cols, rpt = [], [0]
+    for i in range(M):
+        if i in empty:
+            c = np.zeros(0, np.int32)
+        elif i in heavy:
+            c = np.sort(rng.choice(M, size=heavy[i], replace=False)).astype(np.int32)
+        else:
+            c = base.col[base.rpt[i]:base.rpt[i + 1]]
+        cols.append(c)
+        rpt.append(rpt[-1] + c.size)
+    col = np.concatenate(cols)
+    A = Csr(M, M, np.array(rpt, np.int64), col, rng.uniform(-1, 1, size=col.size))
+    Ah = TorchCsr.from_csr(A, pin=True)
+    for _ in range(2):
+        rows, ncols, hrpt, hcol, hval = ctx.brmerge_spgemm_host(Ah, Ah, mode)
+        assert (rows, ncols) == (M, M)
+        compare((hrpt.copy(), hcol.copy(), hval.copy()), A, A)
