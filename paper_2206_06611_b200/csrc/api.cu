@@ -68,11 +68,14 @@ struct brm_context {
   HostBuf h_hv;
   // host-buffer form for large A: row blocks, C copied back per block on a
   // copy stream (brmerge_spgemm_host, "pipelined")
-  static constexpr int kPipeBlocks = 8;
+  static constexpr int kPipeBlocks = 16;
   cudaStream_t copy_st = nullptr;
   cudaEvent_t ev_blk[kPipeBlocks] = {};
   DevBuf blk_rpt[kPipeBlocks], blk_col[kPipeBlocks], blk_val[kPipeBlocks], hb_nprod, hb_off, hb_bounds;
-  HostBuf h_prpt, h_pcol, h_pval, h_bounds;
+  HostBuf h_prpt, h_pcol, h_pval, h_bounds, h_rb;
+  // readbacks by a copy kernel instead of a copy engine (set while the
+  // pipelined host entry keeps a copy engine busy with C)
+  bool kernel_readback = false;
 };
 
 namespace {
@@ -150,6 +153,16 @@ cudaError_t ensure_host(HostBuf& b, size_t bytes) {
   }
   b.cap = want;
   return cudaSuccess;
+}
+
+// Small device -> host readbacks of the library's own host logic (summaries,
+// heavy-row info) into PINNED memory: a copy engine normally, a copy kernel
+// (SM stores through the pinned buffer's host mapping) while the pipelined
+// host entry's bulk copies occupy the copy engine -- queued behind them, a
+// readback would stall the compute stream until the bulk copy ended.
+cudaError_t readback(brm_context_t* ctx, void* pinned_dst, const void* src, size_t bytes) {
+  if (ctx->kernel_readback) return launch_copy_to_host(pinned_dst, src, (int64_t)bytes, 4, ctx->stream);
+  return cudaMemcpyAsync(pinned_dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream);
 }
 
 void free_dev(brm_context_t* ctx, DevBuf& b) {
@@ -267,9 +280,10 @@ brm_status_t hv_upload(brm_context_t* ctx, HvSet& set, bool sort) {
 }
 
 brm_status_t hv_check_err(brm_context_t* ctx) {
-  unsigned int e = 0;
-  CK(cudaMemcpyAsync(&e, &small_dev(ctx)->hv_err, 4, cudaMemcpyDeviceToHost, ctx->stream), "copy heavy flags");
+  CK(ensure_host(ctx->h_rb, 16), "alloc pinned readback");
+  CK(readback(ctx, ctx->h_rb.p, &small_dev(ctx)->hv_err, 4), "copy heavy flags");
   CK(cudaStreamSynchronize(ctx->stream), "sync heavy flags");
+  const unsigned int e = *static_cast<const unsigned int*>(ctx->h_rb.p);
   if (e) return fail(ctx, BRM_ERR_CUDA, "heavy rows: internal inconsistency (flags " + std::to_string(e) + ")");
   return BRM_OK;
 }
@@ -406,9 +420,10 @@ brm_status_t hv_run_multi(brm_context_t* ctx, int out, const RowOut& o, const st
         CK(ensure(ctx, ctx->hv_tmp, nv * 8), "alloc heavy block sizes");
         CK(launch_hv_vrow_nprod(a, static_cast<int64_t*>(ctx->hv_tmp.p), ctx->stream), "k_hv_vrow_nprod");
         ++ctx->launches;
-        std::vector<int64_t> np(nv);
-        CK(cudaMemcpyAsync(np.data(), ctx->hv_tmp.p, nv * 8, cudaMemcpyDeviceToHost, ctx->stream), "copy block sizes");
+        CK(ensure_host(ctx->h_rb, nv * 8), "alloc pinned readback");
+        CK(readback(ctx, ctx->h_rb.p, ctx->hv_tmp.p, nv * 8), "copy block sizes");
         CK(cudaStreamSynchronize(ctx->stream), "sync block sizes");
+        const int64_t* np = static_cast<const int64_t*>(ctx->h_rb.p);
         for (size_t v = 0; v < nv; ++v) set.rows[v].nprod = np[v];
       }
       // sort heaviest first, keeping each virtual row's Cur entry
@@ -437,9 +452,11 @@ brm_status_t hv_run_multi(brm_context_t* ctx, int out, const RowOut& o, const st
       std::vector<Cur> next;
       if (blocks) {
         // block results: contiguous per row, in block order
-        std::vector<int64_t> tot(nv);
-        CK(cudaMemcpyAsync(tot.data(), set.total.p, nv * 8, cudaMemcpyDeviceToHost, ctx->stream), "copy block totals");
+        CK(ensure_host(ctx->h_rb, nv * 8), "alloc pinned readback");
+        CK(readback(ctx, ctx->h_rb.p, set.total.p, nv * 8), "copy block totals");
         CK(cudaStreamSynchronize(ctx->stream), "sync block totals");
+        const std::vector<int64_t> tot(static_cast<const int64_t*>(ctx->h_rb.p),
+                                       static_cast<const int64_t*>(ctx->h_rb.p) + nv);
         std::vector<std::vector<size_t>> of(cur.size());  // block virtual rows of each Cur, in block order
         for (size_t v = 0; v < nv; ++v)
           if (set.rows[v].out == 1) of[owner[v]].push_back(v);
@@ -501,16 +518,14 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
        "k_heavy_info");
     ++ctx->launches;
     CK(ensure_host(ctx->h_heavy, (size_t)nh * 16), "alloc pinned heavy info");
-    CK(cudaMemcpyAsync(ctx->h_heavy.p, ctx->heavy_info.p, (size_t)nh * 16, cudaMemcpyDeviceToHost,
-                       ctx->stream),
-       "copy heavy info");
+    CK(readback(ctx, ctx->h_heavy.p, ctx->heavy_info.p, (size_t)nh * 16), "copy heavy info");
     CK(cudaStreamSynchronize(ctx->stream), "sync heavy info");
     const int64_t* hi = static_cast<const int64_t*>(ctx->h_heavy.p);
     ctx->heavy.assign(hi, hi + 2 * nh);
     ctx->heavy_loaded = true;
   }
   CK(ensure_host(ctx->h_rows, (size_t)nh * 4), "alloc pinned heavy rows");
-  CK(cudaMemcpyAsync(ctx->h_rows.p, hrows, (size_t)nh * 4, cudaMemcpyDeviceToHost, ctx->stream), "copy heavy rows");
+  CK(readback(ctx, ctx->h_rows.p, hrows, (size_t)nh * 4), "copy heavy rows");
   CK(cudaStreamSynchronize(ctx->stream), "sync heavy rows");
   const int32_t* hr = static_cast<const int32_t*>(ctx->h_rows.p);
   if (ctx->heavy_route == BRM_HEAVY_AUTO) {
@@ -656,7 +671,7 @@ brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
      "k_bin_scatter");
   if (M > 0) ctx->launches += 2;
   ev_record(ctx, 1);
-  CK(cudaMemcpyAsync(ctx->h_small.p, sd, sizeof(SmallDev), cudaMemcpyDeviceToHost, ctx->stream), "copy summary");
+  CK(readback(ctx, ctx->h_small.p, sd, sizeof(SmallDev)), "copy summary");
   CK(cudaStreamSynchronize(ctx->stream), "sync summary");
   ctx->sum = static_cast<SmallDev*>(ctx->h_small.p)->summary;
   ctx->stats.nprod_total = ctx->sum.nprod_total;
@@ -694,7 +709,7 @@ brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
   // Step 5 (UPPER) / Step 4 (PRECISE): prefix sum of row sizes -> rpt, nnz(C)
   if ((s = run_scan(ctx, row_size, M, c_rpt, &sd->nnz_total)) != BRM_OK) return s;
   ev_record(ctx, 4);
-  CK(cudaMemcpyAsync(ctx->h_small.p, sd, sizeof(SmallDev), cudaMemcpyDeviceToHost, ctx->stream), "copy nnz");
+  CK(readback(ctx, ctx->h_small.p, sd, sizeof(SmallDev)), "copy nnz");
   CK(cudaStreamSynchronize(ctx->stream), "sync nnz");
   ctx->nnz_c = static_cast<SmallDev*>(ctx->h_small.p)->nnz_total;
   *c_nnz = ctx->nnz_c;
@@ -732,8 +747,8 @@ brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
   return BRM_OK;
 }
 
-// Host-buffer form for large A, pipelined: the rows are cut into
-// kPipeBlocks blocks of balanced n_prod (the §III.D rule, by the library's
+// Host-buffer form for large A, pipelined: the rows are cut into 8 or 16
+// blocks of balanced n_prod (the §III.D rule, by the library's
 // own n_prod / scan / partition kernels), and each block runs structure +
 // fill on the context stream into its own device C slice; an event then
 // lets a separate copy stream bring the block's rpt / col / val back to
@@ -747,24 +762,41 @@ constexpr int64_t kPipeMinRows = 65536;
 
 brm_status_t host_pipelined(brm_context_t* ctx, const brm_csr_t* Ah, const brm_csr_t* Bh, const brm_csr_t* Ad,
                             const brm_csr_t* Bd, brm_mode_t mode, brm_csr_t* Ch) {
-  constexpr int K = brm_context::kPipeBlocks;
+  constexpr int KMAX = brm_context::kPipeBlocks;
+  static const bool diag_nocopy = getenv("BRM_PIPE_NOCOPY") != nullptr;  // diagnostics: skip the copies
+  static const bool diag_trace = getenv("BRM_PIPE_TRACE") != nullptr;    // diagnostics: block timeline
+  cudaEvent_t tr0 = nullptr, trc[KMAX] = {}, trd[KMAX] = {};
+  if (diag_trace) {
+    cudaEventCreate(&tr0);
+    for (int k = 0; k < KMAX; ++k) {
+      cudaEventCreate(&trc[k]);
+      cudaEventCreate(&trd[k]);
+    }
+    cudaEventRecord(tr0, ctx->stream);
+  }
   const int64_t M = Ah->rows;
   brm_status_t s;
   if (Ad->cols != Bd->rows) return fail(ctx, BRM_ERR_DIM, "A.cols != B.rows");
   // (1) row blocks of balanced n_prod
   CK(ensure(ctx, ctx->hb_nprod, (size_t)M * 8), "alloc n_prod");
   CK(ensure(ctx, ctx->hb_off, (size_t)(M + 1) * 8), "alloc n_prod offsets");
-  CK(ensure(ctx, ctx->hb_bounds, (size_t)(K + 1) * 8), "alloc block bounds");
+  CK(ensure(ctx, ctx->hb_bounds, (size_t)(KMAX + 1) * 8), "alloc block bounds");
   CK(ensure(ctx, ctx->small, sizeof(SmallDev)), "alloc small");
   CK(launch_row_nprod(CsrView{Ad->rpt, Ad->col, Ad->val}, Bd->rpt, M, static_cast<int64_t*>(ctx->hb_nprod.p),
                       ctx->stream), "k_row_nprod");
   if ((s = run_scan(ctx, static_cast<const int64_t*>(ctx->hb_nprod.p), M, static_cast<int64_t*>(ctx->hb_off.p),
                     nullptr)) != BRM_OK)
     return s;
+  // blocks: 16 for large outputs (the first block's SpGEMM is the part no
+  // copy overlaps), else 8
+  CK(ensure_host(ctx->h_bounds, (size_t)(KMAX + 1) * 8), "alloc pinned bounds");
+  int64_t* bounds = static_cast<int64_t*>(ctx->h_bounds.p);
+  CK(cudaMemcpyAsync(bounds, static_cast<const int64_t*>(ctx->hb_off.p) + M, 8, cudaMemcpyDeviceToHost, ctx->stream),
+     "D2H n_prod total");
+  CK(cudaStreamSynchronize(ctx->stream), "sync n_prod total");
+  const int K = bounds[0] >= (4ll << 30) ? KMAX : KMAX / 2;
   CK(launch_partition(static_cast<const int64_t*>(ctx->hb_off.p), M, K, static_cast<int64_t*>(ctx->hb_bounds.p),
                       ctx->stream), "k_partition");
-  CK(ensure_host(ctx->h_bounds, (size_t)(K + 1) * 8), "alloc pinned bounds");
-  int64_t* bounds = static_cast<int64_t*>(ctx->h_bounds.p);
   CK(cudaMemcpyAsync(bounds, ctx->hb_bounds.p, (size_t)(K + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream),
      "D2H block bounds");
   CK(cudaStreamSynchronize(ctx->stream), "sync block bounds");
@@ -777,19 +809,27 @@ brm_status_t host_pipelined(brm_context_t* ctx, const brm_csr_t* Ah, const brm_c
   CK(ensure_host(ctx->h_prpt, (size_t)(M + 1) * 8), "alloc pinned C.rpt");
   int64_t* hrpt = static_cast<int64_t*>(ctx->h_prpt.p);
   // (2) the blocks: compute on the context stream, copies on the copy stream
-  int64_t boff[K + 1] = {};
+  int64_t boff[KMAX + 1] = {};
   bool fits = true;
+  // bulk copies on a copy engine (a copy kernel on the SMs measured ~29 GB/s
+  // against the engine's ~48); the blocks' own small readbacks go through a
+  // copy kernel meanwhile (readback()), so they do not queue behind the bulk
+  auto d2h = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->copy_st);
+  };
+  struct ReadbackMode {
+    brm_context_t* c;
+    ~ReadbackMode() { c->kernel_readback = false; }
+  } rb_mode{ctx};
+  ctx->kernel_readback = true;
   auto copy_block = [&](int k) -> cudaError_t {
     const int64_t r0 = bounds[k], r1 = bounds[k + 1], nb = boff[k + 1] - boff[k];
     cudaError_t e = cudaSuccess;
-    if (r1 > r0)
-      e = cudaMemcpyAsync(hrpt + r0, ctx->blk_rpt[k].p, (size_t)(r1 - r0) * 8, cudaMemcpyDeviceToHost, ctx->copy_st);
+    if (r1 > r0) e = d2h(hrpt + r0, ctx->blk_rpt[k].p, (size_t)(r1 - r0) * 8);
     if (e == cudaSuccess && nb)
-      e = cudaMemcpyAsync(static_cast<double*>(ctx->h_pval.p) + boff[k], ctx->blk_val[k].p, (size_t)nb * 8,
-                          cudaMemcpyDeviceToHost, ctx->copy_st);
+      e = d2h(static_cast<double*>(ctx->h_pval.p) + boff[k], ctx->blk_val[k].p, (size_t)nb * 8);
     if (e == cudaSuccess && nb)
-      e = cudaMemcpyAsync(static_cast<int32_t*>(ctx->h_pcol.p) + boff[k], ctx->blk_col[k].p, (size_t)nb * 4,
-                          cudaMemcpyDeviceToHost, ctx->copy_st);
+      e = d2h(static_cast<int32_t*>(ctx->h_pcol.p) + boff[k], ctx->blk_col[k].p, (size_t)nb * 4);
     return e;
   };
   for (int k = 0; k < K; ++k) {
@@ -809,12 +849,21 @@ brm_status_t host_pipelined(brm_context_t* ctx, const brm_csr_t* Ah, const brm_c
     boff[k + 1] = boff[k] + nb;
     CK(cudaEventRecord(ctx->ev_blk[k], ctx->stream), "record block event");
     fits = fits && ctx->h_pcol.cap >= (size_t)boff[k + 1] * 4 && ctx->h_pval.cap >= (size_t)boff[k + 1] * 8;
-    if (fits) {
+    if (fits && !diag_nocopy) {
       CK(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_blk[k], 0), "copy waits for block");
       CK(copy_block(k), "D2H block");
     }
+    if (diag_trace) {
+      cudaEventRecord(trc[k], ctx->stream);
+      cudaEventRecord(trd[k], ctx->copy_st);
+    }
   }
   const int64_t nnz = boff[K];
+  if (diag_nocopy) {
+    CK(ensure_host(ctx->h_pcol, (size_t)nnz * 4), "alloc pinned C.col");
+    CK(ensure_host(ctx->h_pval, (size_t)nnz * 8), "alloc pinned C.val");
+    fits = true;
+  }
   if (!fits) {  // first call at this size: grow the pinned output, then copy every block
     CK(cudaStreamSynchronize(ctx->copy_st), "sync copies");
     CK(ensure_host(ctx->h_pcol, (size_t)nnz * 4), "alloc pinned C.col");
@@ -824,6 +873,20 @@ brm_status_t host_pipelined(brm_context_t* ctx, const brm_csr_t* Ah, const brm_c
   }
   CK(cudaStreamSynchronize(ctx->copy_st), "sync copies");
   CK(cudaStreamSynchronize(ctx->stream), "sync blocks");
+  if (diag_trace) {
+    for (int k = 0; k < K; ++k) {
+      float tc = 0, td = 0;
+      cudaEventElapsedTime(&tc, tr0, trc[k]);
+      cudaEventElapsedTime(&td, tr0, trd[k]);
+      fprintf(stderr, "block %d: rows %lld nnz %lld compute done %.1f ms, copy done %.1f ms\n", k,
+              (long long)(bounds[k + 1] - bounds[k]), (long long)(boff[k + 1] - boff[k]), tc, td);
+    }
+    for (int k = 0; k < KMAX; ++k) {
+      cudaEventDestroy(trc[k]);
+      cudaEventDestroy(trd[k]);
+    }
+    cudaEventDestroy(tr0);
+  }
   for (int k = 0; k < K; ++k)
     for (int64_t r = bounds[k]; r < bounds[k + 1]; ++r) hrpt[r] += boff[k];
   hrpt[M] = nnz;
@@ -894,7 +957,7 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
       cudaStreamDestroy(ctx->copy_st);
     }
     for (HostBuf* b : {&ctx->h_small, &ctx->h_heavy, &ctx->h_gws_off, &ctx->h_C, &ctx->h_rows, &ctx->h_prpt,
-                       &ctx->h_pcol, &ctx->h_pval, &ctx->h_bounds})
+                       &ctx->h_pcol, &ctx->h_pval, &ctx->h_bounds, &ctx->h_rb})
       if (b->p) cudaFreeHost(b->p);
     for (auto& e : ctx->ev)
       if (e) cudaEventDestroy(e);

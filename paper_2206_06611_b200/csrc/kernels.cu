@@ -834,4 +834,38 @@ cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, i
   return cudaGetLastError();
 }
 
+// Device -> pinned host copy by the SMs (stores through the host mapping of
+// the pinned buffer) instead of a copy engine: a bulk copy on a copy engine
+// queues the library's small readbacks (row-size summaries, heavy-row info)
+// behind it. W-byte words, coalesced, grid-stride.
+template <class W>
+__global__ void __launch_bounds__(256) k_copy_to_host(W* __restrict__ dst, const W* __restrict__ src, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int U = 4;  // loads in flight per thread
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    W v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = __ldcs(src + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < U; ++u) __stcs(dst + i + u * stride, v[u]);
+  }
+  for (; i < n; i += stride) __stcs(dst + i, __ldcs(src + i));
+}
+
+cudaError_t launch_copy_to_host(void* dst, const void* src, int64_t bytes, int ctas, cudaStream_t st) {
+  if (bytes <= 0) return cudaSuccess;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | (uintptr_t)bytes;
+  if ((a & 15) == 0)
+    k_copy_to_host<int4><<<ctas, 256, 0, st>>>(static_cast<int4*>(dst), static_cast<const int4*>(src), bytes / 16);
+  else if ((a & 7) == 0)
+    k_copy_to_host<long long><<<ctas, 256, 0, st>>>(static_cast<long long*>(dst), static_cast<const long long*>(src),
+                                                   bytes / 8);
+  else if ((a & 3) == 0)
+    k_copy_to_host<int><<<ctas, 256, 0, st>>>(static_cast<int*>(dst), static_cast<const int*>(src), bytes / 4);
+  else
+    k_copy_to_host<char><<<ctas, 256, 0, st>>>(static_cast<char*>(dst), static_cast<const char*>(src), bytes);
+  return cudaGetLastError();
+}
+
 }  // namespace brm

@@ -39,5 +39,7 @@ cudaError_t launch_compact(int64_t M, int64_t nnz, const int64_t* nprod_off, con
                            const double* cbar_val, int32_t* ccol, double* cval, cudaStream_t st);
 cudaError_t launch_partition(const int64_t* nprod_off, int64_t M, int p, int64_t* bounds, cudaStream_t st);
 cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod, cudaStream_t st);
+// device -> pinned (host-mapped) memory copy by `ctas` CTAs of the SMs
+cudaError_t launch_copy_to_host(void* dst, const void* src, int64_t bytes, int ctas, cudaStream_t st);
 
 }  // namespace brm
