@@ -133,6 +133,12 @@ BRM_API brm_status_t brm_set_timing(brm_context_t* ctx, int enable);
 #define BRM_HEAVY_AUTO 0
 #define BRM_HEAVY_GLOBAL 1
 BRM_API brm_status_t brm_set_heavy_route(brm_context_t* ctx, int route);
+/* Host-buffer form (brmerge_spgemm_host) for A of >= 65,536 rows: row blocks
+ * of balanced n_prod whose C is copied back on a copy stream while the next
+ * block computes, used when A*B has at least `min_products` intermediate
+ * products (default 2^26; 0: always). Smaller products run the one-shot
+ * form. Results are identical. Errors: BRM_ERR_INVALID (negative).        */
+BRM_API brm_status_t brm_set_host_pipeline(brm_context_t* ctx, int64_t min_products);
 /* Last error message of this context (static storage owned by ctx). */
 BRM_API const char* brm_last_error(const brm_context_t* ctx);
 BRM_API const char* brm_status_string(brm_status_t s);

@@ -66,6 +66,7 @@ SIGNATURES = {
     "brm_set_stream": [_P, _P],
     "brm_set_timing": [_P, ctypes.c_int],
     "brm_set_heavy_route": [_P, ctypes.c_int],
+    "brm_set_host_pipeline": [_P, ctypes.c_int64],
     "brm_last_error": [_P],
     "brm_status_string": [ctypes.c_int],
     "brm_get_stats": [_P, ctypes.POINTER(brm_stats_t)],
@@ -187,9 +188,14 @@ class Context:
     HEAVY_AUTO, HEAVY_GLOBAL = 0, 1
 
     def brm_set_heavy_route(self, route: int):
-        """Route of the heavy rows: HEAVY_AUTO (column slabs / list blocks) or
-        HEAVY_GLOBAL (all on the global-memory tier); include/brmerge.h."""
+        """Route of the heavy rows: HEAVY_AUTO (windowed BRMerge, levels of
+        list blocks) or HEAVY_GLOBAL (all on the global-memory tier); include/brmerge.h."""
         self._check(self.lib.brm_set_heavy_route(self._h, int(route)))
+
+    def brm_set_host_pipeline(self, min_products: int):
+        """Host-buffer form: pipeline row blocks when A*B has >= min_products
+        intermediate products (0: always; A of >= 65,536 rows); include/brmerge.h."""
+        self._check(self.lib.brm_set_host_pipeline(self._h, int(min_products)))
 
     def stats(self) -> dict:
         s = brm_stats_t()

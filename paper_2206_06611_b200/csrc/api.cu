@@ -76,6 +76,7 @@ struct brm_context {
   // readbacks by a copy kernel instead of a copy engine (set while the
   // pipelined host entry keeps a copy engine busy with C)
   bool kernel_readback = false;
+  int64_t pipe_min_products = int64_t(1) << 26;  // brm_set_host_pipeline
 };
 
 namespace {
@@ -747,8 +748,8 @@ brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
   return BRM_OK;
 }
 
-// Host-buffer form for large A, pipelined: the rows are cut into 8 or 16
-// blocks of balanced n_prod (the §III.D rule, by the library's
+// Host-buffer form for large A (>= 65,536 rows, >= 2^26 intermediate
+// products by default: brm_set_host_pipeline), pipelined: the rows are cut into 8 or 16 blocks of balanced n_prod (the §III.D rule, by the library's
 // own n_prod / scan / partition kernels), and each block runs structure +
 // fill on the context stream into its own device C slice; an event then
 // lets a separate copy stream bring the block's rpt / col / val back to
@@ -761,7 +762,7 @@ brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
 constexpr int64_t kPipeMinRows = 65536;
 
 brm_status_t host_pipelined(brm_context_t* ctx, const brm_csr_t* Ah, const brm_csr_t* Bh, const brm_csr_t* Ad,
-                            const brm_csr_t* Bd, brm_mode_t mode, brm_csr_t* Ch) {
+                            const brm_csr_t* Bd, brm_mode_t mode, brm_csr_t* Ch, bool* declined) {
   constexpr int KMAX = brm_context::kPipeBlocks;
   static const bool diag_nocopy = getenv("BRM_PIPE_NOCOPY") != nullptr;  // diagnostics: skip the copies
   static const bool diag_trace = getenv("BRM_PIPE_TRACE") != nullptr;    // diagnostics: block timeline
@@ -794,6 +795,10 @@ brm_status_t host_pipelined(brm_context_t* ctx, const brm_csr_t* Ah, const brm_c
   CK(cudaMemcpyAsync(bounds, static_cast<const int64_t*>(ctx->hb_off.p) + M, 8, cudaMemcpyDeviceToHost, ctx->stream),
      "D2H n_prod total");
   CK(cudaStreamSynchronize(ctx->stream), "sync n_prod total");
+  // small outputs: the blocks' fixed costs (host syncs, launches) outweigh
+  // the copy they hide -- the one-shot form runs instead
+  *declined = bounds[0] < ctx->pipe_min_products;
+  if (*declined) return BRM_OK;
   const int K = bounds[0] >= (4ll << 30) ? KMAX : KMAX / 2;
   CK(launch_partition(static_cast<const int64_t*>(ctx->hb_off.p), M, K, static_cast<int64_t*>(ctx->hb_bounds.p),
                       ctx->stream), "k_partition");
@@ -988,6 +993,13 @@ brm_status_t brm_set_timing(brm_context_t* ctx, int enable) {
   return BRM_OK;
 }
 
+brm_status_t brm_set_host_pipeline(brm_context_t* ctx, int64_t min_products) {
+  if (!ctx) return BRM_ERR_INVALID;
+  if (min_products < 0) return fail(ctx, BRM_ERR_INVALID, "min_products < 0");
+  ctx->pipe_min_products = min_products;
+  return BRM_OK;
+}
+
 brm_status_t brm_set_heavy_route(brm_context_t* ctx, int route) {
   if (!ctx || (route != BRM_HEAVY_AUTO && route != BRM_HEAVY_GLOBAL)) return BRM_ERR_INVALID;
   ctx->heavy_route = route;
@@ -1108,7 +1120,11 @@ brm_status_t brmerge_spgemm_host(brm_context_t* ctx, const brm_csr_t* Ah, const 
   const DevBuf& bv = same ? ctx->stA_val : ctx->stB_val;
   brm_csr_t Bd{Bh->rows, Bh->cols, Bh->nnz, static_cast<int64_t*>(br.p), static_cast<int32_t*>(bc.p),
                static_cast<double*>(bv.p)};
-  if (Ah->rows >= kPipeMinRows) return host_pipelined(ctx, Ah, Bh, &Ad, &Bd, mode, Ch);
+  if (Ah->rows >= kPipeMinRows) {
+    bool declined = false;
+    s = host_pipelined(ctx, Ah, Bh, &Ad, &Bd, mode, Ch, &declined);
+    if (s != BRM_OK || !declined) return s;
+  }
   CK(ensure(ctx, ctx->stC_rpt, (size_t)(Ah->rows + 1) * 8), "alloc C.rpt");
   int64_t nnz = 0;
   if ((s = structure_impl(ctx, &Ad, &Bd, mode, static_cast<int64_t*>(ctx->stC_rpt.p), &nnz)) != BRM_OK) return s;

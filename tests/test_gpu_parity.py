@@ -409,13 +409,15 @@ def test_host_form_large(ctx, oracle_mod, mode):
     A = uniform_random(70001, 70001, 6, seed=31)
     B = random_sparse(70001, 300, 0.01, seed=32)
     Ah = TorchCsr.from_csr(A, pin=True)
-    for _ in range(2):
-        rows, cols, rpt, col, val = ctx.brmerge_spgemm_host(Ah, Ah, mode)
-        assert (rows, cols) == (70001, 70001)
-        compare((rpt.copy(), col.copy(), val.copy()), A, A)
     Bh = TorchCsr.from_csr(B, pin=True)
-    rows, cols, rpt, col, val = ctx.brmerge_spgemm_host(Ah, Bh, mode)
-    compare((rpt.copy(), col.copy(), val.copy()), A, B)
+    for pipe in (0, 1 << 26):  # row-blocked pipeline forced, then the one-shot form (small product)
+        ctx.brm_set_host_pipeline(pipe)
+        for _ in range(2):
+            rows, cols, rpt, col, val = ctx.brmerge_spgemm_host(Ah, Ah, mode)
+            assert (rows, cols) == (70001, 70001)
+            compare((rpt.copy(), col.copy(), val.copy()), A, A)
+        rows, cols, rpt, col, val = ctx.brmerge_spgemm_host(Ah, Bh, mode)
+        compare((rpt.copy(), col.copy(), val.copy()), A, B)
 
 
 def test_alg1_pairing_order_hand_derived(ctx):
@@ -498,7 +500,11 @@ def test_host_form_pipelined_heavy_rows(ctx, oracle_mod, mode):
     col = np.concatenate(cols)
     A = Csr(M, M, np.array(rpt, np.int64), col, rng.uniform(-1, 1, size=col.size))
     Ah = TorchCsr.from_csr(A, pin=True)
-    for _ in range(2):
-        rows, ncols, hrpt, hcol, hval = ctx.brmerge_spgemm_host(Ah, Ah, mode)
-        assert (rows, ncols) == (M, M)
-        compare((hrpt.copy(), hcol.copy(), hval.copy()), A, A)
+    ctx.brm_set_host_pipeline(0)  # pipeline at any product count
+    try:
+        for _ in range(2):
+            rows, ncols, hrpt, hcol, hval = ctx.brmerge_spgemm_host(Ah, Ah, mode)
+            assert (rows, ncols) == (M, M)
+            compare((hrpt.copy(), hcol.copy(), hval.copy()), A, A)
+    finally:
+        ctx.brm_set_host_pipeline(1 << 26)

@@ -1,4 +1,4 @@
-OUT=gpurun_out/e2e1; mkdir -p $OUT
+OUT=gpurun_out/${TAG:-e2e1}; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
 timeout 900 python -m pytest tests -m gpu -q -x -k "host" > $OUT/pytest_host.log 2>&1; echo "rc=$?" >> $OUT/pytest_host.log
 timeout 1200 python bench.py --no-cpu-baseline > $OUT/bench_rmat20.json 2> $OUT/bench_rmat20.err
