@@ -60,8 +60,8 @@ struct brm_context {
   // rows of more lists ("multi", planned and merged within one call)
   struct HvSet {
     std::vector<HvRow> rows;
-    int64_t ntasks = 0;
-    DevBuf d_rows, cuts, wout, nwin, total;
+    int64_t ntasks = 0;  // upper bound (from the plan capacities): the merge grid
+    DevBuf d_rows, cuts, wout, nwin, total, ntask, toff, tmap;
   } hv_single, hv_multi;
   bool hv_single_planned = false;
   DevBuf hv_lt[2], hv_ws_col[2], hv_ws_val[2], hv_tmp;
@@ -313,11 +313,32 @@ brm_status_t hv_plan_single(brm_context_t* ctx, const std::vector<int32_t>& rows
   return BRM_OK;
 }
 
+// The merge tasks of a planned set: ceil(windows / kHvWch) per virtual row,
+// their offsets (scan) and the task -> virtual row map, on the device.
+brm_status_t hv_tasks(brm_context_t* ctx, HvSet& set, HvArgs& a) {
+  const size_t n = set.rows.size();
+  CK(ensure(ctx, set.ntask, n * 8), "alloc heavy tasks");
+  CK(ensure(ctx, set.toff, (n + 1) * 8), "alloc heavy tasks");
+  CK(ensure(ctx, set.tmap, (size_t)set.ntasks * 4), "alloc heavy task map");
+  CK(launch_hv_ntask(a, static_cast<int64_t*>(set.ntask.p), ctx->stream), "k_hv_ntask");
+  brm_status_t s = run_scan(ctx, static_cast<const int64_t*>(set.ntask.p), (int64_t)n,
+                            static_cast<int64_t*>(set.toff.p), nullptr);
+  if (s != BRM_OK) return s;
+  CK(launch_hv_taskmap(a, static_cast<HvRow*>(set.d_rows.p), static_cast<const int64_t*>(set.toff.p),
+                       static_cast<int32_t*>(set.tmap.p), ctx->stream), "k_hv_taskmap");
+  ctx->launches += 3;
+  a.tmap = static_cast<const int32_t*>(set.tmap.p);
+  a.ntask_total = static_cast<const int64_t*>(set.toff.p) + n;
+  return BRM_OK;
+}
+
 brm_status_t hv_merge_single(brm_context_t* ctx, int out, const RowOut& o) {
   HvSet& set = ctx->hv_single;
   if (set.rows.empty()) return BRM_OK;
   if (!ctx->hv_single_planned) return fail(ctx, BRM_ERR_STATE, "heavy rows merged without a plan");
   HvArgs a = hv_args(ctx, set);
+  brm_status_t s = hv_tasks(ctx, set, a);
+  if (s != BRM_OK) return s;
   ev_record(ctx, kEvHv + 2);
   CK(launch_hv_merge(out, a, set.ntasks, o, ctx->stream), "k_hv_merge");
   ev_record(ctx, kEvHv + 3);
@@ -486,6 +507,7 @@ brm_status_t hv_run_multi(brm_context_t* ctx, int out, const RowOut& o, const st
         a.wo_col = static_cast<int32_t*>(ctx->hv_ws_col[outb].p);
         a.wo_val = static_cast<double*>(ctx->hv_ws_val[outb].p);
       }
+      if ((s = hv_tasks(ctx, set, a)) != BRM_OK) return s;
       CK(launch_hv_merge(out == OUT_C ? OUT_C : OUT_CBAR, a, set.ntasks, o, ctx->stream), "k_hv_merge");
       ++ctx->launches;
       // the next level reads this level's workspace (ordered on the stream)
@@ -949,6 +971,8 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
                       &ctx->stA_val, &ctx->stB_rpt, &ctx->stB_col, &ctx->stB_val, &ctx->stC_rpt, &ctx->stC_col,
                       &ctx->stC_val, &ctx->glob_rows, &ctx->hv_single.d_rows,
                       &ctx->hv_single.cuts, &ctx->hv_single.wout, &ctx->hv_single.nwin, &ctx->hv_single.total,
+                      &ctx->hv_single.ntask, &ctx->hv_single.toff, &ctx->hv_single.tmap, &ctx->hv_multi.ntask,
+                      &ctx->hv_multi.toff, &ctx->hv_multi.tmap,
                       &ctx->hv_multi.d_rows, &ctx->hv_multi.cuts, &ctx->hv_multi.wout, &ctx->hv_multi.nwin,
                       &ctx->hv_multi.total, &ctx->hv_lt[0], &ctx->hv_lt[1], &ctx->hv_ws_col[0], &ctx->hv_ws_col[1],
                       &ctx->hv_ws_val[0], &ctx->hv_ws_val[1], &ctx->hv_tmp, &ctx->hb_nprod, &ctx->hb_off,

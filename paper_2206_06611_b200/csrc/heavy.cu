@@ -637,22 +637,13 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
   double* rv = reinterpret_cast<double*>(take((kHvCap + 2) * 8));     // their values (move with them)
   unsigned short* own = reinterpret_cast<unsigned short*>(take(kHvCap * 2));
   int* wtmp = reinterpret_cast<int*>(take(64));
-  __shared__ int s_v, s_na;
+  __shared__ int s_na;
   const int rank = threadIdx.x;
   const int64_t t = blockIdx.x;
-  if (rank == 0) {  // the virtual row of this task: last v with rows[v].task0 <= t
-    int64_t lo = 0, hi = a.nrows - 1;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) >> 1;
-      if (a.rows[mid].task0 <= t)
-        lo = mid;
-      else
-        hi = mid - 1;
-    }
-    s_v = static_cast<int>(lo);
-  }
-  __syncthreads();
-  const int v = s_v;
+  // the grid covers the plan's upper bound of tasks; the task map holds the
+  // virtual row of each of the planned windows' tasks
+  if (t >= *a.ntask_total) return;
+  const int v = a.tmap[t];
   const HvRow r = a.rows[v];
   const int nwin = a.nwin[v];
   const int w0 = static_cast<int>(t - r.task0) * r.wch;
@@ -927,6 +918,22 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
   }
 }
 
+__global__ void k_hv_ntask(HvArgs a, int64_t* ntask) {
+  const int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= a.nrows) return;
+  const int wch = a.rows[v].wch;
+  ntask[v] = (a.nwin[v] + wch - 1) / wch;
+}
+
+__global__ void k_hv_taskmap(HvArgs a, HvRow* rows, const int64_t* toff, int32_t* tmap) {
+  const int64_t v = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= a.nrows) return;
+  const int64_t t0 = toff[v], n = toff[v + 1] - t0;
+  if (lane == 0) rows[v].task0 = t0;
+  for (int64_t j = lane; j < n; j += 32) tmap[t0 + j] = static_cast<int32_t>(v);
+}
+
 // products of each (src 0) virtual row: one warp per row
 __global__ void k_hv_vrow_nprod(HvArgs a, int64_t* out) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -980,6 +987,18 @@ cudaError_t launch_hv_merge(int out_kind, const HvArgs& a, int64_t ntasks, const
     case OUT_C: return launch_hv_merge_t<OUT_C>(a, ntasks, o, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_hv_ntask(const HvArgs& a, int64_t* ntask, cudaStream_t st) {
+  if (a.nrows <= 0) return cudaSuccess;
+  k_hv_ntask<<<static_cast<unsigned>((a.nrows + 255) / 256), 256, 0, st>>>(a, ntask);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hv_taskmap(const HvArgs& a, HvRow* rows, const int64_t* toff, int32_t* tmap, cudaStream_t st) {
+  if (a.nrows <= 0) return cudaSuccess;
+  k_hv_taskmap<<<static_cast<unsigned>((a.nrows * 32 + 255) / 256), 256, 0, st>>>(a, rows, toff, tmap);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_hv_vrow_nprod(const HvArgs& a, int64_t* out, cudaStream_t st) {

@@ -90,6 +90,8 @@ struct HvArgs {
   int64_t* total;         // per virtual row: entries of its result
   int64_t* row_size;      // out 0 rows: row_size[row] = total (null: not written)
   unsigned int* err;      // bit 0: plan overflow; bit 1: window size mismatch
+  const int32_t* tmap;    // merge: virtual row of each task (k_hv_taskmap)
+  const int64_t* ntask_total;  // merge: number of tasks (device scalar)
 };
 
 // plan shared memory: bitmap, histogram, fine counts, bin slots, list table
@@ -118,5 +120,10 @@ cudaError_t launch_hv_plan(const HvArgs& a, bool count_only, cudaStream_t st);
 cudaError_t launch_hv_merge(int out_kind, const HvArgs& a, int64_t ntasks, const RowOut& o, cudaStream_t st);
 // products of each virtual row (src 0 rows) -> a.total (as a staging array)
 cudaError_t launch_hv_vrow_nprod(const HvArgs& a, int64_t* out, cudaStream_t st);
+// merge tasks from the planned window counts: ntask[v] = ceil(nwin[v] / wch);
+// then (after an exclusive scan toff of ntask) rows[v].task0 = toff[v] and
+// tmap[toff[v] + j] = v for the row's tasks
+cudaError_t launch_hv_ntask(const HvArgs& a, int64_t* ntask, cudaStream_t st);
+cudaError_t launch_hv_taskmap(const HvArgs& a, HvRow* rows, const int64_t* toff, int32_t* tmap, cudaStream_t st);
 
 }  // namespace brm
