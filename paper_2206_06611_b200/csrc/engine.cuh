@@ -131,15 +131,35 @@ __device__ __forceinline__ void tiny_row(const CsrView& A, const CsrView& B, int
                                          int* pc, int* qc, double* pv, double* qv) {
   const int64_t a0 = A.rpt[row];
   const int nl = static_cast<int>(A.rpt[row + 1] - a0);
-  // Alg. 1 lines 10-15: list l into the ping buffer at [off[l], off[l+1])
+  // Alg. 1 lines 10-15: list l into the ping buffer at [off[l], off[l+1]);
+  // the B row bounds of all lists are loaded before any list is gathered
+#ifndef BRM_TINY_BATCH
+#define BRM_TINY_BATCH 1  // tuning switch: 0 loads each list's bounds in the list loop
+#endif
+  int64_t bb[kTinyL], be[kTinyL];
+  if (BRM_TINY_BATCH) {
+#pragma unroll
+    for (int l = 0; l < kTinyL; ++l) {
+      bb[l] = be[l] = 0;
+      if (l < nl) {
+        const int k = __ldg(A.col + a0 + l);
+        bb[l] = __ldg(B.rpt + k);
+        be[l] = __ldg(B.rpt + k + 1);
+      }
+    }
+  }
   int off[kTinyL + 1];
   int P = 0;
 #pragma unroll
   for (int l = 0; l < kTinyL; ++l) {
     off[l] = P;
     if (l < nl) {
-      const int k = __ldg(A.col + a0 + l);
-      const int64_t b0 = __ldg(B.rpt + k), b1 = __ldg(B.rpt + k + 1);
+      int64_t b0 = bb[l], b1 = be[l];
+      if (!BRM_TINY_BATCH) {
+        const int k = __ldg(A.col + a0 + l);
+        b0 = __ldg(B.rpt + k);
+        b1 = __ldg(B.rpt + k + 1);
+      }
       const double a = VALS ? __ldg(A.val + a0 + l) : 0.0;
       for (int64_t q = b0; q < b1; ++q, ++P) {
         pc[P * NT] = __ldg(B.col + q);
