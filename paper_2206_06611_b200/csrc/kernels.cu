@@ -765,12 +765,19 @@ static cudaError_t launch_hash_t(const CsrView& A, const CsrView& B, const int32
 template <bool VALS, int OUT>
 static cudaError_t launch_tier_dispatch(int bin, const CsrView& A, const CsrView& B, int64_t b_cols, const int32_t* rows,
                                         int64_t n, const RowOut& o, cudaStream_t st) {
+#ifndef BRM_SYM_MERGE_T56
+#define BRM_SYM_MERGE_T56 1  // tiers 5-6 count by the column-only record merge (0: hashing; A/B switch)
+#endif
   if constexpr (OUT == OUT_SYMBOLIC) {  // PRECISE step 3: hash counting on tiers 3-6
     switch (bin) {
       case 3: return launch_hash_t<BRM_HASH3>(A, B, rows, n, o, st);
       case 4: return launch_hash_t<BRM_HASH4>(A, B, rows, n, o, st);
-      case 5: return launch_hash_t<BRM_HASH5>(A, B, rows, n, o, st);
-      case 6: return launch_hash_t<BRM_HASH6>(A, B, rows, n, o, st);
+      case 5:
+        if (!BRM_SYM_MERGE_T56) return launch_hash_t<BRM_HASH5>(A, B, rows, n, o, st);
+        break;
+      case 6:
+        if (!BRM_SYM_MERGE_T56) return launch_hash_t<BRM_HASH6>(A, B, rows, n, o, st);
+        break;
       default: break;
     }
   }
