@@ -35,7 +35,7 @@ struct brm_context {
   bool timing = false;
   int heavy_route = BRM_HEAVY_AUTO;
   // workspace (grow-only)
-  DevBuf nprod_off, row_size, bins, status, small, cbar_col, cbar_val, gws, gws_off, heavy_info;
+  DevBuf nprod_off, row_size, bins, status, small, cbar_col, cbar_val, gws, gws_off, heavy_info, long_list, long_np;
   DevBuf stA_rpt, stA_col, stA_val, stB_rpt, stB_col, stB_val, stC_rpt, stC_col, stC_val;
   HostBuf h_small, h_heavy, h_gws_off, h_C;
   // plan (structure -> fill)
@@ -48,6 +48,8 @@ struct brm_context {
   DevSummary sum{};
   bool heavy_loaded = false;
   std::vector<int64_t> heavy;  // (n_prod, nl) per global-tier row
+  std::vector<int32_t> heavy_rows;  // the global-tier rows (bin order)
+  cudaEvent_t ev_heavy = nullptr;   // their readback landed
   brm_stats_t stats{};
   cudaEvent_t ev[32] = {};
   cudaEvent_t handoff = nullptr;  // orders a stream switch after the old stream's work
@@ -193,6 +195,18 @@ struct SmallDev {
 };
 
 SmallDev* small_dev(brm_context_t* ctx) { return static_cast<SmallDev*>(ctx->small.p); }
+
+// n_prod of A's rows of more than kLongRow nonzeros, ahead of the per-warp
+// n_prod passes (needs ctx->small; uses its counter[2])
+brm_status_t long_rows(brm_context_t* ctx, const CsrView& A, const int64_t* brpt, int64_t M) {
+  CK(ensure(ctx, ctx->long_list, (size_t)M * 4), "alloc long rows");
+  CK(ensure(ctx, ctx->long_np, (size_t)M * 8), "alloc long rows");
+  CK(cudaMemsetAsync(&small_dev(ctx)->counter[2], 0, 4, ctx->stream), "memset long-row counter");
+  CK(launch_long_rows(A, brpt, M, static_cast<int32_t*>(ctx->long_list.p), &small_dev(ctx)->counter[2],
+                      static_cast<int64_t*>(ctx->long_np.p), ctx->stream), "k_long_rows");
+  ctx->launches += 2;
+  return BRM_OK;
+}
 
 // Timing events (no synchronisation when recorded; resolved in brm_get_stats):
 // 0/1 n_prod+scan+bin, 2/3 structure merge, 3/4 row_size scan, 5/6 fill,
@@ -533,6 +547,25 @@ brm_status_t hv_run_multi(brm_context_t* ctx, int out, const RowOut& o, const st
 // Launch the merge of every non-empty bin with output kind `out`.
 brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bin) {
   const int32_t* bins = static_cast<const int32_t*>(ctx->bins.p);
+  const int64_t nh = ctx->bin_rows[kBinGlobal];
+  const int32_t* hrows = bins + ctx->bin_start[kBinGlobal];
+  // the heavy rows' (n_prod, nl) and ids are read back first (once per
+  // structure call), so the host prepares their plans while the tier
+  // kernels launched below run
+  const bool load = nh && !ctx->heavy_loaded;
+  if (load) {
+    CK(ensure(ctx, ctx->heavy_info, (size_t)nh * 16), "alloc heavy info");
+    CK(launch_heavy_info(ctx->A, static_cast<const int64_t*>(ctx->nprod_off.p), hrows, nh,
+                         static_cast<int64_t*>(ctx->heavy_info.p), ctx->stream),
+       "k_heavy_info");
+    ++ctx->launches;
+    CK(ensure_host(ctx->h_heavy, (size_t)nh * 16), "alloc pinned heavy info");
+    CK(ensure_host(ctx->h_rows, (size_t)nh * 4), "alloc pinned heavy rows");
+    CK(readback(ctx, ctx->h_heavy.p, ctx->heavy_info.p, (size_t)nh * 16), "copy heavy info");
+    CK(readback(ctx, ctx->h_rows.p, hrows, (size_t)nh * 4), "copy heavy rows");
+    if (!ctx->ev_heavy) CK(cudaEventCreateWithFlags(&ctx->ev_heavy, cudaEventDisableTiming), "create event");
+    CK(cudaEventRecord(ctx->ev_heavy, ctx->stream), "record heavy readback");
+  }
   for (int b = 1; b < kBinGlobal; ++b) {
     if (!ctx->bin_rows[b]) continue;
     if (per_bin) ev_record(ctx, kEvBin + 2 * b);
@@ -541,27 +574,17 @@ brm_status_t run_merge(brm_context_t* ctx, int out, const RowOut& o, bool per_bi
     ++ctx->launches;
     if (per_bin) ev_record(ctx, kEvBin + 2 * b + 1);
   }
-  const int64_t nh = ctx->bin_rows[kBinGlobal];
   if (!nh) return BRM_OK;
   if (per_bin) ev_record(ctx, kEvBin + 2 * kBinGlobal);
-  const int32_t* hrows = bins + ctx->bin_start[kBinGlobal];
-  if (!ctx->heavy_loaded) {
-    CK(ensure(ctx, ctx->heavy_info, (size_t)nh * 16), "alloc heavy info");
-    CK(launch_heavy_info(ctx->A, static_cast<const int64_t*>(ctx->nprod_off.p), hrows, nh,
-                         static_cast<int64_t*>(ctx->heavy_info.p), ctx->stream),
-       "k_heavy_info");
-    ++ctx->launches;
-    CK(ensure_host(ctx->h_heavy, (size_t)nh * 16), "alloc pinned heavy info");
-    CK(readback(ctx, ctx->h_heavy.p, ctx->heavy_info.p, (size_t)nh * 16), "copy heavy info");
-    CK(cudaStreamSynchronize(ctx->stream), "sync heavy info");
+  if (load) {
+    CK(cudaEventSynchronize(ctx->ev_heavy), "sync heavy readback");
     const int64_t* hi = static_cast<const int64_t*>(ctx->h_heavy.p);
     ctx->heavy.assign(hi, hi + 2 * nh);
+    const int32_t* hr0 = static_cast<const int32_t*>(ctx->h_rows.p);
+    ctx->heavy_rows.assign(hr0, hr0 + nh);
     ctx->heavy_loaded = true;
   }
-  CK(ensure_host(ctx->h_rows, (size_t)nh * 4), "alloc pinned heavy rows");
-  CK(readback(ctx, ctx->h_rows.p, hrows, (size_t)nh * 4), "copy heavy rows");
-  CK(cudaStreamSynchronize(ctx->stream), "sync heavy rows");
-  const int32_t* hr = static_cast<const int32_t*>(ctx->h_rows.p);
+  const int32_t* hr = ctx->heavy_rows.data();
   if (ctx->heavy_route == BRM_HEAVY_AUTO) {
     // windowed BRMerge (heavy.cuh): rows of <= kHvLists lists in one level,
     // the rest in levels of aligned kHvLists-list blocks
@@ -696,8 +719,9 @@ brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
     CK(cudaMemsetAsync(nprod_off, 0, 8, ctx->stream), "memset");
   }
   // Step 1: n_prod per row + prefix sum (+ bin histogram)
+  if ((s = long_rows(ctx, ctx->A, B->rpt, M)) != BRM_OK) return s;
   CK(launch_nprod_scan(ctx->A, B->rpt, M, nprod_off, static_cast<unsigned long long*>(ctx->status.p),
-                       &sd->counter[0], &sd->summary, ctx->stream),
+                       &sd->counter[0], &sd->summary, static_cast<const int64_t*>(ctx->long_np.p), ctx->stream),
      "k_nprod_scan");
   // row binning
   CK(launch_bin_scatter(ctx->A, nprod_off, M, &sd->summary, sd->cursor, static_cast<int32_t*>(ctx->bins.p),
@@ -816,8 +840,9 @@ brm_status_t host_pipelined(brm_context_t* ctx, const brm_csr_t* Ah, const brm_c
   CK(ensure(ctx, ctx->hb_off, (size_t)(M + 1) * 8), "alloc n_prod offsets");
   CK(ensure(ctx, ctx->hb_bounds, (size_t)(KMAX + 1) * 8), "alloc block bounds");
   CK(ensure(ctx, ctx->small, sizeof(SmallDev)), "alloc small");
+  if ((s = long_rows(ctx, CsrView{Ad->rpt, Ad->col, Ad->val}, Bd->rpt, M)) != BRM_OK) return s;
   CK(launch_row_nprod(CsrView{Ad->rpt, Ad->col, Ad->val}, Bd->rpt, M, static_cast<int64_t*>(ctx->hb_nprod.p),
-                      ctx->stream), "k_row_nprod");
+                      static_cast<const int64_t*>(ctx->long_np.p), ctx->stream), "k_row_nprod");
   if ((s = run_scan(ctx, static_cast<const int64_t*>(ctx->hb_nprod.p), M, static_cast<int64_t*>(ctx->hb_off.p),
                     nullptr)) != BRM_OK)
     return s;
@@ -978,6 +1003,7 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
     DeviceGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (DevBuf* b : {&ctx->nprod_off, &ctx->row_size, &ctx->bins, &ctx->status, &ctx->small, &ctx->cbar_col,
+                      &ctx->long_list, &ctx->long_np,
                       &ctx->cbar_val, &ctx->gws, &ctx->gws_off, &ctx->heavy_info, &ctx->stA_rpt, &ctx->stA_col,
                       &ctx->stA_val, &ctx->stB_rpt, &ctx->stB_col, &ctx->stB_val, &ctx->stC_rpt, &ctx->stC_col,
                       &ctx->stC_val, &ctx->glob_rows, &ctx->hv_single.d_rows,
@@ -1004,6 +1030,7 @@ brm_status_t brm_destroy(brm_context_t* ctx) {
     for (auto& e : ctx->ev_blk)
       if (e) cudaEventDestroy(e);
     if (ctx->handoff) cudaEventDestroy(ctx->handoff);
+    if (ctx->ev_heavy) cudaEventDestroy(ctx->ev_heavy);
   }
   delete ctx;
   return BRM_OK;
@@ -1194,7 +1221,10 @@ brm_status_t brm_row_nprod(brm_context_t* ctx, const brm_csr_t* A, const brm_csr
   if (A->cols != B->rows) return fail(ctx, BRM_ERR_DIM, "A.cols != B.rows");
   if (!nprod && A->rows) return fail(ctx, BRM_ERR_INVALID, "nprod is null");
   DeviceGuard g(ctx->device);
-  CK(launch_row_nprod(CsrView{A->rpt, A->col, A->val}, B->rpt, A->rows, nprod, ctx->stream), "k_row_nprod");
+  CK(ensure(ctx, ctx->small, sizeof(SmallDev)), "alloc small");
+  if ((s = long_rows(ctx, CsrView{A->rpt, A->col, A->val}, B->rpt, A->rows)) != BRM_OK) return s;
+  CK(launch_row_nprod(CsrView{A->rpt, A->col, A->val}, B->rpt, A->rows, nprod,
+                      static_cast<const int64_t*>(ctx->long_np.p), ctx->stream), "k_row_nprod");
   return BRM_OK;
 }
 

@@ -112,6 +112,8 @@ __device__ __forceinline__ int64_t block_scan_i64(int64_t x, int64_t& total, int
   return wsum[wid] + inc - x;
 }
 
+constexpr int kLongRow = 512;  // rows of more nonzeros: k_long_rows / k_long_nprod
+
 // n_prod of the 32 rows [r0, r0 + 32) by one warp, nonzero-parallel: lanes
 // stride over the rows' nonzeros (coalesced A.col reads, B.rpt gathers; four
 // 32-nonzero batches in flight), find each nonzero's row by a shuffle search
@@ -119,19 +121,25 @@ __device__ __forceinline__ int64_t block_scan_i64(int64_t x, int64_t& total, int
 // scan; the last lane of a run adds it to out[row - r0]. *nl_out = lane's
 // row length.
 __device__ __forceinline__ void warp_rows_nprod(const CsrView& A, const int64_t* __restrict__ brpt, int64_t M,
-                                                int64_t r0, int64_t* out, int* nl_out) {
+                                                int64_t r0, int64_t* out, int* nl_out,
+                                                const int64_t* __restrict__ long_np) {
   constexpr int U = 4;
   const int lane = threadIdx.x & 31;
   const int64_t rs = A.rpt[min(r0 + lane, M)];  // start of row r0 + lane (clamped)
   const int64_t pend = A.rpt[min(r0 + 32, M)];
-  const int64_t pbeg = __shfl_sync(0xffffffffu, rs, 0);
   const int64_t rnext = __shfl_down_sync(0xffffffffu, rs, 1);
   const int nl = lane < 31 ? (int)(rnext - rs) : (int)(pend - rs);
   *nl_out = nl;
-  if (__reduce_max_sync(0xffffffffu, r0 + lane < M ? (unsigned)nl : 0u) <= 64u) {
+  const bool valid = r0 + lane < M;
+  // rows of more than kLongRow nonzeros were summed by k_long_nprod
+  const bool lng = valid && nl > kLongRow;
+  const unsigned longm = __ballot_sync(0xffffffffu, lng);
+  if (__reduce_max_sync(0xffffffffu, valid && !lng ? (unsigned)nl : 0u) <= 64u) {
     // short rows: one lane per row, independent gathers (no shuffles)
     int64_t acc = 0;
-    if (r0 + lane < M) {
+    if (lng) {
+      acc = long_np[r0 + lane];
+    } else if (valid) {
 #pragma unroll 4
       for (int64_t p = rs; p < rs + nl; ++p) {
         const int k = __ldg(A.col + p);
@@ -142,39 +150,90 @@ __device__ __forceinline__ void warp_rows_nprod(const CsrView& A, const int64_t*
     __syncwarp();
     return;
   }
-  out[lane] = 0;
+  out[lane] = lng ? long_np[r0 + lane] : 0;
   __syncwarp();
-  for (int64_t pb = pbeg; pb < pend; pb += 32 * U) {
-    int k[U];
-    int64_t d[U];
+  // the other rows nonzero-parallel, one run of consecutive such rows at a time
+  const int nvalid = (int)min((int64_t)32, M - r0);
+  int ra = 0;
+  while (ra < nvalid) {
+    if ((longm >> ra) & 1u) {
+      ++ra;
+      continue;
+    }
+    const unsigned after = longm & ~((2u << ra) - 1u);  // long rows past ra
+    const int rb = after ? __ffs(after) - 1 : nvalid;
+    const int64_t pbeg = __shfl_sync(0xffffffffu, rs, ra);
+    const int64_t rbs = __shfl_sync(0xffffffffu, rs, rb < nvalid ? rb : 0);
+    const int64_t prun = rb < nvalid ? rbs : pend;  // the run's nonzeros: [pbeg, prun)
+    ra = rb;
+    for (int64_t pb = pbeg; pb < prun; pb += 32 * U) {
+      int k[U];
+      int64_t d[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t p = pb + 32 * u + lane;
-      k[u] = p < pend ? __ldg(A.col + p) : -1;
+      for (int u = 0; u < U; ++u) {
+        const int64_t p = pb + 32 * u + lane;
+        k[u] = p < prun ? __ldg(A.col + p) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) d[u] = k[u] >= 0 ? __ldg(brpt + k[u] + 1) - __ldg(brpt + k[u]) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t p = pb + 32 * u + lane;
+        if (pb + 32 * u >= prun) break;  // warp-uniform
+        int lo = 0;  // row of nonzero p: last lane whose row start <= p
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int64_t v = __shfl_sync(0xffffffffu, rs, lo + step);
+          if (v <= p) lo += step;
+        }
+        int64_t x = d[u];  // segmented inclusive scan over lanes with equal rows
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+          const int ro = __shfl_up_sync(0xffffffffu, lo, o);
+          if (lane >= o && ro == lo) x += y;
+        }
+        const int rn = __shfl_down_sync(0xffffffffu, lo, 1);
+        if (p < prun && (lane == 31 || rn != lo || p + 1 >= prun)) out[lo] += x;
+        __syncwarp();
+      }
+    }
+  }
+}
+
+// Rows of more than kLongRow nonzeros (power-law rows): listed first, then
+// summed by a CTA each, so no warp of k_nprod_scan carries a huge row alone
+// (rmat20's 32-row chunk holding the first rows took the whole 10.8 ms).
+__global__ void k_long_rows(CsrView A, int64_t M, int32_t* __restrict__ list, unsigned int* count) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < M && A.rpt[r + 1] - A.rpt[r] > kLongRow) list[atomicAdd(count, 1u)] = (int32_t)r;
+}
+
+__global__ void __launch_bounds__(256) k_long_nprod(CsrView A, const int64_t* __restrict__ brpt,
+                                                    const int32_t* __restrict__ list, const unsigned int* count,
+                                                    int64_t* __restrict__ long_np) {
+  __shared__ int64_t red[8];
+  const unsigned n = *count;
+  for (unsigned i = blockIdx.x; i < n; i += gridDim.x) {
+    const int64_t r = list[i];
+    const int64_t p0 = A.rpt[r], p1 = A.rpt[r + 1];
+    int64_t s = 0;
+#pragma unroll 4
+    for (int64_t p = p0 + threadIdx.x; p < p1; p += 256) {
+      const int k = __ldg(A.col + p);
+      s += __ldg(brpt + k + 1) - __ldg(brpt + k);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) d[u] = k[u] >= 0 ? __ldg(brpt + k[u] + 1) - __ldg(brpt + k[u]) : 0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t t = 0;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t p = pb + 32 * u + lane;
-      if (pb + 32 * u >= pend) break;  // warp-uniform
-      int lo = 0;  // row of nonzero p: last lane whose row start <= p
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int64_t v = __shfl_sync(0xffffffffu, rs, lo + step);
-        if (v <= p) lo += step;
-      }
-      int64_t x = d[u];  // segmented inclusive scan over lanes with equal rows
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-        const int ro = __shfl_up_sync(0xffffffffu, lo, o);
-        if (lane >= o && ro == lo) x += y;
-      }
-      const int rn = __shfl_down_sync(0xffffffffu, lo, 1);
-      if (p < pend && (lane == 31 || rn != lo || p + 1 >= pend)) out[lo] += x;
-      __syncwarp();
+      for (int w = 0; w < 8; ++w) t += red[w];
+      long_np[r] = t;
     }
+    __syncthreads();
   }
 }
 
@@ -188,7 +247,8 @@ __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const in
                                                              int64_t M, int64_t* __restrict__ nprod_off,
                                                              unsigned long long* status,
                                                              unsigned int* tile_counter,
-                                                             DevSummary* summary) {
+                                                             DevSummary* summary,
+                                                             const int64_t* __restrict__ long_np) {
   __shared__ int s_tile;
   __shared__ int64_t s_wsum[kScanThreads / 32 + 1];
   __shared__ int64_t s_prefix;
@@ -213,7 +273,7 @@ __global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const in
     const int64_t r0 = t0 + loc;
     if (r0 >= M) break;  // warp-uniform
     int nl;
-    warp_rows_nprod(A, brpt, M, r0, s_np + loc, &nl);
+    warp_rows_nprod(A, brpt, M, r0, s_np + loc, &nl, long_np);
     const bool valid = r0 + lane < M;
     const int64_t s = valid ? s_np[loc + lane] : 0;
     const int bin = valid ? tier_of(s, nl, tb) : -1;
@@ -611,17 +671,16 @@ __global__ void k_partition(const int64_t* __restrict__ nprod_off, int64_t M, in
   bounds[g] = lo;
 }
 
-// n_prod per row only (stage entry point).
-__global__ void k_row_nprod(CsrView A, const int64_t* __restrict__ brpt, int64_t M,
-                            int64_t* __restrict__ nprod) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= M) return;
-  int64_t s = 0;
-  for (int64_t p = A.rpt[r]; p < A.rpt[r + 1]; ++p) {
-    const int k = A.col[p];
-    s += brpt[k + 1] - brpt[k];
-  }
-  nprod[r] = s;
+// n_prod per row only (stage entry point): 32 rows per warp as in k_nprod_scan.
+__global__ void __launch_bounds__(256) k_row_nprod(CsrView A, const int64_t* __restrict__ brpt, int64_t M,
+                                                   int64_t* __restrict__ nprod, const int64_t* __restrict__ long_np) {
+  __shared__ int64_t s_np[256];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = (int64_t)blockIdx.x * 256 + wid * 32;
+  if (r0 >= M) return;  // warp-uniform
+  int nl;
+  warp_rows_nprod(A, brpt, M, r0, s_np + wid * 32, &nl, long_np);
+  if (r0 + lane < M) nprod[r0 + lane] = s_np[wid * 32 + lane];
 }
 
 // ---------------------------------------------------------------------------
@@ -669,11 +728,20 @@ int64_t scan_tiles(int64_t n) { return (n + kScanTile - 1) / kScanTile; }
 
 int64_t nprod_tiles(int64_t M) { return (M + kNpTile - 1) / kNpTile; }
 
+cudaError_t launch_long_rows(const CsrView& A, const int64_t* brpt, int64_t M, int32_t* list, unsigned int* count,
+                             int64_t* long_np, cudaStream_t st) {
+  if (M <= 0) return cudaSuccess;
+  k_long_rows<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(A, M, list, count);
+  k_long_nprod<<<(unsigned)(num_sms() * 8), 256, 0, st>>>(A, brpt, list, count, long_np);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_nprod_scan(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod_off,
                               unsigned long long* status, unsigned int* counter, DevSummary* summary,
-                              cudaStream_t st) {
+                              const int64_t* long_np, cudaStream_t st) {
   const int64_t tiles = nprod_tiles(M);
-  if (tiles > 0) k_nprod_scan<<<(unsigned)tiles, kScanThreads, 0, st>>>(A, brpt, M, nprod_off, status, counter, summary);
+  if (tiles > 0)
+    k_nprod_scan<<<(unsigned)tiles, kScanThreads, 0, st>>>(A, brpt, M, nprod_off, status, counter, summary, long_np);
   return cudaGetLastError();
 }
 
@@ -836,8 +904,9 @@ cudaError_t launch_partition(const int64_t* nprod_off, int64_t M, int p, int64_t
   return cudaGetLastError();
 }
 
-cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod, cudaStream_t st) {
-  if (M > 0) k_row_nprod<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(A, brpt, M, nprod);
+cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod, const int64_t* long_np,
+                             cudaStream_t st) {
+  if (M > 0) k_row_nprod<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(A, brpt, M, nprod, long_np);
   return cudaGetLastError();
 }
 

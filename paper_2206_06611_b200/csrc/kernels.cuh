@@ -19,9 +19,13 @@ struct DevSummary {
 
 int64_t scan_tiles(int64_t n);
 int64_t nprod_tiles(int64_t M);
+// rows of A with more than kLongRow nonzeros: listed (list, *count) and their
+// n_prod summed into long_np[row] by a CTA each; run before the two below
+cudaError_t launch_long_rows(const CsrView& A, const int64_t* brpt, int64_t M, int32_t* list, unsigned int* count,
+                             int64_t* long_np, cudaStream_t st);
 cudaError_t launch_nprod_scan(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod_off,
                               unsigned long long* status, unsigned int* counter, DevSummary* summary,
-                              cudaStream_t st);
+                              const int64_t* long_np, cudaStream_t st);
 cudaError_t launch_scan_i64(const int64_t* in, int64_t n, int64_t* out, unsigned long long* status,
                             unsigned int* counter, int64_t* total_out, cudaStream_t st);
 cudaError_t launch_bin_scatter(const CsrView& A, const int64_t* nprod_off, int64_t M, const DevSummary* summary,
@@ -38,7 +42,8 @@ cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B,
 cudaError_t launch_compact(int64_t M, int64_t nnz, const int64_t* nprod_off, const int64_t* crpt, const int32_t* cbar_col,
                            const double* cbar_val, int32_t* ccol, double* cval, cudaStream_t st);
 cudaError_t launch_partition(const int64_t* nprod_off, int64_t M, int p, int64_t* bounds, cudaStream_t st);
-cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod, cudaStream_t st);
+cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod, const int64_t* long_np,
+                             cudaStream_t st);
 // device -> pinned (host-mapped) memory copy by `ctas` CTAs of the SMs
 cudaError_t launch_copy_to_host(void* dst, const void* src, int64_t bytes, int ctas, cudaStream_t st);
 

@@ -333,6 +333,19 @@ def test_stage_nprod_scan_partition(ctx, oracle_mod):
     B = random_sparse(2000, 1000, 0.02, seed=9)
     nprod = ctx.brm_row_nprod(TorchCsr.from_csr(A), TorchCsr.from_csr(B)).cpu().numpy()
     np.testing.assert_array_equal(nprod, oracle_mod.row_nprod(A, B))
+    # long rows (> 512 nonzeros: summed by a CTA each) between short and
+    # empty ones, in 32-row chunks with several runs, and at the matrix end
+    rng = np.random.default_rng(5)
+    lens = rng.integers(0, 40, size=700)
+    lens[[3, 4, 31, 32, 60, 100, 101, 102, 699]] = [513, 2000, 900, 4000, 600, 513, 1, 3000, 1500]
+    lens[[5, 33]] = 0
+    Bw = random_sparse(5000, 300, 0.02, seed=10)
+    cols = [np.sort(rng.choice(5000, size=n, replace=False)).astype(np.int32) for n in lens]
+    rpt = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    Al = Csr(lens.size, 5000, rpt, np.concatenate(cols), rng.uniform(-1, 1, size=int(rpt[-1])))
+    got = ctx.brm_row_nprod(TorchCsr.from_csr(Al), TorchCsr.from_csr(Bw)).cpu().numpy()
+    np.testing.assert_array_equal(got, oracle_mod.row_nprod(Al, Bw))
+    compare(run(ctx, Al, Bw, "precise"), Al, Bw)
     rng = np.random.default_rng(0)
     for n in (0, 1, 2047, 2048, 2049, 100_000, 3_000_001):
         x = rng.integers(0, 1 << 40, size=n, dtype=np.int64)
