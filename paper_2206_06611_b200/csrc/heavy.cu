@@ -98,7 +98,10 @@ __device__ int plan_scan(int* x, int n, int* wtmp) {
 template <class Fn>
 __device__ __forceinline__ void plan_for_products(const int32_t* scol, const int64_t* lstart, const int* loff, int nc,
                                                   int pc, int* ioff, int* wtmp, Fn fn) {
-  constexpr int NW = kHvPlanG / 32, U = 4, ITEM = 1024;
+#ifndef BRM_PLAN_U
+#define BRM_PLAN_U 16  // column loads in flight per lane in the plan's product pass (4 / 8 / 16: rmat20 one-level plan 47.6 / 45.7 / 45.5 ms)
+#endif
+  constexpr int NW = kHvPlanG / 32, U = BRM_PLAN_U, ITEM = 1024;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int j = threadIdx.x; j < nc; j += kHvPlanG) ioff[j] = (loff[j + 1] - loff[j] + ITEM - 1) / ITEM;
   __syncthreads();
