@@ -372,6 +372,9 @@ def test_errors_are_reported(ctx):
     with pytest.raises(BrmError) as e:
         fresh.brmerge_spgemm_fill(10, 8, torch.zeros(11, dtype=torch.int64, device="cuda"), 0)
     assert e.value.code == 6  # BRM_ERR_STATE
+    with pytest.raises(BrmError) as e:
+        fresh.brm_set_host_pipeline(-1)
+    assert e.value.code == 1  # BRM_ERR_INVALID
     fresh.close()
 
 
