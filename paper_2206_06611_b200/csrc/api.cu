@@ -197,14 +197,21 @@ struct SmallDev {
 SmallDev* small_dev(brm_context_t* ctx) { return static_cast<SmallDev*>(ctx->small.p); }
 
 // n_prod of A's rows of more than kLongRow nonzeros, ahead of the per-warp
-// n_prod passes (needs ctx->small; uses its counter[2])
-brm_status_t long_rows(brm_context_t* ctx, const CsrView& A, const int64_t* brpt, int64_t M) {
+// n_prod passes (needs ctx->small; uses its counter[2]); *long_np = their
+// values for those passes. Below 65,536 rows the warps take long rows
+// themselves (*long_np = null): no skew worth the pass's fixed cost.
+brm_status_t long_rows(brm_context_t* ctx, const CsrView& A, const int64_t* brpt, int64_t M,
+                       const int64_t** long_np) {
+  *long_np = nullptr;
+  if (M < 65536) return BRM_OK;
+  CK(ensure(ctx, ctx->long_np, (size_t)M * 8), "alloc long rows");
   CK(ensure(ctx, ctx->long_list, (size_t)M * 4), "alloc long rows");
   CK(ensure(ctx, ctx->long_np, (size_t)M * 8), "alloc long rows");
   CK(cudaMemsetAsync(&small_dev(ctx)->counter[2], 0, 4, ctx->stream), "memset long-row counter");
   CK(launch_long_rows(A, brpt, M, static_cast<int32_t*>(ctx->long_list.p), &small_dev(ctx)->counter[2],
                       static_cast<int64_t*>(ctx->long_np.p), ctx->stream), "k_long_rows");
   ctx->launches += 2;
+  *long_np = static_cast<const int64_t*>(ctx->long_np.p);
   return BRM_OK;
 }
 
@@ -719,9 +726,10 @@ brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
     CK(cudaMemsetAsync(nprod_off, 0, 8, ctx->stream), "memset");
   }
   // Step 1: n_prod per row + prefix sum (+ bin histogram)
-  if ((s = long_rows(ctx, ctx->A, B->rpt, M)) != BRM_OK) return s;
+  const int64_t* lnp = nullptr;
+  if ((s = long_rows(ctx, ctx->A, B->rpt, M, &lnp)) != BRM_OK) return s;
   CK(launch_nprod_scan(ctx->A, B->rpt, M, nprod_off, static_cast<unsigned long long*>(ctx->status.p),
-                       &sd->counter[0], &sd->summary, static_cast<const int64_t*>(ctx->long_np.p), ctx->stream),
+                       &sd->counter[0], &sd->summary, lnp, ctx->stream),
      "k_nprod_scan");
   // row binning
   CK(launch_bin_scatter(ctx->A, nprod_off, M, &sd->summary, sd->cursor, static_cast<int32_t*>(ctx->bins.p),
@@ -840,9 +848,10 @@ brm_status_t host_pipelined(brm_context_t* ctx, const brm_csr_t* Ah, const brm_c
   CK(ensure(ctx, ctx->hb_off, (size_t)(M + 1) * 8), "alloc n_prod offsets");
   CK(ensure(ctx, ctx->hb_bounds, (size_t)(KMAX + 1) * 8), "alloc block bounds");
   CK(ensure(ctx, ctx->small, sizeof(SmallDev)), "alloc small");
-  if ((s = long_rows(ctx, CsrView{Ad->rpt, Ad->col, Ad->val}, Bd->rpt, M)) != BRM_OK) return s;
+  const int64_t* lnp = nullptr;
+  if ((s = long_rows(ctx, CsrView{Ad->rpt, Ad->col, Ad->val}, Bd->rpt, M, &lnp)) != BRM_OK) return s;
   CK(launch_row_nprod(CsrView{Ad->rpt, Ad->col, Ad->val}, Bd->rpt, M, static_cast<int64_t*>(ctx->hb_nprod.p),
-                      static_cast<const int64_t*>(ctx->long_np.p), ctx->stream), "k_row_nprod");
+                      lnp, ctx->stream), "k_row_nprod");
   if ((s = run_scan(ctx, static_cast<const int64_t*>(ctx->hb_nprod.p), M, static_cast<int64_t*>(ctx->hb_off.p),
                     nullptr)) != BRM_OK)
     return s;
@@ -1222,9 +1231,9 @@ brm_status_t brm_row_nprod(brm_context_t* ctx, const brm_csr_t* A, const brm_csr
   if (!nprod && A->rows) return fail(ctx, BRM_ERR_INVALID, "nprod is null");
   DeviceGuard g(ctx->device);
   CK(ensure(ctx, ctx->small, sizeof(SmallDev)), "alloc small");
-  if ((s = long_rows(ctx, CsrView{A->rpt, A->col, A->val}, B->rpt, A->rows)) != BRM_OK) return s;
-  CK(launch_row_nprod(CsrView{A->rpt, A->col, A->val}, B->rpt, A->rows, nprod,
-                      static_cast<const int64_t*>(ctx->long_np.p), ctx->stream), "k_row_nprod");
+  const int64_t* lnp = nullptr;
+  if ((s = long_rows(ctx, CsrView{A->rpt, A->col, A->val}, B->rpt, A->rows, &lnp)) != BRM_OK) return s;
+  CK(launch_row_nprod(CsrView{A->rpt, A->col, A->val}, B->rpt, A->rows, nprod, lnp, ctx->stream), "k_row_nprod");
   return BRM_OK;
 }
 

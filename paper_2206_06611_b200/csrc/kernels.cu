@@ -131,8 +131,8 @@ __device__ __forceinline__ void warp_rows_nprod(const CsrView& A, const int64_t*
   const int nl = lane < 31 ? (int)(rnext - rs) : (int)(pend - rs);
   *nl_out = nl;
   const bool valid = r0 + lane < M;
-  // rows of more than kLongRow nonzeros were summed by k_long_nprod
-  const bool lng = valid && nl > kLongRow;
+  // rows of more than kLongRow nonzeros were summed by k_long_nprod (if it ran)
+  const bool lng = long_np != nullptr && valid && nl > kLongRow;
   const unsigned longm = __ballot_sync(0xffffffffu, lng);
   if (__reduce_max_sync(0xffffffffu, valid && !lng ? (unsigned)nl : 0u) <= 64u) {
     // short rows: one lane per row, independent gathers (no shuffles)
@@ -732,7 +732,7 @@ cudaError_t launch_long_rows(const CsrView& A, const int64_t* brpt, int64_t M, i
                              int64_t* long_np, cudaStream_t st) {
   if (M <= 0) return cudaSuccess;
   k_long_rows<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(A, M, list, count);
-  k_long_nprod<<<(unsigned)(num_sms() * 8), 256, 0, st>>>(A, brpt, list, count, long_np);
+  k_long_nprod<<<(unsigned)(num_sms() * 2), 256, 0, st>>>(A, brpt, list, count, long_np);
   return cudaGetLastError();
 }
 

@@ -333,19 +333,24 @@ def test_stage_nprod_scan_partition(ctx, oracle_mod):
     B = random_sparse(2000, 1000, 0.02, seed=9)
     nprod = ctx.brm_row_nprod(TorchCsr.from_csr(A), TorchCsr.from_csr(B)).cpu().numpy()
     np.testing.assert_array_equal(nprod, oracle_mod.row_nprod(A, B))
-    # long rows (> 512 nonzeros: summed by a CTA each) between short and
-    # empty ones, in 32-row chunks with several runs, and at the matrix end
+    # long rows (> 512 nonzeros: summed by a CTA each from 65,536 rows on,
+    # by the warps below) between short and empty ones, in 32-row chunks with
+    # several runs, and at the matrix end
     rng = np.random.default_rng(5)
-    lens = rng.integers(0, 40, size=700)
-    lens[[3, 4, 31, 32, 60, 100, 101, 102, 699]] = [513, 2000, 900, 4000, 600, 513, 1, 3000, 1500]
+    lens = np.zeros(70000, np.int64)
+    lens[:700] = rng.integers(0, 40, size=700)
+    lens[69000:] = rng.integers(0, 5, size=1000)
+    lens[[3, 4, 31, 32, 60, 100, 101, 102, 699, 69998, 69999]] = [513, 2000, 900, 4000, 600, 513, 1, 3000, 1500,
+                                                                  700, 800]
     lens[[5, 33]] = 0
     Bw = random_sparse(5000, 300, 0.02, seed=10)
     cols = [np.sort(rng.choice(5000, size=n, replace=False)).astype(np.int32) for n in lens]
     rpt = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     Al = Csr(lens.size, 5000, rpt, np.concatenate(cols), rng.uniform(-1, 1, size=int(rpt[-1])))
-    got = ctx.brm_row_nprod(TorchCsr.from_csr(Al), TorchCsr.from_csr(Bw)).cpu().numpy()
-    np.testing.assert_array_equal(got, oracle_mod.row_nprod(Al, Bw))
-    compare(run(ctx, Al, Bw, "precise"), Al, Bw)
+    for X in (Al, _row_slice(Al, 0, 700)):  # with and without the long-row pass
+        got = ctx.brm_row_nprod(TorchCsr.from_csr(X), TorchCsr.from_csr(Bw)).cpu().numpy()
+        np.testing.assert_array_equal(got, oracle_mod.row_nprod(X, Bw))
+        compare(run(ctx, X, Bw, "precise"), X, Bw)
     rng = np.random.default_rng(0)
     for n in (0, 1, 2047, 2048, 2049, 100_000, 3_000_001):
         x = rng.integers(0, 1 << 40, size=n, dtype=np.int64)
@@ -357,6 +362,11 @@ def test_stage_nprod_scan_partition(ctx, oracle_mod):
     for p in (1, 2, 3, 4, 8, 64):
         got = ctx.brm_partition_rows(off, p).cpu().tolist()
         assert got == oracle_mod.balance_by_nprod(nprod, p), p
+
+
+def _row_slice(X, r0, r1):
+    a0, a1 = int(X.rpt[r0]), int(X.rpt[r1])
+    return Csr(r1 - r0, X.cols, (X.rpt[r0:r1 + 1] - a0).astype(np.int64), X.col[a0:a1].copy(), X.val[a0:a1].copy())
 
 
 def test_errors_are_reported(ctx):
