@@ -103,6 +103,11 @@ struct TierBounds {
 // tier 4 on stencil27_64: 0.617 ms on 64 threads per row, 0.529 on one warp
 // per row (2 rows per CTA; 4 per CTA 0.538), 8 loads in flight (4: 0.636,
 // 2: 0.841), HQ 5 (4: 0.621, 8: 0.674) -- profiles/r02c_hash.
+// PRECISE symbolic of one-warp rows: a direct-mapped table (a bitmap over
+// the row's column span) when the span fits the table's bits, else hashing
+#ifndef BRM_SYM_BITMAP
+#define BRM_SYM_BITMAP 1
+#endif
 #ifndef BRM_H3_HB
 #define BRM_H3_HB 1
 #endif

@@ -1094,7 +1094,9 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
   const int rank = g.rank;
   const int64_t a0 = A.rpt[row];
   const int nl = static_cast<int>(A.rpt[row + 1] - a0);
+  constexpr bool BM = BRM_SYM_BITMAP && G <= 32;
   int P = 0;
+  int cmin = INT_MAX, cmax = -1;  // BM: the row's column span (first / last column of every list)
   for (int lb = 0; lb < nl; lb += G) {
     const int l = lb + rank;
     int n = 0;
@@ -1103,6 +1105,10 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
       const int64_t st = __ldg(B.rpt + k);
       n = static_cast<int>(__ldg(B.rpt + k + 1) - st);
       hb.bst[l] = st;
+      if (BM && n > 0) {
+        cmin = min(cmin, __ldg(B.col + st));
+        cmax = max(cmax, __ldg(B.col + st + n - 1));
+      }
     }
     int tot;
     const int ex = group_excl_scan<G>(g, n, tot, hb.scan_tmp);
@@ -1110,6 +1116,15 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
     P += tot;
   }
   if (rank == 0) hb.off[nl] = P;
+  // Rows whose columns span at most the table's bits count with a
+  // direct-mapped table instead: a bitmap over [cmin, cmax] (the hash is the
+  // identity, no probing); a product is new iff it sets its bit first.
+  bool use_bm = false;
+  if constexpr (BM) {
+    cmin = __reduce_min_sync(g.mask, cmin);
+    cmax = __reduce_max_sync(g.mask, cmax);
+    use_bm = cmax >= 0 && cmax - cmin < hash_cap<CAP, HQ>() * 32;
+  }
   // a column's slot is the HIGH bits of its multiplicative hash (the low bits
   // of c * K follow c's low bits, which cluster for structured rows: the
   // stencil's symbolic pass ran 2.7x slower with them)
@@ -1118,8 +1133,12 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
     H <<= 1;
     ++hbits;
   }
-  for (int e = rank; e < (H >> 2); e += G)
-    reinterpret_cast<int4*>(hb.table)[e] = make_int4(kHashEmpty, kHashEmpty, kHashEmpty, kHashEmpty);
+  if (use_bm) {
+    for (int e = rank; e < (((cmax - cmin) >> 7) + 1); e += G) reinterpret_cast<int4*>(hb.table)[e] = make_int4(0, 0, 0, 0);
+  } else {
+    for (int e = rank; e < (H >> 2); e += G)
+      reinterpret_cast<int4*>(hb.table)[e] = make_int4(kHashEmpty, kHashEmpty, kHashEmpty, kHashEmpty);
+  }
   g.sync();
   for (int l = rank; l < nl; l += G) owner_fill(hb.owner, 1, hb.off[l], hb.off[l + 1], l);
   g.sync();
@@ -1135,6 +1154,19 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
         const int l = hb.owner[e];
         cc[u] = __ldg(B.col + hb.bst[l] + (e - hb.off[l]));
       }
+    }
+    if (use_bm) {
+      const volatile unsigned* bv = reinterpret_cast<const volatile unsigned*>(hb.table);
+#pragma unroll
+      for (int u = 0; u < HB; ++u) {
+        const int c = cc[u];
+        if (c < 0) continue;
+        const int rel = c - cmin;
+        const unsigned bit = 1u << (rel & 31);
+        if (!(bv[rel >> 5] & bit))  // a set bit is final: only a clear one is claimed
+          cnt += !(atomicOr(reinterpret_cast<unsigned*>(hb.table) + (rel >> 5), bit) & bit);
+      }
+      continue;
     }
 #pragma unroll
     for (int u = 0; u < HB; ++u) {

@@ -131,6 +131,43 @@ def test_record_packing_boundary(ctx, oracle_mod, mode, tier, slot_bits, list_le
     compare(run(ctx, A, B, mode), A, B)
 
 
+def _span_matrix(nl, list_len, span, base, seed, pool=96):
+    """One A row of nl lists; B rows draw list_len sorted columns from a pool
+    of `pool` columns in [base, base + span] holding both ends (first list:
+    base, last list: base + span), so the row's column span is exactly span
+    and its columns repeat across lists."""
+    rng = np.random.default_rng(seed)
+    pc = np.unique(np.concatenate([[base, base + span], rng.integers(base, base + span + 1, size=pool)]))
+    rows = []
+    for j in range(nl):
+        c = rng.choice(pc, size=list_len, replace=False)
+        if j == 0:
+            c[0] = base
+        if j == nl - 1:
+            c[0] = base + span
+        rows.append(np.unique(c))
+    rpt = np.zeros(nl + 1, np.int64)
+    np.cumsum([len(r) for r in rows], out=rpt[1:])
+    col = np.concatenate(rows).astype(np.int32)
+    B = Csr(nl, base + span + 1, rpt, col, rng.uniform(-1, 1, size=col.size))
+    A = Csr(1, nl, np.array([0, nl], np.int64), np.arange(nl, dtype=np.int32), rng.uniform(-1, 1, size=nl))
+    return A, B
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("nl,list_len", [(16, 16), (27, 27)])  # tier 3 (P 256) and tier 4 (P 729)
+@pytest.mark.parametrize("span", [1, 32766, 32767, 32768, 40000])
+@pytest.mark.parametrize("base", [0, 2_000_000_000])
+def test_symbolic_direct_table_span(ctx, oracle_mod, mode, nl, list_len, span, base):
+    """PRECISE symbolic of one-warp rows: a bitmap over the row's column span
+    while span <= 32767 (the table's 32768 bits), hashing above; both sides
+    of the boundary, near column 0 and near 2^31."""
+    if span < list_len:
+        list_len = span + 1
+    A, B = _span_matrix(nl, list_len, span, base, seed=span + nl)
+    compare(run(ctx, A, B, mode), A, B)
+
+
 @pytest.mark.parametrize("mode", MODES)
 def test_misaligned_b_arrays(ctx, oracle_mod, mode):
     """B's col/val arrays at addresses that are not 16-byte aligned (views one
