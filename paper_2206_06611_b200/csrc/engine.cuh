@@ -916,6 +916,9 @@ __device__ __forceinline__ int rec_merge_lists(const Group<G>& g, const CsrView&
   return end - 1;  // list 0 = records [0, end - 1), then its sentinel
 }
 
+#ifndef BRM_REC_PREFETCH
+#define BRM_REC_PREFETCH 0  // record tiers: L2 prefetch of up to 32 * this many entries of each list (0: none)
+#endif
 template <int G, int NV, class R, int OUT, bool PLAIN = false>
 __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, const CsrView& B, int64_t row,
                                         const RowOut& o, const RecBufs& rb) {
@@ -939,6 +942,18 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
       st = __ldg(B.rpt + k);
       n = static_cast<int>(__ldg(B.rpt + k + 1) - st);
       if (VALS) av = __ldg(A.val + a0 + l);
+      if constexpr (BRM_REC_PREFETCH > 0) {
+        // the list's B entries start towards L2 now; the gather below reads
+        // them after the scan, the owner fill and a group sync
+        const int m = min(n, BRM_REC_PREFETCH * 32);
+        for (int e = 0; e < m; e += 32) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(B.col + st + e));
+          if (VALS) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(B.val + st + e));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(B.val + st + e + 16));
+          }
+        }
+      }
     }
     int tot;
     const int ex = group_excl_scan<G>(g, n, tot, rb.scan_tmp);
