@@ -139,6 +139,28 @@ BRM_API brm_status_t brm_set_heavy_route(brm_context_t* ctx, int route);
  * products (default 2^26; 0: always). Smaller products run the one-shot
  * form. Results are identical. Errors: BRM_ERR_INVALID (negative).        */
 BRM_API brm_status_t brm_set_host_pipeline(brm_context_t* ctx, int64_t min_products);
+/* Multi-GPU write-out over peer memory (the row partition
+ * of PAPER.md:281 gives every rank a block of C's rows, Eq. (2) rows being
+ * independent). After brm_set_mirrors(ctx, n, col, val), every
+ * brmerge_spgemm_fill on this context stores each entry of C -- the column
+ * and the value it writes at index i of C->col / C->val -- also at index i of
+ * col[p] / val[p] for p < n, so a rank's row block lands in its peers' copies
+ * of C by the merge kernels' (UPPER: the compaction kernel's) own stores and
+ * no all-gather of col/val follows. col[p] / val[p] are DEVICE pointers that
+ * this device can write: peer memory opened through CUDA IPC or enabled with
+ * brm_enable_peer_access, normally a peer's whole-C array advanced by this
+ * rank's first entry. They are host arrays of n pointers, copied by the
+ * call; the memory they name stays owned by the caller and must outlive the
+ * fill and the work it enqueues. n = 0 clears. The other forms (one-call,
+ * host-buffer) never mirror. The stores are plain global stores: a peer may
+ * read them after this stream's work has completed and the ranks have
+ * synchronised. Errors: BRM_ERR_INVALID (n outside [0, 7], null pointers). */
+#define BRM_MAX_MIRRORS 7
+BRM_API brm_status_t brm_set_mirrors(brm_context_t* ctx, int n, int32_t* const* col, double* const* val);
+/* Let the context's device write `peer_device`'s memory (cudaDeviceEnablePeerAccess;
+ * already enabled is not an error; the context's own device is a no-op).
+ * Errors: BRM_ERR_INVALID (no P2P path), BRM_ERR_CUDA.                      */
+BRM_API brm_status_t brm_enable_peer_access(brm_context_t* ctx, int peer_device);
 /* Last error message of this context (static storage owned by ctx). */
 BRM_API const char* brm_last_error(const brm_context_t* ctx);
 BRM_API const char* brm_status_string(brm_status_t s);

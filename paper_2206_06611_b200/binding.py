@@ -67,6 +67,8 @@ SIGNATURES = {
     "brm_set_timing": [_P, ctypes.c_int],
     "brm_set_heavy_route": [_P, ctypes.c_int],
     "brm_set_host_pipeline": [_P, ctypes.c_int64],
+    "brm_set_mirrors": [_P, ctypes.c_int, ctypes.POINTER(_P), ctypes.POINTER(_P)],
+    "brm_enable_peer_access": [_P, ctypes.c_int],
     "brm_last_error": [_P],
     "brm_status_string": [ctypes.c_int],
     "brm_get_stats": [_P, ctypes.POINTER(brm_stats_t)],
@@ -197,6 +199,19 @@ class Context:
         intermediate products (0: always; A of >= 65,536 rows); include/brmerge.h."""
         self._check(self.lib.brm_set_host_pipeline(self._h, int(min_products)))
 
+    def brm_set_mirrors(self, col_ptrs=(), val_ptrs=()):
+        """Peers' copies of C that brmerge_spgemm_fill also writes (device
+        pointers as ints; empty: none); include/brmerge.h."""
+        n = len(col_ptrs)
+        if n != len(val_ptrs):
+            raise ValueError("one value pointer per column pointer")
+        cols = (_P * max(n, 1))(*[int(x) for x in col_ptrs])
+        vals = (_P * max(n, 1))(*[int(x) for x in val_ptrs])
+        self._check(self.lib.brm_set_mirrors(self._h, n, cols, vals))
+
+    def brm_enable_peer_access(self, peer_device: int):
+        self._check(self.lib.brm_enable_peer_access(self._h, int(peer_device)))
+
     def stats(self) -> dict:
         s = brm_stats_t()
         self._check(self.lib.brm_get_stats(self._h, ctypes.byref(s)))
@@ -214,10 +229,17 @@ class Context:
                                                       ctypes.byref(nnz)))
         return c_rpt, int(nnz.value)
 
-    def brmerge_spgemm_fill(self, rows: int, cols: int, c_rpt: torch.Tensor, nnz: int) -> TorchCsr:
+    def brmerge_spgemm_fill(self, rows: int, cols: int, c_rpt: torch.Tensor, nnz: int,
+                            col: torch.Tensor = None, val: torch.Tensor = None) -> TorchCsr:
+        """col / val: caller-owned output arrays of nnz entries (e.g. this
+        rank's slice of a whole-C array); allocated here when not given."""
         self._bind_stream()
-        col = torch.empty(max(nnz, 0), dtype=torch.int32, device=self.device)
-        val = torch.empty(max(nnz, 0), dtype=torch.float64, device=self.device)
+        if col is None:
+            col = torch.empty(max(nnz, 0), dtype=torch.int32, device=self.device)
+            val = torch.empty(max(nnz, 0), dtype=torch.float64, device=self.device)
+        elif (col.dtype != torch.int32 or val.dtype != torch.float64 or col.numel() != nnz
+              or val.numel() != nnz or not col.is_contiguous() or not val.is_contiguous()):
+            raise ValueError("col / val must be contiguous int32 / float64 arrays of nnz entries")
         C = TorchCsr(rows, cols, c_rpt, col, val)
         c = brm_csr_t(rows, cols, nnz, c_rpt.data_ptr(), col.data_ptr() if nnz else 0,
                       val.data_ptr() if nnz else 0)

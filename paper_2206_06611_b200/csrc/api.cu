@@ -79,6 +79,7 @@ struct brm_context {
   // pipelined host entry keeps a copy engine busy with C)
   bool kernel_readback = false;
   int64_t pipe_min_products = int64_t(1) << 26;  // brm_set_host_pipeline
+  Mirrors mirrors{};  // brm_set_mirrors: peers' copies of C written by brmerge_spgemm_fill
 };
 
 namespace {
@@ -784,7 +785,9 @@ brm_status_t structure_impl(brm_context_t* ctx, const brm_csr_t* A, const brm_cs
   return BRM_OK;
 }
 
-brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
+// mir: the peers' copies of C (brmerge_spgemm_fill only; the other forms
+// pass none)
+brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C, const Mirrors& mir = Mirrors{}) {
   if (!ctx->planned) return fail(ctx, BRM_ERR_STATE, "fill without a preceding structure call");
   if (!C || !C->rpt || (ctx->nnz_c > 0 && (!C->col || !C->val)))
     return fail(ctx, BRM_ERR_INVALID, "C arrays are null");
@@ -796,7 +799,7 @@ brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
     // Step 6 of Fig. 4a: copy C_bar -> C
     CK(launch_compact(ctx->M, ctx->nnz_c, static_cast<const int64_t*>(ctx->nprod_off.p), C->rpt,
                       static_cast<const int32_t*>(ctx->cbar_col.p), static_cast<const double*>(ctx->cbar_val.p),
-                      C->col, C->val, ctx->stream),
+                      C->col, C->val, mir, ctx->stream),
        "k_compact");
     ++ctx->launches;
     ev_record(ctx, 6);
@@ -806,6 +809,7 @@ brm_status_t fill_impl(brm_context_t* ctx, brm_csr_t* C) {
     o.base = C->rpt;
     o.col = C->col;
     o.val = C->val;
+    o.mir = mir;
     brm_status_t s = run_merge(ctx, OUT_C, o, true);
     if (s != BRM_OK) return s;
     ev_record(ctx, 6);
@@ -1071,6 +1075,37 @@ brm_status_t brm_set_host_pipeline(brm_context_t* ctx, int64_t min_products) {
   return BRM_OK;
 }
 
+brm_status_t brm_set_mirrors(brm_context_t* ctx, int n, int32_t* const* col, double* const* val) {
+  if (!ctx) return BRM_ERR_INVALID;
+  if (n < 0 || n > kMaxMirrors) return fail(ctx, BRM_ERR_INVALID, "mirror count outside [0, 7]");
+  if (n > 0 && (!col || !val)) return fail(ctx, BRM_ERR_INVALID, "mirror arrays are null");
+  Mirrors m{};
+  for (int p = 0; p < n; ++p) {
+    if (!col[p] || !val[p]) return fail(ctx, BRM_ERR_INVALID, "a mirror pointer is null");
+    m.col[p] = col[p];
+    m.val[p] = val[p];
+  }
+  m.n = n;
+  ctx->mirrors = m;
+  return BRM_OK;
+}
+
+brm_status_t brm_enable_peer_access(brm_context_t* ctx, int peer_device) {
+  if (!ctx) return BRM_ERR_INVALID;
+  if (peer_device == ctx->device) return BRM_OK;
+  DeviceGuard g(ctx->device);
+  int can = 0;
+  CK(cudaDeviceCanAccessPeer(&can, ctx->device, peer_device), "cudaDeviceCanAccessPeer");
+  if (!can) return fail(ctx, BRM_ERR_INVALID, "the peer device is not reachable over P2P");
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return BRM_OK;
+  }
+  CK(e, "cudaDeviceEnablePeerAccess");
+  return BRM_OK;
+}
+
 brm_status_t brm_set_heavy_route(brm_context_t* ctx, int route) {
   if (!ctx || (route != BRM_HEAVY_AUTO && route != BRM_HEAVY_GLOBAL)) return BRM_ERR_INVALID;
   ctx->heavy_route = route;
@@ -1113,7 +1148,7 @@ brm_status_t brmerge_spgemm_structure(brm_context_t* ctx, const brm_csr_t* A, co
 brm_status_t brmerge_spgemm_fill(brm_context_t* ctx, brm_csr_t* C) {
   if (!ctx) return BRM_ERR_INVALID;
   DeviceGuard g(ctx->device);
-  return fill_impl(ctx, C);
+  return fill_impl(ctx, C, ctx->mirrors);
 }
 
 brm_status_t brmerge_spgemm(brm_context_t* ctx, const brm_csr_t* A, const brm_csr_t* B, brm_mode_t mode,

@@ -26,12 +26,38 @@ enum OutKind { OUT_SYMBOLIC = 0, OUT_CBAR = 1, OUT_C = 2 };
 
 constexpr int kHashEmpty = -1;  // empty slot of the shared hash tables (columns are >= 0)
 
+// Mirrors (multi-GPU write-out over peer memory): under
+// OUT_C every stored entry of C also goes, at the same index, into the
+// peers' copies of C -- device pointers into peer memory (NVLink P2P), so the
+// row blocks are assembled by the merge kernels' own stores instead of an
+// all-gather after them.
+constexpr int kMaxMirrors = 7;  // the peers of an 8-GPU node
+struct Mirrors {
+  int n;
+  int32_t* col[kMaxMirrors];
+  double* val[kMaxMirrors];
+};
 struct RowOut {
   const int64_t* base;  // OUT_CBAR: n_prod offsets; OUT_C: C.rpt
   int32_t* col;
   double* val;
   int64_t* row_size;    // OUT_SYMBOLIC / OUT_CBAR: nnz of each output row
+  Mirrors mir;          // OUT_C only (n = 0: none)
 };
+
+// entry i of C into every mirror (static indices: the pointers stay kernel
+// parameters); a uniform branch when there are none
+template <bool VALS>
+__device__ __forceinline__ void mirror_store(const Mirrors& m, int64_t i, int32_t c, double v) {
+  if (m.n == 0) return;
+#pragma unroll
+  for (int p = 0; p < kMaxMirrors; ++p) {
+    if (p < m.n) {
+      m.col[p][i] = c;
+      if (VALS) m.val[p][i] = v;
+    }
+  }
+}
 
 #ifndef BRM_OWNER_ROT
 #define BRM_OWNER_ROT 4
@@ -214,6 +240,7 @@ __device__ __forceinline__ void tiny_row(const CsrView& A, const CsrView& B, int
     for (int e = 0; e < n; ++e) {
       o.col[ob + e] = pc[e * NT];
       if (VALS) o.val[ob + e] = pv[e * NT];
+      if (OUT == OUT_C) mirror_store<VALS>(o.mir, ob + e, pc[e * NT], VALS ? pv[e * NT] : 0.0);
     }
   }
   if (OUT != OUT_C) o.row_size[row] = n;
@@ -341,6 +368,7 @@ __device__ __forceinline__ void reg_row(const Group<G>& g, const CsrView& A, con
     const int64_t ob = o.base[row];
     o.col[ob + lane] = c;
     if (VALS) o.val[ob + lane] = v;
+    if (OUT == OUT_C) mirror_store<VALS>(o.mir, ob + lane, c, v);
   }
   if (OUT != OUT_C && lane == 0) o.row_size[row] = T;
   g.sync();
@@ -975,7 +1003,9 @@ __device__ __forceinline__ void rec_row(const Group<G>& g, const CsrView& A, con
     for (int e = rank; e < T; e += G) {
       const typename R::T r = rec[e];
       o.col[ob + e] = R::col(r);
-      if (VALS) o.val[ob + e] = rb.val[R::slot(r)];
+      double v = 0.0;
+      if (VALS) o.val[ob + e] = v = rb.val[R::slot(r)];
+      if (OUT == OUT_C) mirror_store<VALS>(o.mir, ob + e, R::col(r), v);
     }
   }
   if (OUT != OUT_C && rank == 0) o.row_size[row] = T;
@@ -1057,7 +1087,9 @@ __device__ __forceinline__ void chunk_row(const Group<G>& g, const CsrView& A, c
     const double s0 = (VALS && nl == 1) ? cb.av[0] : 1.0;  // a single list was never scaled
     for (int e = rank; e < T; e += G) {
       o.col[ob + e] = sc[e];
-      if (VALS) o.val[ob + e] = nl == 1 ? __dmul_rn(s0, sv[e]) : sv[e];
+      double v = 0.0;
+      if (VALS) o.val[ob + e] = v = nl == 1 ? __dmul_rn(s0, sv[e]) : sv[e];
+      if (OUT == OUT_C) mirror_store<VALS>(o.mir, ob + e, sc[e], v);
     }
   }
   if (OUT != OUT_C && rank == 0) o.row_size[row] = T;

@@ -961,8 +961,11 @@ __global__ void __launch_bounds__(kHvG, kHvMinBlocks) k_hv_merge(HvArgs a, RowOu
     const int ob = a.wout[r.plan + w];
     if (rank == 0 && T != a.wout[r.plan + w + 1] - ob) atomicOr(a.err, 2u);
     for (int e = rank; e < T; e += kHvG) {
-      ocol[obase + ob + e] = static_cast<int>(rk[e] & kColMask) + c0;
-      oval[obase + ob + e] = rv[e];
+      const int c = static_cast<int>(rk[e] & kColMask) + c0;
+      const double v = rv[e];
+      ocol[obase + ob + e] = c;
+      oval[obase + ob + e] = v;
+      if (OUT == OUT_C && r.out == 0) mirror_store<true>(o.mir, obase + ob + e, c, v);
     }
     for (int l = rank; l < nl; l += kHvG) cur[l] += cnt[l];
     __syncthreads();

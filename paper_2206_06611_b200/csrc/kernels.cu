@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(256) k_compact(int64_t M, const int64_t* __res
                                                  const int64_t* __restrict__ crpt,
                                                  const int32_t* __restrict__ cbar_col,
                                                  const double* __restrict__ cbar_val,
-                                                 int32_t* __restrict__ ccol, double* __restrict__ cval) {
+                                                 int32_t* __restrict__ ccol, double* __restrict__ cval, Mirrors mir) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -644,6 +644,7 @@ __global__ void __launch_bounds__(256) k_compact(int64_t M, const int64_t* __res
           if (dst[u] >= 0) {
             ccol[dst[u]] = cv[u];
             cval[dst[u]] = vv[u];
+            mirror_store<true>(mir, dst[u], cv[u], vv[u]);
           }
       }
       eb0 = wend;
@@ -890,12 +891,12 @@ cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B,
 }
 
 cudaError_t launch_compact(int64_t M, int64_t nnz, const int64_t* nprod_off, const int64_t* crpt, const int32_t* cbar_col,
-                           const double* cbar_val, int32_t* ccol, double* cval, cudaStream_t st) {
+                           const double* cbar_val, int32_t* ccol, double* cval, const Mirrors& mir, cudaStream_t st) {
   if (M <= 0 || nnz <= 0) return cudaSuccess;
   int64_t blocks = (nnz + 8 * kCompactChunk - 1) / (8 * kCompactChunk);  // one chunk per warp
   const int64_t cap = (int64_t)num_sms() * 16;
   if (blocks > cap) blocks = cap;
-  k_compact<<<(unsigned)blocks, 256, 0, st>>>(M, nprod_off, crpt, cbar_col, cbar_val, ccol, cval);
+  k_compact<<<(unsigned)blocks, 256, 0, st>>>(M, nprod_off, crpt, cbar_col, cbar_val, ccol, cval, mir);
   return cudaGetLastError();
 }
 

@@ -40,7 +40,7 @@ int64_t global_row_bytes(int64_t nprod, int64_t nl, bool vals);
 cudaError_t launch_global_tier(int out_kind, const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n,
                                const int64_t* ws_off, unsigned char* ws, const RowOut& o, cudaStream_t st);
 cudaError_t launch_compact(int64_t M, int64_t nnz, const int64_t* nprod_off, const int64_t* crpt, const int32_t* cbar_col,
-                           const double* cbar_val, int32_t* ccol, double* cval, cudaStream_t st);
+                           const double* cbar_val, int32_t* ccol, double* cval, const Mirrors& mir, cudaStream_t st);
 cudaError_t launch_partition(const int64_t* nprod_off, int64_t M, int p, int64_t* bounds, cudaStream_t st);
 cudaError_t launch_row_nprod(const CsrView& A, const int64_t* brpt, int64_t M, int64_t* nprod, const int64_t* long_np,
                              cudaStream_t st);

@@ -5,7 +5,10 @@ rows: rank g computes the row block [bounds[g], bounds[g+1]) where the bounds
 balance n_prod across ranks (§III.D; reading R7, computed on the
 device by brm_partition_rows). B is broadcast from one rank, each rank runs
 the whole path on its block through the C ABI, and C's row_ptr offsets (and
-optionally the C row blocks themselves) are assembled with all-gathers.
+optionally the C row blocks themselves) are assembled with all-gathers -- or,
+with PeerAssembly, the row blocks are written into every rank's copy of C by
+the merge kernels themselves over peer memory (brm_set_mirrors), and only the
+row pointers are all-gathered.
 
 This module only moves and re-indexes tensors with torch.distributed (NCCL on
 GPUs, gloo in the CPU tests); no step of the SpGEMM itself runs here.
@@ -108,3 +111,80 @@ def assemble_csr(C_blk: TorchCsr, total_rows: int, group=None) -> TorchCsr:
         torch.tensor(rows, dtype=torch.int64, device=dev))
     rpt = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), rp + shift])
     return TorchCsr(total_rows, C_blk.cols, rpt, col, val)
+
+
+def share_tensor(t: torch.Tensor, group=None) -> list[torch.Tensor]:
+    """Every rank's `t` opened on every rank: out[g] is rank g's tensor (this
+    rank's own `t` at its own index), mapped through CUDA IPC by torch's
+    tensor-sharing machinery (the handle travels by all_gather_object). `t`
+    must come from torch's caching allocator and stay alive on its owner while
+    any peer uses the mapping."""
+    from torch.multiprocessing.reductions import reduce_tensor
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    infos = [None] * world
+    dist.all_gather_object(infos, reduce_tensor(t), group=group)
+    return [t if g == rank else fn(*args) for g, (fn, args) in enumerate(infos)]
+
+
+class PeerAssembly:
+    """C = A*B over the ranks' row blocks with the write-out fused into the
+    assembly: every rank holds a whole-C col/val array, opens its peers' arrays
+    (share_tensor), and its fill stores each entry of its row block into its
+    own array AND, through brm_set_mirrors, into every peer's at the block's
+    global offset -- the numeric merge kernels' stores travel over NVLink P2P,
+    so no all-gather of col/val follows the merge. Only the block sizes and the
+    row pointers are all-gathered (assemble_rpt). At most 8 ranks (7 mirrors).
+
+    The arrays are kept and re-shared only when C outgrows them (every rank
+    sees the same total, so the ranks decide alike)."""
+
+    def __init__(self, ctx, group=None):
+        self.ctx, self.group = ctx, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        if self.world > 8:
+            raise ValueError("PeerAssembly serves at most 8 ranks (7 mirrors)")
+        self.cap = 0
+        self.col = self.val = None
+        self.peer_col = self.peer_val = None
+
+    def _ensure(self, total: int):
+        if total <= self.cap and self.col is not None:
+            return
+        dev = self.ctx.device
+        self.peer_col = self.peer_val = None  # drop the old mappings first
+        self.col = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        self.val = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+        self.cap = max(total, 1)
+        self.peer_col = share_tensor(self.col, self.group)
+        self.peer_val = share_tensor(self.val, self.group)
+        for g, t in enumerate(self.peer_col):
+            if g != self.rank and t.device != dev:
+                self.ctx.brm_enable_peer_access(t.device.index)
+
+    def spgemm(self, A_blk: TorchCsr, B: TorchCsr, mode, total_rows: int) -> TorchCsr:
+        """This rank's row block A_blk (blocks in rank order cover A); returns
+        the whole C on every rank (views of the kept arrays, valid until the
+        next call)."""
+        ctx, dev = self.ctx, self.ctx.device
+        cdev = dev if dist.get_backend(self.group) == "nccl" else torch.device("cpu")  # where the collectives run
+        c_rpt, nnz = ctx.brmerge_spgemm_structure(A_blk, B, mode)
+        nnzs = block_nnz(nnz, cdev, self.group).tolist()
+        total, off = sum(nnzs), sum(nnzs[: self.rank])
+        self._ensure(total)
+        # every rank has finished reading the previous C before anyone overwrites it
+        torch.cuda.synchronize(dev)
+        dist.barrier(self.group)
+        others = [g for g in range(self.world) if g != self.rank]
+        ctx.brm_set_mirrors([self.peer_col[g].data_ptr() + 4 * off for g in others],
+                            [self.peer_val[g].data_ptr() + 8 * off for g in others])
+        try:
+            Cb = ctx.brmerge_spgemm_fill(A_blk.rows, B.cols, c_rpt, nnz,
+                                         col=self.col[off:off + nnz], val=self.val[off:off + nnz])
+        finally:
+            ctx.brm_set_mirrors()
+        # the peers' stores are complete once every rank's stream has drained
+        torch.cuda.synchronize(dev)
+        dist.barrier(self.group)
+        # row_ptr offsets by all-gather (assemble_rpt reads only rpt, rows and nnz of the block)
+        rpt = assemble_rpt(TorchCsr(Cb.rows, Cb.cols, Cb.rpt.to(cdev), Cb.col, Cb.val), total_rows, self.group)
+        return TorchCsr(total_rows, B.cols, rpt.to(dev), self.col[:total], self.val[:total])

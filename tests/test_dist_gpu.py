@@ -3,7 +3,10 @@ its n_prod-balanced row block (§III.D): the partition comes from
 the library's own kernels (brm_row_nprod -> brm_exclusive_scan_i64 ->
 brm_partition_rows), B is broadcast from rank 0, each rank computes its block
 of C on cuda:0, and dist.assemble_csr all-gathers the row blocks and row_ptr
-offsets. The assembled C must equal the oracle's bit for bit (columns, row
+offsets -- or ("peer") dist.PeerAssembly has each rank's fill store its block
+into both ranks' whole-C arrays over peer memory (brm_set_mirrors, the other
+rank's array opened through CUDA IPC) and all-gathers only the row pointers.
+The assembled C must equal the oracle's bit for bit (columns, row
 pointers, Algorithm-1 values). This is the multi-GPU path of bench.py with
 both ranks' kernels on one device (they never wait on each other's kernels)."""
 import os
@@ -27,7 +30,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, mode, q):
+def _worker(rank, world, port, case, mode, q, assemble="allgather"):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -52,10 +55,25 @@ def _worker(rank, world, port, case, mode, q):
         bounds = ctx.brm_partition_rows(ctx.brm_exclusive_scan_i64(nprod), world).cpu().tolist()
         assert bounds == oracle.balance_by_nprod(oracle.row_nprod(A, B), world)
         blk = bd.row_block(Ad, bounds[rank], bounds[rank + 1])
-        Cb = ctx.spgemm(blk, Bd, mode)
-        torch.cuda.synchronize()
-        C = bd.assemble_csr(Cb.to("cpu"), A.rows)
         ref, _ = oracle.spgemm_brmerge(A, B)
+        if assemble == "peer":
+            # write-out over peer memory: each rank's fill stores its block into
+            # both ranks' whole-C arrays (the other rank's opened through CUDA IPC)
+            pa = bd.PeerAssembly(ctx)
+            small = uniform_random(4000, A.rows, 5, seed=3)  # a first, smaller product: the arrays regrow after it
+            Sd = TorchCsr.from_csr(small)
+            half = [0, 1500, 4000]
+            Cs = pa.spgemm(bd.row_block(Sd, half[rank], half[rank + 1]), Bd, mode, small.rows).to("cpu")
+            rs, _ = oracle.spgemm_brmerge(small, B)
+            if not (np.array_equal(Cs.rpt.numpy(), rs.rpt) and np.array_equal(Cs.col.numpy(), rs.col)
+                    and np.array_equal(Cs.val.numpy(), rs.val)):
+                raise AssertionError("peer assembly of the first product differs from the oracle")
+            for _ in range(2):  # the second call reuses the shared arrays
+                C = pa.spgemm(blk, Bd, mode, A.rows).to("cpu")
+        else:
+            Cb = ctx.spgemm(blk, Bd, mode)
+            torch.cuda.synchronize()
+            C = bd.assemble_csr(Cb.to("cpu"), A.rows)
         ok = (np.array_equal(C.rpt.numpy(), ref.rpt) and np.array_equal(C.col.numpy(), ref.col)
               and np.array_equal(C.val.numpy(), ref.val))
         q.put((rank, ok, bounds))
@@ -69,12 +87,13 @@ def _worker(rank, world, port, case, mode, q):
 
 @pytest.mark.parametrize("case,mode", [("uniform", "precise"), ("uniform", "upper"), ("rmat", "precise"),
                                        ("rmat", "upper")])
-def test_two_ranks_one_gpu(case, mode, oracle_mod):
+@pytest.mark.parametrize("assemble", ["allgather", "peer"])
+def test_two_ranks_one_gpu(case, mode, assemble, oracle_mod):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, mode, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, mode, q, assemble)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in range(world)]

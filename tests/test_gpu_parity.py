@@ -571,3 +571,72 @@ def test_host_form_pipelined_heavy_rows(ctx, oracle_mod, mode):
             compare((hrpt.copy(), hcol.copy(), hval.copy()), A, A)
     finally:
         ctx.brm_set_host_pipeline(1 << 26)
+
+
+@pytest.mark.parametrize("route", ["auto", "global"])
+@pytest.mark.parametrize("mode", MODES)
+def test_mirrors_receive_every_entry(oracle_mod, mode, route):
+    """brm_set_mirrors: the fill stores each entry of C at the same index of
+    every mirror (here: two more arrays on the same device, pre-filled with
+    junk and offset by 5 entries) from every store site -- tiers 1-6, heavy
+    rows of one level and of 512-list blocks (or the global tier), and the
+    UPPER compaction. C itself still matches the oracle; clearing the mirrors
+    stops the extra stores; bad arguments are rejected."""
+    import torch
+    from paper_2206_06611_b200 import BrmError, Context, TorchCsr
+    c = Context()
+    try:
+        if route == "global":
+            c.brm_set_heavy_route(c.HEAVY_GLOBAL)
+        # rows of 1..600 lists over B rows of 12 entries: n_prod from 12 to 7200 covers every tier;
+        # plus heavy rows (200 / 1000 lists of 100 entries)
+        for A, B in (_lists_matrix([1, 2, 3, 8, 20, 21, 60, 64, 200, 250, 400, 512, 600, 0, 5], 12, 5000, seed=21),
+                     _lists_matrix([200, 1000, 20], 100, 20000, seed=22)):
+            At, Bt = TorchCsr.from_csr(A), TorchCsr.from_csr(B)
+            c_rpt, nnz = c.brmerge_spgemm_structure(At, Bt, mode)
+            off = 5
+            mcol = [torch.full((nnz + off,), -7, dtype=torch.int32, device="cuda") for _ in range(2)]
+            mval = [torch.full((nnz + off,), -7.0, dtype=torch.float64, device="cuda") for _ in range(2)]
+            c.brm_set_mirrors([t.data_ptr() + 4 * off for t in mcol], [t.data_ptr() + 8 * off for t in mval])
+            C = c.brmerge_spgemm_fill(A.rows, B.cols, c_rpt, nnz)
+            c.brm_set_mirrors()
+            torch.cuda.synchronize()
+            compare(C.to_numpy(), A, B)
+            for p in range(2):
+                assert torch.equal(mcol[p][off:], C.col) and torch.equal(mval[p][off:], C.val), (mode, p)
+                assert bool((mcol[p][:off] == -7).all()) and bool((mval[p][:off] == -7.0).all())
+            # cleared: a second pair stays untouched
+            c_rpt, nnz = c.brmerge_spgemm_structure(At, Bt, mode)
+            mcol[0].fill_(-7)
+            C2 = c.brmerge_spgemm_fill(A.rows, B.cols, c_rpt, nnz)
+            torch.cuda.synchronize()
+            assert bool((mcol[0] == -7).all()) and torch.equal(C2.val, C.val)
+        t = torch.zeros(4, dtype=torch.int32, device="cuda")
+        v = torch.zeros(4, dtype=torch.float64, device="cuda")
+        with pytest.raises(BrmError) as e:
+            c.brm_set_mirrors([t.data_ptr()] * 8, [v.data_ptr()] * 8)
+        assert e.value.code == 1  # BRM_ERR_INVALID: more than 7 mirrors
+        with pytest.raises(BrmError) as e:
+            c.brm_set_mirrors([0], [v.data_ptr()])
+        assert e.value.code == 1  # a null mirror pointer
+        c.brm_enable_peer_access(0)  # the context's own device: a no-op
+    finally:
+        c.close()
+
+
+def test_fill_into_caller_arrays(ctx, oracle_mod):
+    """brmerge_spgemm_fill into caller-owned col/val (a slice of a larger
+    array, as PeerAssembly passes); wrong sizes are rejected by the binding."""
+    import torch
+    from paper_2206_06611_b200 import TorchCsr
+    A = uniform_random(3000, 3000, 7, seed=4)
+    At = TorchCsr.from_csr(A)
+    c_rpt, nnz = ctx.brmerge_spgemm_structure(At, At, "precise")
+    col = torch.full((nnz + 9,), -1, dtype=torch.int32, device="cuda")
+    val = torch.zeros(nnz + 9, dtype=torch.float64, device="cuda")
+    C = ctx.brmerge_spgemm_fill(A.rows, A.cols, c_rpt, nnz, col=col[9:], val=val[9:])
+    compare(C.to_numpy(), A, A)
+    assert bool((col[:9] == -1).all())
+    c_rpt, nnz = ctx.brmerge_spgemm_structure(At, At, "precise")
+    with pytest.raises(ValueError):
+        ctx.brmerge_spgemm_fill(A.rows, A.cols, c_rpt, nnz, col=col, val=val)
