@@ -208,8 +208,10 @@ def workload_config(name, desc, mode, A, nprod, nnz_c, world=1, assemble="rpt"):
             "compression_ratio": nprod / max(nnz_c, 1),
             "l2": "flushed (256 MiB write) between timed steps, outside the events",
             "parallelism": f"dp{world} rows by balanced n_prod",
-            "assembly": (("global row_ptr all-gathered, C row-distributed" if assemble == "rpt"
-                          else "whole C all-gathered") if world > 1 else "n/a (one GPU)")}
+            "assembly": ({"rpt": "global row_ptr all-gathered, C row-distributed",
+                          "full": "whole C all-gathered",
+                          "peer": "whole C on every rank, row blocks stored by the merge kernels over peer "
+                                  "memory, row_ptr all-gathered"}[assemble] if world > 1 else "n/a (one GPU)")}
 
 
 def resolve_mode(mode, nprod, total_mem):
@@ -298,9 +300,12 @@ def main():
                     help="auto: BRMerge-Upper when its C_bar (12 B per intermediate product) fits in "
                          "half of the GPU memory, else BRMerge-Precise")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--assemble", default="rpt", choices=["rpt", "full"],
-                    help="N > 1: all-gather the global row_ptr (C's col/val stay row-distributed) "
-                         "or the whole C (row_ptr + col/val) on every rank, inside the timed step")
+    ap.add_argument("--assemble", default="rpt", choices=["rpt", "full", "peer"],
+                    help="N > 1: all-gather the global row_ptr (C's col/val stay row-distributed), "
+                         "or the whole C (row_ptr + col/val) on every rank, inside the timed step; "
+                         "peer: the whole C on every rank too, but written by each rank's merge kernels "
+                         "straight into its peers' arrays over NVLink P2P (brm_set_mirrors), only "
+                         "row_ptr all-gathered")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-prod", type=float, default=2e6, help="probe sample (products)")
@@ -347,7 +352,13 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    peer = bdist.PeerAssembly(ctx) if world > 1 and args.assemble == "peer" else None
+
     def step():
+        if peer is not None:  # the fill writes this rank's block into every rank's whole C
+            Cg = peer.spgemm(Ad, Bd, args.mode, A.rows)
+            o0, o1 = int(Cg.rpt[r0]), int(Cg.rpt[r1])
+            return TorchCsr(Ablk.rows, Cg.cols, Cg.rpt[r0:r1 + 1] - o0, Cg.col[o0:o1], Cg.val[o0:o1])  # this rank's block
         C = ctx.spgemm(Ad, Bd, args.mode)
         if world > 1:  # C's row blocks assembled with all-gathers (NCCL)
             if args.assemble == "full":  # row_ptr + col/val of every block on every rank
