@@ -644,8 +644,12 @@ __global__ void __launch_bounds__(256) k_compact(int64_t M, const int64_t* __res
           if (dst[u] >= 0) {
             ccol[dst[u]] = cv[u];
             cval[dst[u]] = vv[u];
-            mirror_store<true>(mir, dst[u], cv[u], vv[u]);
           }
+        if (mir.n) {  // (one test per batch)
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (dst[u] >= 0) mirror_store<true>(mir, dst[u], cv[u], vv[u]);
+        }
       }
       eb0 = wend;
       r0 += 32;
