@@ -135,6 +135,16 @@ struct TierBounds {
 #define BRM_HASH6 BRM_H6_G, 6656, 512, 1, 8, 5, false
 constexpr int kGlobalG = 1024;
 
+// Routing caps of tiers 5-6 (<= their kernels' CAP; 0: the tier takes no
+// rows, they go on to the next one / the windowed heavy path) -- tuning
+// switches, BRM_NVCC_FLAGS="-DBRM_T6_ROUTE=0"
+#ifndef BRM_T5_ROUTE
+#define BRM_T5_ROUTE 3072
+#endif
+#ifndef BRM_T6_ROUTE
+#define BRM_T6_ROUTE 6656
+#endif
+static_assert(BRM_T5_ROUTE <= 3072 && BRM_T6_ROUTE <= 6656, "routing caps within the kernels' capacity");
 __host__ __device__ inline TierBounds tier_bounds() {
   TierBounds t{};
   t.cap[0] = 0;    t.lcap[0] = 0;
@@ -142,8 +152,8 @@ __host__ __device__ inline TierBounds tier_bounds() {
   t.cap[2] = 32;   t.lcap[2] = 32;
   t.cap[3] = 256;  t.lcap[3] = 64;
   t.cap[4] = 768;  t.lcap[4] = 64;
-  t.cap[5] = 3072; t.lcap[5] = 256;
-  t.cap[6] = 6656; t.lcap[6] = 512;
+  t.cap[5] = BRM_T5_ROUTE; t.lcap[5] = 256;
+  t.cap[6] = BRM_T6_ROUTE; t.lcap[6] = 512;
   t.cap[7] = INT_MAX; t.lcap[7] = INT_MAX;
   return t;
 }
