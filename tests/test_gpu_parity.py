@@ -640,3 +640,55 @@ def test_fill_into_caller_arrays(ctx, oracle_mod):
     c_rpt, nnz = ctx.brmerge_spgemm_structure(At, At, "precise")
     with pytest.raises(ValueError):
         ctx.brmerge_spgemm_fill(A.rows, A.cols, c_rpt, nnz, col=col, val=val)
+
+
+def _fuzz_matrix(seed):
+    """A random product drawn from a family of shapes: power-law list counts
+    per row of A (so one matrix spreads over many tiers), B rows of mixed
+    lengths (empty, short, long) whose columns are clustered (many repeated
+    columns per output row) or spread (few), values with exact zeros and
+    cancelling pairs mixed in."""
+    rng = np.random.default_rng(1000 + seed)
+    kb = int(rng.integers(50, 1500))
+    ncols = int(rng.choice([64, 700, 5000, 200000, 3_000_000]))
+    max_len = int(rng.choice([1, 4, 30, 200, 1500]))
+    lens = rng.integers(0, min(max_len, ncols) + 1, size=kb)
+    lens[rng.random(kb) < 0.15] = 0
+    clustered = rng.random() < 0.5
+    cols = []
+    for n in lens:
+        if clustered:  # columns from a narrow band: heavy duplication across lists
+            lo = int(rng.integers(0, max(ncols - 4 * max_len, 1)))
+            hi = min(ncols, lo + max(4 * max_len, int(n)))
+            cols.append(np.sort(rng.choice(np.arange(lo, hi), size=int(n), replace=False)))
+        else:
+            cols.append(np.sort(rng.choice(ncols, size=int(n), replace=False)))
+    rpt = np.zeros(kb + 1, np.int64)
+    np.cumsum(lens, out=rpt[1:])
+    bcol = np.concatenate(cols).astype(np.int32) if rpt[-1] else np.zeros(0, np.int32)
+    bval = rng.uniform(-1, 1, size=bcol.size)
+    bval[rng.random(bcol.size) < 0.05] = 0.0  # stored zeros stay structural entries
+    half = rng.random(bcol.size) < 0.2
+    bval[half] = np.round(bval[half] * 4) / 4  # coarse values: exact cancellations happen
+    B = Csr(kb, ncols, rpt, bcol, bval)
+    m = int(rng.integers(1, 400))
+    nls = np.minimum((rng.pareto(1.1, size=m) * 3).astype(np.int64), kb)
+    nls[rng.random(m) < 0.1] = 0
+    arpt = np.zeros(m + 1, np.int64)
+    np.cumsum(nls, out=arpt[1:])
+    acol = np.concatenate([np.sort(rng.choice(kb, size=int(n), replace=False)) for n in nls]).astype(np.int32) \
+        if arpt[-1] else np.zeros(0, np.int32)
+    aval = rng.uniform(-1, 1, size=acol.size)
+    coarse = rng.random(acol.size) < 0.3
+    aval[coarse] = np.round(aval[coarse] * 2) / 2
+    return Csr(m, kb, arpt, acol, aval), B
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_shapes(ctx, oracle_mod, seed):
+    """Random shapes across the tiers (see _fuzz_matrix), both modes: rpt and
+    col bit-exact against Eq. (2), values within the tolerance and
+    bit-identical to Algorithm 1."""
+    A, B = _fuzz_matrix(seed)
+    for mode in MODES:
+        compare(run(ctx, A, B, mode), A, B)
