@@ -14,8 +14,9 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def test_tier_table_matches_kernels():
     src = (ROOT / "paper_2206_06611_b200" / "csrc" / "brm_internal.cuh").read_text()
-    caps = {int(t): (int(c), int(l)) for t, c, l in
-            re.findall(r"t\.cap\[(\d)\] = (\d+);\s+t\.lcap\[\d\] = (\d+);", src)}
+    macros = {m: int(v) for m, v in re.findall(r"#define (BRM_T\d_ROUTE) (\d+)", src)}  # routing caps' defaults
+    caps = {int(t): (int(macros.get(c, c)), int(l)) for t, c, l in
+            re.findall(r"t\.cap\[(\d)\] = (\w+);\s+t\.lcap\[\d\] = (\d+);", src)}
     for t in range(1, bench.NUM_BINS - 1):
         assert caps[t] == (bench.TIER_CAP[t], bench.TIER_LCAP[t]), t
         m = re.search(rf"#define BRM_TIER{t} (\w+), (\d+), (\d+), (\w+)", src)
