@@ -48,7 +48,11 @@ def block_ms(r0, r1):
     a0, a1 = int(A.rpt[r0]), int(A.rpt[r1])
     Ab = gen.Csr(r1 - r0, A.cols, (A.rpt[r0:r1 + 1] - a0).astype(np.int64), A.col[a0:a1].copy(), A.val[a0:a1].copy())
     Ad = TorchCsr.from_csr(Ab)
-    C = ctx.spgemm(Ad, Bd, mode)  # warm-up
+    # a rank of the real run owns a whole GPU: give the cached blocks of the
+    # previous (larger) C back first -- the heavy rows' level batches are sized
+    # by the free memory
+    torch.cuda.empty_cache()
+    C = ctx.spgemm(Ad, Bd, mode)  # warm-up (its C blocks stay cached for the timed runs)
     del C
     ts = []
     for _ in range(args.reps):
