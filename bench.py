@@ -201,13 +201,13 @@ def measured_traffic(config: str, mode: str, kernel: str):
         return None
 
 
-def workload_config(name, desc, mode, A, nprod, nnz_c, world=1, assemble="rpt"):
+def workload_config(name, desc, mode, A, nprod, nnz_c, world=1, assemble="rpt", partition=None):
     """`config` of a bench line (both arms: the same workload gives the same dict)."""
     return {"workload": name, "desc": desc, "mode": mode, "rows": A.rows,
             "nnz_a": A.nnz, "nprod": nprod, "nnz_c": nnz_c,
             "compression_ratio": nprod / max(nnz_c, 1),
             "l2": "flushed (256 MiB write) between timed steps, outside the events",
-            "parallelism": f"dp{world} rows by balanced n_prod",
+            "parallelism": f"dp{world} rows by balanced n_prod" + (f" ({partition})" if world > 1 and partition else ""),
             "assembly": ({"rpt": "global row_ptr all-gathered, C row-distributed",
                           "full": "whole C all-gathered",
                           "peer": "whole C on every rank, row blocks stored by the merge kernels over peer "
@@ -306,6 +306,12 @@ def main():
                          "peer: the whole C on every rank too, but written by each rank's merge kernels "
                          "straight into its peers' arrays over NVLink P2P (brm_set_mirrors), only "
                          "row_ptr all-gathered")
+    ap.add_argument("--partition", default=None, choices=["contiguous", "cyclic"],
+                    help="N > 1: every rank gets the same n_prod either way (PAPER.md:281); contiguous: one "
+                         "row block per rank; cyclic: N * --chunks row ranges of equal n_prod, range j to "
+                         "rank j mod N (spreads the rows whose products cost more than average). Default: cyclic, "
+                         "contiguous under --assemble peer")
+    ap.add_argument("--chunks", type=int, default=8, help="--partition cyclic: row ranges per rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-prod", type=float, default=2e6, help="probe sample (products)")
@@ -339,20 +345,33 @@ def main():
     # row partition by balanced n_prod (§III.D), computed by the library's kernels
     nprod_dev = ctx.brm_row_nprod(Afull, Bd)
     off = ctx.brm_exclusive_scan_i64(nprod_dev)
-    bounds = ctx.brm_partition_rows(off, world).cpu().numpy()
-    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    if args.partition is None:
+        args.partition = "contiguous" if args.assemble == "peer" else "cyclic"
+    cyclic = world > 1 and args.partition == "cyclic"
+    if cyclic and args.assemble == "peer":
+        raise SystemExit("--assemble peer writes contiguous row blocks: use --partition contiguous")
+    bounds = ctx.brm_partition_rows(off, world * args.chunks if cyclic else world).cpu().numpy()
+    # this rank's rows: one block, or every world-th range of the world * chunks ranges
+    ranges = bdist.cyclic_ranges(bounds, rank, world) if cyclic else [(int(bounds[rank]), int(bounds[rank + 1]))]
+    my_rows = np.concatenate([np.arange(a, b) for a, b in ranges])
+    r0, r1 = ranges[0][0], ranges[-1][1]  # (contiguous: the block itself)
     nprod_h = nprod_dev.cpu().numpy()
     del Afull
-    a0, a1 = int(A.rpt[r0]), int(A.rpt[r1])
-    Ablk = gen.Csr(r1 - r0, A.cols, (A.rpt[r0:r1 + 1] - a0).astype(np.int64), A.col[a0:a1].copy(), A.val[a0:a1].copy())
+    lens = np.diff(A.rpt)[my_rows]
+    brpt = np.zeros(my_rows.size + 1, np.int64)
+    np.cumsum(lens, out=brpt[1:])
+    Ablk = gen.Csr(my_rows.size, A.cols, brpt,
+                   np.concatenate([A.col[int(A.rpt[a]):int(A.rpt[b])] for a, b in ranges]),
+                   np.concatenate([A.val[int(A.rpt[a]):int(A.rpt[b])] for a, b in ranges]))
     Ad = TorchCsr.from_csr(Ablk)
-    local_nprod = int(nprod_h[r0:r1].sum())
+    local_nprod = int(nprod_h[my_rows].sum())
     args.mode = resolve_mode(args.mode, local_nprod, torch.cuda.get_device_properties(dev).total_memory)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     peer = bdist.PeerAssembly(ctx) if world > 1 and args.assemble == "peer" else None
+    order = bdist.cyclic_row_order(bounds, world, dev) if cyclic else None  # rank-major -> global rows (setup)
 
     def step():
         if peer is not None:  # the fill writes this rank's block into every rank's whole C
@@ -362,9 +381,9 @@ def main():
         C = ctx.spgemm(Ad, Bd, args.mode)
         if world > 1:  # C's row blocks assembled with all-gathers (NCCL)
             if args.assemble == "full":  # row_ptr + col/val of every block on every rank
-                bdist.assemble_csr(C, A.rows)
+                bdist.assemble_csr_cyclic(C, bounds, order=order) if cyclic else bdist.assemble_csr(C, A.rows)
             else:  # the global row_ptr on every rank; col/val stay row-distributed
-                bdist.assemble_rpt(C, A.rows)
+                bdist.assemble_rpt_cyclic(C, bounds, order=order) if cyclic else bdist.assemble_rpt(C, A.rows)
         return C
 
     C = None
@@ -420,7 +439,7 @@ def main():
     # per bin) or the windowed merge of the one-level heavy rows (k_hv_merge)
     peak, peak_kind = measured_peak_hbm()
     nl_loc = np.diff(Ablk.rpt)
-    np_loc = nprod_h[r0:r1]
+    np_loc = nprod_h[my_rows]
     tiers = tier_of(np_loc, nl_loc)
     cand = {}
     for b in range(1, NUM_BINS - 1):
@@ -481,11 +500,11 @@ def main():
         try:
             import oracle
             # a probe sample sizes the timed sample to ~args.cpu_seconds of oracle work
-            rows, _ = _sample_rows(nprod_h[r0:r1], args.cpu_sample_prod)
+            rows, _ = _sample_rows(np_loc, args.cpu_sample_prod)
             t0 = time.perf_counter()
             oracle.spgemm_gustavson(Ablk, B, rows=rows)
             rate = int(np_loc[rows].sum()) / max(time.perf_counter() - t0, 1e-6)
-            rows, sample = _sample_rows(nprod_h[r0:r1], rate * args.cpu_seconds)
+            rows, sample = _sample_rows(np_loc, rate * args.cpu_seconds)
             t0 = time.perf_counter()
             oracle.spgemm_gustavson(Ablk, B, rows=rows)
             dt = time.perf_counter() - t0
@@ -501,7 +520,8 @@ def main():
             "value": gflops, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": SCALING[args.config], "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args.config, desc, args.mode, A, nprod_all, nnz_all, world, args.assemble),
+            "config": workload_config(args.config, desc, args.mode, A, nprod_all, nnz_all, world, args.assemble,
+                                      (f"{args.chunks} cyclic row ranges per rank" if cyclic else "one row block per rank")),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": measured_traffic(args.config, args.mode, dom_name),
                          "kernel": dom_name, "kernel_ms": dom_ms, "kernel_rows": int(dom_rows.size),

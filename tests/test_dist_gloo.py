@@ -1,6 +1,7 @@
 """World-size-2 gloo tests (CPU) of the multi-GPU plumbing in
 paper_2206_06611_b200/dist.py: B broadcast, n_prod-balanced row blocks
-(§III.D), row_ptr offsets and C row-block assembly. The per-rank
+(§III.D; contiguous, or cyclic ranges dealt round-robin), row_ptr
+offsets and C row-block assembly. The per-rank
 SpGEMM is stood in for by the oracle (no GPU here); the product path on GPUs
 calls the C ABI instead (bench.py)."""
 import os
@@ -23,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, q, partition="contiguous"):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -49,13 +50,24 @@ def _worker(rank, world, port, case, q):
         nprod = oracle.row_nprod(A, B)
         bounds = oracle.balance_by_nprod(nprod, world)
         At = TorchCsr.from_csr(A, device="cpu")
-        blk = bd.row_block(At, bounds[rank], bounds[rank + 1])
+        if partition == "cyclic":  # 3 ranges of equal n_prod per rank, dealt round-robin
+            bounds = oracle.balance_by_nprod(nprod, world * 3)
+            ranges = bd.cyclic_ranges(bounds, rank, world)
+            assert len(ranges) == 3 and ranges[0][0] == bounds[rank]
+            blk = bd.row_ranges_block(At, ranges)
+        else:
+            blk = bd.row_block(At, bounds[rank], bounds[rank + 1])
         # per-rank compute (oracle stands in for the C ABI on the CPU)
         Ab = Csr(blk.rows, blk.cols, blk.rpt.numpy(), blk.col.numpy(), blk.val.numpy())
         Cb = oracle.spgemm_brmerge(Ab, B)[0]
         counts = bd.block_nnz(Cb.nnz, "cpu").tolist()
-        C = bd.assemble_csr(TorchCsr.from_csr(Cb, device="cpu"), A.rows)
         ref = oracle.spgemm_brmerge(A, B)[0]
+        if partition == "cyclic":
+            Ct = TorchCsr.from_csr(Cb, device="cpu")
+            C = bd.assemble_csr_cyclic(Ct, bounds)
+            assert np.array_equal(bd.assemble_rpt_cyclic(Ct, bounds).numpy(), ref.rpt)
+        else:
+            C = bd.assemble_csr(TorchCsr.from_csr(Cb, device="cpu"), A.rows)
         ok = (np.array_equal(C.rpt.numpy(), ref.rpt) and np.array_equal(C.col.numpy(), ref.col)
               and np.array_equal(C.val.numpy(), ref.val) and sum(counts) == ref.nnz
               and counts[rank] == Cb.nnz)
@@ -66,13 +78,14 @@ def _worker(rank, world, port, case, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("partition", ["contiguous", "cyclic"])
 @pytest.mark.parametrize("case", ["square", "skewed", "tiny"])
-def test_two_rank_assembly(case, oracle_mod):
+def test_two_rank_assembly(case, partition, oracle_mod):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, partition)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=180) for _ in range(world)]

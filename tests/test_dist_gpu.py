@@ -6,8 +6,10 @@ of C on cuda:0, and dist.assemble_csr all-gathers the row blocks and row_ptr
 offsets -- or ("peer") dist.PeerAssembly has each rank's fill store its block
 into both ranks' whole-C arrays over peer memory (brm_set_mirrors, the other
 rank's array opened through CUDA IPC) and all-gathers only the row pointers.
-The assembled C must equal the oracle's bit for bit (columns, row
-pointers, Algorithm-1 values). This is the multi-GPU path of bench.py with
+"cyclic" deals 4 ranges of equal n_prod per rank round-robin
+(dist.cyclic_ranges) and reassembles C in global row order. The assembled C
+must equal the oracle's bit for bit (columns, row pointers, Algorithm-1
+values). This is the multi-GPU path of bench.py with
 both ranks' kernels on one device (they never wait on each other's kernels)."""
 import os
 import socket
@@ -70,6 +72,16 @@ def _worker(rank, world, port, case, mode, q, assemble="allgather"):
                 raise AssertionError("peer assembly of the first product differs from the oracle")
             for _ in range(2):  # the second call reuses the shared arrays
                 C = pa.spgemm(blk, Bd, mode, A.rows).to("cpu")
+        elif assemble == "cyclic":
+            # 4 row ranges of equal n_prod per rank, dealt round-robin (the library's partition kernel)
+            cb = ctx.brm_partition_rows(ctx.brm_exclusive_scan_i64(nprod), world * 4).cpu().tolist()
+            assert cb == oracle.balance_by_nprod(oracle.row_nprod(A, B), world * 4)
+            Cb = ctx.spgemm(bd.row_ranges_block(Ad, bd.cyclic_ranges(cb, rank, world)), Bd, mode)
+            torch.cuda.synchronize()
+            Cc = Cb.to("cpu")
+            C = bd.assemble_csr_cyclic(Cc, cb)
+            if not np.array_equal(bd.assemble_rpt_cyclic(Cc, cb).numpy(), ref.rpt):
+                raise AssertionError("cyclic row_ptr assembly differs from the oracle")
         else:
             Cb = ctx.spgemm(blk, Bd, mode)
             torch.cuda.synchronize()
@@ -87,7 +99,7 @@ def _worker(rank, world, port, case, mode, q, assemble="allgather"):
 
 @pytest.mark.parametrize("case,mode", [("uniform", "precise"), ("uniform", "upper"), ("rmat", "precise"),
                                        ("rmat", "upper")])
-@pytest.mark.parametrize("assemble", ["allgather", "peer"])
+@pytest.mark.parametrize("assemble", ["allgather", "peer", "cyclic"])
 def test_two_ranks_one_gpu(case, mode, assemble, oracle_mod):
     world = 2
     ctx = mp.get_context("spawn")

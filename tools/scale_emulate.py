@@ -27,8 +27,10 @@ ap.add_argument("--config", default="rmat20_ef16")
 ap.add_argument("--mode", default="auto")
 ap.add_argument("--ns", default="1,2,4,8")
 ap.add_argument("--reps", type=int, default=3)
-ap.add_argument("--balance", default="nprod", choices=["nprod", "work"],
-                help="work: weight n_prod * (1 + ceil(log2 nl)) per row, partitioned on the host by R7's rule")
+ap.add_argument("--balance", default="nprod", choices=["nprod", "work", "cyclic"],
+                help="work: weight n_prod * (1 + ceil(log2 nl)) per row, partitioned on the host by R7's rule; "
+                     "cyclic: N * --chunks row ranges of equal n_prod (brm_partition_rows), range j to rank j mod N")
+ap.add_argument("--chunks", type=int, default=8, help="cyclic: row ranges per rank")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
@@ -44,9 +46,18 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 mode = bench.resolve_mode(args.mode, int(nprod_h.sum()), torch.cuda.get_device_properties(dev).total_memory)
 
 
-def block_ms(r0, r1):
-    a0, a1 = int(A.rpt[r0]), int(A.rpt[r1])
-    Ab = gen.Csr(r1 - r0, A.cols, (A.rpt[r0:r1 + 1] - a0).astype(np.int64), A.col[a0:a1].copy(), A.val[a0:a1].copy())
+def rows_csr(ranges):
+    """The rows of the given [r0, r1) ranges of A, concatenated, as a CSR."""
+    lens = np.concatenate([np.diff(A.rpt[r0:r1 + 1]) for r0, r1 in ranges]) if ranges else np.zeros(0, np.int64)
+    rpt = np.zeros(lens.size + 1, np.int64)
+    np.cumsum(lens, out=rpt[1:])
+    col = np.concatenate([A.col[int(A.rpt[r0]):int(A.rpt[r1])] for r0, r1 in ranges])
+    val = np.concatenate([A.val[int(A.rpt[r0]):int(A.rpt[r1])] for r0, r1 in ranges])
+    return gen.Csr(lens.size, A.cols, rpt, col, val)
+
+
+def block_ms(r0, r1=None):
+    Ab = rows_csr([(r0, r1)] if r1 is not None else r0)
     Ad = TorchCsr.from_csr(Ab)
     # a rank of the real run owns a whole GPU: give the cached blocks of the
     # previous (larger) C back first -- the heavy rows' level batches are sized
@@ -84,14 +95,22 @@ def host_bounds(n):
 
 out["balance"] = args.balance
 for n in [int(x) for x in args.ns.split(",")]:
-    bounds = ctx.brm_partition_rows(off, n).cpu().numpy() if args.balance == "nprod" else host_bounds(n)
-    ms = [block_ms(int(bounds[r]), int(bounds[r + 1])) for r in range(n)]
-    share = [float(nprod_h[bounds[r]:bounds[r + 1]].sum() / nprod_h.sum()) for r in range(n)]
+    if args.balance == "cyclic" and n > 1:
+        cb = ctx.brm_partition_rows(off, n * args.chunks).cpu().numpy()
+        parts = [[(int(cb[j]), int(cb[j + 1])) for j in range(r, n * args.chunks, n)] for r in range(n)]
+        ms = [block_ms(p) for p in parts]
+        share = [float(sum(nprod_h[a:b].sum() for a, b in p) / nprod_h.sum()) for p in parts]
+        bounds = None
+    else:
+        bounds = ctx.brm_partition_rows(off, n).cpu().numpy() if args.balance != "work" else host_bounds(n)
+        ms = [block_ms(int(bounds[r]), int(bounds[r + 1])) for r in range(n)]
+        share = [float(nprod_h[bounds[r]:bounds[r + 1]].sum() / nprod_h.sum()) for r in range(n)]
     if n == 1:
         t1 = ms[0]
     eff = t1 / (n * max(ms)) if t1 else None
     out["per_n"][n] = {"block_ms": ms, "nprod_share": share, "max_ms": max(ms), "bound_efficiency": eff,
-                       "rows": [int(bounds[r + 1] - bounds[r]) for r in range(n)]}
+                       "rows": ([int(bounds[r + 1] - bounds[r]) for r in range(n)] if bounds is not None
+                                else [sum(b - a for a, b in p) for p in parts])}
     print(f"N={n}: max {max(ms):.1f} ms, blocks {[round(x, 1) for x in ms]}, bound efficiency {eff}",
           file=sys.stderr, flush=True)
 print(json.dumps(out))
