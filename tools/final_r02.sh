@@ -23,7 +23,7 @@ for cm in stencil27_64:upper stencil27_64:precise uniform1m_k16:upper uniform1m_
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file $OUT/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_launch.log 2>&1
-for spec in rmat20_ef16:precise:k_hv_merge:full_hv_merge stencil27_64:upper:k_tierILi32ELi768:full_stencil_t4 uniform1m_k16:upper:k_tierILi32ELi256:full_uniform_t3 amg_lap2048_agg2x2:precise:k_tiny:full_amg_t1; do
+for spec in rmat20_ef16:precise:k_hv_merge:full_hv_merge stencil27_64:upper:k_tierILi32ELi768:full_stencil_t4 uniform1m_k16:upper:k_tierILi32ELi256:full_uniform_t3 amg_lap2048_agg2x2:precise:k_tinyILb1ELi2:full_amg_t1; do
   IFS=: read cfg mode K N <<< "$spec"
   timeout 1500 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:$K -c 1 -o $OUT/$N \
     python bench.py --config $cfg --mode $mode --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/ncu_$N.log 2>&1
