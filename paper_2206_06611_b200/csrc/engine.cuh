@@ -173,6 +173,25 @@ __device__ __forceinline__ void tiny_row(const CsrView& A, const CsrView& B, int
         be[l] = __ldg(B.rpt + k + 1);
       }
     }
+#ifndef BRM_TINY_PREFETCH
+#define BRM_TINY_PREFETCH 0  // tuning switch: 1 / 2 prefetch every list's first entry to L2 / L1 before the gather loop
+#endif
+    if constexpr (BRM_TINY_PREFETCH > 0) {
+      // the gather loop below takes the lists one after another (a load
+      // latency each); their first entries start towards the cache together
+#pragma unroll
+      for (int l = 0; l < kTinyL; ++l) {
+        if (l < nl && bb[l] < be[l]) {
+          if constexpr (BRM_TINY_PREFETCH == 1) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(B.col + bb[l]));
+            if (VALS) asm volatile("prefetch.global.L2 [%0];" ::"l"(B.val + bb[l]));
+          } else {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(B.col + bb[l]));
+            if (VALS) asm volatile("prefetch.global.L1 [%0];" ::"l"(B.val + bb[l]));
+          }
+        }
+      }
+    }
   }
   int off[kTinyL + 1];
   int P = 0;
