@@ -157,10 +157,9 @@ __host__ __device__ constexpr int tiny_block_bytes() {
 }
 
 template <int NT, bool VALS, int OUT>
-__device__ __forceinline__ void tiny_row(const CsrView& A, const CsrView& B, int64_t row, const RowOut& o,
-                                         int* pc, int* qc, double* pv, double* qv) {
-  const int64_t a0 = A.rpt[row];
-  const int nl = static_cast<int>(A.rpt[row + 1] - a0);
+__device__ __forceinline__ void tiny_row(const CsrView& A, const CsrView& B, int64_t row, int64_t a0, int nl,
+                                         const RowOut& o, int* pc, int* qc, double* pv, double* qv) {
+  // (a0 = A.rpt[row], nl = A.rpt[row + 1] - a0: loaded by the caller, one row ahead)
   // Alg. 1 lines 10-15: list l into the ping buffer at [off[l], off[l+1]);
   // the B row bounds of all lists are loaded before any list is gathered
 #ifndef BRM_TINY_BATCH
