@@ -243,7 +243,12 @@ __global__ void __launch_bounds__(256) k_long_nprod(CsrView A, const int64_t* __
 // thread) with a decoupled look-back across tiles. Large tiles keep the
 // look-back chain short (4.2M rows -> 2048 tiles).
 constexpr int kNpTile = kScanTile;
-__global__ void __launch_bounds__(kScanThreads) k_nprod_scan(CsrView A, const int64_t* __restrict__ brpt,
+#ifndef BRM_NPS_MINB
+#define BRM_NPS_MINB 5  // launch-bounds CTAs per SM of k_nprod_scan: 48 registers, 5 CTAs (63 / 4 without a bound);
+// the pass waits on dependent loads (long-scoreboard 10.7 per issue on AMG): AMG 0.1946 -> 0.1734 ms with 5,
+// 0.1765 with 6 (spills); uniform1m_k16 0.1739 -> 0.1788 (profiles/r02k/nps)
+#endif
+__global__ void __launch_bounds__(kScanThreads, BRM_NPS_MINB) k_nprod_scan(CsrView A, const int64_t* __restrict__ brpt,
                                                              int64_t M, int64_t* __restrict__ nprod_off,
                                                              unsigned long long* status,
                                                              unsigned int* tile_counter,
