@@ -140,7 +140,14 @@ __device__ __forceinline__ void warp_rows_nprod(const CsrView& A, const int64_t*
     if (lng) {
       acc = long_np[r0 + lane];
     } else if (valid) {
+#ifndef BRM_NPS_U8
+#define BRM_NPS_U8 0  // 1: eight of a row's gathers in flight instead of four (tuning switch)
+#endif
+#if BRM_NPS_U8
+#pragma unroll 8
+#else
 #pragma unroll 4
+#endif
       for (int64_t p = rs; p < rs + nl; ++p) {
         const int k = __ldg(A.col + p);
         acc += __ldg(brpt + k + 1) - __ldg(brpt + k);
