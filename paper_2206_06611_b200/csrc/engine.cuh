@@ -1169,7 +1169,21 @@ __host__ __device__ constexpr int hash_cap() {
   return h;
 }
 
+#ifndef BRM_HASH_CPASYNC
+#define BRM_HASH_CPASYNC 0  // 1: hash symbolic with one load in flight per thread (tier 3) stages the row's columns by cp.async first (A/B switch)
+#endif
+// the hash loop with HB = 1 waits for a column load in every iteration (more
+// loads in flight cost it registers: profiles/r02_variants); staged, all of
+// the row's columns are in flight at once and the loop reads shared memory.
+// Measured on B200 (profiles/r02m): uniform1m_k16's tier-3 symbolic 1.599 ->
+// 1.670 ms (4 KB more shared memory per CTA: fewer resident rows), uniform2k_k8
+// 0.0140 -> 0.0106 ms; off.
+template <int G, int HB>
+__host__ __device__ constexpr bool hash_staged() {
+  return BRM_HASH_CPASYNC && HB == 1 && G <= 32;
+}
 struct HashBufs {
+  int* stage;           // CAP columns (hash_staged only)
   int* table;           // HCAP slots
   unsigned short* owner;  // CAP: list of each product
   int* off;             // LCAP + 1 list offsets (product index)
@@ -1177,10 +1191,10 @@ struct HashBufs {
   int* scan_tmp;
 };
 
-template <int G, int CAP, int LCAP, int HQ>
+template <int G, int CAP, int LCAP, int HQ, bool STAGE = false>
 __host__ __device__ constexpr int hash_group_bytes() {
   return align16(hash_cap<CAP, HQ>() * 4) + align16(CAP * 2) + align16((LCAP + 1) * 4) + align16(LCAP * 8) +
-         (G > 32 ? align16((G / 32 + 2) * 4) : 0);
+         (G > 32 ? align16((G / 32 + 2) * 4) : 0) + (STAGE ? align16(CAP * 4) : 0);
 }
 
 // DIRECT: insert by atomicCAS straight away; else read the slot first and
@@ -1241,6 +1255,19 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
   for (int l = rank; l < nl; l += G) owner_fill(hb.owner, 1, hb.off[l], hb.off[l + 1], l);
   g.sync();
   int cnt = 0;
+  constexpr bool STAGE = hash_staged<G, HB>();
+  if constexpr (STAGE) {
+    // every column of the row copied to shared memory by cp.async; a thread
+    // hashes the entries it copied (no other thread's copies are read)
+    for (int e = rank; e < P; e += G) {
+      const int l = hb.owner[e];
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(hb.stage + e)),
+                   "l"(B.col + hb.bst[l] + (e - hb.off[l]))
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  }
   // HB column loads in flight per thread before they are hashed
   for (int eb = rank; eb < P; eb += G * HB) {
     int cc[HB];
@@ -1249,8 +1276,12 @@ __device__ __forceinline__ void hash_row(const Group<G>& g, const CsrView& A, co
       const int e = eb + u * G;
       cc[u] = -1;
       if (e < P) {
-        const int l = hb.owner[e];
-        cc[u] = __ldg(B.col + hb.bst[l] + (e - hb.off[l]));
+        if constexpr (STAGE) {
+          cc[u] = hb.stage[e];
+        } else {
+          const int l = hb.owner[e];
+          cc[u] = __ldg(B.col + hb.bst[l] + (e - hb.off[l]));
+        }
       }
     }
     if (use_bm) {

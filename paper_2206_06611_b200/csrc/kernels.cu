@@ -528,7 +528,8 @@ __global__ void __launch_bounds__(G * GPC) k_hash_symbolic(CsrView A, CsrView B,
   extern __shared__ __align__(16) unsigned char smem[];
   const Group<G> g = make_group<G>();
   const int gid = threadIdx.x / G;
-  unsigned char* p = smem + gid * hash_group_bytes<G, CAP, LCAP, HQ>();
+  constexpr bool STAGE = hash_staged<G, HB>();
+  unsigned char* p = smem + gid * hash_group_bytes<G, CAP, LCAP, HQ, STAGE>();
   auto take = [&](int n) {
     unsigned char* q = p;
     p += align16(n);
@@ -540,6 +541,7 @@ __global__ void __launch_bounds__(G * GPC) k_hash_symbolic(CsrView A, CsrView B,
   hb.off = reinterpret_cast<int*>(take((LCAP + 1) * 4));
   hb.bst = reinterpret_cast<int64_t*>(take(LCAP * 8));
   hb.scan_tmp = G > 32 ? reinterpret_cast<int*>(take((G / 32 + 2) * 4)) : nullptr;
+  hb.stage = STAGE ? reinterpret_cast<int*>(take(CAP * 4)) : nullptr;
   for (int64_t r = (int64_t)blockIdx.x * GPC + gid; r < nrows; r += (int64_t)gridDim.x * GPC)
     hash_row<G, CAP, HB, HQ, DIRECT>(g, A, B, rows[r], o, hb);
 }
@@ -840,7 +842,7 @@ template <int G, int CAP, int LCAP, int GPC, int HB, int HQ, bool DIRECT>
 static cudaError_t launch_hash_t(const CsrView& A, const CsrView& B, const int32_t* rows, int64_t n, const RowOut& o,
                                  cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  constexpr int smem = hash_group_bytes<G, CAP, LCAP, HQ>() * GPC;
+  constexpr int smem = hash_group_bytes<G, CAP, LCAP, HQ, hash_staged<G, HB>()>() * GPC;
   static_assert(smem <= 232448, "hash tier shared memory exceeds 227 KB");
   static_assert(G <= 32 || GPC == 1, "a group of more than 32 threads is the whole CTA");
   auto kern = k_hash_symbolic<G, CAP, LCAP, GPC, HB, HQ, DIRECT>;
